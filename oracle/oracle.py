@@ -1,0 +1,163 @@
+"""ctypes front-end for the C oracle (test infrastructure only; see __init__)."""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+OK, ERR_EMPTY, ERR_ARG, ERR_TOKEN_K, ERR_BEAM_DIED = 0, 1, 2, 3, 4
+
+
+class OracleError(ValueError):
+    pass
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [
+        ("beam", ctypes.c_int64),
+        ("beam_size_token", ctypes.c_int64),
+        ("n_best", ctypes.c_int64),
+        ("blank", ctypes.c_int64),
+        ("merge_max", ctypes.c_int32),
+        ("beam_threshold", ctypes.c_double),
+        ("skip_threshold", ctypes.c_double),
+    ]
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "build", "libctc_oracle.so")
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (oracle/Makefile)."""
+    path = lib_path()
+    src = os.path.join(_HERE, "ctc_oracle.c")
+    if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return path
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        path = lib_path()
+        if not os.path.exists(path):
+            build()
+        lib = ctypes.CDLL(path)
+        p = ctypes.POINTER
+        lib.ctco_decode.argtypes = [
+            p(ctypes.c_double), ctypes.c_int64, ctypes.c_int64, p(_Opts),
+            p(ctypes.c_int32), p(ctypes.c_int32), p(ctypes.c_int32), p(ctypes.c_int32),
+            p(ctypes.c_double), p(ctypes.c_int32), p(ctypes.c_int64), p(ctypes.c_int64),
+        ]
+        lib.ctco_decode.restype = ctypes.c_int
+        lib.ctco_blank_keep.argtypes = [
+            p(ctypes.c_double), ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+            ctypes.c_double, p(ctypes.c_int32), p(ctypes.c_int64),
+        ]
+        lib.ctco_blank_keep.restype = ctypes.c_int
+        _LIB = lib
+    return _LIB
+
+
+@dataclass
+class OracleResult:
+    """n-best of one utterance: like ctcforge's NBestList (decoder.py:69-99)."""
+
+    tokens: list = field(default_factory=list)      # list[list[int]]
+    scores: list = field(default_factory=list)      # list[float]
+    timesteps: list = field(default_factory=list)   # list[list[int]]
+    frame_map: np.ndarray | None = None             # kept original frames
+
+    def __len__(self):
+        return len(self.tokens)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def blank_keep(lp: np.ndarray, threshold: float, blank: int = 0) -> np.ndarray:
+    """Kept-frame indices of blank_collapse (emissions.py:284-306)."""
+    lp = np.ascontiguousarray(lp, dtype=np.float64)
+    t, v = lp.shape
+    fm = np.zeros(max(t, 1), dtype=np.int32)
+    n = ctypes.c_int64(0)
+    rc = _lib().ctco_blank_keep(_ptr(lp, ctypes.c_double), t, v, blank, float(threshold),
+                                _ptr(fm, ctypes.c_int32), ctypes.byref(n))
+    if rc != OK:
+        raise OracleError(f"threshold must be in (0, 1], got {threshold}")
+    return fm[: n.value].copy()
+
+
+def decode(lp: np.ndarray, beam_size: int = 10, n_best: int = 1, blank_skip_threshold: float = 1.0,
+           beam_threshold: float = 50.0, beam_size_token: int | None = None,
+           merge_mode: str = "logadd", blank: int = 0) -> OracleResult:
+    """Decode one utterance ``lp`` [T, V] (float32 is upcast exactly to float64,
+    as EmissionMatrix does at emissions.py:129)."""
+    lp = np.ascontiguousarray(lp, dtype=np.float64)
+    if lp.ndim != 2:
+        raise OracleError(f"log_probs must be 2-D, got shape {lp.shape}")
+    t, v = lp.shape
+    opts = _Opts(beam_size, 0 if beam_size_token is None else beam_size_token, n_best, blank,
+                 1 if merge_mode == "max" else 0,
+                 float(beam_threshold), float(blank_skip_threshold))
+    cnt = ctypes.c_int32(0)
+    nk = ctypes.c_int64(0)
+    ef = ctypes.c_int64(-1)
+    tmax = max(t, 1)
+    out_len = np.zeros(max(n_best, 1), dtype=np.int32)
+    out_tok = np.zeros((max(n_best, 1), tmax), dtype=np.int32)
+    out_ts = np.zeros((max(n_best, 1), tmax), dtype=np.int32)
+    out_sc = np.zeros(max(n_best, 1), dtype=np.float64)
+    fm = np.zeros(tmax, dtype=np.int32)
+    rc = _lib().ctco_decode(_ptr(lp, ctypes.c_double), t, v, ctypes.byref(opts), ctypes.byref(cnt),
+                            _ptr(out_len, ctypes.c_int32), _ptr(out_tok, ctypes.c_int32),
+                            _ptr(out_ts, ctypes.c_int32), _ptr(out_sc, ctypes.c_double),
+                            _ptr(fm, ctypes.c_int32), ctypes.byref(nk), ctypes.byref(ef))
+    if rc == ERR_EMPTY:
+        raise OracleError("empty emissions")
+    if rc == ERR_ARG:
+        raise OracleError("invalid decoder options")
+    if rc == ERR_TOKEN_K:
+        raise OracleError(f"beam_size_token {beam_size_token} exceeds vocabulary size {v}")
+    if rc == ERR_BEAM_DIED:
+        raise OracleError(f"beam died at frame {ef.value}: no extension survives "
+                          f"(beam_size_token={beam_size_token if beam_size_token else v} may be too small)")
+    res = OracleResult(frame_map=fm[: nk.value].copy())
+    for r in range(cnt.value):
+        n = int(out_len[r])
+        res.tokens.append(out_tok[r, :n].tolist())
+        res.timesteps.append(out_ts[r, :n].tolist())
+        res.scores.append(float(out_sc[r]))
+    return res
+
+
+def decode_batch(log_probs: np.ndarray, lens, threads: int | None = None, **kw) -> list[OracleResult]:
+    """Decode utterances ``log_probs[b, :lens[b]]`` on ``threads`` host threads
+    (the C call releases the GIL).  Errors carry the utterance index, as
+    decode_batch does at decoder.py:156-157."""
+    threads = threads or os.cpu_count() or 1
+
+    def one(b):
+        try:
+            return decode(log_probs[b, : int(lens[b])], **kw)
+        except OracleError as exc:
+            raise OracleError(f"utterance {b}: {exc}") from exc
+
+    if threads <= 1 or len(lens) <= 1:
+        return [one(b) for b in range(len(lens))]
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        return list(pool.map(one, range(len(lens))))
+
+
+INF = math.inf
