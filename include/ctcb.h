@@ -1,0 +1,123 @@
+/*
+ * ctcb — B200-native (sm_100a) CTC prefix beam-search decoder: C ABI.
+ *
+ * The reference has no FFI for this path: its boundary is the Python call
+ *   ctcforge.beam_search_decode(emissions, tokens, opts)
+ *       /root/reference/pkg/src/ctcforge/decoder.py:102-135
+ *   ctcforge.decode_batch(emissions, tokens, opts, workers)
+ *       /root/reference/pkg/src/ctcforge/decoder.py:138-170
+ * with blank skipping in ctcforge.blank_collapse (emissions.py:284-306).
+ * These entry points are what a binding for that path attaches to (ctypes
+ * stub in INTEGRATION.md); the Python façade `cuda_ctc_decoder` /
+ * `CUCTCDecoder` (paper_2310_17864_b200/decoder.py) is built on them.
+ *
+ * Conventions: plain pointers and sizes; every function returns a ctcb status
+ * (0 = OK).  Device pointers are CUDA device memory on the handle's device.
+ * ctcb_decode only enqueues work on `stream`; outputs are valid once the
+ * stream has been synchronised.  A handle is not thread-safe: use one handle
+ * per host thread / stream.
+ */
+#ifndef CTCB_H
+#define CTCB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ctcb_handle ctcb_t;
+
+enum {
+  CTCB_OK = 0,
+  CTCB_ERR_ARG = 1,          /* invalid argument (message: ctcb_last_error) */
+  CTCB_ERR_CUDA = 2,         /* CUDA runtime error */
+  CTCB_ERR_WORKSPACE = 3,    /* workspace too small */
+  CTCB_ERR_UNSUPPORTED = 4,  /* configuration exceeds device limits */
+};
+
+/* Per-utterance status written to out_status by ctcb_decode. */
+enum {
+  CTCB_UTT_OK = 0,
+  CTCB_UTT_EMPTY = 1,      /* len == 0: "empty emissions" (decoder.py:117-118) */
+  CTCB_UTT_BAD_LEN = 2,    /* len < 0 or len > t_max */
+  CTCB_UTT_BEAM_DIED = 3,  /* no finite extension survives (decoder.py:616-620) */
+};
+
+/* Create a decoder.  Replaces DecoderOptions (decoder.py:34-66) + the
+ * TokenDictionary blank index (emissions.py:36-63) for the lexicon-free,
+ * LM-free, full-vocabulary, logadd-merge configuration:
+ *   vocab           V (number of emission columns)
+ *   blank           blank index, 0 <= blank < V
+ *   beam            beam_size, 1 <= beam <= 512
+ *   nbest           n_best, 1 <= nbest <= beam
+ *   skip_cutoff     drop frame t iff log_probs[t, blank] >= skip_cutoff
+ *                   (+INFINITY disables skipping: blank_skip_threshold == 1.0;
+ *                   see ctcb_skip_cutoff)
+ *   beam_threshold  > 0; +INFINITY disables the cut (decoder.py:621-623)
+ *   device          CUDA device ordinal */
+int ctcb_create(int vocab, int blank, int beam, int nbest, float skip_cutoff, double beam_threshold,
+                int device, ctcb_t** out);
+int ctcb_destroy(ctcb_t* h);
+
+/* fp32 cutoff c(thr) such that, for every finite fp32 x,
+ *   x >= c  <=>  exp((double)x) >= thr - 1e-12
+ * i.e. ctcforge's skip rule (emissions.py:300-301, BLANK_SKIP_EPS :29).
+ * thr in (0, 1]; thr == 1 returns +INFINITY (skipping disabled, :298-299). */
+int ctcb_skip_cutoff(double threshold, float* cutoff);
+
+/* Tokens kept per frame by the exact reduced search: min(2*beam, V-1). */
+int ctcb_topk_size(const ctcb_t* h, int* k);
+
+/* Device workspace needed to decode `batch` utterances padded to `t_max`. */
+int ctcb_workspace_bytes(const ctcb_t* h, int batch, int t_max, size_t* bytes);
+
+/* Decode a batch.  Replaces decode_batch (decoder.py:138-170):
+ *   log_probs   device fp32, element (b, t, v) at b*stride_b + t*stride_t + v
+ *   lens        device int32 [batch] valid frames per utterance
+ *   workspace   device buffer of >= ctcb_workspace_bytes (NULL: the handle
+ *               allocates and caches one)
+ *   stream      cudaStream_t (NULL: legacy default stream)
+ * Outputs (device):
+ *   out_tokens     int32 [batch, nbest, t_max] token ids of each hypothesis
+ *   out_timesteps  int32 [batch, nbest, t_max] original frame of each token
+ *                  (Hypothesis.timesteps, decoder.py:69-83), or NULL
+ *   out_len        int32 [batch, nbest] tokens per hypothesis
+ *   out_score      float64 [batch, nbest] hypothesis score (logadd of the
+ *                  prefix's blank / non-blank variants, decoder.py:789-791)
+ *   out_count      int32 [batch] hypotheses returned (<= nbest)
+ *   out_status     int32 [batch] CTCB_UTT_* per utterance */
+int ctcb_decode(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
+                int batch, int t_max, void* workspace, size_t workspace_bytes, void* stream,
+                int32_t* out_tokens, int32_t* out_timesteps, int32_t* out_len, double* out_score,
+                int32_t* out_count, int32_t* out_status);
+
+/* Debug / minimum slice: blank-skip compaction and per-frame top-k only.
+ * Replaces blank_collapse (emissions.py:284-306) and the token selection of
+ * _BeamSearch._step (decoder.py:431-460, :440):
+ *   out_frame_map  int32 [batch, t_max]   kept original frames (first out_kept[b])
+ *   out_kept       int32 [batch]
+ *   out_topk_tok   int32 [batch, t_max, k] best non-blank tokens of each kept
+ *                  frame by (log-prob desc, index asc), k = ctcb_topk_size
+ *   out_topk_val   float [batch, t_max, k] their log-probs
+ *   out_blank      float [batch, t_max]   the blank log-prob of each kept frame */
+int ctcb_debug_frames(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t,
+                      const int32_t* lens, int batch, int t_max, void* stream, int32_t* out_frame_map,
+                      int32_t* out_kept, int32_t* out_topk_tok, float* out_topk_val, float* out_blank);
+
+/* Validation pass mirroring EmissionMatrix(strict=True) (emissions.py:128-150):
+ * first offending (b, t, v) of: non-finite value (code 1), value > 1e-4
+ * (code 2), |logsumexp(row)| > 1e-3 (code 3, v = -1).  out_error: device
+ * int64 [4] = {code, b, t, v}, code 0 if clean. Frames t >= lens[b] are ignored. */
+int ctcb_validate(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
+                  int batch, int t_max, int strict, void* stream, int64_t* out_error);
+
+const char* ctcb_status_string(int status);
+/* Message of the last error on this host thread. */
+const char* ctcb_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTCB_H */

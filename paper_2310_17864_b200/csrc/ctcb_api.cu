@@ -1,0 +1,315 @@
+// C ABI of the ctcb decoder (include/ctcb.h): argument checks, workspace
+// layout, launch configuration.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/ctcb.h"
+#include "ctcb_internal.h"
+
+namespace ctcb {
+__global__ void ctcb_decode_generic_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter);
+__global__ void ctcb_debug_kernel(const __grid_constant__ Params P, int32_t* out_topk_tok, float* out_topk_val,
+                                  float* out_blank);
+__global__ void ctcb_validate_kernel(const float* lp, long long sb, long long st, const int32_t* lens, int B,
+                                     int T, int V, int strict, unsigned long long* out_key);
+__global__ void ctcb_validate_decode_kernel(const unsigned long long* key, int T, int V, int64_t* out);
+}  // namespace ctcb
+
+struct ctcb_handle {
+  int V, blank, beam, nbest, k, kpad, device;
+  float cutoff;
+  double beam_threshold;
+  int num_sms, max_smem_optin;
+  void* ws;
+  size_t ws_bytes;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(CTCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CTCB_CUDA(call)                               \
+  do {                                                \
+    cudaError_t e__ = (call);                         \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+struct WsLayout {
+  size_t frame_map, kept, trellis, order, counter, seqbuf, total;
+};
+WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
+  WsLayout w{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = ctcb::align_up(o, 256);
+    o = r + bytes;
+    return r;
+  };
+  w.frame_map = take((size_t)B * T * 4);
+  w.kept = take((size_t)B * 4);
+  w.trellis = take((size_t)B * T * h->beam * 4);
+  w.order = take((size_t)B * 4);
+  w.counter = take(4);
+  w.seqbuf = take((size_t)B * 2 * (T + 1) * 4);
+  w.total = ctcb::align_up(o, 256);
+  return w;
+}
+
+int ring_for(int row_bytes) { return row_bytes <= 4096 ? 4 : (row_bytes <= 16384 ? 3 : 2); }
+
+// Fill the launch parameters shared by the decode and debug kernels.
+int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
+                void* ws, size_t ws_bytes, ctcb::Params& P, WsLayout& L) {
+  if (!lp || !lens) return fail(CTCB_ERR_ARG, "log_probs and lens must be device pointers");
+  if (B < 0 || T < 0) return fail(CTCB_ERR_ARG, "batch and t_max must be >= 0");
+  if (st < h->V || sb < (int64_t)st * (T > 0 ? T : 1))
+    return fail(CTCB_ERR_ARG, "strides must describe a [batch, t_max, vocab] layout with unit vocab stride");
+  L = ws_layout(h, B, T);
+  if (!ws) {
+    if (h->ws_bytes < L.total) {
+      if (h->ws) cudaFree(h->ws);
+      h->ws = nullptr;
+      h->ws_bytes = 0;
+      CTCB_CUDA(cudaMalloc(&h->ws, L.total));
+      h->ws_bytes = L.total;
+    }
+    ws = h->ws;
+  } else if (ws_bytes < L.total) {
+    return fail(CTCB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
+  }
+  char* base = (char*)ws;
+  memset(&P, 0, sizeof(P));
+  P.lp = lp;
+  P.stride_b = sb;
+  P.stride_t = st;
+  P.lens = lens;
+  P.B = B;
+  P.T_max = T;
+  P.V = h->V;
+  P.blank = h->blank;
+  P.beam = h->beam;
+  P.nbest = h->nbest;
+  P.k = h->k;
+  P.kpad = h->kpad;
+  P.cutoff = h->cutoff;
+  P.skip = std::isfinite(h->cutoff) || h->cutoff < 0 ? 1 : 0;
+  P.beam_threshold = h->beam_threshold;
+  P.threshold_inf = std::isinf(h->beam_threshold) ? 1 : 0;
+  P.frame_map = (int32_t*)(base + L.frame_map);
+  P.kept = (int32_t*)(base + L.kept);
+  P.trellis = (uint32_t*)(base + L.trellis);
+  P.order = (int32_t*)(base + L.order);
+  P.counter = (int32_t*)(base + L.counter);
+  P.seqbuf = (int32_t*)(base + L.seqbuf);
+  P.row_bytes = (int)ctcb::align_up((size_t)h->V * 4, 16);
+  P.ring = ring_for(P.row_bytes);
+  P.bulk_ok = ((uintptr_t)lp % 16 == 0) && ((h->V * 4) % 16 == 0) && ((st * 4) % 16 == 0) && ((sb * 4) % 16 == 0);
+  return CTCB_OK;
+}
+
+int launch_config(ctcb_handle* h, ctcb::Params& P, int B) {
+  for (;;) {
+    ctcb::WarpLayout WL = ctcb::make_layout(P.beam, P.kpad, P.V, P.ring, P.row_bytes);
+    P.smem_per_warp = (int)WL.total;
+    if ((int)WL.total <= h->max_smem_optin) break;
+    if (P.ring > 1) { P.ring--; continue; }
+    return fail(CTCB_ERR_UNSUPPORTED, "beam/vocabulary too large for one warp's shared memory");
+  }
+  int wpb = h->max_smem_optin / P.smem_per_warp;
+  wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+  P.warps_per_block = wpb;
+  return CTCB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ctcb_status_string(int status) {
+  switch (status) {
+    case CTCB_OK: return "ok";
+    case CTCB_ERR_ARG: return "invalid argument";
+    case CTCB_ERR_CUDA: return "CUDA error";
+    case CTCB_ERR_WORKSPACE: return "workspace too small";
+    case CTCB_ERR_UNSUPPORTED: return "unsupported configuration";
+    default: return "unknown status";
+  }
+}
+
+const char* ctcb_last_error(void) { return g_last_error.c_str(); }
+
+int ctcb_skip_cutoff(double thr, float* cutoff) {
+  if (!cutoff) return fail(CTCB_ERR_ARG, "cutoff must not be NULL");
+  if (!(thr > 0.0 && thr <= 1.0)) return fail(CTCB_ERR_ARG, "blank_skip_threshold must be in (0, 1]");
+  if (thr == 1.0) { *cutoff = INFINITY; return CTCB_OK; }
+  const double target = thr - 1e-12;  // emissions.py:29, :300-301
+  if (!(target > 0.0)) { *cutoff = -INFINITY; return CTCB_OK; }
+  auto drop = [&](float x) { return std::exp((double)x) >= target; };
+  float c = (float)std::log(target);
+  while (drop(std::nextafter(c, -INFINITY))) c = std::nextafter(c, -INFINITY);
+  while (!drop(c)) c = std::nextafter(c, INFINITY);
+  *cutoff = c;
+  return CTCB_OK;
+}
+
+int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double beam_threshold, int device,
+                ctcb_t** out) {
+  if (!out) return fail(CTCB_ERR_ARG, "out must not be NULL");
+  *out = nullptr;
+  if (V < 2) return fail(CTCB_ERR_ARG, "vocabulary must have at least 2 tokens (blank + 1)");
+  if (V >= (1 << 22) - 1) return fail(CTCB_ERR_UNSUPPORTED, "vocabulary too large (max 4194302)");
+  if (blank < 0 || blank >= V) return fail(CTCB_ERR_ARG, "blank_index " + std::to_string(blank) + " out of range");
+  if (beam < 1) return fail(CTCB_ERR_ARG, "beam_size must be >= 1");
+  if (beam > 512) return fail(CTCB_ERR_UNSUPPORTED, "beam_size must be <= 512");
+  if (nbest < 1 || nbest > beam) return fail(CTCB_ERR_ARG, "n_best must be in [1, beam_size]");
+  if (!(beam_threshold > 0)) return fail(CTCB_ERR_ARG, "beam_threshold must be positive");
+  if (std::isnan(skip_cutoff)) return fail(CTCB_ERR_ARG, "skip_cutoff must not be NaN");
+  int ndev = 0;
+  CTCB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(CTCB_ERR_ARG, "invalid CUDA device " + std::to_string(device));
+  ctcb_handle* h = new ctcb_handle();
+  h->V = V;
+  h->blank = blank;
+  h->beam = beam;
+  h->nbest = nbest;
+  h->k = 2 * beam < V - 1 ? 2 * beam : V - 1;
+  h->kpad = ctcb::pow2_at_least(h->k);
+  h->device = device;
+  h->cutoff = skip_cutoff;
+  h->beam_threshold = beam_threshold;
+  h->ws = nullptr;
+  h->ws_bytes = 0;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaGetDeviceProperties"); }
+  if (prop.major < 10) { delete h; return fail(CTCB_ERR_UNSUPPORTED, "ctcb requires an sm_100 (Blackwell) GPU"); }
+  h->num_sms = prop.multiProcessorCount;
+  h->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+  *out = h;
+  return CTCB_OK;
+}
+
+int ctcb_destroy(ctcb_t* h) {
+  if (!h) return CTCB_OK;
+  if (h->ws) cudaFree(h->ws);
+  delete h;
+  return CTCB_OK;
+}
+
+int ctcb_topk_size(const ctcb_t* h, int* k) {
+  if (!h || !k) return fail(CTCB_ERR_ARG, "NULL argument");
+  *k = h->k;
+  return CTCB_OK;
+}
+
+int ctcb_workspace_bytes(const ctcb_t* h, int batch, int t_max, size_t* bytes) {
+  if (!h || !bytes) return fail(CTCB_ERR_ARG, "NULL argument");
+  if (batch < 0 || t_max < 0) return fail(CTCB_ERR_ARG, "batch and t_max must be >= 0");
+  *bytes = ws_layout(h, batch, t_max).total;
+  return CTCB_OK;
+}
+
+int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T, void* ws,
+                size_t ws_bytes, void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len,
+                double* out_score, int32_t* out_count, int32_t* out_status) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  if (!out_tokens || !out_len || !out_score || !out_count || !out_status)
+    return fail(CTCB_ERR_ARG, "output pointers must not be NULL (out_timesteps may be)");
+  if (B == 0) return CTCB_OK;
+  CTCB_CUDA(cudaSetDevice(h->device));
+  ctcb::Params P;
+  WsLayout L;
+  int rc = make_params(h, lp, sb, st, lens, B, T, ws, ws_bytes, P, L);
+  if (rc) return rc;
+  P.status = out_status;
+  P.out_tokens = out_tokens;
+  P.out_ts = out_ts;
+  P.out_len = out_len;
+  P.out_score = out_score;
+  P.out_count = out_count;
+  rc = launch_config(h, P, B);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  int n = 1;
+  while (n < B) n <<= 1;
+  size_t order_smem = n <= 8192 ? (size_t)n * 8 : 0;
+  CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  ctcb::ctcb_order_kernel<<<1, 1024, order_smem, s>>>(lens, B, P.order, P.counter);
+  CTCB_CUDA(cudaGetLastError());
+  size_t smem = (size_t)P.smem_per_warp * P.warps_per_block;
+  CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_decode_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  int blocks_per_sm = 0;
+  CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ctcb::ctcb_decode_generic_kernel,
+                                                          32 * P.warps_per_block, smem));
+  if (blocks_per_sm < 1) blocks_per_sm = 1;
+  int need = (B + P.warps_per_block - 1) / P.warps_per_block;
+  int grid = h->num_sms * blocks_per_sm;
+  if (grid > need) grid = need;
+  ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
+  CTCB_CUDA(cudaGetLastError());
+  return CTCB_OK;
+}
+
+int ctcb_debug_frames(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
+                      void* stream, int32_t* out_frame_map, int32_t* out_kept, int32_t* out_topk_tok,
+                      float* out_topk_val, float* out_blank) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  if (!out_frame_map || !out_kept || !out_topk_tok || !out_topk_val || !out_blank)
+    return fail(CTCB_ERR_ARG, "output pointers must not be NULL");
+  if (B == 0) return CTCB_OK;
+  CTCB_CUDA(cudaSetDevice(h->device));
+  ctcb::Params P;
+  WsLayout L;
+  int rc = make_params(h, lp, sb, st, lens, B, T, nullptr, 0, P, L);
+  if (rc) return rc;
+  P.frame_map = out_frame_map;
+  P.kept = out_kept;
+  rc = launch_config(h, P, B);
+  if (rc) return rc;
+  size_t smem = (size_t)P.smem_per_warp;
+  CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_debug_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ctcb::ctcb_debug_kernel<<<B, 32, smem, (cudaStream_t)stream>>>(P, out_topk_tok, out_topk_val, out_blank);
+  CTCB_CUDA(cudaGetLastError());
+  return CTCB_OK;
+}
+
+int ctcb_validate(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T, int strict,
+                  void* stream, int64_t* out_error) {
+  if (!h || !lp || !lens || !out_error) return fail(CTCB_ERR_ARG, "NULL argument");
+  if (st < h->V || sb < (int64_t)st * (T > 0 ? T : 1))
+    return fail(CTCB_ERR_ARG, "strides must describe a [batch, t_max, vocab] layout with unit vocab stride");
+  CTCB_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->ws || h->ws_bytes < 256) {
+    if (h->ws) cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+    CTCB_CUDA(cudaMalloc(&h->ws, 256));
+    h->ws_bytes = 256;
+  }
+  unsigned long long* key = (unsigned long long*)h->ws;
+  CTCB_CUDA(cudaMemsetAsync(key, 0xff, sizeof(unsigned long long), s));
+  if (B > 0 && T > 0) {
+    dim3 grid((unsigned)((T + 7) / 8), (unsigned)B);
+    ctcb::ctcb_validate_kernel<<<grid, 256, 0, s>>>(lp, sb, st, lens, B, T, h->V, strict, key);
+    CTCB_CUDA(cudaGetLastError());
+  }
+  ctcb::ctcb_validate_decode_kernel<<<1, 1, 0, s>>>(key, T, h->V, out_error);
+  CTCB_CUDA(cudaGetLastError());
+  return CTCB_OK;
+}
+
+}  // extern "C"

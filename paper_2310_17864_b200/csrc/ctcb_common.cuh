@@ -1,0 +1,110 @@
+// Device utilities shared by the ctcb kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CTCB_LN2 0.693147180559945309417232121458176568
+
+namespace ctcb {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- ordering
+// Order-preserving unsigned key of an fp32 value (float comparison semantics:
+// -0.0 and +0.0 map to the same key, as numpy's lexsort compares them equal).
+__device__ __forceinline__ uint32_t ord32(float x) {
+  uint32_t u = __float_as_uint(__fadd_rn(x, 0.0f));
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord32(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+// Order-preserving key of an fp64 score.
+__device__ __forceinline__ uint64_t ord64(double d) {
+  if (d == 0.0) d = 0.0;
+  uint64_t u = (uint64_t)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// numpy's npy_logaddexp: the fold np.logaddexp.reduceat performs when the
+// reference merges candidates (decoder.py:611) and flag variants (:791).
+__device__ __forceinline__ double np_logaddexp(double x, double y) {
+  if (x == y) return x + CTCB_LN2;
+  double tmp = x - y;
+  if (tmp > 0) return x + log1p(exp(-tmp));
+  if (tmp <= 0) return y + log1p(exp(tmp));
+  return tmp;
+}
+
+// ---------------------------------------------------------------- prefixes
+// Content-defined prefix identity: a chained 64-bit hash of the token
+// sequence (plus its length, compared alongside).  The reference interns
+// prefixes globally per utterance through child_table (decoder.py:700-711),
+// so two hypotheses share a merge key iff their token sequences are equal;
+// a chained hash reproduces that equivalence (collision odds ~n^2/2^64).
+constexpr uint64_t kEmptyPrefixHash = 0x9e3779b97f4a7c15ull;
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27; x *= 0x94d049bb133111ebull;
+  x ^= x >> 31; return x;
+}
+__device__ __forceinline__ uint64_t child_hash(uint64_t h, int token) {
+  return mix64(h ^ ((uint64_t)(token + 1) * 0xd6e8feb86659fd93ull));
+}
+
+// Trellis back-pointer record: source slot (10 bits) | appended token + 1 (22 bits).
+constexpr int kSrcShift = 22;
+constexpr uint32_t kTokMask = (1u << kSrcShift) - 1;
+__device__ __forceinline__ uint32_t pack_trel(int src, int tok) {
+  return ((uint32_t)src << kSrcShift) | (uint32_t)(tok + 1);
+}
+__device__ __forceinline__ int trel_src(uint32_t r) { return (int)(r >> kSrcShift); }
+__device__ __forceinline__ int trel_tok(uint32_t r) { return (int)(r & kTokMask) - 1; }
+
+// ---------------------------------------------------------------- warp
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------- TMA bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine (UBLKCP), completing
+// on the mbarrier's transaction count.  dst/src 16 B aligned, bytes % 16 == 0.
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+}  // namespace ctcb

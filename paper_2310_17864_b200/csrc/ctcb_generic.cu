@@ -1,0 +1,723 @@
+// Generic CTC prefix beam-search decode kernel: one warp per utterance,
+// any beam <= 1024, any vocabulary.  Semantics follow the reference CPU
+// decoder (ctcforge, decoder.py:102-817; emissions.py:284-306) exactly; see
+// DESIGN.md for the derivation of the reduced candidate set.
+//
+// Per utterance (one warp, persistent loop over a longest-first work queue):
+//   A. blank-skip compaction: warp ballot + prefix popcount over the blank
+//      column builds the kept-frame map (emissions.py:298-306);
+//   B. per kept frame, the row is staged into shared memory by a TMA bulk copy
+//      (ring of `ring` rows, prefetched ahead), then
+//      1. top-k: radix select of the k = min(2*beam, V-1) best non-blank
+//         tokens by (log-prob desc, index asc) + bitonic sort;
+//      2. merge groups are formed analytically:
+//         blank groups (R,1), repeat groups (R',0) for beam entries, and
+//         append groups (R+c,0) as one sorted list per distinct prefix R;
+//      3. the next beam is a k-way merge of those sorted lists under the
+//         reference's total order (score desc, token sequence asc, flag asc)
+//         with the beam_threshold cut (decoder.py:615-681);
+//      4. back-pointers go to a device-resident trellis;
+//   C. finalize: log-add the flag variants of each prefix, order, backtrace
+//      the n-best through the trellis (decoder.py:753-817).
+#include <cfloat>
+#include <cmath>
+
+#include "ctcb_common.cuh"
+#include "ctcb_internal.h"
+
+namespace ctcb {
+
+namespace {
+
+struct Warp {
+  const Params* P;
+  int lane, u, steps_done;
+  uint8_t* rows;
+  uint64_t* mbar;
+  double *cs, *ns, *headsc, *spsc;
+  uint64_t *ch, *cph, *nh, *nph, *skey, *spkey;
+  int *cl, *cn, *cf, *nl, *nn, *nf;
+  uint32_t *ntrel, *excl, *hist;
+  int *first, *dpi, *pd, *e1, *e2, *headj;
+  float* sval;
+  int *stok, *spord, *spbase, *spx, *spflag, *spsrc, *sptok, *misc;
+  uint16_t* pos;
+  int kw;
+
+  __device__ void swap_state() {
+    double* d = cs; cs = ns; ns = d;
+    uint64_t* h = ch; ch = nh; nh = h;
+    h = cph; cph = nph; nph = h;
+    int* x = cl; cl = nl; nl = x;
+    x = cn; cn = nn; nn = x;
+    x = cf; cf = nf; nf = x;
+  }
+};
+
+__device__ void carve(Warp& w, uint8_t* base, const Params& P) {
+  int kpad = P.kpad;
+  WarpLayout L = make_layout(P.beam, kpad, P.V, P.ring, P.row_bytes);
+  w.rows = base + L.rows;
+  w.mbar = (uint64_t*)(base + L.mbar);
+  w.cs = (double*)(base + L.cur_score);
+  w.ch = (uint64_t*)(base + L.cur_hash);
+  w.cph = (uint64_t*)(base + L.cur_phash);
+  w.ns = (double*)(base + L.nxt_score);
+  w.nh = (uint64_t*)(base + L.nxt_hash);
+  w.nph = (uint64_t*)(base + L.nxt_phash);
+  w.headsc = (double*)(base + L.head_sc);
+  w.skey = (uint64_t*)(base + L.skey);
+  w.spsc = (double*)(base + L.sp_sc);
+  w.spkey = (uint64_t*)(base + L.sp_key);
+  w.cl = (int*)(base + L.cur_last);
+  w.cn = (int*)(base + L.cur_len);
+  w.cf = (int*)(base + L.cur_flag);
+  w.nl = (int*)(base + L.nxt_last);
+  w.nn = (int*)(base + L.nxt_len);
+  w.nf = (int*)(base + L.nxt_flag);
+  w.ntrel = (uint32_t*)(base + L.nxt_trel);
+  w.first = (int*)(base + L.first);
+  w.dpi = (int*)(base + L.dpi);
+  w.pd = (int*)(base + L.pd);
+  w.e1 = (int*)(base + L.dp_e1);
+  w.e2 = (int*)(base + L.dp_e2);
+  w.headj = (int*)(base + L.head_j);
+  w.excl = (uint32_t*)(base + L.excl);
+  w.sval = (float*)(base + L.sval);
+  w.stok = (int*)(base + L.stok);
+  w.spord = (int*)(base + L.sp_ord);
+  w.spbase = (int*)(base + L.sp_base);
+  w.spx = (int*)(base + L.sp_x);
+  w.spflag = (int*)(base + L.sp_flag);
+  w.spsrc = (int*)(base + L.sp_src);
+  w.sptok = (int*)(base + L.sp_tok);
+  w.hist = (uint32_t*)(base + L.hist);
+  w.misc = (int*)(base + L.misc);
+  w.pos = (uint16_t*)(base + L.pos);
+  w.kw = L.kw;
+}
+
+// ------------------------------------------------------------------ sorting
+// Warp bitonic sort of u64 keys, descending.
+__device__ void bitonic_desc_u64(uint64_t* key, int n, int lane) {
+  for (int size = 2; size <= n; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = lane; t < (n >> 1); t += 32) {
+        int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
+        int j = i + stride;
+        uint64_t a = key[i], b = key[j];
+        bool desc = (i & size) == 0;
+        if (desc ? (a < b) : (a > b)) { key[i] = b; key[j] = a; }
+      }
+      __syncwarp();
+    }
+}
+// Warp bitonic sort of (key desc, idx asc) pairs.
+__device__ void bitonic_pairs(uint64_t* key, int* idx, int n, int lane) {
+  for (int size = 2; size <= n; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = lane; t < (n >> 1); t += 32) {
+        int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
+        int j = i + stride;
+        uint64_t a = key[i], b = key[j];
+        int ia = idx[i], ib = idx[j];
+        bool a_first = a > b || (a == b && ia < ib);
+        bool desc = (i & size) == 0;
+        if (desc ? !a_first : a_first) { key[i] = b; key[j] = a; idx[i] = ib; idx[j] = ia; }
+      }
+      __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ token sequences
+// Token sequence of current beam entry `e` (len `len`), read back through the
+// trellis.  Single-lane slow path used only to break exact score ties.
+__device__ int materialize(const Warp& w, int e, int len, int* buf) {
+  const Params& P = *w.P;
+  int pos = len, slot = e;
+  for (int i = w.steps_done - 1; i >= 0 && pos > 0; --i) {
+    uint32_t r = P.trellis[((size_t)w.u * P.T_max + i) * P.beam + slot];
+    int tok = trel_tok(r);
+    if (tok >= 0) buf[--pos] = tok;
+    slot = trel_src(r);
+  }
+  return len;
+}
+// Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token).
+__device__ int seq_cmp(const Warp& w, int ea, int xa, int eb, int xb) {
+  if (w.ch[ea] == w.ch[eb] && w.cn[ea] == w.cn[eb]) {
+    if (xa == xb) return 0;
+    return xa < xb ? -1 : 1;
+  }
+  const Params& P = *w.P;
+  int* A = P.seqbuf + (size_t)w.u * 2 * (P.T_max + 1);
+  int* Bq = A + P.T_max + 1;
+  int la = materialize(w, ea, w.cn[ea], A);
+  if (xa >= 0) A[la++] = xa;
+  int lb = materialize(w, eb, w.cn[eb], Bq);
+  if (xb >= 0) Bq[lb++] = xb;
+  int n = la < lb ? la : lb;
+  for (int i = 0; i < n; i++)
+    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
+  return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+// Candidate descriptor: (score, base entry, extra token, blank flag).
+struct Desc { double sc; int base, x, flag; };
+// true if a precedes b in the reference's rank order (decoder.py:651-681).
+__device__ bool precedes(const Warp& w, const Desc& a, const Desc& b) {
+  if (a.sc != b.sc) return a.sc > b.sc;
+  int c = seq_cmp(w, a.base, a.x, b.base, b.x);
+  if (c) return c < 0;
+  return a.flag < b.flag;
+}
+__device__ Desc spec_desc(const Warp& w, int s) { return Desc{w.spsc[s], w.spbase[s], w.spx[s], w.spflag[s]}; }
+
+// Re-sort runs of exactly equal scores in a sorted specials order (lane 0).
+__device__ void fix_tie_runs(const Warp& w, int n) {
+  if (w.lane == 0) {
+    int a = 0;
+    while (a < n) {
+      int b = a + 1;
+      while (b < n && w.spkey[b] == w.spkey[a]) b++;
+      if (b - a > 1)
+        for (int i = a + 1; i < b; i++) {
+          int x = w.spord[i], j = i;
+          Desc dx = spec_desc(w, x);
+          while (j > a && precedes(w, dx, spec_desc(w, w.spord[j - 1]))) { w.spord[j] = w.spord[j - 1]; j--; }
+          w.spord[j] = x;
+        }
+      a = b;
+    }
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ top-k
+// S = the k best non-blank tokens of `row` by (value desc, index asc),
+// written sorted to sval/stok; pos[token] = rank in S.
+__device__ void topk(Warp& w, const float* row) {
+  const Params& P = *w.P;
+  const int V = P.V, blank = P.blank, k = P.k, lane = w.lane;
+  uint32_t kth = 0;
+  int need = V;
+  if (k < V - 1) {
+    uint32_t prefix = 0, pmask = 0;
+    need = k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int b = lane; b < 256; b += 32) w.hist[b] = 0;
+      __syncwarp();
+      for (int c = lane; c < V; c += 32) {
+        if (c == blank) continue;
+        uint32_t key = ord32(row[c]);
+        if ((key & pmask) == prefix) atomicAdd(&w.hist[(key >> shift) & 255u], 1u);
+      }
+      __syncwarp();
+      uint32_t h[8], s = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) { h[q] = w.hist[lane * 8 + q]; s += h[q]; }
+      uint32_t incl = s;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        uint32_t v = __shfl_down_sync(FULL, incl, off);
+        if (lane + off < 32) incl += v;
+      }
+      uint32_t cum = incl - s;  // tokens in digits owned by higher lanes
+      int found = -1;
+      uint32_t cgt = 0;
+#pragma unroll
+      for (int q = 7; q >= 0; q--) {
+        if (found < 0 && cum < (uint32_t)need && cum + h[q] >= (uint32_t)need) { found = lane * 8 + q; cgt = cum; }
+        cum += h[q];
+      }
+      unsigned bal = __ballot_sync(FULL, found >= 0);
+      int src = __ffs(bal) - 1;
+      int digit = __shfl_sync(FULL, found, src);
+      cgt = __shfl_sync(FULL, cgt, src);
+      need -= (int)cgt;
+      prefix |= (uint32_t)digit << shift;
+      pmask |= 0xffu << shift;
+      __syncwarp();
+    }
+    kth = prefix;
+  }
+  // ordered compaction: keys > kth, then the `need` lowest-index keys == kth
+  int n = 0, eq_taken = 0;
+  const unsigned lt = lanemask_lt();
+  for (int c0 = 0; c0 < V; c0 += 32) {
+    int c = c0 + lane;
+    bool valid = c < V && c != blank;
+    uint32_t key = valid ? ord32(row[c]) : 0u;
+    bool gt = valid && key > kth, eq = valid && key == kth;
+    unsigned beq = __ballot_sync(FULL, eq);
+    bool acc = gt || (eq && eq_taken + __popc(beq & lt) < need);
+    unsigned bsel = __ballot_sync(FULL, acc);
+    if (acc) w.skey[n + __popc(bsel & lt)] = ((uint64_t)key << 32) | (uint64_t)(0xffffffffu - (uint32_t)c);
+    n += __popc(bsel);
+    eq_taken += __popc(beq);
+  }
+  for (int j = n + lane; j < P.kpad; j += 32) w.skey[j] = 0;
+  __syncwarp();
+  bitonic_desc_u64(w.skey, P.kpad, lane);
+  for (int j = lane; j < k; j += 32) {
+    int c = (int)(0xffffffffu - (uint32_t)(w.skey[j] & 0xffffffffu));
+    w.stok[j] = c;
+    w.sval[j] = row[c];
+    w.pos[c] = (uint16_t)j;
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ beam step
+__device__ __forceinline__ bool excl_bit(const Warp& w, int d, int j) {
+  return (w.excl[d * w.kw + (j >> 5)] >> (j & 31)) & 1u;
+}
+__device__ __forceinline__ int next_valid(const Warp& w, int d, int j) {
+  const int k = w.P->k;
+  for (++j; j < k; ++j)
+    if (!excl_bit(w, d, j)) break;
+  return j;
+}
+// score of the append group (R_d + S[j], 0): fold of the prefix's entries in
+// rank order (candidate order is hypothesis-major, decoder.py:531-543).
+__device__ __forceinline__ double gen_score(const Warp& w, int d, int j) {
+  double v = (double)w.sval[j];
+  int a = w.e1[d], b = w.e2[d];
+  double s = w.cs[a] + v;
+  if (b >= 0) s = np_logaddexp(s, w.cs[b] + v);
+  return s;
+}
+
+// One frame-synchronous step over the current beam (H entries) with emission
+// row `row`.  Returns the new beam size (0: beam died).
+__device__ int beam_step(Warp& w, const float* row, int H) {
+  const Params& P = *w.P;
+  const int lane = w.lane, k = P.k, beam = P.beam;
+  const double eb = (double)row[P.blank];
+
+  // -- prefix grouping: entries sharing a token sequence (flag 0 / flag 1)
+  for (int e = lane; e < H; e += 32) {
+    int f = e;
+    for (int q = 0; q < e; q++)
+      if (w.ch[q] == w.ch[e] && w.cn[q] == w.cn[e]) { f = q; break; }
+    w.first[e] = f;
+  }
+  __syncwarp();
+  int nD = 0;
+  for (int b0 = 0; b0 < H; b0 += 32) {
+    int e = b0 + lane;
+    bool isf = e < H && w.first[e] == e;
+    unsigned bal = __ballot_sync(FULL, isf);
+    if (isf) {
+      int d = nD + __popc(bal & lanemask_lt());
+      w.dpi[e] = d; w.e1[d] = e; w.e2[d] = -1;
+    }
+    nD += __popc(bal);
+  }
+  __syncwarp();
+  for (int e = lane; e < H; e += 32)
+    if (w.first[e] != e) { int d = w.dpi[w.first[e]]; w.dpi[e] = d; w.e2[d] = e; }
+  for (int i = lane; i < nD * w.kw; i += 32) w.excl[i] = 0u;
+  if (lane == 0) w.misc[0] = 0;
+  __syncwarp();
+  // -- parent links of flag-0 entries; children exclude their token from the
+  //    parent's generic list (they become repeat groups)
+  for (int e = lane; e < H; e += 32) {
+    int p = -1;
+    if (w.cf[e] == 0) {
+      for (int q = 0; q < H; q++)
+        if (w.first[q] == q && w.ch[q] == w.cph[e] && w.cn[q] == w.cn[e] - 1) { p = w.dpi[q]; break; }
+      if (p >= 0) {
+        int j = w.pos[w.cl[e]];
+        if (j != 0xffff) atomicOr(&w.excl[p * w.kw + (j >> 5)], 1u << (j & 31));
+      }
+    }
+    w.pd[e] = p;
+  }
+  __syncwarp();
+  // -- specials: blank groups, repeat groups, last-token appends
+  for (int d = lane; d < nD; d += 32) {
+    int a = w.e1[d], b = w.e2[d];
+    double sc = w.cs[a] + eb;
+    if (b >= 0) sc = np_logaddexp(sc, w.cs[b] + eb);
+    int s = atomicAdd(&w.misc[0], 1);
+    w.spsc[s] = sc; w.spbase[s] = a; w.spx[s] = -1; w.spflag[s] = 1; w.spsrc[s] = a; w.sptok[s] = -1;
+    int c = w.cl[a];
+    if (c >= 0) {
+      int j = w.pos[c];
+      if (j != 0xffff && !excl_bit(w, d, j)) {
+        int f = w.cf[a] == 1 ? a : ((b >= 0 && w.cf[b] == 1) ? b : -1);
+        if (f >= 0) {
+          int s2 = atomicAdd(&w.misc[0], 1);
+          w.spsc[s2] = w.cs[f] + (double)w.sval[j];
+          w.spbase[s2] = a; w.spx[s2] = c; w.spflag[s2] = 0; w.spsrc[s2] = f; w.sptok[s2] = c;
+        }
+        w.excl[d * w.kw + (j >> 5)] |= 1u << (j & 31);
+      }
+    }
+  }
+  for (int e = lane; e < H; e += 32) {
+    if (w.cf[e] != 0) continue;
+    int c = w.cl[e];
+    double ec = (double)row[c];
+    double sc = w.cs[e] + ec, best = sc;  // repeat candidate comes first (decoder.py:522-530)
+    int src = e, tok = -1;
+    int p = w.pd[e];
+    if (p >= 0) {
+      int srcs[2] = {w.e1[p], w.e2[p]};
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        int h = srcs[q];
+        if (h < 0 || (w.cf[h] == 0 && w.cl[h] == c)) continue;  // blocked repeat (decoder.py:495)
+        double x = w.cs[h] + ec;
+        sc = np_logaddexp(sc, x);
+        if (x > best) { best = x; src = h; tok = c; }
+      }
+    }
+    int s = atomicAdd(&w.misc[0], 1);
+    w.spsc[s] = sc; w.spbase[s] = e; w.spx[s] = -1; w.spflag[s] = 0; w.spsrc[s] = src; w.sptok[s] = tok;
+  }
+  __syncwarp();
+  const int nS = w.misc[0];
+  const int sp_pad = pow2_at_least(nS);
+  for (int s = lane; s < sp_pad; s += 32) {
+    w.spkey[s] = s < nS ? ord64(w.spsc[s]) : 0ull;
+    w.spord[s] = s < nS ? s : 0x7fffffff;
+  }
+  __syncwarp();
+  bitonic_pairs(w.spkey, w.spord, sp_pad, lane);
+  fix_tie_runs(w, nS);
+  // -- generic list heads
+  for (int d = lane; d < nD; d += 32) {
+    int j = next_valid(w, d, -1);
+    w.headj[d] = j;
+    w.headsc[d] = j < k ? gen_score(w, d, j) : -INFINITY;
+  }
+  __syncwarp();
+
+  // -- k-way merge under the reference order, with the beam_threshold cut
+  int sp_ptr = 0, Hn = 0;
+  double best = -INFINITY;
+  for (int r = 0; r < beam; r++) {
+    uint64_t lk = 0;
+    int li = -1, lcnt = 0;
+    for (int i = lane; i <= nD; i += 32) {
+      uint64_t kk;
+      if (i < nD) kk = w.headj[i] < k ? ord64(w.headsc[i]) : 0ull;
+      else kk = sp_ptr < nS ? w.spkey[sp_ptr] : 0ull;
+      if (kk > lk) { lk = kk; li = i; lcnt = 1; }
+      else if (kk == lk && kk != 0ull) lcnt++;
+    }
+    uint64_t m = lk;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      uint64_t o = __shfl_xor_sync(FULL, m, off);
+      m = o > m ? o : m;
+    }
+    if (m == 0ull) break;
+    int ties = __reduce_add_sync(FULL, lk == m ? lcnt : 0);
+    int win;
+    if (ties == 1) {
+      unsigned bal = __ballot_sync(FULL, lk == m);
+      win = __shfl_sync(FULL, li, __ffs(bal) - 1);
+    } else {
+      win = -1;
+      if (lane == 0) {
+        Desc dw{};
+        for (int i = 0; i <= nD; i++) {
+          Desc di;
+          if (i < nD) {
+            if (w.headj[i] >= k || ord64(w.headsc[i]) != m) continue;
+            di = Desc{w.headsc[i], w.e1[i], w.stok[w.headj[i]], 0};
+          } else {
+            if (sp_ptr >= nS || w.spkey[sp_ptr] != m) continue;
+            di = spec_desc(w, w.spord[sp_ptr]);
+          }
+          if (win < 0 || precedes(w, di, dw)) { win = i; dw = di; }
+        }
+      }
+      win = __shfl_sync(FULL, win, 0);
+    }
+    double sc = win < nD ? w.headsc[win] : w.spsc[w.spord[sp_ptr]];
+    if (r == 0) best = sc;
+    if (sc == -INFINITY) break;
+    if (!P.threshold_inf && sc < best - P.beam_threshold) break;
+    if (lane == 0) {
+      if (win < nD) {
+        int a = w.e1[win], j = w.headj[win], c = w.stok[j];
+        w.ns[r] = sc; w.nh[r] = child_hash(w.ch[a], c); w.nph[r] = w.ch[a];
+        w.nl[r] = c; w.nn[r] = w.cn[a] + 1; w.nf[r] = 0; w.ntrel[r] = pack_trel(a, c);
+        int jn = next_valid(w, win, j);
+        w.headj[win] = jn;
+        w.headsc[win] = jn < k ? gen_score(w, win, jn) : -INFINITY;
+      } else {
+        int s = w.spord[sp_ptr];
+        int a = w.spbase[s], x = w.spx[s];
+        w.ns[r] = sc;
+        if (x >= 0) {
+          w.nh[r] = child_hash(w.ch[a], x); w.nph[r] = w.ch[a]; w.nl[r] = x; w.nn[r] = w.cn[a] + 1;
+        } else {
+          w.nh[r] = w.ch[a]; w.nph[r] = w.cph[a]; w.nl[r] = w.cl[a]; w.nn[r] = w.cn[a];
+        }
+        w.nf[r] = w.spflag[s];
+        w.ntrel[r] = pack_trel(w.spsrc[s], w.sptok[s]);
+      }
+    }
+    if (win == nD) sp_ptr++;
+    Hn = r + 1;
+    __syncwarp();
+  }
+  // reset the token -> S rank map for the next frame
+  for (int j = lane; j < k; j += 32) w.pos[w.stok[j]] = 0xffff;
+  __syncwarp();
+  return Hn;
+}
+
+// ------------------------------------------------------------------ finalize
+__device__ void finalize(Warp& w, int H, int kept) {
+  const Params& P = *w.P;
+  const int lane = w.lane, u = w.u;
+  for (int e = lane; e < H; e += 32) {
+    int f = e;
+    for (int q = 0; q < e; q++)
+      if (w.ch[q] == w.ch[e] && w.cn[q] == w.cn[e]) { f = q; break; }
+    w.first[e] = f;
+  }
+  if (lane == 0) w.misc[0] = 0;
+  __syncwarp();
+  for (int e = lane; e < H; e += 32) {
+    if (w.first[e] != e) continue;
+    double sc = w.cs[e];  // entries are in rank order: the first is the payload (decoder.py:794-797)
+    for (int q = e + 1; q < H; q++)
+      if (w.first[q] == e) sc = np_logaddexp(sc, w.cs[q]);
+    int s = atomicAdd(&w.misc[0], 1);
+    w.spsc[s] = sc; w.spbase[s] = e; w.spx[s] = -1; w.spflag[s] = 0;
+  }
+  __syncwarp();
+  const int nF = w.misc[0];
+  const int pad = pow2_at_least(nF);
+  for (int s = lane; s < pad; s += 32) {
+    w.spkey[s] = s < nF ? ord64(w.spsc[s]) : 0ull;
+    w.spord[s] = s < nF ? s : 0x7fffffff;
+  }
+  __syncwarp();
+  bitonic_pairs(w.spkey, w.spord, pad, lane);
+  fix_tie_runs(w, nF);
+  const int nOut = nF < P.nbest ? nF : P.nbest;
+  for (int r = lane; r < nOut; r += 32) {
+    int s = w.spord[r], e = w.spbase[s];
+    int len = w.cn[e];
+    size_t o = ((size_t)u * P.nbest + r);
+    P.out_score[o] = w.spsc[s];
+    P.out_len[o] = len;
+    int* tok_out = P.out_tokens + o * P.T_max;
+    int* ts_out = P.out_ts ? P.out_ts + o * P.T_max : nullptr;
+    int pos = len, slot = e;
+    for (int i = kept - 1; i >= 0 && pos > 0; --i) {
+      uint32_t rec = P.trellis[((size_t)u * P.T_max + i) * P.beam + slot];
+      int tok = trel_tok(rec);
+      if (tok >= 0) {
+        --pos;
+        tok_out[pos] = tok;
+        if (ts_out) ts_out[pos] = P.frame_map[(size_t)u * P.T_max + i];
+      }
+      slot = trel_src(rec);
+    }
+  }
+  if (lane == 0) P.out_count[u] = nOut;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ kernel
+__global__ void __launch_bounds__(256) ctcb_decode_generic_kernel(const __grid_constant__ Params P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Warp w;
+  w.P = &P;
+  w.lane = lane;
+  carve(w, smem + (size_t)wid * P.smem_per_warp, P);
+  if (lane == 0)
+    for (int s = 0; s < P.ring; s++) mbar_init(&w.mbar[s], 1);
+  for (int c = lane; c < P.V; c += 32) w.pos[c] = 0xffff;
+  fence_mbar_init();
+  __syncwarp();
+  uint32_t n_issue = 0, n_cons = 0;  // ring bookkeeping across utterances
+  const uint32_t row_bytes_copy = (uint32_t)P.V * 4u;
+
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(P.counter, 1);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= P.B) break;
+    const int u = P.order[item];
+    w.u = u;
+    const int len = P.lens[u];
+    if (len <= 0 || len > P.T_max) {
+      if (lane == 0) {
+        P.status[u] = len == 0 ? kUttEmpty : kUttBadLen;
+        P.out_count[u] = 0;
+        P.kept[u] = 0;
+      }
+      continue;
+    }
+    const float* ubase = P.lp + (size_t)u * P.stride_b;
+    int32_t* fmap = P.frame_map + (size_t)u * P.T_max;
+    // -- A. blank-skip compaction (warp ballot + prefix popcount)
+    int kept = 0;
+    for (int t0 = 0; t0 < len; t0 += 32) {
+      int t = t0 + lane;
+      bool keep = t < len;
+      if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
+      unsigned bal = __ballot_sync(FULL, keep);
+      if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
+      kept += __popc(bal);
+    }
+    if (lane == 0) P.kept[u] = kept;
+    __syncwarp();
+
+    // -- B. frame loop
+    if (lane == 0) { w.cs[0] = 0.0; w.ch[0] = kEmptyPrefixHash; w.cph[0] = 0ull; w.cl[0] = -1; w.cn[0] = 0; w.cf[0] = 1; }
+    int H = 1;
+    w.steps_done = 0;
+    auto issue = [&](int i) {
+      uint32_t slot = n_issue % (uint32_t)P.ring;
+      const float* src = ubase + (size_t)fmap[i] * P.stride_t;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&w.mbar[slot], row_bytes_copy);
+      tma_bulk_g2s(w.rows + (size_t)slot * P.row_bytes, src, row_bytes_copy, &w.mbar[slot]);
+      n_issue++;
+    };
+    if (P.bulk_ok) {
+      const int pre = kept < P.ring - 1 ? kept : P.ring - 1;
+      for (int i = 0; i < pre; i++)
+        if (lane == 0) issue(i); else n_issue++;
+    }
+    __syncwarp();
+    bool died = false;
+    for (int i = 0; i < kept; i++) {
+      const float* row;
+      if (P.bulk_ok) {
+        if (i + P.ring - 1 < kept) {
+          if (lane == 0) issue(i + P.ring - 1); else n_issue++;
+        }
+        uint32_t slot = n_cons % (uint32_t)P.ring;
+        mbar_wait(&w.mbar[slot], (n_cons / (uint32_t)P.ring) & 1u);
+        n_cons++;
+        row = (const float*)(w.rows + (size_t)slot * P.row_bytes);
+      } else {
+        float* dst = (float*)w.rows;
+        const float* src = ubase + (size_t)fmap[i] * P.stride_t;
+        for (int c = lane; c < P.V; c += 32) dst[c] = __ldg(src + c);
+        __syncwarp();
+        row = dst;
+      }
+      topk(w, row);
+      int Hn = beam_step(w, row, H);
+      if (Hn == 0) { died = true; break; }
+      uint32_t* trow = P.trellis + ((size_t)u * P.T_max + i) * P.beam;
+      for (int r = lane; r < Hn; r += 32) trow[r] = w.ntrel[r];
+      w.swap_state();
+      H = Hn;
+      w.steps_done = i + 1;
+      __syncwarp();
+    }
+    if (died) {
+      // drain outstanding row copies of this utterance before moving on
+      while (n_cons < n_issue) {
+        uint32_t slot = n_cons % (uint32_t)P.ring;
+        mbar_wait(&w.mbar[slot], (n_cons / (uint32_t)P.ring) & 1u);
+        n_cons++;
+      }
+      if (lane == 0) { P.status[u] = kUttBeamDied; P.out_count[u] = 0; }
+      __syncwarp();
+      continue;
+    }
+    // -- C. finalize
+    finalize(w, H, kept);
+    if (lane == 0) P.status[u] = kUttOk;
+    __syncwarp();
+  }
+}
+
+// Minimum-slice debug entry: blank-skip compaction + per-frame top-k only
+// (one warp per utterance; rows loaded directly).
+__global__ void __launch_bounds__(32) ctcb_debug_kernel(const __grid_constant__ Params P, int32_t* out_topk_tok,
+                                                        float* out_topk_val, float* out_blank) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x;
+  Warp w;
+  w.P = &P;
+  w.lane = lane;
+  w.u = u;
+  carve(w, smem, P);
+  for (int c = lane; c < P.V; c += 32) w.pos[c] = 0xffff;
+  __syncwarp();
+  int len = P.lens[u];
+  if (len < 0 || len > P.T_max) len = 0;
+  const float* ubase = P.lp + (size_t)u * P.stride_b;
+  int32_t* fmap = P.frame_map + (size_t)u * P.T_max;
+  int kept = 0;
+  for (int t0 = 0; t0 < len; t0 += 32) {
+    int t = t0 + lane;
+    bool keep = t < len;
+    if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
+    unsigned bal = __ballot_sync(FULL, keep);
+    if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
+    kept += __popc(bal);
+  }
+  if (lane == 0) P.kept[u] = kept;
+  __syncwarp();
+  float* row = (float*)w.rows;
+  for (int i = 0; i < kept; i++) {
+    const float* src = ubase + (size_t)fmap[i] * P.stride_t;
+    for (int c = lane; c < P.V; c += 32) row[c] = __ldg(src + c);
+    __syncwarp();
+    topk(w, row);
+    size_t o = ((size_t)u * P.T_max + i) * P.k;
+    for (int j = lane; j < P.k; j += 32) {
+      out_topk_tok[o + j] = w.stok[j];
+      out_topk_val[o + j] = w.sval[j];
+      w.pos[w.stok[j]] = 0xffff;
+    }
+    if (lane == 0) out_blank[(size_t)u * P.T_max + i] = row[P.blank];
+    __syncwarp();
+  }
+}
+
+// Longest-first processing order (LPT within one GPU): one block sorts
+// (len desc, index asc); falls back to index order for very large batches.
+__global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter) {
+  extern __shared__ uint64_t keys[];
+  int n = 1;
+  while (n < B) n <<= 1;
+  if (threadIdx.x == 0) *counter = 0;
+  if (n > 8192) {
+    for (int i = threadIdx.x; i < B; i += blockDim.x) order[i] = i;
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (i < B) {
+      int l = lens[i];
+      uint32_t inv = 0x7fffffffu - (uint32_t)(l < 0 ? 0 : l);
+      keys[i] = ((uint64_t)inv << 32) | (uint32_t)i;
+    } else {
+      keys[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= n; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+        int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
+        int j = i + stride;
+        uint64_t a = keys[i], b = keys[j];
+        bool asc = (i & size) == 0;
+        if (asc ? (a > b) : (a < b)) { keys[i] = b; keys[j] = a; }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < B; i += blockDim.x) order[i] = (int32_t)(keys[i] & 0xffffffffu);
+}
+
+}  // namespace ctcb

@@ -1,0 +1,126 @@
+// Internal launch parameters and the per-warp shared-memory layout, shared by
+// the host side (ctcb_api.cu) and the kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace ctcb {
+
+// Per-utterance status codes written by the kernels (host maps them to the
+// reference's ValueError messages).
+enum UttStatus : int32_t {
+  kUttOk = 0,
+  kUttEmpty = 1,      // len_b == 0: "empty emissions" (decoder.py:117-118)
+  kUttBadLen = 2,     // len_b < 0 or len_b > T_max
+  kUttBeamDied = 3,   // "beam died" (decoder.py:616-620)
+};
+
+struct Params {
+  // input [B, T_max, V] with element strides
+  const float* lp;
+  long long stride_b, stride_t;
+  const int32_t* lens;
+  int B, T_max, V, blank;
+  // decoder options
+  int beam, nbest, k, kpad;  // k = min(2*beam, V-1) kept tokens per frame, kpad = pow2 >= k
+  float cutoff;              // drop frame iff lp[t, blank] >= cutoff (+inf: no skipping)
+  int skip;                  // cutoff finite
+  double beam_threshold;
+  int threshold_inf;
+  // workspace
+  int32_t* frame_map;   // [B, T_max]
+  int32_t* kept;        // [B]
+  uint32_t* trellis;    // [B, T_max, beam]
+  int32_t* status;      // [B]
+  int32_t* order;       // [B] utterance processing order (longest first)
+  int32_t* counter;     // [1] work claim counter
+  int32_t* seqbuf;      // [B, 2, T_max + 1] scratch for exact-tie token-sequence comparison
+  // outputs
+  int32_t* out_tokens;  // [B, nbest, T_max]
+  int32_t* out_ts;      // [B, nbest, T_max] or null
+  int32_t* out_len;     // [B, nbest]
+  double* out_score;    // [B, nbest]
+  int32_t* out_count;   // [B]
+  // staging
+  int ring;             // row ring depth
+  int row_bytes;        // smem bytes per staged row (multiple of 16)
+  int bulk_ok;          // rows may be staged with cp.async.bulk
+  int warps_per_block;
+  int smem_per_warp;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Byte offsets of the per-warp shared-memory arrays of the generic decode kernel.
+struct WarpLayout {
+  size_t rows, mbar;
+  size_t cur_score, cur_hash, cur_phash, cur_last, cur_len, cur_flag;
+  size_t nxt_score, nxt_hash, nxt_phash, nxt_last, nxt_len, nxt_flag, nxt_trel;
+  size_t first, dpi, pd, dp_e1, dp_e2, excl, head_j, head_sc;
+  size_t skey, sval, stok, pos;
+  size_t sp_sc, sp_key, sp_ord, sp_base, sp_x, sp_flag, sp_src, sp_tok;
+  size_t hist, misc;
+  size_t total;
+  int kw, sp_cap, sp_pad;
+};
+
+__host__ __device__ inline int pow2_at_least(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+__host__ __device__ inline WarpLayout make_layout(int beam, int kpad, int V, int ring, int row_bytes) {
+  WarpLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes, size_t align) {
+    o = align_up(o, align);
+    size_t r = o;
+    o += bytes;
+    return r;
+  };
+  L.kw = (kpad + 31) / 32;
+  L.sp_cap = 3 * beam;
+  L.sp_pad = pow2_at_least(L.sp_cap);
+  L.rows = take((size_t)ring * row_bytes, 128);
+  L.mbar = take((size_t)ring * 8, 8);
+  L.cur_score = take(8 * (size_t)beam, 8);
+  L.cur_hash = take(8 * (size_t)beam, 8);
+  L.cur_phash = take(8 * (size_t)beam, 8);
+  L.nxt_score = take(8 * (size_t)beam, 8);
+  L.nxt_hash = take(8 * (size_t)beam, 8);
+  L.nxt_phash = take(8 * (size_t)beam, 8);
+  L.head_sc = take(8 * (size_t)beam, 8);
+  L.skey = take(8 * (size_t)kpad, 8);
+  L.sp_sc = take(8 * (size_t)L.sp_cap, 8);
+  L.sp_key = take(8 * (size_t)L.sp_pad, 8);
+  L.cur_last = take(4 * (size_t)beam, 4);
+  L.cur_len = take(4 * (size_t)beam, 4);
+  L.cur_flag = take(4 * (size_t)beam, 4);
+  L.nxt_last = take(4 * (size_t)beam, 4);
+  L.nxt_len = take(4 * (size_t)beam, 4);
+  L.nxt_flag = take(4 * (size_t)beam, 4);
+  L.nxt_trel = take(4 * (size_t)beam, 4);
+  L.first = take(4 * (size_t)beam, 4);
+  L.dpi = take(4 * (size_t)beam, 4);
+  L.pd = take(4 * (size_t)beam, 4);
+  L.dp_e1 = take(4 * (size_t)beam, 4);
+  L.dp_e2 = take(4 * (size_t)beam, 4);
+  L.head_j = take(4 * (size_t)beam, 4);
+  L.excl = take(4 * (size_t)beam * L.kw, 4);
+  L.sval = take(4 * (size_t)kpad, 4);
+  L.stok = take(4 * (size_t)kpad, 4);
+  L.sp_ord = take(4 * (size_t)L.sp_pad, 4);
+  L.sp_base = take(4 * (size_t)L.sp_cap, 4);
+  L.sp_x = take(4 * (size_t)L.sp_cap, 4);
+  L.sp_flag = take(4 * (size_t)L.sp_cap, 4);
+  L.sp_src = take(4 * (size_t)L.sp_cap, 4);
+  L.sp_tok = take(4 * (size_t)L.sp_cap, 4);
+  L.hist = take(4 * 256, 4);
+  L.misc = take(4 * 16, 4);
+  L.pos = take(2 * (size_t)V, 2);
+  L.total = align_up(o, 128);
+  return L;
+}
+
+}  // namespace ctcb

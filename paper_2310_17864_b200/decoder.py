@@ -1,0 +1,328 @@
+"""Drop-in CUDA CTC decoder façade: ``cuda_ctc_decoder`` / ``CUCTCDecoder``.
+
+Signature of the north-star API (TorchAudio's ``cuda_ctc_decoder``), semantics
+of the reference CPU decoder (ctcforge):
+
+    decoder = cuda_ctc_decoder(tokens, nbest=1, beam_size=10, blank_skip_threshold=0.95)
+    hyps = decoder(log_probs, encoder_out_lens)   # List[List[CUCTCHypothesis]]
+
+For every utterance b the result equals the reference call
+
+    beam_search_decode(EmissionMatrix(log_probs[b, :len_b] as float64),
+                       TokenDictionary(tokens, blank_index=0),
+                       DecoderOptions(beam_size, n_best=nbest,
+                                      blank_skip_threshold=blank_skip_threshold,
+                                      beam_size_token=None, beam_threshold=50.0,
+                                      merge_mode="logadd"))
+
+(decoder.py:102-135) mapped to ``CUCTCHypothesis(tokens, words=[tokens[i]...],
+score)``.  Errors follow ctcforge: option errors raise ``ValueError`` with
+DecoderOptions' messages (decoder.py:54-66), token-dictionary errors with
+TokenDictionary's (emissions.py:49-58), a zero-length utterance raises
+``ValueError("utterance b: empty emissions")`` (decoder.py:117-118, :157).
+
+All compute runs in libctcb.so (sm_100a kernels); this module only checks
+arguments, allocates through PyTorch's caching allocator and converts results.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import List, NamedTuple, Optional, Union
+
+import numpy as np
+import torch
+
+from . import _lib
+
+__all__ = ["CUCTCHypothesis", "CUCTCDecoder", "cuda_ctc_decoder", "skip_cutoff", "DecodeOutput"]
+
+_DEFAULT_BLANK_SKIP_THRESHOLD = 0.95
+BLANK_SKIP_EPS = 1e-12  # emissions.py:29
+MAX_BEAM = 512
+
+
+class CUCTCHypothesis(NamedTuple):
+    """One n-best entry (TorchAudio's CUCTCHypothesis fields)."""
+
+    tokens: List[int]
+    words: List[str]
+    score: float
+
+
+class DecodeOutput(NamedTuple):
+    """Raw device outputs of one decode call (see include/ctcb.h)."""
+
+    tokens: torch.Tensor      # int32 [B, nbest, T]
+    timesteps: Optional[torch.Tensor]  # int32 [B, nbest, T] or None
+    lengths: torch.Tensor     # int32 [B, nbest]
+    scores: torch.Tensor      # float64 [B, nbest]
+    counts: torch.Tensor      # int32 [B]
+    status: torch.Tensor      # int32 [B]
+
+
+def _read_vocab(path: str) -> list[str]:
+    # first whitespace-separated field of each line (TorchAudio's _get_vocab_list)
+    vocab = []
+    with open(path, "r", encoding="utf-8") as fh:
+        for line in fh:
+            fields = line.strip().split()
+            vocab.append(fields[0] if fields else "")
+    return vocab
+
+
+def _check_tokens(tokens: list[str]) -> None:
+    # TokenDictionary invariants, emissions.py:49-58
+    if not tokens:
+        raise ValueError("token dictionary is empty")
+    if any(not t for t in tokens):
+        raise ValueError("token strings must be non-empty")
+    if len(set(tokens)) != len(tokens):
+        raise ValueError("token strings must be unique")
+
+
+def skip_cutoff(threshold: float) -> float:
+    """fp32 cutoff c with ``x >= c  <=>  exp(float64(x)) >= threshold - 1e-12``
+    for every finite fp32 x: ctcforge's blank-skip rule (emissions.py:300-301)
+    evaluated with numpy's exp exactly as the reference does.  +inf for
+    threshold == 1.0 (skipping disabled, emissions.py:298-299)."""
+    if not 0.0 < threshold <= 1.0:
+        raise ValueError("blank_skip_threshold must be in (0, 1]")
+    if threshold == 1.0:
+        return float("inf")
+    target = threshold - BLANK_SKIP_EPS
+    if not target > 0.0:
+        return float("-inf")
+
+    def drop(x: np.float32) -> bool:
+        return bool(np.exp(np.array([x], dtype=np.float32).astype(np.float64))[0] >= target)
+
+    c = np.float32(np.log(target))
+    down = np.float32(-np.inf)
+    while drop(np.nextafter(c, down)):
+        c = np.nextafter(c, down)
+    while not drop(c):
+        c = np.nextafter(c, np.float32(np.inf))
+    return float(c)
+
+
+class CUCTCDecoder:
+    """CUDA CTC prefix beam-search decoder (build with :func:`cuda_ctc_decoder`)."""
+
+    def __init__(
+        self,
+        vocab_list: List[str],
+        blank_id: int = 0,
+        beam_size: int = 10,
+        nbest: int = 1,
+        blank_skip_threshold: float = _DEFAULT_BLANK_SKIP_THRESHOLD,
+        cuda_stream: Optional[torch.cuda.Stream] = None,
+        beam_threshold: float = 50.0,
+        validate: bool = False,
+        device: Optional[Union[int, torch.device]] = None,
+    ):
+        vocab_list = list(vocab_list)
+        _check_tokens(vocab_list)
+        if not 0 <= blank_id < len(vocab_list):
+            raise ValueError(f"blank_index {blank_id} out of range")
+        # DecoderOptions.__post_init__, decoder.py:54-66
+        if beam_size < 1:
+            raise ValueError("beam_size must be >= 1")
+        if not beam_threshold > 0:
+            raise ValueError("beam_threshold must be positive")
+        if not 0.0 < blank_skip_threshold <= 1.0:
+            raise ValueError("blank_skip_threshold must be in (0, 1]")
+        if not 1 <= nbest <= beam_size:
+            raise ValueError("n_best must be in [1, beam_size]")
+        if beam_size > MAX_BEAM:
+            raise ValueError(f"beam_size must be <= {MAX_BEAM} for the CUDA decoder")
+        if cuda_stream is not None and not isinstance(cuda_stream, torch.cuda.Stream):
+            raise TypeError("cuda_stream must be torch.cuda.Stream")
+        self.vocab_list = vocab_list
+        self.blank_id = blank_id
+        self.beam_size = beam_size
+        self.nbest = nbest
+        self.blank_skip_threshold = blank_skip_threshold
+        self.beam_threshold = float(beam_threshold)
+        self.validate = validate
+        self.cuda_stream = cuda_stream
+        self.cutoff = skip_cutoff(blank_skip_threshold)
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device if isinstance(device, int) else device.index or 0)
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(lib.ctcb_create(len(vocab_list), blank_id, beam_size, nbest, ctypes.c_float(self.cutoff),
+                                   self.beam_threshold, self.device.index, ctypes.byref(h)), "ctcb_create")
+        self._h = h
+        k = ctypes.c_int()
+        _lib.check(lib.ctcb_topk_size(h, ctypes.byref(k)), "ctcb_topk_size")
+        self.topk = k.value
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib._lib is not None:
+            _lib._lib.ctcb_destroy(h)
+            self._h = None
+
+    # ------------------------------------------------------------------ helpers
+    def _stream(self):
+        s = self.cuda_stream if self.cuda_stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def _check_inputs(self, log_prob: torch.Tensor, lens: torch.Tensor):
+        if not isinstance(log_prob, torch.Tensor) or log_prob.dim() != 3:
+            raise ValueError("log_prob must be a 3-D tensor [batch, frames, tokens]")
+        if log_prob.dtype != torch.float32:
+            raise ValueError(f"log_prob must be float32, got {log_prob.dtype}")
+        if not log_prob.is_cuda:
+            raise ValueError("log_prob must be a CUDA tensor")
+        B, T, V = log_prob.shape
+        if V != len(self.vocab_list):
+            raise ValueError(f"emissions have {V} columns but the token dictionary has "
+                             f"{len(self.vocab_list)} tokens")  # decoder.py:119-123
+        if not isinstance(lens, torch.Tensor) or lens.dim() != 1 or lens.shape[0] != B:
+            raise ValueError("encoder_out_lens must be a 1-D tensor with one length per utterance")
+        if log_prob.device != self.device:
+            raise ValueError(f"log_prob is on {log_prob.device}, decoder on {self.device}")
+        if log_prob.stride(2) != 1 and V > 1:
+            log_prob = log_prob.contiguous()
+        # strides of size-1 dims are arbitrary (numpy's [None] gives 0): use the dense value
+        st = log_prob.stride(1) if T > 1 else V
+        sb = log_prob.stride(0) if B > 1 else st * max(T, 1)
+        if st < V or sb < st * max(T, 1):
+            log_prob = log_prob.contiguous()
+            st, sb = V, V * max(T, 1)
+        lens = lens.to(device=self.device, dtype=torch.int32).contiguous()
+        self._strides = (sb, st)
+        return log_prob, lens
+
+    def _workspace(self, B: int, T: int) -> torch.Tensor:
+        lib = _lib.load()
+        n = ctypes.c_size_t()
+        _lib.check(lib.ctcb_workspace_bytes(self._h, B, T, ctypes.byref(n)), "ctcb_workspace_bytes")
+        if self._ws is None or self._ws.numel() < n.value:
+            self._ws = torch.empty(max(n.value, 1), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _validate(self, log_prob: torch.Tensor, lens: torch.Tensor) -> None:
+        lib = _lib.load()
+        B, T, _ = log_prob.shape
+        err = torch.empty(4, dtype=torch.int64, device=self.device)
+        _lib.check(lib.ctcb_validate(self._h, ctypes.c_void_p(log_prob.data_ptr()), self._strides[0],
+                                     self._strides[1], ctypes.c_void_p(lens.data_ptr()), B, T, 1,
+                                     self._stream(), ctypes.c_void_p(err.data_ptr())), "ctcb_validate")
+        code, b, t, v = err.cpu().tolist()
+        if code == 0:
+            return
+        x = float(log_prob[b, t, v]) if v >= 0 else None
+        # EmissionMatrix.__post_init__ messages (emissions.py:133-150), tagged as decode_batch does
+        if code == 1:
+            raise ValueError(f"utterance {b}: non-finite log-probability at frame {t}, token {v}")
+        if code == 2:
+            raise ValueError(f"utterance {b}: log-probability above 0 at frame {t}, token {v}: {x:.6g}")
+        row = log_prob[b, t].double()
+        norm = float(torch.logsumexp(row, 0))
+        raise ValueError(f"utterance {b}: frame {t} is not normalized: log-sum-exp = {norm:.6g} "
+                         f"(tolerance 0.001); pass strict=False to skip this check")
+
+    # ------------------------------------------------------------------ API
+    def decode(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor, timesteps: bool = False) -> DecodeOutput:
+        """Enqueue a decode on the decoder's stream and return device tensors
+        (no synchronisation)."""
+        log_prob, lens = self._check_inputs(log_prob, encoder_out_lens)
+        if self.validate:
+            self._validate(log_prob, lens)
+        lib = _lib.load()
+        B, T, _ = log_prob.shape
+        dev = self.device
+        nb = self.nbest
+        out_tok = torch.empty((B, nb, max(T, 1)), dtype=torch.int32, device=dev)
+        out_ts = torch.empty((B, nb, max(T, 1)), dtype=torch.int32, device=dev) if timesteps else None
+        out_len = torch.zeros((B, nb), dtype=torch.int32, device=dev)
+        out_score = torch.zeros((B, nb), dtype=torch.float64, device=dev)
+        out_count = torch.zeros(B, dtype=torch.int32, device=dev)
+        out_status = torch.zeros(B, dtype=torch.int32, device=dev)
+        ws = self._workspace(B, T)
+        vp = ctypes.c_void_p
+        _lib.check(lib.ctcb_decode(
+            self._h, vp(log_prob.data_ptr()), self._strides[0], self._strides[1], vp(lens.data_ptr()), B, T,
+            vp(ws.data_ptr()), ws.numel(), self._stream(), vp(out_tok.data_ptr()),
+            vp(out_ts.data_ptr()) if out_ts is not None else None, vp(out_len.data_ptr()),
+            vp(out_score.data_ptr()), vp(out_count.data_ptr()), vp(out_status.data_ptr())), "ctcb_decode")
+        return DecodeOutput(out_tok, out_ts, out_len, out_score, out_count, out_status)
+
+    def to_host(self, out: DecodeOutput):
+        """Synchronise and copy results to the host; raise the reference's
+        errors for failed utterances.  Returns numpy arrays
+        (tokens [B, nbest, Lmax], timesteps or None, lengths, scores, counts)."""
+        status = out.status.cpu().numpy()
+        bad = np.flatnonzero(status != _lib.UTT_OK)
+        if bad.size:
+            b = int(bad[0])
+            if status[b] == _lib.UTT_EMPTY:
+                raise ValueError(f"utterance {b}: empty emissions")
+            if status[b] == _lib.UTT_BEAM_DIED:
+                raise ValueError(f"utterance {b}: beam died: no extension survives")
+            raise ValueError(f"utterance {b}: length out of range [1, {out.tokens.shape[2]}]")
+        counts = out.counts.cpu().numpy()
+        lengths = out.lengths.cpu().numpy()
+        scores = out.scores.cpu().numpy()
+        lmax = int(lengths.max()) if lengths.size else 0
+        tokens = out.tokens[:, :, :lmax].cpu().numpy()
+        ts = out.timesteps[:, :, :lmax].cpu().numpy() if out.timesteps is not None else None
+        return tokens, ts, lengths, scores, counts
+
+    def __call__(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor) -> List[List[CUCTCHypothesis]]:
+        """Decode a batch: ``log_prob`` CUDA float32 [B, T, V] (log-softmax
+        output), ``encoder_out_lens`` [B] valid frames per utterance.  Returns
+        the sorted n-best per utterance (fewer than ``nbest`` when fewer
+        distinct prefixes survive, decoder.py:801)."""
+        out = self.decode(log_prob, encoder_out_lens)
+        tokens, _, lengths, scores, counts = self.to_host(out)
+        vocab = self.vocab_list
+        result = []
+        for b in range(tokens.shape[0]):
+            hyps = []
+            for j in range(int(counts[b])):
+                t = tokens[b, j, : lengths[b, j]].tolist()
+                hyps.append(CUCTCHypothesis(tokens=t, words=[vocab[i] for i in t], score=float(scores[b, j])))
+            result.append(hyps)
+        return result
+
+    def debug_frames(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor):
+        """Minimum slice: (frame_map [B,T], kept [B], topk_tok [B,T,k],
+        topk_val [B,T,k], blank [B,T]) device tensors after synchronisation."""
+        log_prob, lens = self._check_inputs(log_prob, encoder_out_lens)
+        lib = _lib.load()
+        B, T, _ = log_prob.shape
+        dev = self.device
+        k = self.topk
+        fm = torch.full((B, max(T, 1)), -1, dtype=torch.int32, device=dev)
+        kept = torch.zeros(B, dtype=torch.int32, device=dev)
+        tt = torch.full((B, max(T, 1), k), -1, dtype=torch.int32, device=dev)
+        tv = torch.zeros((B, max(T, 1), k), dtype=torch.float32, device=dev)
+        bl = torch.zeros((B, max(T, 1)), dtype=torch.float32, device=dev)
+        vp = ctypes.c_void_p
+        _lib.check(lib.ctcb_debug_frames(self._h, vp(log_prob.data_ptr()), self._strides[0], self._strides[1],
+                                         vp(lens.data_ptr()), B, T, self._stream(), vp(fm.data_ptr()),
+                                         vp(kept.data_ptr()), vp(tt.data_ptr()), vp(tv.data_ptr()),
+                                         vp(bl.data_ptr())), "ctcb_debug_frames")
+        torch.cuda.synchronize(dev)
+        return fm, kept, tt, tv, bl
+
+
+def cuda_ctc_decoder(
+    tokens: Union[str, List[str]],
+    nbest: int = 1,
+    beam_size: int = 10,
+    blank_skip_threshold: float = _DEFAULT_BLANK_SKIP_THRESHOLD,
+    **kwargs,
+) -> CUCTCDecoder:
+    """Build a :class:`CUCTCDecoder`.  ``tokens``: a list of token strings or
+    a file with one token per line (first whitespace field); blank is index 0."""
+    if isinstance(tokens, str):
+        tokens = _read_vocab(tokens)
+    return CUCTCDecoder(vocab_list=tokens, beam_size=beam_size, nbest=nbest,
+                        blank_skip_threshold=blank_skip_threshold, **kwargs)

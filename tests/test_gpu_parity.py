@@ -1,0 +1,269 @@
+"""CUDA decoder parity against the reference outputs (golden vectors) and the
+C oracle, through the C ABI (paper_2310_17864_b200 -> libctcb.so).
+
+Tolerances (north star): best-path tokens bit-exact on inputs whose final
+top-1/top-2 gap exceeds 1e-3; scores within 1e-4 absolute (fp64 device math
+typically agrees to ~1e-12); blank-skip frame maps bit-exact.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from paper_2310_17864_b200 import CUCTCDecoder, cuda_ctc_decoder, synth  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SCORE_TOL = 1e-4
+NEAR_TIE = 1e-3
+
+
+def vocab(v):
+    return ["-"] + [f"t{i}" for i in range(1, v)]
+
+
+def run(lp, lens, beam, nbest=1, thr=1.0, bthr=50.0, timesteps=False):
+    dec = CUCTCDecoder(vocab(lp.shape[2]), beam_size=beam, nbest=nbest, blank_skip_threshold=thr,
+                       beam_threshold=bthr)
+    out = dec.decode(torch.from_numpy(np.ascontiguousarray(lp)).cuda(), torch.from_numpy(np.asarray(lens, np.int32)).cuda(),
+                     timesteps=timesteps)
+    tokens, ts, lengths, scores, counts = dec.to_host(out)
+    res = []
+    for b in range(lp.shape[0]):
+        n = int(counts[b])
+        res.append({
+            "tokens": [tokens[b, j, : lengths[b, j]].tolist() for j in range(n)],
+            "timesteps": [ts[b, j, : lengths[b, j]].tolist() for j in range(n)] if ts is not None else None,
+            "scores": [float(scores[b, j]) for j in range(n)],
+        })
+    return res
+
+
+def assert_same(got, exp_tokens, exp_scores, exp_ts=None, gap=None, ctx=""):
+    assert len(got["scores"]) == len(exp_scores), ctx
+    for a, b in zip(got["scores"], exp_scores):
+        assert abs(a - b) <= SCORE_TOL, f"{ctx}: score {a} vs {b}"
+    if gap is None or gap > NEAR_TIE:
+        assert got["tokens"] == exp_tokens, ctx
+        if exp_ts is not None and got["timesteps"] is not None:
+            assert got["timesteps"] == exp_ts, ctx
+
+
+def test_known_answers(golden):
+    for case in golden["known"]:
+        lp = np.array(case["lp"], dtype=np.float32)[None]
+        got = run(lp, [lp.shape[1]], case["beam"], case["n_best"], case["thr"], timesteps=True)[0]
+        ref = oracle.decode(lp[0], beam_size=case["beam"], n_best=case["n_best"], blank_skip_threshold=case["thr"])
+        assert_same(got, ref.tokens, ref.scores, ref.timesteps, ctx=case["name"])
+        # the reference's own answers survive the fp32 cast for these inputs
+        assert got["tokens"] == case["tokens"], case["name"]
+    one_hot = golden["known"][0]
+    lp = np.array(one_hot["lp"], dtype=np.float32)[None]
+    got = run(lp, [5], 4, timesteps=True)[0]
+    assert got["tokens"][0] == [1, 2, 3] and got["timesteps"][0] == [0, 3, 4] and abs(got["scores"][0]) < 1e-5
+
+
+def test_small_random_fp32_against_reference(golden):
+    for case in golden["small"]:
+        if case["merge"] != "logadd" or case["k"] is not None:
+            continue
+        lp = np.array(case["lp"], dtype=np.float32)[None]
+        got = run(lp, [lp.shape[1]], case["beam"], case["n_best"], case["thr"], case["beam_threshold"],
+                  timesteps=True)[0]
+        if case["dtype"] == "float32":  # golden = ctcforge on these exact fp32 values
+            assert_same(got, case["tokens"], case["scores"], case["timesteps"], ctx=f"seed {case['seed']}")
+            for a, b in zip(got["scores"], case["scores"]):
+                assert abs(a - b) <= 1e-9
+        ref = oracle.decode(lp[0], beam_size=case["beam"], n_best=case["n_best"], blank_skip_threshold=case["thr"],
+                            beam_threshold=case["beam_threshold"])
+        assert_same(got, ref.tokens, ref.scores, ref.timesteps, ctx=f"seed {case['seed']} oracle")
+
+
+def test_config_shapes_against_reference(golden):
+    for case in golden["configs"]:
+        cfg = synth.CONFIGS[case["cfg"]]
+        n = int(synth.lengths(cfg)[case["b"]])
+        x = synth.utterance(cfg, case["b"], n)
+        assert hashlib.sha256(x.tobytes()).hexdigest() == case["sha256"], "generator drift"
+        got = run(x[None], [n], case["beam"], case["n_best"], case["thr"], timesteps=True)[0]
+        assert_same(got, case["tokens"], case["scores"], case["timesteps"], gap=case["gap12"],
+                    ctx=f"cfg{case['cfg']} b{case['b']} beam{case['beam']}")
+
+
+def _batch_vs_oracle(cfg_id, indices=None, beam=None, nbest=None):
+    cfg = synth.CONFIGS[cfg_id]
+    beam = beam or cfg.beam
+    nbest = nbest or (min(beam, 10) if cfg_id == 2 else cfg.nbest)
+    lp, lens = synth.batch(cfg, indices=indices)
+    got = run(lp, lens, beam, nbest, cfg.threshold)
+    full = oracle.decode_batch(lp, lens, beam_size=beam, n_best=min(beam, max(nbest, 2)), blank_skip_threshold=cfg.threshold)
+    mism = 0
+    for b, (g, r) in enumerate(zip(got, full)):
+        gap = r.scores[0] - r.scores[1] if len(r.scores) > 1 else None
+        exp_tokens, exp_scores = r.tokens[:nbest], r.scores[:nbest]
+        assert len(g["scores"]) == len(exp_scores)
+        for a, e in zip(g["scores"], exp_scores):
+            assert abs(a - e) <= SCORE_TOL, f"cfg{cfg_id} utt {b}: {a} vs {e}"
+        if g["tokens"][0] != exp_tokens[0]:
+            assert gap is not None and gap <= NEAR_TIE, f"cfg{cfg_id} utt {b}: top-1 tokens differ (gap {gap})"
+            mism += 1
+    return mism
+
+
+def test_cfg0_full_batch():
+    assert _batch_vs_oracle(0) == 0
+
+
+def test_cfg1_full_batch():
+    _batch_vs_oracle(1)
+
+
+@pytest.mark.parametrize("beam", [1, 10, 50, 100])
+def test_cfg2_beam_sweep(beam):
+    _batch_vs_oracle(2, indices=range(8 if beam >= 50 else 32), beam=beam)
+
+
+def test_cfg3_large_vocab():
+    _batch_vs_oracle(3, indices=range(6))
+
+
+def test_cfg4_sample():
+    _batch_vs_oracle(4, indices=[0, 1, 2, 4093, 4094, 4095])
+
+
+def test_debug_frames_match_blank_collapse_and_topk():
+    for cfg_id in (0, 1, 3):
+        cfg = synth.CONFIGS[cfg_id]
+        lp, lens = synth.batch(cfg, indices=range(3))
+        dec = cuda_ctc_decoder(vocab(cfg.vocab), beam_size=cfg.beam, blank_skip_threshold=cfg.threshold)
+        fm, kept, tt, tv, bl = dec.debug_frames(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+        fm, kept, tt, tv, bl = (x.cpu().numpy() for x in (fm, kept, tt, tv, bl))
+        k = dec.topk
+        for b in range(3):
+            x = lp[b, : lens[b]]
+            ref_fm = oracle.blank_keep(x, cfg.threshold)
+            assert kept[b] == len(ref_fm)
+            assert fm[b, : kept[b]].tolist() == ref_fm.tolist()
+            for i in range(0, kept[b], max(1, kept[b] // 40)):
+                row = x[ref_fm[i]]
+                order = np.lexsort((np.arange(cfg.vocab), -row.astype(np.float64)))
+                order = order[order != 0][:k]
+                assert tt[b, i].tolist() == order.tolist()
+                assert np.array_equal(tv[b, i], row[order])
+                assert bl[b, i] == row[0]
+
+
+# -- edge cases --------------------------------------------------------------
+
+
+def test_empty_utterance_raises():
+    cfg = synth.CONFIGS[0]
+    lp, lens = synth.batch(cfg, indices=range(3))
+    lens[1] = 0
+    dec = cuda_ctc_decoder(vocab(32))
+    with pytest.raises(ValueError, match="utterance 1: empty emissions"):
+        dec(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+
+
+def test_ragged_and_single_frame_lengths():
+    cfg = synth.CONFIGS[1]
+    lp, lens = synth.batch(cfg, indices=range(6))
+    lens = np.array([1, 2, 3, 31, 32, 33], dtype=np.int32)
+    got = run(lp, lens, 10, 3, 0.95)
+    ref = oracle.decode_batch(lp, lens, beam_size=10, n_best=3, blank_skip_threshold=0.95)
+    for g, r in zip(got, ref):
+        assert g["tokens"] == r.tokens
+        assert np.allclose(g["scores"], r.scores, atol=1e-9, rtol=0)
+
+
+def test_all_frames_skipped_gives_empty_hypothesis():
+    lp = np.log(np.full((1, 4, 3), [0.98, 0.01, 0.01])).astype(np.float32)
+    got = run(lp, [4], 10, 1, 0.9)[0]
+    assert got["tokens"] == [[]] and got["scores"] == [0.0]
+
+
+def test_threshold_one_is_identity_and_no_skip():
+    cfg = synth.CONFIGS[0]
+    lp, lens = synth.batch(cfg, indices=range(2))
+    got = run(lp, lens, 10, 2, 1.0)
+    ref = oracle.decode_batch(lp, lens, beam_size=10, n_best=2, blank_skip_threshold=1.0)
+    for g, r in zip(got, ref):
+        assert g["tokens"] == r.tokens and np.allclose(g["scores"], r.scores, atol=1e-9, rtol=0)
+
+
+def test_batch_permutation_and_determinism():
+    cfg = synth.CONFIGS[1]
+    lp, lens = synth.batch(cfg, indices=range(12))
+    a = run(lp, lens, 10, 2, 0.95)
+    b = run(lp, lens, 10, 2, 0.95)
+    assert a == b
+    perm = np.array([5, 3, 11, 0, 1, 2, 4, 6, 7, 8, 9, 10])
+    c = run(lp[perm], lens[perm], 10, 2, 0.95)
+    for i, j in enumerate(perm):
+        assert c[i] == a[j]
+
+
+def test_large_beam_exhaustive_small():
+    rng = np.random.default_rng(22)
+    for _ in range(10):
+        t, v = int(rng.integers(1, 5)), int(rng.integers(2, 4))
+        x = rng.normal(size=(t, v))
+        lp = (x - np.log(np.exp(x).sum(1, keepdims=True))).astype(np.float32)[None]
+        got = run(lp, [t], 512, 1, 1.0, float("inf"))[0]
+        ref = oracle.decode(lp[0], beam_size=512, n_best=1, beam_threshold=float("inf"))
+        assert got["tokens"] == ref.tokens and abs(got["scores"][0] - ref.scores[0]) < 1e-9
+
+
+def test_uniform_rows_exact_ties():
+    lp = np.log(np.full((1, 5, 4), 0.25)).astype(np.float32)
+    got = run(lp, [5], 6, 6, 1.0, timesteps=True)[0]
+    ref = oracle.decode(lp[0], beam_size=6, n_best=6)
+    assert got["tokens"] == ref.tokens and got["timesteps"] == ref.timesteps
+    assert np.allclose(got["scores"], ref.scores, atol=1e-12, rtol=0)
+
+
+def test_argument_errors():
+    with pytest.raises(ValueError, match="beam_size must be >= 1"):
+        cuda_ctc_decoder(vocab(4), beam_size=0)
+    with pytest.raises(ValueError, match="n_best"):
+        cuda_ctc_decoder(vocab(4), beam_size=2, nbest=3)
+    with pytest.raises(ValueError, match="blank_skip_threshold"):
+        cuda_ctc_decoder(vocab(4), blank_skip_threshold=0.0)
+    with pytest.raises(ValueError, match="unique"):
+        cuda_ctc_decoder(["-", "a", "a"])
+    dec = cuda_ctc_decoder(vocab(4))
+    with pytest.raises(ValueError, match="columns"):
+        dec(torch.zeros((1, 3, 5), device="cuda"), torch.tensor([3], dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError, match="length out of range"):
+        dec(torch.full((1, 3, 4), -1.3862944, device="cuda"), torch.tensor([7], dtype=torch.int32, device="cuda"))
+
+
+def test_validate_mode_messages():
+    lp = np.log(np.full((2, 3, 4), 0.25)).astype(np.float32)
+    lp[1, 2, 3] = np.nan
+    dec = cuda_ctc_decoder(vocab(4), validate=True)
+    with pytest.raises(ValueError, match="utterance 1: non-finite log-probability at frame 2, token 3"):
+        dec(torch.from_numpy(lp).cuda(), torch.tensor([3, 3], dtype=torch.int32).cuda())
+    lp[1, 2, 3] = np.log(0.25)
+    lp[0, 1, 2] = 0.5
+    with pytest.raises(ValueError, match="utterance 0: log-probability above 0 at frame 1, token 2"):
+        dec(torch.from_numpy(lp).cuda(), torch.tensor([3, 3], dtype=torch.int32).cuda())
+    lp[0, 1, 2] = -3.0
+    with pytest.raises(ValueError, match="utterance 0: frame 1 is not normalized"):
+        dec(torch.from_numpy(lp).cuda(), torch.tensor([3, 3], dtype=torch.int32).cuda())
+
+
+def test_strided_input_view():
+    cfg = synth.CONFIGS[0]
+    lp, lens = synth.batch(cfg, indices=range(2))
+    big = torch.zeros((2, lp.shape[1] * 2, 32), device="cuda")
+    big[:, ::2] = torch.from_numpy(lp).cuda()
+    view = big[:, ::2]  # stride_t = 64 elements
+    dec = cuda_ctc_decoder(vocab(32))
+    got = dec(view, torch.from_numpy(lens).cuda())
+    ref = oracle.decode_batch(lp, lens, beam_size=10, n_best=1, blank_skip_threshold=0.95)
+    assert [[h.tokens for h in g] for g in got] == [r.tokens for r in ref]
