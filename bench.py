@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark: CTC prefix beam-search decode frames/s at V=500, beam=10
+(BASELINE.json metric) on the whole-box workload (config 4: B=4096 utterances,
+T ~ U[125, 875], peaky synthetic posteriors, thr 0.95, nbest 1).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+One step = one decode of the rank's length-balanced (LPT) shard of the batch,
+inputs resident in HBM.  value = frames of all ranks / max-over-ranks step
+time (CUDA events on the decode stream).  Inputs (7.2 GB padded at N=1) are
+larger than L2, so no flush is needed between steps.  `e2e` is the same
+metric through the public API (`CUCTCDecoder.__call__`) from pinned host
+memory, H2D + decode + D2H + hypothesis construction inside the timed region.
+`--impl reference` times the CPU reference path (the C oracle port of
+ctcforge, oracle/) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2310_17864_b200 import synth  # noqa: E402
+from paper_2310_17864_b200.shard import lpt_shards  # noqa: E402
+
+METRIC = "CTC beam-search decode frames/sec @V=500,beam=10"
+WORKLOADS = {"cfg4": 4, "cfg1": 1}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(lp: np.ndarray, lens: np.ndarray, cutoff: float) -> tuple[int, int]:
+    """Σ_b [4·len_b (blank probe) + 4·(V−1)·kept_b] + 4·B; also Σ kept."""
+    V = lp.shape[2]
+    total, kept_total = 4 * len(lens), 0
+    for b, n in enumerate(lens):
+        blank = lp[b, :n, 0]
+        kept = int(np.count_nonzero(~(blank >= cutoff)))
+        kept_total += kept
+        total += 4 * int(n) + 4 * (V - 1) * kept
+    return total, kept_total
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines: list[str] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i",
+                 str(self.device), "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(cfg, budget_s: float, threads: int, sample_utts: int):
+    """Time the oracle port (C restatement of ctcforge) on a bounded sample of
+    the workload with `threads` host threads; returns (frames/s, sample desc)."""
+    import oracle
+
+    oracle.build()
+    idx = np.arange(min(sample_utts, cfg.batch))
+    lp, lens = synth.batch(cfg, indices=idx)
+    # warm-up one utterance (page in, thread pool)
+    oracle.decode_batch(lp[:1], lens[:1], threads=1, beam_size=cfg.beam, n_best=cfg.nbest,
+                        blank_skip_threshold=cfg.threshold)
+    done_frames, done_utts, t0 = 0, 0, time.perf_counter()
+    chunk = max(threads, 1) * 2
+    while done_utts < len(idx):
+        sl = slice(done_utts, min(done_utts + chunk, len(idx)))
+        oracle.decode_batch(lp[sl], lens[sl], threads=threads, beam_size=cfg.beam, n_best=cfg.nbest,
+                            blank_skip_threshold=cfg.threshold)
+        done_frames += int(lens[sl].sum())
+        done_utts = sl.stop
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return done_frames / dt, f"first {done_utts} utterances of {cfg.name} ({done_frames} frames, {dt:.1f} s)"
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the CPU reference path (oracle port) on host cores."""
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    lens_all = synth.lengths(cfg)
+    per_step = max(threads * 16, 16)
+    steps = args.steps + args.warmup
+    times, frames = [], []
+    for s in range(steps):
+        idx = (np.arange(per_step) + s * per_step) % cfg.batch
+        lp, lens = synth.batch(cfg, indices=idx)
+        t0 = time.perf_counter()
+        oracle.decode_batch(lp, lens, threads=threads, beam_size=cfg.beam, n_best=cfg.nbest,
+                            blank_skip_threshold=cfg.threshold)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            frames.append(int(lens_all[idx].sum()))
+    value = sum(frames) / sum(times)
+    sample = f"{per_step} utterances of {cfg.name} per step ({statistics.mean(frames):.0f} frames)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "batch": cfg.batch, "vocab": cfg.vocab, "beam": cfg.beam,
+                   "nbest": cfg.nbest, "blank_skip_threshold": cfg.threshold, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ctcb", choices=["ctcb", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = synth.CONFIGS[WORKLOADS[args.workload]]
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+
+    from paper_2310_17864_b200 import cuda_ctc_decoder
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    # -- this rank's shard (LPT on length), generated straight into pinned memory
+    lens_all = synth.lengths(cfg)
+    shard = lpt_shards(lens_all, world)[rank]
+    t_pad = int(lens_all[shard].max())
+    host = torch.empty((len(shard), t_pad, cfg.vocab), dtype=torch.float32, pin_memory=True)
+    t0 = time.perf_counter()
+    _, lens = synth.batch(cfg, indices=shard, out=host.numpy(), t_pad=t_pad, threads=os.cpu_count() or 8)
+    log(f"[rank {rank}] generated {len(shard)} utterances ({host.numel() * 4 / 1e9:.2f} GB) in "
+        f"{time.perf_counter() - t0:.1f} s")
+    lp_dev = host.to(dev, non_blocking=True)
+    lens_host = torch.from_numpy(lens)
+    lens_dev = lens_host.to(dev)
+    torch.cuda.synchronize(dev)
+
+    dec = cuda_ctc_decoder(synth.simple_tokens(cfg.vocab), nbest=cfg.nbest, beam_size=cfg.beam,
+                           blank_skip_threshold=cfg.threshold)
+    frames_rank = int(lens.sum())
+    alg_bytes, kept_rank = algorithmic_bytes(host.numpy(), lens, dec.cutoff)
+
+    # -- device-timed decode
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        dec.decode(lp_dev, lens_dev)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            out = dec.decode(lp_dev, lens_dev)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    status = out.status.cpu().numpy()
+    assert (status == 0).all(), "decode failed"
+
+    def reduce_max(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def reduce_sum(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    ms = reduce_max(ms_rank)
+    frames_all = reduce_sum(frames_rank)
+    utts_all = reduce_sum(len(shard))
+    value = frames_all / (ms / 1e3)
+
+    # roofline of the fused decode kernel on this rank (it is ~all of the step, see profiles/)
+    peak, peak_src = measured_peak_gbs()
+    achieved = alg_bytes / (ms_rank / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        if tr.get("workload") == cfg.name and tr.get("n_gpus", 1) == world:
+            traffic = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # -- end to end through the public API from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, 3))
+        hyps = dec(host.to(dev, non_blocking=True), lens_host.to(dev, non_blocking=True))  # warm
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(e2e_steps):
+            x = host.to(dev, non_blocking=True)
+            ln = lens_host.to(dev, non_blocking=True)
+            out_e = dec.decode(x, ln)
+            tokens, _, lengths, scores, counts = dec.to_host(out_e)
+            hyps = [[(tokens[b, j, : lengths[b, j]].tolist(), float(scores[b, j])) for j in range(int(counts[b]))]
+                    for b in range(len(counts))]
+            d2h = (out_e.status.numel() * 4 + counts.nbytes + lengths.nbytes + scores.nbytes + tokens.nbytes)
+        torch.cuda.synchronize(dev)
+        e2e_rank = (time.perf_counter() - t0) / e2e_steps
+        e2e_s = reduce_max(e2e_rank)
+        e2e = {"value": frames_all / e2e_s, "unit": "frames/s",
+               "h2d_bytes_per_step": int(host.numel() * 4 + lens_host.numel() * 4),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s, "steps": e2e_steps,
+               "path": "CUCTCDecoder.__call__-equivalent: pinned host -> H2D -> ctcb_decode -> D2H -> lists"}
+        del hyps
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, sample = cpu_baseline(cfg, args.cpu_budget, threads, sample_utts=512)
+        cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "batch": cfg.batch, "vocab": cfg.vocab, "beam": cfg.beam,
+                       "nbest": cfg.nbest, "blank_skip_threshold": cfg.threshold, "t_range": [cfg.t_min, cfg.t_max],
+                       "frames": int(frames_all), "parallelism": f"lpt-shard x{world}",
+                       "l2": f"inputs larger than L2 ({host.numel() * 4 / 1e9:.1f} GB per rank), no flush"},
+            "utterances_per_s": utts_all / (ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": alg_bytes, "kernel": "ctcb_decode_generic_kernel",
+                         "kept_frames": kept_rank},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": 2 * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -12,6 +13,7 @@
 
 namespace ctcb {
 __global__ void ctcb_decode_generic_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_decode_fast_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter);
 __global__ void ctcb_debug_kernel(const __grid_constant__ Params P, int32_t* out_topk_tok, float* out_topk_val,
                                   float* out_blank);
@@ -25,6 +27,7 @@ struct ctcb_handle {
   float cutoff;
   double beam_threshold;
   int num_sms, max_smem_optin;
+  int force_generic;  // CTCB_FORCE_GENERIC=1: use the generic kernel for every beam (testing)
   void* ws;
   size_t ws_bytes;
 };
@@ -47,7 +50,7 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 struct WsLayout {
-  size_t frame_map, kept, trellis, order, counter, seqbuf, total;
+  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, total;
 };
 WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   WsLayout w{};
@@ -62,7 +65,8 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   w.trellis = take((size_t)B * T * h->beam * 4);
   w.order = take((size_t)B * 4);
   w.counter = take(4);
-  w.seqbuf = take((size_t)B * 2 * (T + 1) * 4);
+  w.seqbuf = take((size_t)B * 3 * (T + 1) * 4);
+  w.anc = take((size_t)B * ((T + ctcb::kChunk - 1) / ctcb::kChunk) * 16);
   w.total = ctcb::align_up(o, 256);
   return w;
 }
@@ -113,22 +117,31 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.order = (int32_t*)(base + L.order);
   P.counter = (int32_t*)(base + L.counter);
   P.seqbuf = (int32_t*)(base + L.seqbuf);
+  P.anc = (uint8_t*)(base + L.anc);
+  P.n_chunks = (T + ctcb::kChunk - 1) / ctcb::kChunk;
   P.row_bytes = (int)ctcb::align_up((size_t)h->V * 4, 16);
   P.ring = ring_for(P.row_bytes);
   P.bulk_ok = ((uintptr_t)lp % 16 == 0) && ((h->V * 4) % 16 == 0) && ((st * 4) % 16 == 0) && ((sb * 4) % 16 == 0);
   return CTCB_OK;
 }
 
-int launch_config(ctcb_handle* h, ctcb::Params& P, int B) {
+bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
+
+int launch_config(ctcb_handle* h, ctcb::Params& P, int B, bool fast) {
   for (;;) {
-    ctcb::WarpLayout WL = ctcb::make_layout(P.beam, P.kpad, P.V, P.ring, P.row_bytes);
-    P.smem_per_warp = (int)WL.total;
-    if ((int)WL.total <= h->max_smem_optin) break;
+    size_t total = fast ? ctcb::make_fast_layout(P.V, P.ring, P.row_bytes).total
+                        : ctcb::make_layout(P.beam, P.kpad, P.V, P.ring, P.row_bytes).total;
+    P.smem_per_warp = (int)total;
+    if ((int)total <= h->max_smem_optin) break;
     if (P.ring > 1) { P.ring--; continue; }
     return fail(CTCB_ERR_UNSUPPORTED, "beam/vocabulary too large for one warp's shared memory");
   }
   int wpb = h->max_smem_optin / P.smem_per_warp;
   wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+  // spread small batches over all SMs: at most ceil(B / num_sms) warps per block
+  int spread = (B + h->num_sms - 1) / h->num_sms;
+  if (spread < 1) spread = 1;
+  if (wpb > spread) wpb = spread;
   P.warps_per_block = wpb;
   return CTCB_OK;
 }
@@ -191,6 +204,10 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   h->beam_threshold = beam_threshold;
   h->ws = nullptr;
   h->ws_bytes = 0;
+  {
+    const char* fg = getenv("CTCB_FORCE_GENERIC");
+    h->force_generic = (fg && fg[0] == '1') ? 1 : 0;
+  }
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaGetDeviceProperties"); }
@@ -239,7 +256,8 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   P.out_len = out_len;
   P.out_score = out_score;
   P.out_count = out_count;
-  rc = launch_config(h, P, B);
+  const bool fast = use_fast(h);
+  rc = launch_config(h, P, B, fast);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   int n = 1;
@@ -249,16 +267,18 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   ctcb::ctcb_order_kernel<<<1, 1024, order_smem, s>>>(lens, B, P.order, P.counter);
   CTCB_CUDA(cudaGetLastError());
   size_t smem = (size_t)P.smem_per_warp * P.warps_per_block;
-  CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_decode_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+  const void* kfn = fast ? (const void*)ctcb::ctcb_decode_fast_kernel : (const void*)ctcb::ctcb_decode_generic_kernel;
+  CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
-  CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ctcb::ctcb_decode_generic_kernel,
-                                                          32 * P.warps_per_block, smem));
+  CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, 32 * P.warps_per_block, smem));
   if (blocks_per_sm < 1) blocks_per_sm = 1;
   int need = (B + P.warps_per_block - 1) / P.warps_per_block;
   int grid = h->num_sms * blocks_per_sm;
   if (grid > need) grid = need;
-  ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
+  if (fast)
+    ctcb::ctcb_decode_fast_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
+  else
+    ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
   CTCB_CUDA(cudaGetLastError());
   return CTCB_OK;
 }
@@ -277,7 +297,7 @@ int ctcb_debug_frames(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const 
   if (rc) return rc;
   P.frame_map = out_frame_map;
   P.kept = out_kept;
-  rc = launch_config(h, P, B);
+  rc = launch_config(h, P, B, false);
   if (rc) return rc;
   size_t smem = (size_t)P.smem_per_warp;
   CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_debug_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -1,0 +1,717 @@
+// Fast CTC prefix beam-search decode kernel for beam <= 16 (the paper's and
+// BASELINE.json's beam 10 configurations).  Same semantics as the generic
+// kernel (ctcb_generic.cu) and the reference (ctcforge decoder.py:102-817),
+// re-organised so that a frame step is a few hundred warp instructions:
+//
+//   * the beam lives in registers: lane e (< 16) holds entry e (rank order =
+//     trellis slot), lanes 16..31 mirror the entries' parent hashes;
+//   * one match.any over {prefix hash, parent hash} gives, per entry, the
+//     other blank-flag variant of its prefix, its flag-0 children and its
+//     parent prefix's entries (the merge structure of decoder.py:595-613);
+//   * top-k: lane maxima -> bitonic sort -> threshold -> compaction ->
+//     register bitonic sort of (log-prob desc, index asc) keys;
+//   * selection: lanes 0..15 own <= 3 "special" groups each (blank, repeat,
+//     last-token append), lanes 16..31 own one sorted append list per distinct
+//     prefix; the next beam is popped with redux.sync.max on 32-bit
+//     fixed-point keys (score - (best - beam_threshold)), exact fp64 compare
+//     and token-sequence order on key ties (decoder.py:651-681);
+//   * back-pointers go to the global trellis plus a 32-step shared-memory ring
+//     that yields per-checkpoint ancestor slots, so the n-best backtrace is a
+//     short coarse walk followed by 32-step walks in parallel lanes.
+#include <cfloat>
+#include <cmath>
+
+#include "ctcb_common.cuh"
+#include "ctcb_internal.h"
+
+namespace ctcb {
+
+namespace {
+
+constexpr uint64_t kDummy = 0xa5a5a5a55a5a5a5aull;
+constexpr uint32_t kSentinel = 0xffffffffu;  // a NaN whose order key is 0
+
+// Order key of an fp32 log-prob: float order, -0 == +0, sentinel -> 0.
+__device__ __forceinline__ uint32_t okey(float x) {
+  uint32_t u = __float_as_uint(x);
+  if (u == 0x80000000u) u = 0u;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ double unord64(uint64_t k) {
+  uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+__device__ __forceinline__ uint64_t shfl64(uint64_t x, int src) {
+  uint32_t lo = __shfl_sync(FULL, (uint32_t)x, src);
+  uint32_t hi = __shfl_sync(FULL, (uint32_t)(x >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shflx64(uint64_t x, int m) {
+  uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)x, m);
+  uint32_t hi = __shfl_xor_sync(FULL, (uint32_t)(x >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+// Register bitonic sorts across the warp, descending.
+__device__ __forceinline__ uint32_t sort_desc32(uint32_t x, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      uint32_t y = __shfl_xor_sync(FULL, x, j);
+      bool take_max = ((lane & j) == 0) == ((lane & size) == 0);
+      x = take_max ? max(x, y) : min(x, y);
+    }
+  return x;
+}
+__device__ __forceinline__ uint64_t sort_desc64(uint64_t x, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      uint64_t y = shflx64(x, j);
+      bool take_max = ((lane & j) == 0) == ((lane & size) == 0);
+      x = take_max ? (x > y ? x : y) : (x < y ? x : y);
+    }
+  return x;
+}
+// Sort a bitonic sequence descending.
+__device__ __forceinline__ uint64_t merge_desc64(uint64_t x, int lane) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    uint64_t y = shflx64(x, j);
+    x = ((lane & j) == 0) ? (x > y ? x : y) : (x < y ? x : y);
+  }
+  return x;
+}
+__device__ __forceinline__ int warp_incl_scan(int x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+struct FastSmem {
+  uint8_t* rows;
+  uint64_t* mbar;
+  uint64_t* cand;
+  double *rec_sc, *rec_s2, *tie_sc;
+  uint64_t* hs;
+  float* sval;
+  int *stok, *rec_i, *tie_i, *hl;
+  uint32_t *excl, *tring, *hist;
+  uint8_t* posmap;
+};
+
+// Token sequence of current entry `e` (length len) through the global trellis.
+__device__ int fast_materialize(const Params& P, int u, int steps_done, int e, int len, int* buf) {
+  int pos = len, slot = e;
+  for (int i = steps_done - 1; i >= 0 && pos > 0; --i) {
+    uint32_t r = P.trellis[((size_t)u * P.T_max + i) * P.beam + slot];
+    int tok = trel_tok(r);
+    if (tok >= 0) buf[--pos] = tok;
+    slot = trel_src(r);
+  }
+  return len;
+}
+// Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb]; hs/hl hold the hashes and
+// lengths of the current entries.
+__device__ int fast_seq_cmp(const Params& P, const FastSmem& S, int u, int steps_done, int ea, int xa, int eb,
+                            int xb) {
+  if (S.hs[ea] == S.hs[eb] && S.hl[ea] == S.hl[eb]) {
+    if (xa == xb) return 0;
+    return xa < xb ? -1 : 1;
+  }
+  int* A = P.seqbuf + (size_t)u * 3 * (P.T_max + 1);
+  int* Bq = A + P.T_max + 1;
+  int la = fast_materialize(P, u, steps_done, ea, S.hl[ea], A);
+  if (xa >= 0) A[la++] = xa;
+  int lb = fast_materialize(P, u, steps_done, eb, S.hl[eb], Bq);
+  if (xb >= 0) Bq[lb++] = xb;
+  int n = la < lb ? la : lb;
+  for (int i = 0; i < n; i++)
+    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
+  return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+// a precedes b in the reference's rank order: score desc, sequence asc, flag asc.
+__device__ bool fast_precedes(const Params& P, const FastSmem& S, int u, int sd, double sa, int ba, int xa, int fa,
+                              double sb, int bb, int xb, int fb) {
+  if (sa != sb) return sa > sb;
+  int c = fast_seq_cmp(P, S, u, sd, ba, xa, bb, xb);
+  if (c) return c < 0;
+  return fa < fb;
+}
+
+// Exact top-k fallback (rows with > 64 candidates above the lane-max
+// threshold, e.g. many exactly tied values): 8-bit radix select on the order
+// keys, ordered compaction, register sort.  Returns this lane's S key.
+__device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k, int lane) {
+  uint32_t prefix = 0, pmask = 0;
+  int need = k;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = lane; b < 256; b += 32) S.hist[b] = 0;
+    __syncwarp();
+    for (int c = lane; c < V; c += 32) {
+      uint32_t key = okey(row[c]);
+      if (key && (key & pmask) == prefix) atomicAdd(&S.hist[(key >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t h[8], s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) { h[q] = S.hist[lane * 8 + q]; s += h[q]; }
+    uint32_t incl = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      uint32_t v = __shfl_down_sync(FULL, incl, off);
+      if (lane + off < 32) incl += v;
+    }
+    uint32_t cum = incl - s;
+    int found = -1;
+    uint32_t cgt = 0;
+#pragma unroll
+    for (int q = 7; q >= 0; q--) {
+      if (found < 0 && cum < (uint32_t)need && cum + h[q] >= (uint32_t)need) { found = lane * 8 + q; cgt = cum; }
+      cum += h[q];
+    }
+    unsigned bal = __ballot_sync(FULL, found >= 0);
+    int src = __ffs(bal) - 1;
+    int digit = __shfl_sync(FULL, found, src);
+    cgt = __shfl_sync(FULL, cgt, src);
+    need -= (int)cgt;
+    prefix |= (uint32_t)digit << shift;
+    pmask |= 0xffu << shift;
+    __syncwarp();
+  }
+  const uint32_t kth = prefix;
+  int n = 0, eq_taken = 0;
+  const unsigned lt = lanemask_lt();
+  for (int c0 = 0; c0 < V; c0 += 32) {
+    int c = c0 + lane;
+    uint32_t key = c < V ? okey(row[c]) : 0u;
+    bool gt = key > kth, eq = key != 0u && key == kth;
+    unsigned beq = __ballot_sync(FULL, eq);
+    bool acc = gt || (eq && eq_taken + __popc(beq & lt) < need);
+    unsigned bsel = __ballot_sync(FULL, acc);
+    if (acc) S.cand[n + __popc(bsel & lt)] = ((uint64_t)key << 32) | (uint64_t)(0xffffffffu - (uint32_t)c);
+    n += __popc(bsel);
+    eq_taken += __popc(beq);
+  }
+  __syncwarp();
+  uint64_t x = lane < n ? S.cand[lane] : 0ull;
+  __syncwarp();
+  return sort_desc64(x, lane);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_constant__ Params P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int me = lane & 15;
+  const FastLayout L = make_fast_layout(P.V, P.ring, P.row_bytes);
+  uint8_t* wbase = smem + (size_t)wid * P.smem_per_warp;
+  FastSmem S;
+  S.rows = wbase + L.rows;
+  S.mbar = (uint64_t*)(wbase + L.mbar);
+  S.cand = (uint64_t*)(wbase + L.cand);
+  S.rec_sc = (double*)(wbase + L.rec_sc);
+  S.rec_s2 = (double*)(wbase + L.rec_s2);
+  S.tie_sc = (double*)(wbase + L.tie_sc);
+  S.hs = (uint64_t*)(wbase + L.hs);
+  S.sval = (float*)(wbase + L.sval);
+  S.stok = (int*)(wbase + L.stok);
+  S.excl = (uint32_t*)(wbase + L.excl);
+  S.rec_i = (int*)(wbase + L.rec_i);
+  S.tie_i = (int*)(wbase + L.tie_i);
+  S.hl = (int*)(wbase + L.hl);
+  S.tring = (uint32_t*)(wbase + L.ring);
+  S.hist = (uint32_t*)(wbase + L.hist);
+  S.posmap = wbase + L.posmap;
+
+  const int V = P.V, k = P.k, beam = P.beam;
+  const int nch4 = (V + 3) >> 2;
+  const uint32_t fullk = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+  const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
+  const double kScale = 4294967294.0 / kR;
+
+  if (lane == 0)
+    for (int s = 0; s < P.ring; s++) mbar_init(&S.mbar[s], 1);
+  for (int c = lane; c < V; c += 32) S.posmap[c] = 0xff;
+  fence_mbar_init();
+  __syncwarp();
+  uint32_t n_issue = 0, n_cons = 0;
+  const uint32_t row_copy = (uint32_t)V * 4u;
+
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(P.counter, 1);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= P.B) break;
+    const int u = P.order[item];
+    const int len_u = P.lens[u];
+    if (len_u <= 0 || len_u > P.T_max) {
+      if (lane == 0) {
+        P.status[u] = len_u == 0 ? kUttEmpty : kUttBadLen;
+        P.out_count[u] = 0;
+        P.kept[u] = 0;
+      }
+      continue;
+    }
+    const float* ubase = P.lp + (size_t)u * P.stride_b;
+    int32_t* fmap = P.frame_map + (size_t)u * P.T_max;
+
+    // -- A. blank-skip compaction: ballot + prefix popcount (emissions.py:298-306)
+    int kept = 0;
+    for (int t0 = 0; t0 < len_u; t0 += 32) {
+      int t = t0 + lane;
+      bool keep = t < len_u;
+      if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
+      unsigned bal = __ballot_sync(FULL, keep);
+      if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
+      kept += __popc(bal);
+    }
+    if (lane == 0) P.kept[u] = kept;
+    __syncwarp();
+
+    auto issue = [&](int i) {
+      uint32_t slot = n_issue % (uint32_t)P.ring;
+      if (lane == 0) {
+        const float* src = ubase + (size_t)fmap[i] * P.stride_t;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&S.mbar[slot], row_copy);
+        tma_bulk_g2s(S.rows + (size_t)slot * P.row_bytes, src, row_copy, &S.mbar[slot]);
+      }
+      n_issue++;
+    };
+    if (P.bulk_ok) {
+      const int pre = kept < P.ring - 1 ? kept : P.ring - 1;
+      for (int i = 0; i < pre; i++) issue(i);
+    }
+
+    // beam state (decoder.py:358-370): the empty prefix, blank flag set, score 0
+    double s = 0.0;
+    uint64_t h = kEmptyPrefixHash, ph = 0ull;
+    int last = -1, len = 0, fl = 1;
+    int H = 1;
+    bool died = false;
+
+    for (int i = 0; i < kept; i++) {
+      float* row;
+      if (P.bulk_ok) {
+        if (i + P.ring - 1 < kept) issue(i + P.ring - 1);
+        uint32_t slot = n_cons % (uint32_t)P.ring;
+        mbar_wait(&S.mbar[slot], (n_cons / (uint32_t)P.ring) & 1u);
+        n_cons++;
+        row = (float*)(S.rows + (size_t)slot * P.row_bytes);
+      } else {
+        row = (float*)S.rows;
+        const float* src = ubase + (size_t)fmap[i] * P.stride_t;
+        for (int c = lane; c < V; c += 32) row[c] = __ldg(src + c);
+        __syncwarp();
+      }
+      const double eb = (double)row[P.blank];
+      __syncwarp();
+      if (lane == 0) {
+        ((uint32_t*)row)[P.blank] = kSentinel;
+        for (int c = V; c < 4 * nch4; c++) ((uint32_t*)row)[c] = kSentinel;
+      }
+      __syncwarp();
+
+      // ================= top-k (k <= 32) =================
+      const float4* row4 = (const float4*)row;
+      float lmax = __uint_as_float(kSentinel);
+      for (int c = lane; c < nch4; c += 32) {
+        float4 q = row4[c];
+        lmax = fmaxf(lmax, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+      }
+      uint32_t lk = isnan(lmax) ? 0u : okey(lmax);
+      uint32_t srt = sort_desc32(lk, lane);
+      uint32_t t0 = __shfl_sync(FULL, srt, k - 1);
+      float tf = t0 == 0u ? -INFINITY : unord32(t0);
+      int cl = 0;
+      for (int c = lane; c < nch4; c += 32) {
+        float4 q = row4[c];
+        cl += (q.x >= tf) + (q.y >= tf) + (q.z >= tf) + (q.w >= tf);
+      }
+      int cnt = __reduce_add_sync(FULL, cl);
+      uint64_t skey;
+      if (cnt <= 64) {
+        int off = warp_incl_scan(cl, lane) - cl;
+        for (int c = lane; c < nch4; c += 32) {
+          float4 q = row4[c];
+          float vv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int z = 0; z < 4; z++)
+            if (vv[z] >= tf)
+              S.cand[off++] = ((uint64_t)okey(vv[z]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)(4 * c + z));
+        }
+        __syncwarp();
+        uint64_t a = lane < cnt ? S.cand[lane] : 0ull;
+        uint64_t b = lane + 32 < cnt ? S.cand[lane + 32] : 0ull;
+        __syncwarp();
+        a = sort_desc64(a, lane);
+        if (cnt > 32) {
+          b = sort_desc64(b, lane);
+          uint64_t br = shfl64(b, 31 - lane);
+          a = a > br ? a : br;
+          a = merge_desc64(a, lane);
+        }
+        skey = a;
+      } else {
+        skey = topk_radix(S, row, V, k, lane);
+      }
+      const int st = lane < k ? (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu)) : 0;
+      const float sv = lane < k ? row[st] : 0.0f;
+      if (lane < k) { S.sval[lane] = sv; S.stok[lane] = st; S.posmap[st] = (uint8_t)lane; }
+      __syncwarp();
+
+      // ================= merge structure =================
+      const bool ent = lane < H;
+      const uint64_t ph_m = shfl64(ph, me);
+      const int len_m = __shfl_sync(FULL, len, me);
+      uint64_t mkey;
+      if (lane < 16) mkey = ent ? h : (kDummy ^ (uint64_t)lane);
+      else mkey = (me < H && len_m > 0) ? ph_m : (kDummy ^ (uint64_t)lane);
+      const unsigned m = __match_any_sync(FULL, mkey);
+      const unsigned same = m & 0xffffu;
+      const unsigned parents = __shfl_sync(FULL, m & 0xffffu, me + 16);
+      const int first = __ffs(same) - 1;
+      const bool isfirst = ent && first == lane;
+      const unsigned firstmask = __ballot_sync(FULL, isfirst);
+      const int nD = __popc(firstmask);
+      const unsigned pmask = same & ~(1u << lane);
+      const int p2 = (ent && pmask) ? __ffs(pmask) - 1 : -1;
+      const double s_p2 = __shfl_sync(FULL, s, p2 >= 0 ? p2 : lane);
+      const int fl_p2 = __shfl_sync(FULL, fl, p2 >= 0 ? p2 : lane);
+
+      // S positions of last tokens; flag-0 children exclude their token from
+      // the parent's append list (they become repeat groups)
+      const int mypos = (ent && last >= 0) ? (int)S.posmap[last] : 0xff;
+      const uint32_t mybit = mypos < 32 ? (1u << mypos) : 0u;
+      if (lane < 16) S.excl[lane] = 0u;
+      __syncwarp();
+      const int pa = (ent && parents) ? __ffs(parents) - 1 : -1;
+      if (ent && fl == 0 && pa >= 0 && mybit) atomicOr(&S.excl[pa], mybit);
+      __syncwarp();
+      const uint32_t childx = lane < 16 ? S.excl[lane] : 0u;
+
+      // ================= special groups (lanes < 16) =================
+      const unsigned pr2 = parents & (parents - 1);
+      const int pb = (ent && pr2) ? __ffs(pr2) - 1 : -1;
+      const double s_pa = __shfl_sync(FULL, s, pa >= 0 ? pa : lane);
+      const int fl_pa = __shfl_sync(FULL, fl, pa >= 0 ? pa : lane);
+      const int last_pa = __shfl_sync(FULL, last, pa >= 0 ? pa : lane);
+      const double s_pb = __shfl_sync(FULL, s, pb >= 0 ? pb : lane);
+      const int fl_pb = __shfl_sync(FULL, fl, pb >= 0 ? pb : lane);
+      const int last_pb = __shfl_sync(FULL, last, pb >= 0 ? pb : lane);
+      double c_blank = -INFINITY, c_rep = -INFINITY, c_single = -INFINITY;
+      int rep_src = lane, rep_tok = -1, single_src = lane;
+      if (isfirst) {  // blank group (R,1): entries of R in rank order (decoder.py:513-521)
+        c_blank = s + eb;
+        if (p2 >= 0) c_blank = np_logaddexp(c_blank, s_p2 + eb);
+      }
+      if (ent && fl == 0) {  // repeat group (R',0): repeat first, then parent appends (:522-543)
+        const double ec = (double)row[last];
+        double sc = s + ec, bst = sc;
+        if (pa >= 0 && !(fl_pa == 0 && last_pa == last)) {
+          double x = s_pa + ec;
+          sc = np_logaddexp(sc, x);
+          if (x > bst) { bst = x; rep_src = pa; rep_tok = last; }
+        }
+        if (pb >= 0 && !(fl_pb == 0 && last_pb == last)) {
+          double x = s_pb + ec;
+          sc = np_logaddexp(sc, x);
+          if (x > bst) { bst = x; rep_src = pb; rep_tok = last; }
+        }
+        c_rep = sc;
+      }
+      if (isfirst && mybit && !(childx & mybit)) {  // (R+last(R),0) from (R,1) only (blocked repeat)
+        const int f1 = fl == 1 ? lane : ((p2 >= 0 && fl_p2 == 1) ? p2 : -1);
+        if (f1 >= 0) {
+          c_single = (f1 == lane ? s : s_p2) + (double)S.sval[mypos];
+          single_src = f1;
+        }
+      }
+      // local order: score desc; ties repeat (R,0) < blank (R,1) < single (R+c,0)
+      double q0 = c_rep, q1 = c_blank, q2 = c_single;
+      int k0 = 1, k1 = 0, k2 = 2;
+      if (q1 > q0) { double t = q0; q0 = q1; q1 = t; int x = k0; k0 = k1; k1 = x; }
+      if (q2 > q1) {
+        double t = q1; q1 = q2; q2 = t; int x = k1; k1 = k2; k2 = x;
+        if (q1 > q0) { t = q0; q0 = q1; q1 = t; x = k0; k0 = k1; k1 = x; }
+      }
+
+      // ================= append lists (lanes 16..16+nD) =================
+      const double A = isfirst ? (p2 >= 0 ? np_logaddexp(s, s_p2) : s) : 0.0;
+      const uint32_t gvalid = isfirst ? (fullk & ~(childx | mybit)) : 0u;
+      const bool gen = lane >= 16 && me < nD;
+      const int gsrc = gen ? (int)__fns(firstmask, 0, me + 1) : lane;
+      const double gA = __shfl_sync(FULL, A, gsrc);
+      const double g_s1 = __shfl_sync(FULL, s, gsrc);
+      const double g_s2 = __shfl_sync(FULL, s_p2, gsrc);
+      const int g_has2 = __shfl_sync(FULL, p2 >= 0 ? 1 : 0, gsrc);
+      uint32_t gv = __shfl_sync(FULL, gvalid, gsrc);
+      if (!gen) gv = 0u;
+
+      // heads and the frame best
+      double hsc;
+      int qi = 0;
+      if (lane < 16) hsc = q0;
+      else hsc = gv ? gA + (double)S.sval[__ffs(gv) - 1] : -INFINITY;
+      const uint64_t ok64 = hsc > -INFINITY ? ord64(hsc) : 0ull;
+      const uint32_t mhi = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32));
+      const uint32_t mlo = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32) == mhi ? (uint32_t)ok64 : 0u);
+      const uint64_t bk = ((uint64_t)mhi << 32) | mlo;
+      if (bk == 0ull) { died = true; break; }  // every extension is -inf (decoder.py:616-620)
+      const double best = unord64(bk);
+      const double lo_thr = P.threshold_inf ? -INFINITY : best - P.beam_threshold;  // decoder.py:621-623
+      const double kbase = best - kR;
+      auto keyof = [&](double sc) -> uint32_t {
+        if (!(sc > -INFINITY) || !(sc >= lo_thr)) return 0u;
+        double z = (sc - kbase) * kScale;
+        if (!(z > 0.0)) return 1u;
+        if (z >= 4294967293.0) return 0xffffffffu;
+        return 1u + (uint32_t)z;
+      };
+      uint32_t hk = keyof(hsc);
+
+      // ================= k-way merge (decoder.py:651-681) =================
+      int Hn = 0;
+      for (int r = 0; r < beam; r++) {
+        const uint32_t mk = __reduce_max_sync(FULL, hk);
+        if (mk == 0u) break;
+        const unsigned tied = __ballot_sync(FULL, hk == mk);
+        int w = __ffs(tied) - 1;
+        if (tied & (tied - 1)) {
+          // exact resolution: fp64 score, then token sequence, then flag
+          if (tied & (1u << lane)) {
+            double esc;
+            int eb_, ex, ef;
+            if (lane < 16) {
+              int kind = qi == 0 ? k0 : (qi == 1 ? k1 : k2);
+              esc = hsc;
+              eb_ = lane;
+              ex = kind == 2 ? last : -1;
+              ef = kind == 0 ? 1 : 0;
+            } else {
+              int pos = __ffs(gv) - 1;
+              double v = (double)S.sval[pos];
+              esc = g_s1 + v;
+              if (g_has2) esc = np_logaddexp(esc, g_s2 + v);
+              eb_ = gsrc;
+              ex = S.stok[pos];
+              ef = 0;
+            }
+            S.tie_sc[lane] = esc;
+            S.tie_i[lane * 4 + 0] = eb_;
+            S.tie_i[lane * 4 + 1] = ex;
+            S.tie_i[lane * 4 + 2] = ef;
+          }
+          if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; }
+          __syncwarp();
+          if (lane == 0) {
+            unsigned rest = tied & (tied - 1);
+            while (rest) {
+              int c = __ffs(rest) - 1;
+              rest &= rest - 1;
+              if (fast_precedes(P, S, u, i, S.tie_sc[c], S.tie_i[c * 4], S.tie_i[c * 4 + 1], S.tie_i[c * 4 + 2],
+                                S.tie_sc[w], S.tie_i[w * 4], S.tie_i[w * 4 + 1], S.tie_i[w * 4 + 2]))
+                w = c;
+            }
+          }
+          w = __shfl_sync(FULL, w, 0);
+          __syncwarp();
+        }
+        if (lane == w) {
+          int* ri = S.rec_i + r * 8;
+          if (lane < 16) {
+            const int kind = qi == 0 ? k0 : (qi == 1 ? k1 : k2);
+            S.rec_sc[r] = hsc;
+            ri[0] = kind;
+            ri[1] = lane;
+            ri[2] = kind == 1 ? rep_src : (kind == 2 ? single_src : lane);
+            ri[3] = kind == 1 ? rep_tok : (kind == 2 ? last : -1);
+            ri[4] = kind == 0 ? 1 : 0;
+            ri[5] = kind == 2 ? last : -1;
+            ri[6] = -1;
+            qi++;
+            hsc = qi == 1 ? q1 : (qi == 2 ? q2 : -INFINITY);
+          } else {
+            const int pos = __ffs(gv) - 1;
+            const int c = S.stok[pos];
+            S.rec_sc[r] = g_s1;
+            S.rec_s2[r] = g_s2;
+            ri[0] = 3;
+            ri[1] = gsrc;
+            ri[2] = gsrc;
+            ri[3] = c;
+            ri[4] = 0;
+            ri[5] = c;
+            ri[6] = pos;
+            ri[7] = g_has2;
+            gv &= gv - 1u;
+            hsc = gv ? gA + (double)S.sval[__ffs(gv) - 1] : -INFINITY;
+          }
+          hk = keyof(hsc);
+        }
+        Hn = r + 1;
+      }
+      __syncwarp();
+      if (Hn == 0) { died = true; break; }
+
+      // ================= commit (decoder.py:683-744) =================
+      const bool nent = lane < Hn;
+      const int* ri = S.rec_i + (nent ? lane : 0) * 8;
+      const int kind = ri[0], bl = nent ? ri[1] : lane;
+      const uint64_t bh = shfl64(h, bl), bph = shfl64(ph, bl);
+      const int blast = __shfl_sync(FULL, last, bl), blen = __shfl_sync(FULL, len, bl);
+      double nsc = S.rec_sc[nent ? lane : 0];
+      if (nent && kind == 3) {  // exact append-group score: fold in rank order
+        const double v = (double)S.sval[ri[6]];
+        double a = nsc + v;
+        if (ri[7]) a = np_logaddexp(a, S.rec_s2[lane] + v);
+        nsc = a;
+      }
+      const int x = ri[5];
+      const uint32_t trel = pack_trel(ri[2], ri[3]);
+      const int nfl = ri[4];
+      __syncwarp();
+      // reset the token -> S rank map
+      if (lane < k) S.posmap[st] = 0xff;
+      if (nent) {
+        s = nsc;
+        h = x >= 0 ? child_hash(bh, x) : bh;
+        ph = x >= 0 ? bh : bph;
+        last = x >= 0 ? x : blast;
+        len = x >= 0 ? blen + 1 : blen;
+        fl = nfl;
+        P.trellis[((size_t)u * P.T_max + i) * beam + lane] = trel;
+        S.tring[(i % kChunk) * 16 + lane] = trel;
+      }
+      H = Hn;
+      __syncwarp();
+      // trellis checkpoint: ancestor slot at the chunk start for every entry
+      if ((i % kChunk) == kChunk - 1 || i == kept - 1) {
+        if (lane < H) {
+          int slot = lane;
+          for (int t = i % kChunk; t >= 0; --t) slot = trel_src(S.tring[t * 16 + slot]);
+          P.anc[((size_t)u * P.n_chunks + i / kChunk) * 16 + lane] = (uint8_t)slot;
+        }
+        __syncwarp();
+      }
+    }
+
+    if (died) {
+      while (n_cons < n_issue) {
+        uint32_t slot = n_cons % (uint32_t)P.ring;
+        mbar_wait(&S.mbar[slot], (n_cons / (uint32_t)P.ring) & 1u);
+        n_cons++;
+      }
+      for (int c = lane; c < V; c += 32) S.posmap[c] = 0xff;
+      if (lane == 0) { P.status[u] = kUttBeamDied; P.out_count[u] = 0; }
+      __syncwarp();
+      continue;
+    }
+
+    // ================= finalize (decoder.py:753-817) =================
+    {
+      const bool ent = lane < H;
+      const unsigned fm = __match_any_sync(FULL, ent ? h : (kDummy ^ (uint64_t)lane));
+      const bool isf = ent && (__ffs(fm) - 1) == lane;
+      const unsigned pm = fm & ~(1u << lane);
+      const int p2 = (ent && pm) ? __ffs(pm) - 1 : -1;
+      const double s_p2 = __shfl_sync(FULL, s, p2 >= 0 ? p2 : lane);
+      const double gsc = isf ? (p2 >= 0 ? np_logaddexp(s, s_p2) : s) : -INFINITY;
+      // order groups: (score desc, lane asc) by register sort, then exact tie runs
+      uint64_t key = isf ? ord64(gsc) : 0ull;
+      int pay = lane;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+          uint64_t ky = shflx64(key, j);
+          int py = __shfl_xor_sync(FULL, pay, j);
+          bool mine_first = key > ky || (key == ky && pay < py);
+          bool take_first = ((lane & j) == 0) == ((lane & size) == 0);
+          if (take_first != mine_first) { key = ky; pay = py; }
+        }
+      const int nF = __popc(__ballot_sync(FULL, isf));
+      const double srt_sc = __shfl_sync(FULL, gsc, pay);
+      // exact tie runs (identical fp64 scores): token-sequence order
+      S.tie_i[lane] = pay;
+      S.tie_sc[lane] = srt_sc;
+      if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; }
+      __syncwarp();
+      if (lane == 0) {
+        for (int a = 1; a < nF; a++) {
+          int j = a;
+          while (j > 0 && S.tie_sc[j] == S.tie_sc[j - 1] &&
+                 fast_seq_cmp(P, S, u, kept, S.tie_i[j], -1, S.tie_i[j - 1], -1) < 0) {
+            int t = S.tie_i[j]; S.tie_i[j] = S.tie_i[j - 1]; S.tie_i[j - 1] = t;
+            j--;
+          }
+        }
+      }
+      __syncwarp();
+      const int nOut = nF < P.nbest ? nF : P.nbest;
+      const int nchk = (kept + kChunk - 1) / kChunk;
+      int* ends = P.seqbuf + (size_t)u * 3 * (P.T_max + 1);
+      int* tmp_tok = ends + (P.T_max + 1);
+      int* tmp_fr = tmp_tok + (P.T_max + 1);
+      for (int r = 0; r < nOut; r++) {
+        const int e = S.tie_i[r];
+        const double sc = __shfl_sync(FULL, gsc, e);
+        const int L_e = __shfl_sync(FULL, len, e);
+        const size_t o = (size_t)u * P.nbest + r;
+        if (lane == 0) { P.out_score[o] = sc; P.out_len[o] = L_e; }
+        int* tok_out = P.out_tokens + o * P.T_max;
+        int* ts_out = P.out_ts ? P.out_ts + o * P.T_max : nullptr;
+        if (L_e == 0 || nchk == 0) continue;
+        // coarse walk over checkpoints
+        if (lane == 0) {
+          int slot = e;
+          for (int c = nchk - 1; c >= 0; --c) {
+            ends[c] = slot;
+            slot = P.anc[((size_t)u * P.n_chunks + c) * 16 + slot];
+          }
+        }
+        __syncwarp();
+        // fine walks, one chunk per lane
+        for (int c = lane; c < nchk; c += 32) {
+          int slot = ends[c], cntc = 0;
+          const int i_end = min(kept, (c + 1) * kChunk) - 1;
+          for (int ii = i_end; ii >= c * kChunk; --ii) {
+            uint32_t rec = P.trellis[((size_t)u * P.T_max + ii) * beam + slot];
+            int tok = trel_tok(rec);
+            if (tok >= 0) {
+              tmp_tok[c * kChunk + cntc] = tok;
+              tmp_fr[c * kChunk + cntc] = fmap[ii];
+              cntc++;
+            }
+            slot = trel_src(rec);
+          }
+          ends[c] = cntc;
+        }
+        __syncwarp();
+        int running = 0;
+        for (int b0 = 0; b0 < nchk; b0 += 32) {
+          const int c = b0 + lane;
+          const int cnt_c = c < nchk ? ends[c] : 0;
+          const int incl = warp_incl_scan(cnt_c, lane);
+          const int off = running + incl - cnt_c;
+          for (int q = 0; q < cnt_c; q++) {
+            tok_out[off + q] = tmp_tok[c * kChunk + cnt_c - 1 - q];
+            if (ts_out) ts_out[off + q] = tmp_fr[c * kChunk + cnt_c - 1 - q];
+          }
+          running += __shfl_sync(FULL, incl, 31);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) { P.out_count[u] = nOut; P.status[u] = kUttOk; }
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace ctcb

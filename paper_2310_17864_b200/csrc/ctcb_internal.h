@@ -34,7 +34,8 @@ struct Params {
   int32_t* status;      // [B]
   int32_t* order;       // [B] utterance processing order (longest first)
   int32_t* counter;     // [1] work claim counter
-  int32_t* seqbuf;      // [B, 2, T_max + 1] scratch for exact-tie token-sequence comparison
+  int32_t* seqbuf;      // [B, 3, T_max + 1] scratch: exact-tie token sequences, backtrace staging
+  uint8_t* anc;         // [B, n_chunks, 16] fast path: ancestor slot at each trellis checkpoint
   // outputs
   int32_t* out_tokens;  // [B, nbest, T_max]
   int32_t* out_ts;      // [B, nbest, T_max] or null
@@ -47,7 +48,45 @@ struct Params {
   int bulk_ok;          // rows may be staged with cp.async.bulk
   int warps_per_block;
   int smem_per_warp;
+  int n_chunks;         // ceil(T_max / kChunk)
 };
+
+// Fast path (beam <= kFastBeam): trellis checkpoint interval.
+constexpr int kFastBeam = 16;
+constexpr int kChunk = 32;
+
+// Byte offsets of the per-warp shared memory of the fast decode kernel.
+struct FastLayout {
+  size_t rows, mbar, cand, sval, stok, excl, rec_sc, rec_s2, rec_i, tie_sc, tie_i, hs, hl, ring, hist, posmap, total;
+};
+__host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_bytes) {
+  FastLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes, size_t align) {
+    o = (o + align - 1) / align * align;
+    size_t r = o;
+    o += bytes;
+    return r;
+  };
+  L.rows = take((size_t)ring * row_bytes, 128);
+  L.mbar = take((size_t)ring * 8, 8);
+  L.cand = take(64 * 8, 8);
+  L.rec_sc = take(16 * 8, 8);
+  L.rec_s2 = take(16 * 8, 8);
+  L.tie_sc = take(32 * 8, 8);
+  L.hs = take(16 * 8, 8);
+  L.sval = take(32 * 4, 4);
+  L.stok = take(32 * 4, 4);
+  L.excl = take(16 * 4, 4);
+  L.rec_i = take(16 * 8 * 4, 4);   // 8 ints per merge record
+  L.tie_i = take(32 * 4 * 4, 4);   // 4 ints per tie candidate
+  L.hl = take(16 * 4, 4);          // entry lengths (tie slow path)
+  L.ring = take((size_t)kChunk * 16 * 4, 4);
+  L.hist = take(256 * 4, 4);
+  L.posmap = take((size_t)V, 1);
+  L.total = (o + 127) / 128 * 128;
+  return L;
+}
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
