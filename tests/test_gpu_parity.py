@@ -267,3 +267,21 @@ def test_strided_input_view():
     got = dec(view, torch.from_numpy(lens).cuda())
     ref = oracle.decode_batch(lp, lens, beam_size=10, n_best=1, blank_skip_threshold=0.95)
     assert [[h.tokens for h in g] for g in got] == [r.tokens for r in ref]
+
+
+def test_fast_and_generic_kernels_agree(monkeypatch):
+    """beam <= 16 runs the register-resident fast kernel; CTCB_FORCE_GENERIC=1
+    forces the generic one.  Both must give identical results."""
+    cases = []
+    for cfg_id, idx in ((0, range(4)), (1, range(24)), (3, range(3))):
+        cfg = synth.CONFIGS[cfg_id]
+        lp, lens = synth.batch(cfg, indices=idx)
+        for beam, nb in ((cfg.beam, cfg.nbest), (1, 1), (16, 16)):
+            cases.append((lp, lens, beam, nb, cfg.threshold))
+    fast = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
+    monkeypatch.setenv("CTCB_FORCE_GENERIC", "1")
+    gen = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
+    for a, b in zip(fast, gen):
+        for x, y in zip(a, b):
+            assert x["tokens"] == y["tokens"] and x["timesteps"] == y["timesteps"]
+            assert np.allclose(x["scores"], y["scores"], atol=1e-9, rtol=0)
