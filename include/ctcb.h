@@ -113,6 +113,11 @@ int ctcb_debug_frames(ctcb_t* h, const float* log_probs, int64_t stride_b, int64
 int ctcb_validate(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
                   int batch, int t_max, int strict, void* stream, int64_t* out_error);
 
+/* Diagnostics of the last ctcb_decode on this handle (synchronising read):
+ * {key ties resolved exactly, exact fp64 score ties, token-sequence
+ *  materialisations, trellis steps walked by them, radix top-k fallbacks, 0, 0, 0}. */
+int ctcb_debug_counters(ctcb_t* h, uint64_t* out8);
+
 const char* ctcb_status_string(int status);
 /* Message of the last error on this host thread. */
 const char* ctcb_last_error(void);

@@ -28,6 +28,7 @@ struct ctcb_handle {
   double beam_threshold;
   int num_sms, max_smem_optin;
   int force_generic;  // CTCB_FORCE_GENERIC=1: use the generic kernel for every beam (testing)
+  unsigned long long* dbg;  // device [8] debug counters
   void* ws;
   size_t ws_bytes;
 };
@@ -163,6 +164,15 @@ const char* ctcb_status_string(int status) {
 
 const char* ctcb_last_error(void) { return g_last_error.c_str(); }
 
+int ctcb_debug_counters(ctcb_t* h, uint64_t* out8) {
+  if (!h || !out8) return fail(CTCB_ERR_ARG, "NULL argument");
+  memset(out8, 0, 8 * sizeof(uint64_t));
+  if (!h->dbg) return CTCB_OK;
+  CTCB_CUDA(cudaSetDevice(h->device));
+  CTCB_CUDA(cudaMemcpy(out8, h->dbg, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return CTCB_OK;
+}
+
 int ctcb_skip_cutoff(double thr, float* cutoff) {
   if (!cutoff) return fail(CTCB_ERR_ARG, "cutoff must not be NULL");
   if (!(thr > 0.0 && thr <= 1.0)) return fail(CTCB_ERR_ARG, "blank_skip_threshold must be in (0, 1]");
@@ -204,6 +214,7 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   h->beam_threshold = beam_threshold;
   h->ws = nullptr;
   h->ws_bytes = 0;
+  h->dbg = nullptr;
   {
     const char* fg = getenv("CTCB_FORCE_GENERIC");
     h->force_generic = (fg && fg[0] == '1') ? 1 : 0;
@@ -221,6 +232,7 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
 int ctcb_destroy(ctcb_t* h) {
   if (!h) return CTCB_OK;
   if (h->ws) cudaFree(h->ws);
+  if (h->dbg) cudaFree(h->dbg);
   delete h;
   return CTCB_OK;
 }
@@ -260,6 +272,9 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   rc = launch_config(h, P, B, fast);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!h->dbg) CTCB_CUDA(cudaMalloc(&h->dbg, 8 * sizeof(unsigned long long)));
+  CTCB_CUDA(cudaMemsetAsync(h->dbg, 0, 8 * sizeof(unsigned long long), s));
+  P.dbg = h->dbg;
   int n = 1;
   while (n < B) n <<= 1;
   size_t order_smem = n <= 8192 ? (size_t)n * 8 : 0;

@@ -102,11 +102,15 @@ struct FastSmem {
   int *stok, *rec_i, *tie_i, *hl;
   uint32_t *excl, *tring, *hist;
   uint8_t* posmap;
+  uint64_t* tc_h;
+  int* tc_r;
 };
 
 // Token sequence of current entry `e` (length len) through the global trellis.
 __device__ int fast_materialize(const Params& P, int u, int steps_done, int e, int len, int* buf) {
   int pos = len, slot = e;
+  atomicAdd(&P.dbg[kDbgMaterialize], 1ull);
+  atomicAdd(&P.dbg[kDbgMatSteps], (unsigned long long)steps_done);
   for (int i = steps_done - 1; i >= 0 && pos > 0; --i) {
     uint32_t r = P.trellis[((size_t)u * P.T_max + i) * P.beam + slot];
     int tok = trel_tok(r);
@@ -115,14 +119,64 @@ __device__ int fast_materialize(const Params& P, int u, int steps_done, int e, i
   }
   return len;
 }
+// Tie-order cache: prefix hashes identify token sequences globally, so a
+// cached "seq(h1) vs seq(h2)" stays valid for the whole decode (and across
+// utterances).  Sibling prefixes with identical scores (a duplicated fp32
+// value in some row) tie again every frame; the cache answers those without
+// re-reading their sequences.
+__device__ int tc_lookup(const FastSmem& S, uint64_t ha, uint64_t hb) {
+  for (int i = 0; i < kTieCache; i++) {
+    if (S.tc_h[2 * i] == ha && S.tc_h[2 * i + 1] == hb) return S.tc_r[i];
+    if (S.tc_h[2 * i] == hb && S.tc_h[2 * i + 1] == ha) return -S.tc_r[i];
+  }
+  return 0;
+}
+__device__ void tc_insert(const FastSmem& S, uint64_t ha, uint64_t hb, int r) {
+  if (tc_lookup(S, ha, hb)) return;
+  int i = S.tc_r[kTieCache];
+  S.tc_h[2 * i] = ha;
+  S.tc_h[2 * i + 1] = hb;
+  S.tc_r[i] = r;
+  S.tc_r[kTieCache] = (i + 1) % kTieCache;
+}
+__device__ int fast_seq_cmp_full(const Params& P, const FastSmem& S, int u, int steps_done, int ea, int xa, int eb,
+                                 int xb, bool* strict);
 // Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb]; hs/hl hold the hashes and
-// lengths of the current entries.
+// lengths of the current entries.  Orders of sequence pairs that differ
+// before the end of the shorter one ("strict") are cached: every extension of
+// such a pair keeps the order, so a tie that recurs on the next frame between
+// their descendants is answered from the cache.
 __device__ int fast_seq_cmp(const Params& P, const FastSmem& S, int u, int steps_done, int ea, int xa, int eb,
                             int xb) {
-  if (S.hs[ea] == S.hs[eb] && S.hl[ea] == S.hl[eb]) {
+  const uint64_t hba = S.hs[ea], hbb = S.hs[eb];
+  const int lba = S.hl[ea], lbb = S.hl[eb];
+  if (hba == hbb && lba == lbb) {  // same base prefix: compare the extra tokens
     if (xa == xb) return 0;
     return xa < xb ? -1 : 1;
   }
+  const uint64_t ha = xa >= 0 ? child_hash(hba, xa) : hba, hb = xb >= 0 ? child_hash(hbb, xb) : hbb;
+  const int la = lba + (xa >= 0), lb = lbb + (xb >= 0);
+  if (ha == hb && la == lb) return 0;  // identical sequences (e.g. (R,c) vs (R+c))
+  int r = tc_lookup(S, hba, hbb);
+  if (r) {
+    tc_insert(S, ha, hb, r);
+    return r;
+  }
+  r = tc_lookup(S, ha, hb);
+  if (r) return r;
+  bool strict = false;
+  r = fast_seq_cmp_full(P, S, u, steps_done, ea, -1, eb, -1, &strict);
+  if (strict) {
+    tc_insert(S, hba, hbb, r);
+    tc_insert(S, ha, hb, r);
+    return r;
+  }
+  r = fast_seq_cmp_full(P, S, u, steps_done, ea, xa, eb, xb, &strict);
+  if (strict) tc_insert(S, ha, hb, r);
+  return r;
+}
+__device__ int fast_seq_cmp_full(const Params& P, const FastSmem& S, int u, int steps_done, int ea, int xa, int eb,
+                                 int xb, bool* strict) {
   int* A = P.seqbuf + (size_t)u * 3 * (P.T_max + 1);
   int* Bq = A + P.T_max + 1;
   int la = fast_materialize(P, u, steps_done, ea, S.hl[ea], A);
@@ -130,14 +184,17 @@ __device__ int fast_seq_cmp(const Params& P, const FastSmem& S, int u, int steps
   int lb = fast_materialize(P, u, steps_done, eb, S.hl[eb], Bq);
   if (xb >= 0) Bq[lb++] = xb;
   int n = la < lb ? la : lb;
+  *strict = true;
   for (int i = 0; i < n; i++)
     if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
+  *strict = false;
   return la < lb ? -1 : (la > lb ? 1 : 0);
 }
 // a precedes b in the reference's rank order: score desc, sequence asc, flag asc.
 __device__ bool fast_precedes(const Params& P, const FastSmem& S, int u, int sd, double sa, int ba, int xa, int fa,
                               double sb, int bb, int xb, int fb) {
   if (sa != sb) return sa > sb;
+  atomicAdd(&P.dbg[kDbgExactTies], 1ull);
   int c = fast_seq_cmp(P, S, u, sd, ba, xa, bb, xb);
   if (c) return c < 0;
   return fa < fb;
@@ -228,6 +285,10 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
   S.tring = (uint32_t*)(wbase + L.ring);
   S.hist = (uint32_t*)(wbase + L.hist);
   S.posmap = wbase + L.posmap;
+  S.tc_h = (uint64_t*)(wbase + L.tc_h);
+  S.tc_r = (int*)(wbase + L.tc_r);
+  for (int i = lane; i < 2 * kTieCache; i += 32) S.tc_h[i] = 0ull;
+  for (int i = lane; i <= kTieCache; i += 32) S.tc_r[i] = 0;
 
   const int V = P.V, k = P.k, beam = P.beam;
   const int nch4 = (V + 3) >> 2;
@@ -359,6 +420,7 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
         }
         skey = a;
       } else {
+        if (lane == 0) atomicAdd(&P.dbg[kDbgRadix], 1ull);
         skey = topk_radix(S, row, V, k, lane);
       }
       const int st = lane < k ? (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu)) : 0;
@@ -511,6 +573,7 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
           if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; }
           __syncwarp();
           if (lane == 0) {
+            atomicAdd(&P.dbg[kDbgTies], 1ull);
             unsigned rest = tied & (tied - 1);
             while (rest) {
               int c = __ffs(rest) - 1;

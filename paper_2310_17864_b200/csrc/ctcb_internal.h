@@ -49,15 +49,19 @@ struct Params {
   int warps_per_block;
   int smem_per_warp;
   int n_chunks;         // ceil(T_max / kChunk)
+  unsigned long long* dbg;  // [8] debug counters (kDbg*)
 };
+
+enum DbgCounter { kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5 };
 
 // Fast path (beam <= kFastBeam): trellis checkpoint interval.
 constexpr int kFastBeam = 16;
 constexpr int kChunk = 32;
+constexpr int kTieCache = 32;
 
 // Byte offsets of the per-warp shared memory of the fast decode kernel.
 struct FastLayout {
-  size_t rows, mbar, cand, sval, stok, excl, rec_sc, rec_s2, rec_i, tie_sc, tie_i, hs, hl, ring, hist, posmap, total;
+  size_t rows, mbar, cand, sval, stok, excl, rec_sc, rec_s2, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, ring, hist, posmap, total;
 };
 __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_bytes) {
   FastLayout L{};
@@ -81,6 +85,8 @@ __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_
   L.rec_i = take(16 * 8 * 4, 4);   // 8 ints per merge record
   L.tie_i = take(32 * 4 * 4, 4);   // 4 ints per tie candidate
   L.hl = take(16 * 4, 4);          // entry lengths (tie slow path)
+  L.tc_h = take(2 * kTieCache * 8, 8);  // tie-order cache: (seq hash a, seq hash b)
+  L.tc_r = take((kTieCache + 1) * 4, 4);  // cached order (-1/+1) + replacement cursor
   L.ring = take((size_t)kChunk * 16 * 4, 4);
   L.hist = take(256 * 4, 4);
   L.posmap = take((size_t)V, 1);

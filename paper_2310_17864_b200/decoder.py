@@ -291,6 +291,14 @@ class CUCTCDecoder:
             result.append(hyps)
         return result
 
+    def debug_counters(self) -> dict:
+        """Slow-path counters of the last decode (see include/ctcb.h)."""
+        lib = _lib.load()
+        arr = (ctypes.c_uint64 * 8)()
+        _lib.check(lib.ctcb_debug_counters(self._h, arr), "ctcb_debug_counters")
+        names = ("key_ties", "exact_ties", "materializations", "materialize_steps", "radix_fallbacks")
+        return {n: int(arr[i]) for i, n in enumerate(names)}
+
     def debug_frames(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor):
         """Minimum slice: (frame_map [B,T], kept [B], topk_tok [B,T,k],
         topk_val [B,T,k], blank [B,T]) device tensors after synchronisation."""
