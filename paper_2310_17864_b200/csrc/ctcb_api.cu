@@ -72,7 +72,7 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   return w;
 }
 
-int ring_for(int row_bytes) { return row_bytes <= 4096 ? 4 : (row_bytes <= 16384 ? 3 : 2); }
+int ring_for(int row_bytes) { return row_bytes <= 4096 ? 3 : 2; }
 
 // Fill the launch parameters shared by the decode and debug kernels.
 int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
@@ -128,7 +128,11 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
 
 bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
 
+// Choose the row-ring depth and warps per block: shared memory per warp must
+// fit, then maximise resident warps per SM (occupancy API), and spread small
+// batches over all SMs (at most ceil(B / num_sms) warps per block).
 int launch_config(ctcb_handle* h, ctcb::Params& P, int B, bool fast) {
+  const void* kfn = fast ? (const void*)ctcb::ctcb_decode_fast_kernel : (const void*)ctcb::ctcb_decode_generic_kernel;
   for (;;) {
     size_t total = fast ? ctcb::make_fast_layout(P.V, P.ring, P.row_bytes).total
                         : ctcb::make_layout(P.beam, P.kpad, P.V, P.ring, P.row_bytes).total;
@@ -137,13 +141,19 @@ int launch_config(ctcb_handle* h, ctcb::Params& P, int B, bool fast) {
     if (P.ring > 1) { P.ring--; continue; }
     return fail(CTCB_ERR_UNSUPPORTED, "beam/vocabulary too large for one warp's shared memory");
   }
-  int wpb = h->max_smem_optin / P.smem_per_warp;
-  wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
-  // spread small batches over all SMs: at most ceil(B / num_sms) warps per block
+  int max_wpb = h->max_smem_optin / P.smem_per_warp;
+  max_wpb = max_wpb < 1 ? 1 : (max_wpb > 8 ? 8 : max_wpb);
   int spread = (B + h->num_sms - 1) / h->num_sms;
   if (spread < 1) spread = 1;
-  if (wpb > spread) wpb = spread;
-  P.warps_per_block = wpb;
+  if (max_wpb > spread) max_wpb = spread;
+  int best_wpb = 1, best_warps = -1;
+  CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->max_smem_optin));
+  for (int wpb = max_wpb; wpb >= 1; --wpb) {
+    int bps = 0;
+    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, 32 * wpb, (size_t)P.smem_per_warp * wpb));
+    if (bps * wpb > best_warps) { best_warps = bps * wpb; best_wpb = wpb; }
+  }
+  P.warps_per_block = best_wpb;
   return CTCB_OK;
 }
 

@@ -96,7 +96,7 @@ struct FastSmem {
   uint8_t* rows;
   uint64_t* mbar;
   uint64_t* cand;
-  double *rec_sc, *rec_s2, *tie_sc;
+  double* tie_sc;
   uint64_t* hs;
   float* sval;
   int *stok, *rec_i, *tie_i, *hl;
@@ -104,6 +104,9 @@ struct FastSmem {
   uint8_t* posmap;
   uint64_t* tc_h;
   int* tc_r;
+  uint32_t* gkey;
+  double* hsc;
+  int* hp2;
 };
 
 // Token sequence of current entry `e` (length len) through the global trellis.
@@ -272,8 +275,6 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
   S.rows = wbase + L.rows;
   S.mbar = (uint64_t*)(wbase + L.mbar);
   S.cand = (uint64_t*)(wbase + L.cand);
-  S.rec_sc = (double*)(wbase + L.rec_sc);
-  S.rec_s2 = (double*)(wbase + L.rec_s2);
   S.tie_sc = (double*)(wbase + L.tie_sc);
   S.hs = (uint64_t*)(wbase + L.hs);
   S.sval = (float*)(wbase + L.sval);
@@ -287,11 +288,15 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
   S.posmap = wbase + L.posmap;
   S.tc_h = (uint64_t*)(wbase + L.tc_h);
   S.tc_r = (int*)(wbase + L.tc_r);
+  S.gkey = (uint32_t*)(wbase + L.gkey);
+  S.hsc = (double*)(wbase + L.hsc);
+  S.hp2 = (int*)(wbase + L.hp2);
   for (int i = lane; i < 2 * kTieCache; i += 32) S.tc_h[i] = 0ull;
   for (int i = lane; i <= kTieCache; i += 32) S.tc_r[i] = 0;
 
   const int V = P.V, k = P.k, beam = P.beam;
   const int nch4 = (V + 3) >> 2;
+  const bool small_v = nch4 <= 256;  // <= 8 float4 chunks per lane: predicate bits fit one register
   const uint32_t fullk = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
   const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
   const double kScale = 4294967294.0 / kR;
@@ -380,32 +385,53 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
       __syncwarp();
 
       // ================= top-k (k <= 32) =================
+      // threshold = k-th largest lane maximum (>= k elements reach it);
+      // compaction of the <= 64 elements above it; register bitonic sort of
+      // (log-prob desc, index asc) keys.
       const float4* row4 = (const float4*)row;
       float lmax = __uint_as_float(kSentinel);
       for (int c = lane; c < nch4; c += 32) {
         float4 q = row4[c];
         lmax = fmaxf(lmax, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
       }
-      uint32_t lk = isnan(lmax) ? 0u : okey(lmax);
-      uint32_t srt = sort_desc32(lk, lane);
-      uint32_t t0 = __shfl_sync(FULL, srt, k - 1);
-      float tf = t0 == 0u ? -INFINITY : unord32(t0);
+      const uint32_t t0 = __shfl_sync(FULL, sort_desc32(isnan(lmax) ? 0u : okey(lmax), lane), k - 1);
+      const float tf = t0 == 0u ? -INFINITY : unord32(t0);
+      uint32_t pm = 0u;  // predicate bits (V <= 1024: chunk j of this lane -> bits 4j..4j+3)
       int cl = 0;
-      for (int c = lane; c < nch4; c += 32) {
-        float4 q = row4[c];
-        cl += (q.x >= tf) + (q.y >= tf) + (q.z >= tf) + (q.w >= tf);
+      if (small_v) {
+        int j = 0;
+        for (int c = lane; c < nch4; c += 32, j += 4) {
+          float4 q = row4[c];
+          pm |= ((uint32_t)(q.x >= tf) | ((uint32_t)(q.y >= tf) << 1) | ((uint32_t)(q.z >= tf) << 2) |
+                 ((uint32_t)(q.w >= tf) << 3)) << j;
+        }
+        cl = __popc(pm);
+      } else {
+        for (int c = lane; c < nch4; c += 32) {
+          float4 q = row4[c];
+          cl += (q.x >= tf) + (q.y >= tf) + (q.z >= tf) + (q.w >= tf);
+        }
       }
-      int cnt = __reduce_add_sync(FULL, cl);
+      const int cnt = __reduce_add_sync(FULL, cl);
       uint64_t skey;
       if (cnt <= 64) {
         int off = warp_incl_scan(cl, lane) - cl;
-        for (int c = lane; c < nch4; c += 32) {
-          float4 q = row4[c];
-          float vv[4] = {q.x, q.y, q.z, q.w};
+        if (small_v) {
+          while (pm) {
+            const int bt = __ffs(pm) - 1;
+            pm &= pm - 1u;
+            const int e = 4 * (lane + 32 * (bt >> 2)) + (bt & 3);
+            S.cand[off++] = ((uint64_t)okey(row[e]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)e);
+          }
+        } else {
+          for (int c = lane; c < nch4; c += 32) {
+            float4 q = row4[c];
+            float vv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-          for (int z = 0; z < 4; z++)
-            if (vv[z] >= tf)
-              S.cand[off++] = ((uint64_t)okey(vv[z]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)(4 * c + z));
+            for (int z = 0; z < 4; z++)
+              if (vv[z] >= tf)
+                S.cand[off++] = ((uint64_t)okey(vv[z]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)(4 * c + z));
+          }
         }
         __syncwarp();
         uint64_t a = lane < cnt ? S.cand[lane] : 0ull;
@@ -438,8 +464,7 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
       const unsigned m = __match_any_sync(FULL, mkey);
       const unsigned same = m & 0xffffu;
       const unsigned parents = __shfl_sync(FULL, m & 0xffffu, me + 16);
-      const int first = __ffs(same) - 1;
-      const bool isfirst = ent && first == lane;
+      const bool isfirst = ent && (__ffs(same) - 1) == lane;
       const unsigned firstmask = __ballot_sync(FULL, isfirst);
       const int nD = __popc(firstmask);
       const unsigned pmask = same & ~(1u << lane);
@@ -510,18 +535,12 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
       const bool gen = lane >= 16 && me < nD;
       const int gsrc = gen ? (int)__fns(firstmask, 0, me + 1) : lane;
       const double gA = __shfl_sync(FULL, A, gsrc);
-      const double g_s1 = __shfl_sync(FULL, s, gsrc);
-      const double g_s2 = __shfl_sync(FULL, s_p2, gsrc);
-      const int g_has2 = __shfl_sync(FULL, p2 >= 0 ? 1 : 0, gsrc);
       uint32_t gv = __shfl_sync(FULL, gvalid, gsrc);
       if (!gen) gv = 0u;
 
-      // heads and the frame best
-      double hsc;
-      int qi = 0;
-      if (lane < 16) hsc = q0;
-      else hsc = gv ? gA + (double)S.sval[__ffs(gv) - 1] : -INFINITY;
-      const uint64_t ok64 = hsc > -INFINITY ? ord64(hsc) : 0ull;
+      // frame best (approximate append scores A + v; exact on key ties)
+      const double hsc0 = lane < 16 ? q0 : (gv ? gA + (double)S.sval[__ffs(gv) - 1] : -INFINITY);
+      const uint64_t ok64 = hsc0 > -INFINITY ? ord64(hsc0) : 0ull;
       const uint32_t mhi = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32));
       const uint32_t mlo = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32) == mhi ? (uint32_t)ok64 : 0u);
       const uint64_t bk = ((uint64_t)mhi << 32) | mlo;
@@ -529,14 +548,22 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
       const double best = unord64(bk);
       const double lo_thr = P.threshold_inf ? -INFINITY : best - P.beam_threshold;  // decoder.py:621-623
       const double kbase = best - kR;
+      // 32-bit fixed-point rank key: 0 = dropped, order-preserving above the cut
       auto keyof = [&](double sc) -> uint32_t {
         if (!(sc > -INFINITY) || !(sc >= lo_thr)) return 0u;
-        double z = (sc - kbase) * kScale;
-        if (!(z > 0.0)) return 1u;
-        if (z >= 4294967293.0) return 0xffffffffu;
-        return 1u + (uint32_t)z;
+        const double z = (sc - kbase) * kScale;
+        return z >= 4294967293.0 ? 0xffffffffu : 1u + (z > 0.0 ? (uint32_t)z : 0u);
       };
-      uint32_t hk = keyof(hsc);
+      // append-group keys, one row per distinct prefix: lane j fills column j
+      for (int d = 0; d < nD; d++) {
+        const int f = (int)__fns(firstmask, 0, d + 1);
+        const double Ad = __shfl_sync(FULL, A, f);
+        if (lane < k) S.gkey[d * 32 + lane] = keyof(Ad + (double)sv);
+      }
+      const uint32_t kq0 = keyof(q0), kq1 = keyof(q1), kq2 = keyof(q2);
+      __syncwarp();
+      int qi = 0;
+      uint32_t hk = lane < 16 ? kq0 : (gv ? S.gkey[me * 32 + __ffs(gv) - 1] : 0u);
 
       // ================= k-way merge (decoder.py:651-681) =================
       int Hn = 0;
@@ -551,16 +578,14 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
             double esc;
             int eb_, ex, ef;
             if (lane < 16) {
-              int kind = qi == 0 ? k0 : (qi == 1 ? k1 : k2);
-              esc = hsc;
+              const int kind = qi == 0 ? k0 : (qi == 1 ? k1 : k2);
+              esc = qi == 0 ? q0 : (qi == 1 ? q1 : q2);
               eb_ = lane;
               ex = kind == 2 ? last : -1;
               ef = kind == 0 ? 1 : 0;
             } else {
-              int pos = __ffs(gv) - 1;
-              double v = (double)S.sval[pos];
-              esc = g_s1 + v;
-              if (g_has2) esc = np_logaddexp(esc, g_s2 + v);
+              const int pos = __ffs(gv) - 1;
+              esc = gA + (double)S.sval[pos];  // replaced by the exact fold below
               eb_ = gsrc;
               ex = S.stok[pos];
               ef = 0;
@@ -569,14 +594,29 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
             S.tie_i[lane * 4 + 0] = eb_;
             S.tie_i[lane * 4 + 1] = ex;
             S.tie_i[lane * 4 + 2] = ef;
+            S.tie_i[lane * 4 + 3] = lane < 16 ? -1 : (__ffs(gv) - 1);
           }
-          if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; }
+          if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; S.hsc[lane] = s; S.hp2[lane] = p2; }
           __syncwarp();
           if (lane == 0) {
             atomicAdd(&P.dbg[kDbgTies], 1ull);
+            // exact append-group scores for tied list heads
+            unsigned tl = tied;
+            while (tl) {
+              const int c = __ffs(tl) - 1;
+              tl &= tl - 1;
+              const int pos = S.tie_i[c * 4 + 3];
+              if (pos >= 0) {
+                const int f = S.tie_i[c * 4];
+                const double v = (double)S.sval[pos];
+                double e = S.hsc[f] + v;
+                if (S.hp2[f] >= 0) e = np_logaddexp(e, S.hsc[S.hp2[f]] + v);
+                S.tie_sc[c] = e;
+              }
+            }
             unsigned rest = tied & (tied - 1);
             while (rest) {
-              int c = __ffs(rest) - 1;
+              const int c = __ffs(rest) - 1;
               rest &= rest - 1;
               if (fast_precedes(P, S, u, i, S.tie_sc[c], S.tie_i[c * 4], S.tie_i[c * 4 + 1], S.tie_i[c * 4 + 2],
                                 S.tie_sc[w], S.tie_i[w * 4], S.tie_i[w * 4 + 1], S.tie_i[w * 4 + 2]))
@@ -587,36 +627,16 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
           __syncwarp();
         }
         if (lane == w) {
-          int* ri = S.rec_i + r * 8;
           if (lane < 16) {
-            const int kind = qi == 0 ? k0 : (qi == 1 ? k1 : k2);
-            S.rec_sc[r] = hsc;
-            ri[0] = kind;
-            ri[1] = lane;
-            ri[2] = kind == 1 ? rep_src : (kind == 2 ? single_src : lane);
-            ri[3] = kind == 1 ? rep_tok : (kind == 2 ? last : -1);
-            ri[4] = kind == 0 ? 1 : 0;
-            ri[5] = kind == 2 ? last : -1;
-            ri[6] = -1;
+            S.rec_i[r] = lane | (qi << 8);
             qi++;
-            hsc = qi == 1 ? q1 : (qi == 2 ? q2 : -INFINITY);
+            hk = qi == 1 ? kq1 : (qi == 2 ? kq2 : 0u);
           } else {
             const int pos = __ffs(gv) - 1;
-            const int c = S.stok[pos];
-            S.rec_sc[r] = g_s1;
-            S.rec_s2[r] = g_s2;
-            ri[0] = 3;
-            ri[1] = gsrc;
-            ri[2] = gsrc;
-            ri[3] = c;
-            ri[4] = 0;
-            ri[5] = c;
-            ri[6] = pos;
-            ri[7] = g_has2;
+            S.rec_i[r] = lane | (pos << 8);
             gv &= gv - 1u;
-            hsc = gv ? gA + (double)S.sval[__ffs(gv) - 1] : -INFINITY;
+            hk = gv ? S.gkey[me * 32 + __ffs(gv) - 1] : 0u;
           }
-          hk = keyof(hsc);
         }
         Hn = r + 1;
       }
@@ -624,21 +644,38 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
       if (Hn == 0) { died = true; break; }
 
       // ================= commit (decoder.py:683-744) =================
+      // lane r builds new entry r from the winning lane's registers
       const bool nent = lane < Hn;
-      const int* ri = S.rec_i + (nent ? lane : 0) * 8;
-      const int kind = ri[0], bl = nent ? ri[1] : lane;
-      const uint64_t bh = shfl64(h, bl), bph = shfl64(ph, bl);
-      const int blast = __shfl_sync(FULL, last, bl), blen = __shfl_sync(FULL, len, bl);
-      double nsc = S.rec_sc[nent ? lane : 0];
-      if (nent && kind == 3) {  // exact append-group score: fold in rank order
-        const double v = (double)S.sval[ri[6]];
-        double a = nsc + v;
-        if (ri[7]) a = np_logaddexp(a, S.rec_s2[lane] + v);
-        nsc = a;
+      const int rec = S.rec_i[nent ? lane : 0];
+      const int wl = nent ? (rec & 0xff) : lane, item = rec >> 8;
+      const int kpack = k0 | (k1 << 2) | (k2 << 4);
+      const int wk = __shfl_sync(FULL, kpack, wl);
+      const double w_q0 = __shfl_sync(FULL, q0, wl), w_q1 = __shfl_sync(FULL, q1, wl), w_q2 = __shfl_sync(FULL, q2, wl);
+      const int w_src = __shfl_sync(FULL, rep_src | (single_src << 8), wl);
+      const int w_rtok = __shfl_sync(FULL, rep_tok, wl);
+      const int w_gsrc = __shfl_sync(FULL, gsrc, wl);
+      const bool wgen = wl >= 16;
+      const int base = wgen ? w_gsrc : wl;
+      const uint64_t bh = shfl64(h, base), bph = shfl64(ph, base);
+      const int blast = __shfl_sync(FULL, last, base), blen = __shfl_sync(FULL, len, base);
+      const double b_s1 = __shfl_sync(FULL, s, base), b_s2 = __shfl_sync(FULL, s_p2, base);
+      const int b_p2 = __shfl_sync(FULL, p2, base);
+      double nsc;
+      int x, src, tok, nfl;
+      if (wgen) {  // append group (R+c,0): exact fold of R's entries in rank order
+        const int c = S.stok[item];
+        const double v = (double)S.sval[item];
+        nsc = b_s1 + v;
+        if (b_p2 >= 0) nsc = np_logaddexp(nsc, b_s2 + v);
+        x = c; src = base; tok = c; nfl = 0;
+      } else {
+        const int kind = (wk >> (2 * item)) & 3;
+        nsc = item == 0 ? w_q0 : (item == 1 ? w_q1 : w_q2);
+        if (kind == 0) { x = -1; src = wl; tok = -1; nfl = 1; }                  // blank group
+        else if (kind == 1) { x = -1; src = w_src & 0xff; tok = w_rtok; nfl = 0; }  // repeat group
+        else { x = blast; src = w_src >> 8; tok = blast; nfl = 0; }               // last-token append
       }
-      const int x = ri[5];
-      const uint32_t trel = pack_trel(ri[2], ri[3]);
-      const int nfl = ri[4];
+      const uint32_t trel = pack_trel(src, tok);
       __syncwarp();
       // reset the token -> S rank map
       if (lane < k) S.posmap[st] = 0xff;

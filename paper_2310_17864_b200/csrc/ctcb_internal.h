@@ -61,7 +61,7 @@ constexpr int kTieCache = 32;
 
 // Byte offsets of the per-warp shared memory of the fast decode kernel.
 struct FastLayout {
-  size_t rows, mbar, cand, sval, stok, excl, rec_sc, rec_s2, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, ring, hist, posmap, total;
+  size_t rows, mbar, cand, sval, stok, excl, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, gkey, hsc, hp2, ring, hist, posmap, total;
 };
 __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_bytes) {
   FastLayout L{};
@@ -75,18 +75,19 @@ __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_
   L.rows = take((size_t)ring * row_bytes, 128);
   L.mbar = take((size_t)ring * 8, 8);
   L.cand = take(64 * 8, 8);
-  L.rec_sc = take(16 * 8, 8);
-  L.rec_s2 = take(16 * 8, 8);
   L.tie_sc = take(32 * 8, 8);
   L.hs = take(16 * 8, 8);
   L.sval = take(32 * 4, 4);
   L.stok = take(32 * 4, 4);
   L.excl = take(16 * 4, 4);
-  L.rec_i = take(16 * 8 * 4, 4);   // 8 ints per merge record
+  L.rec_i = take(16 * 4, 4);       // merge record per new entry: winning lane | item << 8
   L.tie_i = take(32 * 4 * 4, 4);   // 4 ints per tie candidate
   L.hl = take(16 * 4, 4);          // entry lengths (tie slow path)
   L.tc_h = take(2 * kTieCache * 8, 8);  // tie-order cache: (seq hash a, seq hash b)
   L.tc_r = take((kTieCache + 1) * 4, 4);  // cached order (-1/+1) + replacement cursor
+  L.gkey = take(16 * 32 * 4, 4);   // append-group rank keys [distinct prefix][S position]
+  L.hsc = take(16 * 8, 8);         // entry scores (tie slow path)
+  L.hp2 = take(16 * 4, 4);         // partner entry of each first entry (tie slow path)
   L.ring = take((size_t)kChunk * 16 * 4, 4);
   L.hist = take(256 * 4, 4);
   L.posmap = take((size_t)V, 1);
