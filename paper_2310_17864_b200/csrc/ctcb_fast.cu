@@ -107,6 +107,9 @@ struct FastSmem {
   uint32_t* gkey;
   double* hsc;
   int* hp2;
+  int* dlane;
+  double* dA;
+  uint32_t* dgv;
 };
 
 // Token sequence of current entry `e` (length len) through the global trellis.
@@ -291,6 +294,9 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
   S.gkey = (uint32_t*)(wbase + L.gkey);
   S.hsc = (double*)(wbase + L.hsc);
   S.hp2 = (int*)(wbase + L.hp2);
+  S.dlane = (int*)(wbase + L.dlane);
+  S.dA = (double*)(wbase + L.dA);
+  S.dgv = (uint32_t*)(wbase + L.dgv);
   for (int i = lane; i < 2 * kTieCache; i += 32) S.tc_h[i] = 0ull;
   for (int i = lane; i <= kTieCache; i += 32) S.tc_r[i] = 0;
 
@@ -530,13 +536,19 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
       }
 
       // ================= append lists (lanes 16..16+nD) =================
+      // first lanes publish (lane, A, valid positions) at their distinct index
       const double A = isfirst ? (p2 >= 0 ? np_logaddexp(s, s_p2) : s) : 0.0;
-      const uint32_t gvalid = isfirst ? (fullk & ~(childx | mybit)) : 0u;
+      if (isfirst) {
+        const int d = __popc(firstmask & lanemask_lt());
+        S.dlane[d] = lane;
+        S.dA[d] = A;
+        S.dgv[d] = fullk & ~(childx | mybit);
+      }
+      __syncwarp();
       const bool gen = lane >= 16 && me < nD;
-      const int gsrc = gen ? (int)__fns(firstmask, 0, me + 1) : lane;
-      const double gA = __shfl_sync(FULL, A, gsrc);
-      uint32_t gv = __shfl_sync(FULL, gvalid, gsrc);
-      if (!gen) gv = 0u;
+      const int gsrc = gen ? S.dlane[me] : lane;
+      const double gA = gen ? S.dA[me] : 0.0;
+      uint32_t gv = gen ? S.dgv[me] : 0u;
 
       // frame best (approximate append scores A + v; exact on key ties)
       const double hsc0 = lane < 16 ? q0 : (gv ? gA + (double)S.sval[__ffs(gv) - 1] : -INFINITY);
@@ -555,10 +567,9 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
         return z >= 4294967293.0 ? 0xffffffffu : 1u + (z > 0.0 ? (uint32_t)z : 0u);
       };
       // append-group keys, one row per distinct prefix: lane j fills column j
-      for (int d = 0; d < nD; d++) {
-        const int f = (int)__fns(firstmask, 0, d + 1);
-        const double Ad = __shfl_sync(FULL, A, f);
-        if (lane < k) S.gkey[d * 32 + lane] = keyof(Ad + (double)sv);
+      if (lane < k) {
+        const double v = (double)sv;
+        for (int d = 0; d < nD; d++) S.gkey[d * 32 + lane] = keyof(S.dA[d] + v);
       }
       const uint32_t kq0 = keyof(q0), kq1 = keyof(q1), kq2 = keyof(q2);
       __syncwarp();

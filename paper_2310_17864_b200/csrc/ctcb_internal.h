@@ -61,7 +61,7 @@ constexpr int kTieCache = 32;
 
 // Byte offsets of the per-warp shared memory of the fast decode kernel.
 struct FastLayout {
-  size_t rows, mbar, cand, sval, stok, excl, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, gkey, hsc, hp2, ring, hist, posmap, total;
+  size_t rows, mbar, cand, sval, stok, excl, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, gkey, hsc, hp2, dlane, dA, dgv, ring, hist, posmap, total;
 };
 __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_bytes) {
   FastLayout L{};
@@ -88,6 +88,9 @@ __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_
   L.gkey = take(16 * 32 * 4, 4);   // append-group rank keys [distinct prefix][S position]
   L.hsc = take(16 * 8, 8);         // entry scores (tie slow path)
   L.hp2 = take(16 * 4, 4);         // partner entry of each first entry (tie slow path)
+  L.dA = take(16 * 8, 8);          // per distinct prefix: A = logaddexp of its entries
+  L.dlane = take(16 * 4, 4);       // per distinct prefix: its first entry lane
+  L.dgv = take(16 * 4, 4);         // per distinct prefix: valid append positions in S
   L.ring = take((size_t)kChunk * 16 * 4, 4);
   L.hist = take(256 * 4, 4);
   L.posmap = take((size_t)V, 1);
