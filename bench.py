@@ -80,7 +80,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i",
-                 str(self.device), "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 str(self.device), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -186,7 +186,7 @@ def run_reference(args, cfg, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ctcb", choices=["ctcb", "reference"])
     ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
@@ -333,7 +333,8 @@ def main():
             "utterances_per_s": utts_all / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": alg_bytes, "kernel": "ctcb_decode_generic_kernel",
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel": "ctcb_decode_fast_kernel" if cfg.beam <= 16 else "ctcb_decode_generic_kernel",
                          "kept_frames": kept_rank},
             "cpu_baseline": cpu,
             "e2e": e2e,
