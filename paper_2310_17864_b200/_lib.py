@@ -12,7 +12,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libctcb.so")
+LIB_PATH = os.environ.get("CTCB_LIB") or os.path.join(_HERE, "libctcb.so")
 
 CTCB_OK, CTCB_ERR_ARG, CTCB_ERR_CUDA, CTCB_ERR_WORKSPACE, CTCB_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 UTT_OK, UTT_EMPTY, UTT_BAD_LEN, UTT_BEAM_DIED = 0, 1, 2, 3

@@ -72,7 +72,7 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   return w;
 }
 
-int ring_for(int row_bytes) { return row_bytes <= 4096 ? 3 : 2; }
+int ring_for(int row_bytes) { (void)row_bytes; return 2; }
 
 // Fill the launch parameters shared by the decode and debug kernels.
 int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
@@ -143,6 +143,7 @@ int launch_config(ctcb_handle* h, ctcb::Params& P, int B, bool fast) {
   }
   int max_wpb = h->max_smem_optin / P.smem_per_warp;
   max_wpb = max_wpb < 1 ? 1 : (max_wpb > 8 ? 8 : max_wpb);
+  if (fast && max_wpb > 4) max_wpb = 4;  // fast kernel: __launch_bounds__(128, 6)
   int spread = (B + h->num_sms - 1) / h->num_sms;
   if (spread < 1) spread = 1;
   if (max_wpb > spread) max_wpb = spread;

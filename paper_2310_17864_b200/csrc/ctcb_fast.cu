@@ -268,7 +268,10 @@ __device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k
 
 }  // namespace
 
-__global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_constant__ Params P) {
+#ifndef CTCB_FAST_MIN_BLOCKS
+#define CTCB_FAST_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int me = lane & 15;
@@ -558,13 +561,13 @@ __global__ void __launch_bounds__(256, 2) ctcb_decode_fast_kernel(const __grid_c
       const uint64_t bk = ((uint64_t)mhi << 32) | mlo;
       if (bk == 0ull) { died = true; break; }  // every extension is -inf (decoder.py:616-620)
       const double best = unord64(bk);
-      const double lo_thr = P.threshold_inf ? -INFINITY : best - P.beam_threshold;  // decoder.py:621-623
-      const double kbase = best - kR;
+      // keep iff score >= best - beam_threshold and score > -inf (decoder.py:621-623)
+      const double lo_thr = P.threshold_inf ? -DBL_MAX : best - P.beam_threshold;
+      const double koff = -(best - kR) * kScale;
       // 32-bit fixed-point rank key: 0 = dropped, order-preserving above the cut
       auto keyof = [&](double sc) -> uint32_t {
-        if (!(sc > -INFINITY) || !(sc >= lo_thr)) return 0u;
-        const double z = (sc - kbase) * kScale;
-        return z >= 4294967293.0 ? 0xffffffffu : 1u + (z > 0.0 ? (uint32_t)z : 0u);
+        const double z = fmin(fmax(fma(sc, kScale, koff), 0.0), 4294967294.0);
+        return sc >= lo_thr ? 1u + (uint32_t)z : 0u;
       };
       // append-group keys, one row per distinct prefix: lane j fills column j
       if (lane < k) {

@@ -56,7 +56,7 @@ enum DbgCounter { kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatS
 
 // Fast path (beam <= kFastBeam): trellis checkpoint interval.
 constexpr int kFastBeam = 16;
-constexpr int kChunk = 32;
+constexpr int kChunk = 16;
 constexpr int kTieCache = 32;
 
 // Byte offsets of the per-warp shared memory of the fast decode kernel.
@@ -92,7 +92,7 @@ __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_
   L.dlane = take(16 * 4, 4);       // per distinct prefix: its first entry lane
   L.dgv = take(16 * 4, 4);         // per distinct prefix: valid append positions in S
   L.ring = take((size_t)kChunk * 16 * 4, 4);
-  L.hist = take(256 * 4, 4);
+  L.hist = L.gkey;                 // radix-select histogram (fallback only) aliases the key matrix
   L.posmap = take((size_t)V, 1);
   L.total = (o + 127) / 128 * 128;
   return L;
