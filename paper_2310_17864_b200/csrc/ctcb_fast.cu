@@ -569,46 +569,63 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
         const double z = fmin(fmax(fma(sc, kScale, koff), 0.0), 4294967294.0);
         return sc >= lo_thr ? 1u + (uint32_t)z : 0u;
       };
-      // append-group keys, one row per distinct prefix: lane j fills column j
-      if (lane < k) {
-        const double v = (double)sv;
-        for (int d = 0; d < nD; d++) S.gkey[d * 32 + lane] = keyof(S.dA[d] + v);
+      // rank-key queues: each lane pops its candidates in order.  Lanes < 16
+      // queue their <= 3 special groups (items 0..2 = local sorted order);
+      // lanes 16.. queue the next four valid positions of their append list
+      // (item = S position), refilled on demand.
+      uint32_t kq[4];
+      uint32_t items;
+      auto refill = [&]() {
+        items = 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          kq[q] = 0u;
+          if (gv) {
+            const int p = __ffs(gv) - 1;
+            gv &= gv - 1u;
+            kq[q] = keyof(gA + (double)S.sval[p]);
+            items = (items & ~(0xffu << (8 * q))) | ((uint32_t)p << (8 * q));
+          }
+        }
+      };
+      if (lane < 16) {
+        kq[0] = keyof(q0); kq[1] = keyof(q1); kq[2] = keyof(q2); kq[3] = 0u;
+        items = 0xff020100u;
+      } else {
+        refill();
       }
-      const uint32_t kq0 = keyof(q0), kq1 = keyof(q1), kq2 = keyof(q2);
-      __syncwarp();
-      int qi = 0;
-      uint32_t hk = lane < 16 ? kq0 : (gv ? S.gkey[me * 32 + __ffs(gv) - 1] : 0u);
+      const int kpack = k0 | (k1 << 2) | (k2 << 4);
 
       // ================= k-way merge (decoder.py:651-681) =================
       int Hn = 0;
       for (int r = 0; r < beam; r++) {
-        const uint32_t mk = __reduce_max_sync(FULL, hk);
+        const uint32_t mk = __reduce_max_sync(FULL, kq[0]);
         if (mk == 0u) break;
-        const unsigned tied = __ballot_sync(FULL, hk == mk);
+        const unsigned tied = __ballot_sync(FULL, kq[0] == mk);
         int w = __ffs(tied) - 1;
         if (tied & (tied - 1)) {
           // exact resolution: fp64 score, then token sequence, then flag
           if (tied & (1u << lane)) {
+            const int it = (int)(items & 0xffu);
             double esc;
             int eb_, ex, ef;
             if (lane < 16) {
-              const int kind = qi == 0 ? k0 : (qi == 1 ? k1 : k2);
-              esc = qi == 0 ? q0 : (qi == 1 ? q1 : q2);
+              const int kind = (kpack >> (2 * it)) & 3;
+              esc = it == 0 ? q0 : (it == 1 ? q1 : q2);
               eb_ = lane;
               ex = kind == 2 ? last : -1;
               ef = kind == 0 ? 1 : 0;
             } else {
-              const int pos = __ffs(gv) - 1;
-              esc = gA + (double)S.sval[pos];  // replaced by the exact fold below
+              esc = gA + (double)S.sval[it];  // replaced by the exact fold below
               eb_ = gsrc;
-              ex = S.stok[pos];
+              ex = S.stok[it];
               ef = 0;
             }
             S.tie_sc[lane] = esc;
             S.tie_i[lane * 4 + 0] = eb_;
             S.tie_i[lane * 4 + 1] = ex;
             S.tie_i[lane * 4 + 2] = ef;
-            S.tie_i[lane * 4 + 3] = lane < 16 ? -1 : (__ffs(gv) - 1);
+            S.tie_i[lane * 4 + 3] = lane < 16 ? -1 : it;
           }
           if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; S.hsc[lane] = s; S.hp2[lane] = p2; }
           __syncwarp();
@@ -641,16 +658,10 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
           __syncwarp();
         }
         if (lane == w) {
-          if (lane < 16) {
-            S.rec_i[r] = lane | (qi << 8);
-            qi++;
-            hk = qi == 1 ? kq1 : (qi == 2 ? kq2 : 0u);
-          } else {
-            const int pos = __ffs(gv) - 1;
-            S.rec_i[r] = lane | (pos << 8);
-            gv &= gv - 1u;
-            hk = gv ? S.gkey[me * 32 + __ffs(gv) - 1] : 0u;
-          }
+          S.rec_i[r] = lane | (int)((items & 0xffu) << 8);
+          items = (items >> 8) | 0xff000000u;
+          kq[0] = kq[1]; kq[1] = kq[2]; kq[2] = kq[3]; kq[3] = 0u;
+          if (kq[0] == 0u && gv) refill();
         }
         Hn = r + 1;
       }
@@ -662,7 +673,6 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       const bool nent = lane < Hn;
       const int rec = S.rec_i[nent ? lane : 0];
       const int wl = nent ? (rec & 0xff) : lane, item = rec >> 8;
-      const int kpack = k0 | (k1 << 2) | (k2 << 4);
       const int wk = __shfl_sync(FULL, kpack, wl);
       const double w_q0 = __shfl_sync(FULL, q0, wl), w_q1 = __shfl_sync(FULL, q1, wl), w_q2 = __shfl_sync(FULL, q2, wl);
       const int w_src = __shfl_sync(FULL, rep_src | (single_src << 8), wl);
