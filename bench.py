@@ -208,13 +208,20 @@ def main():
 
     from paper_2310_17864_b200 import cuda_ctc_decoder
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; CTCB_DIST_BACKEND=gloo lets several ranks share a
+    # GPU to exercise the multi-rank host path (timing reductions only)
+    backend = os.environ.get("CTCB_DIST_BACKEND", "nccl")
+    local_dev = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     # -- this rank's shard (LPT on length), generated straight into pinned memory
     lens_all = synth.lengths(cfg)
@@ -244,7 +251,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(local_dev) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
             out = dec.decode(lp_dev, lens_dev)
@@ -257,17 +264,19 @@ def main():
     status = out.status.cpu().numpy()
     assert (status == 0).all(), "decode failed"
 
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
+
     def reduce_max(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def reduce_sum(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 

@@ -131,6 +131,7 @@ __device__ int fast_materialize(const Params& P, int u, int steps_done, int e, i
 // value in some row) tie again every frame; the cache answers those without
 // re-reading their sequences.
 __device__ int tc_lookup(const FastSmem& S, uint64_t ha, uint64_t hb) {
+#pragma unroll 1
   for (int i = 0; i < kTieCache; i++) {
     if (S.tc_h[2 * i] == ha && S.tc_h[2 * i + 1] == hb) return S.tc_r[i];
     if (S.tc_h[2 * i] == hb && S.tc_h[2 * i + 1] == ha) return -S.tc_r[i];
