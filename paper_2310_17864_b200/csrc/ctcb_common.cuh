@@ -27,13 +27,66 @@ __device__ __forceinline__ uint64_t ord64(double d) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// log1p(exp(-d)) for d >= 0 in ~45 branch-free fp64 instructions (CUDA's
+// exp + log1p expand to ~280 inline instructions each call site).  Absolute
+// error <= 2.3e-16 over d in [0, 700) (validated against numpy on 2.1M points,
+// see DESIGN.md §2); the result is added to a score, so it rounds like
+// numpy's log1p(exp(.)) up to one ulp of the score.
+__device__ __forceinline__ double log1pexp_neg(double d) {
+  const double kLog2e = 1.4426950408889634, kLn2Hi = 0.6931471803691238, kLn2Lo = 1.9082149292705877e-10;
+  // exp(-d) = 2^n * exp(g), n = rint(-d*log2e), |g| <= ln2/2 (Cody-Waite)
+  const double n = rint(-d * kLog2e);
+  const double g = fma(-n, kLn2Lo, fma(-n, kLn2Hi, -d));
+  double p = 1.0 / 6227020800.0;  // 1/13!
+  p = fma(p, g, 1.0 / 479001600.0);
+  p = fma(p, g, 1.0 / 39916800.0);
+  p = fma(p, g, 1.0 / 3628800.0);
+  p = fma(p, g, 1.0 / 362880.0);
+  p = fma(p, g, 1.0 / 40320.0);
+  p = fma(p, g, 1.0 / 5040.0);
+  p = fma(p, g, 1.0 / 720.0);
+  p = fma(p, g, 1.0 / 120.0);
+  p = fma(p, g, 1.0 / 24.0);
+  p = fma(p, g, 1.0 / 6.0);
+  p = fma(p, g, 0.5);
+  p = fma(p, g, 1.0);
+  p = fma(p, g, 1.0);
+  const int ni = d < 700.0 ? (int)n : -1100;
+  const double e = ni > -1022 ? p * __longlong_as_double((long long)(ni + 1023) << 52) : 0.0;
+  // log1p(e) = log(z), z = 1 + e in (1, 2]: split at sqrt(2), atanh series
+  const double z = 1.0 + e;
+  const bool big = z > 1.4142135623730951;
+  const double zz = big ? 0.5 * z : z;
+  const double corr = big ? 0.5 * (e - (z - 1.0)) : (e - (z - 1.0));  // rounding of 1 + e
+  const double num = zz - 1.0, den = zz + 1.0;
+  double r = (double)__frcp_rn((float)den);  // 1/den: fp32 seed + two Newton steps
+  r = fma(r, fma(-den, r, 1.0), r);
+  r = fma(r, fma(-den, r, 1.0), r);
+  double u = num * r;
+  u = fma(r, fma(-den, u, num), u);
+  const double u2 = u * u;
+  double s = 1.0 / 23.0;
+  s = fma(s, u2, 1.0 / 21.0);
+  s = fma(s, u2, 1.0 / 19.0);
+  s = fma(s, u2, 1.0 / 17.0);
+  s = fma(s, u2, 1.0 / 15.0);
+  s = fma(s, u2, 1.0 / 13.0);
+  s = fma(s, u2, 1.0 / 11.0);
+  s = fma(s, u2, 1.0 / 9.0);
+  s = fma(s, u2, 1.0 / 7.0);
+  s = fma(s, u2, 1.0 / 5.0);
+  s = fma(s, u2, 1.0 / 3.0);
+  double res = fma(2.0 * u, u2 * s, 2.0 * u) + corr * (double)__frcp_rn((float)zz);
+  return big ? res + kLn2Hi + kLn2Lo : res;
+}
+
 // numpy's npy_logaddexp: the fold np.logaddexp.reduceat performs when the
 // reference merges candidates (decoder.py:611) and flag variants (:791).
 __device__ __forceinline__ double np_logaddexp(double x, double y) {
   if (x == y) return x + CTCB_LN2;
   double tmp = x - y;
-  if (tmp > 0) return x + log1p(exp(-tmp));
-  if (tmp <= 0) return y + log1p(exp(tmp));
+  if (tmp > 0) return x + log1pexp_neg(tmp);
+  if (tmp <= 0) return y + log1pexp_neg(-tmp);
   return tmp;
 }
 

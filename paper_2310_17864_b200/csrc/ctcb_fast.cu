@@ -566,9 +566,12 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       const double lo_thr = P.threshold_inf ? -DBL_MAX : best - P.beam_threshold;
       const double koff = -(best - kR) * kScale;
       // 32-bit fixed-point rank key: 0 = dropped, order-preserving above the cut
+      // (truncation via the 2^52 magic add: the low word of z + 2^52 rounded
+      // toward zero is floor(z) for 0 <= z < 2^32, no F2I conversion needed)
       auto keyof = [&](double sc) -> uint32_t {
         const double z = fmin(fmax(fma(sc, kScale, koff), 0.0), 4294967294.0);
-        return sc >= lo_thr ? 1u + (uint32_t)z : 0u;
+        const uint32_t t = (uint32_t)__double_as_longlong(__dadd_rz(z, 4503599627370496.0));
+        return sc >= lo_thr ? 1u + t : 0u;
       };
       // rank-key queues: each lane pops its candidates in order.  Lanes < 16
       // queue their <= 3 special groups (items 0..2 = local sorted order);
