@@ -37,7 +37,7 @@ from paper_2310_17864_b200 import synth  # noqa: E402
 from paper_2310_17864_b200.shard import lpt_shards  # noqa: E402
 
 METRIC = "CTC beam-search decode frames/sec @V=500,beam=10"
-WORKLOADS = {"cfg4": 4, "cfg1": 1}
+WORKLOADS = {"cfg4": 4, "cfg1": 1, "cfg0": 0, "cfg2": 2, "cfg3": 3}
 
 
 def log(*a):
@@ -193,12 +193,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--beam", type=int, default=None, help="override the config's beam (cfg2 sweep: 1/10/50/100)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = synth.CONFIGS[WORKLOADS[args.workload]]
+    if args.beam is not None:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, beam=args.beam, nbest=min(args.beam, 10) if cfg.cfg == 2 else min(cfg.nbest, args.beam))
 
     if args.impl == "reference":
         run_reference(args, cfg, rank)

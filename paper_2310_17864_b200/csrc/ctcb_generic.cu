@@ -42,6 +42,8 @@ struct Warp {
   float* sval;
   int *stok, *spord, *spbase, *spx, *spflag, *spsrc, *sptok, *misc;
   uint16_t* pos;
+  uint64_t* tc_h;
+  int* tc_r;
   int kw;
 
   __device__ void swap_state() {
@@ -94,6 +96,8 @@ __device__ void carve(Warp& w, uint8_t* base, const Params& P) {
   w.hist = (uint32_t*)(base + L.hist);
   w.misc = (int*)(base + L.misc);
   w.pos = (uint16_t*)(base + L.pos);
+  w.tc_h = (uint64_t*)(base + L.tc_h);
+  w.tc_r = (int*)(base + L.tc_r);
   w.kw = L.kw;
 }
 
@@ -143,29 +147,78 @@ __device__ int materialize(const Warp& w, int e, int len, int* buf) {
   }
   return len;
 }
-// Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token).
-__device__ int seq_cmp(const Warp& w, int ea, int xa, int eb, int xb) {
-  if (w.ch[ea] == w.ch[eb] && w.cn[ea] == w.cn[eb]) {
-    if (xa == xb) return 0;
-    return xa < xb ? -1 : 1;
-  }
+// Full comparison through the trellis; *strict: the sequences differ before
+// the shorter one ends (then every extension keeps the order).
+__device__ int seq_cmp_full(const Warp& w, int ea, int xa, int eb, int xb, bool* strict) {
   const Params& P = *w.P;
-  int* A = P.seqbuf + (size_t)w.u * 2 * (P.T_max + 1);
+  atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
+  atomicAdd(&P.dbg[kDbgMatSteps], 2ull * (unsigned long long)w.steps_done);
+  int* A = P.seqbuf + (size_t)w.u * 3 * (P.T_max + 1);
   int* Bq = A + P.T_max + 1;
   int la = materialize(w, ea, w.cn[ea], A);
   if (xa >= 0) A[la++] = xa;
   int lb = materialize(w, eb, w.cn[eb], Bq);
   if (xb >= 0) Bq[lb++] = xb;
   int n = la < lb ? la : lb;
+  *strict = true;
   for (int i = 0; i < n; i++)
     if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
+  *strict = false;
   return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+// Strict-order cache keyed by prefix hashes (see the fast kernel): orders of
+// sibling lineages with identical scores are computed once.
+__device__ int gtc_lookup(const Warp& w, uint64_t ha, uint64_t hb) {
+#pragma unroll 1
+  for (int i = 0; i < kTieCache; i++) {
+    if (w.tc_h[2 * i] == ha && w.tc_h[2 * i + 1] == hb) return w.tc_r[i];
+    if (w.tc_h[2 * i] == hb && w.tc_h[2 * i + 1] == ha) return -w.tc_r[i];
+  }
+  return 0;
+}
+__device__ void gtc_insert(const Warp& w, uint64_t ha, uint64_t hb, int r) {
+  if (gtc_lookup(w, ha, hb)) return;
+  int i = w.tc_r[kTieCache];
+  w.tc_h[2 * i] = ha;
+  w.tc_h[2 * i + 1] = hb;
+  w.tc_r[i] = r;
+  w.tc_r[kTieCache] = (i + 1) % kTieCache;
+}
+// Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token).
+__device__ int seq_cmp(const Warp& w, int ea, int xa, int eb, int xb) {
+  const uint64_t hba = w.ch[ea], hbb = w.ch[eb];
+  const int lba = w.cn[ea], lbb = w.cn[eb];
+  if (hba == hbb && lba == lbb) {
+    if (xa == xb) return 0;
+    return xa < xb ? -1 : 1;
+  }
+  const uint64_t ha = xa >= 0 ? child_hash(hba, xa) : hba, hb = xb >= 0 ? child_hash(hbb, xb) : hbb;
+  const int la = lba + (xa >= 0), lb = lbb + (xb >= 0);
+  if (ha == hb && la == lb) return 0;
+  int r = gtc_lookup(w, hba, hbb);
+  if (r) {
+    gtc_insert(w, ha, hb, r);
+    return r;
+  }
+  r = gtc_lookup(w, ha, hb);
+  if (r) return r;
+  bool strict = false;
+  r = seq_cmp_full(w, ea, -1, eb, -1, &strict);
+  if (strict) {
+    gtc_insert(w, hba, hbb, r);
+    gtc_insert(w, ha, hb, r);
+    return r;
+  }
+  r = seq_cmp_full(w, ea, xa, eb, xb, &strict);
+  if (strict) gtc_insert(w, ha, hb, r);
+  return r;
 }
 // Candidate descriptor: (score, base entry, extra token, blank flag).
 struct Desc { double sc; int base, x, flag; };
 // true if a precedes b in the reference's rank order (decoder.py:651-681).
 __device__ bool precedes(const Warp& w, const Desc& a, const Desc& b) {
   if (a.sc != b.sc) return a.sc > b.sc;
+  atomicAdd(&w.P->dbg[kDbgExactTies], 1ull);
   int c = seq_cmp(w, a.base, a.x, b.base, b.x);
   if (c) return c < 0;
   return a.flag < b.flag;
@@ -539,6 +592,8 @@ __global__ void __launch_bounds__(256) ctcb_decode_generic_kernel(const __grid_c
   if (lane == 0)
     for (int s = 0; s < P.ring; s++) mbar_init(&w.mbar[s], 1);
   for (int c = lane; c < P.V; c += 32) w.pos[c] = 0xffff;
+  for (int i = lane; i < 2 * kTieCache; i += 32) w.tc_h[i] = 0ull;
+  for (int i = lane; i <= kTieCache; i += 32) w.tc_r[i] = 0;
   fence_mbar_init();
   __syncwarp();
   uint32_t n_issue = 0, n_cons = 0;  // ring bookkeeping across utterances

@@ -108,7 +108,7 @@ struct WarpLayout {
   size_t first, dpi, pd, dp_e1, dp_e2, excl, head_j, head_sc;
   size_t skey, sval, stok, pos;
   size_t sp_sc, sp_key, sp_ord, sp_base, sp_x, sp_flag, sp_src, sp_tok;
-  size_t hist, misc;
+  size_t hist, misc, tc_h, tc_r;
   size_t total;
   int kw, sp_cap, sp_pad;
 };
@@ -167,6 +167,8 @@ __host__ __device__ inline WarpLayout make_layout(int beam, int kpad, int V, int
   L.sp_tok = take(4 * (size_t)L.sp_cap, 4);
   L.hist = take(4 * 256, 4);
   L.misc = take(4 * 16, 4);
+  L.tc_h = take(2 * kTieCache * 8, 8);
+  L.tc_r = take((kTieCache + 1) * 4, 4);
   L.pos = take(2 * (size_t)V, 2);
   L.total = align_up(o, 128);
   return L;
