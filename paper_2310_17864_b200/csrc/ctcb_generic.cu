@@ -44,7 +44,9 @@ struct Warp {
   uint16_t* pos;
   uint64_t* tc_h;
   int* tc_r;
-  int kw;
+  uint64_t* htk;
+  int *htf, *hslot;
+  int kw, ts;
 
   __device__ void swap_state() {
     double* d = cs; cs = ns; ns = d;
@@ -98,7 +100,11 @@ __device__ void carve(Warp& w, uint8_t* base, const Params& P) {
   w.pos = (uint16_t*)(base + L.pos);
   w.tc_h = (uint64_t*)(base + L.tc_h);
   w.tc_r = (int*)(base + L.tc_r);
+  w.htk = (uint64_t*)(base + L.htk);
+  w.htf = (int*)(base + L.htf);
+  w.hslot = (int*)(base + L.hslot);
   w.kw = L.kw;
+  w.ts = L.ts;
 }
 
 // ------------------------------------------------------------------ sorting
@@ -225,8 +231,12 @@ __device__ bool precedes(const Warp& w, const Desc& a, const Desc& b) {
 }
 __device__ Desc spec_desc(const Warp& w, int s) { return Desc{w.spsc[s], w.spbase[s], w.spx[s], w.spflag[s]}; }
 
-// Re-sort runs of exactly equal scores in a sorted specials order (lane 0).
+// Re-sort runs of exactly equal scores in a sorted specials order (lane 0;
+// only when the parallel check finds a run).
 __device__ void fix_tie_runs(const Warp& w, int n) {
+  bool run = false;
+  for (int s = w.lane; s + 1 < n; s += 32) run |= w.spkey[s] == w.spkey[s + 1];
+  if (!__any_sync(FULL, run)) return;
   if (w.lane == 0) {
     int a = 0;
     while (a < n) {
@@ -347,13 +357,24 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   const int lane = w.lane, k = P.k, beam = P.beam;
   const double eb = (double)row[P.blank];
 
-  // -- prefix grouping: entries sharing a token sequence (flag 0 / flag 1)
+  // -- prefix grouping: entries sharing a token sequence (flag 0 / flag 1),
+  //    through a shared-memory hash table keyed by (prefix hash, length)
+  const int TS = w.ts;
+  for (int i = lane; i < TS; i += 32) { w.htk[i] = 0ull; w.htf[i] = 0x7fffffff; }
+  __syncwarp();
   for (int e = lane; e < H; e += 32) {
-    int f = e;
-    for (int q = 0; q < e; q++)
-      if (w.ch[q] == w.ch[e] && w.cn[q] == w.cn[e]) { f = q; break; }
-    w.first[e] = f;
+    const uint64_t key = (w.ch[e] ^ ((uint64_t)w.cn[e] * 0x9e3779b97f4a7c15ull)) | 1ull;
+    uint32_t i = (uint32_t)mix64(key) & (uint32_t)(TS - 1);
+    for (;;) {
+      const unsigned long long prev = atomicCAS((unsigned long long*)&w.htk[i], 0ull, (unsigned long long)key);
+      if (prev == 0ull || prev == key) break;
+      i = (i + 1) & (uint32_t)(TS - 1);
+    }
+    atomicMin(&w.htf[i], e);
+    w.hslot[e] = (int)i;
   }
+  __syncwarp();
+  for (int e = lane; e < H; e += 32) w.first[e] = w.htf[w.hslot[e]];
   __syncwarp();
   int nD = 0;
   for (int b0 = 0; b0 < H; b0 += 32) {
@@ -377,8 +398,14 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   for (int e = lane; e < H; e += 32) {
     int p = -1;
     if (w.cf[e] == 0) {
-      for (int q = 0; q < H; q++)
-        if (w.first[q] == q && w.ch[q] == w.cph[e] && w.cn[q] == w.cn[e] - 1) { p = w.dpi[q]; break; }
+      const uint64_t key = (w.cph[e] ^ ((uint64_t)(w.cn[e] - 1) * 0x9e3779b97f4a7c15ull)) | 1ull;
+      uint32_t i = (uint32_t)mix64(key) & (uint32_t)(TS - 1);
+      for (;;) {
+        const uint64_t k2 = w.htk[i];
+        if (k2 == 0ull) break;
+        if (k2 == key) { p = w.dpi[w.htf[i]]; break; }
+        i = (i + 1) & (uint32_t)(TS - 1);
+      }
       if (p >= 0) {
         int j = w.pos[w.cl[e]];
         if (j != 0xffff) atomicOr(&w.excl[p * w.kw + (j >> 5)], 1u << (j & 31));
@@ -447,53 +474,67 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   }
   __syncwarp();
 
-  // -- k-way merge under the reference order, with the beam_threshold cut
+  // -- k-way merge under the reference order, with the beam_threshold cut.
+  //    Heads are ranked by 32-bit fixed-point keys of their exact scores over
+  //    [best - R, best]; each lane caches the best key of the heads it owns
+  //    (i = lane + 32 j) and only the winner's lane rescans; equal keys are
+  //    resolved exactly (score, token sequence, flag).
   int sp_ptr = 0, Hn = 0;
-  double best = -INFINITY;
-  for (int r = 0; r < beam; r++) {
-    uint64_t lk = 0;
-    int li = -1, lcnt = 0;
-    for (int i = lane; i <= nD; i += 32) {
-      uint64_t kk;
-      if (i < nD) kk = w.headj[i] < k ? ord64(w.headsc[i]) : 0ull;
-      else kk = sp_ptr < nS ? w.spkey[sp_ptr] : 0ull;
+  const int nH = nD + 1;
+  auto head_sc = [&](int i) -> double {
+    if (i < nD) return w.headj[i] < k ? w.headsc[i] : -INFINITY;
+    return sp_ptr < nS ? w.spsc[w.spord[sp_ptr]] : -INFINITY;
+  };
+  double lbest = -INFINITY;
+  for (int i = lane; i < nH; i += 32) lbest = fmax(lbest, head_sc(i));
+  const uint64_t ok64 = lbest > -INFINITY ? ord64(lbest) : 0ull;
+  const uint32_t mhi = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32));
+  const uint32_t mlo = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32) == mhi ? (uint32_t)ok64 : 0u);
+  const uint64_t bk = ((uint64_t)mhi << 32) | mlo;
+  if (bk == 0ull) return 0;  // every extension is -inf (decoder.py:616-620)
+  const uint64_t bu = (bk >> 63) ? (bk & 0x7fffffffffffffffull) : ~bk;
+  const double best = __longlong_as_double((long long)bu);
+  const double lo_thr = P.threshold_inf ? -DBL_MAX : best - P.beam_threshold;  // decoder.py:621-623
+  const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
+  const double kScale = 4294967294.0 / kR, koff = -(best - kR) * kScale;
+  auto keyof = [&](double sc) -> uint32_t {
+    const double z = fmin(fmax(fma(sc, kScale, koff), 0.0), 4294967294.0);
+    const uint32_t t = (uint32_t)__double_as_longlong(__dadd_rz(z, 4503599627370496.0));
+    return sc >= lo_thr ? 1u + t : 0u;
+  };
+  uint32_t lk = 0u;
+  int li = -1, lcnt = 0;
+  auto rescan = [&]() {
+    lk = 0u; li = -1; lcnt = 0;
+    for (int i = lane; i < nH; i += 32) {
+      const uint32_t kk = keyof(head_sc(i));
       if (kk > lk) { lk = kk; li = i; lcnt = 1; }
-      else if (kk == lk && kk != 0ull) lcnt++;
+      else if (kk == lk && kk != 0u) lcnt++;
     }
-    uint64_t m = lk;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      uint64_t o = __shfl_xor_sync(FULL, m, off);
-      m = o > m ? o : m;
-    }
-    if (m == 0ull) break;
-    int ties = __reduce_add_sync(FULL, lk == m ? lcnt : 0);
+  };
+  rescan();
+  for (int r = 0; r < beam; r++) {
+    const uint32_t mk = __reduce_max_sync(FULL, lk);
+    if (mk == 0u) break;
+    const unsigned tl = __ballot_sync(FULL, lk == mk);
+    const int first_lane = __ffs(tl) - 1;
+    const int cnt0 = __shfl_sync(FULL, lcnt, first_lane);
     int win;
-    if (ties == 1) {
-      unsigned bal = __ballot_sync(FULL, lk == m);
-      win = __shfl_sync(FULL, li, __ffs(bal) - 1);
+    if ((tl & (tl - 1)) == 0u && cnt0 == 1) {
+      win = __shfl_sync(FULL, li, first_lane);
     } else {
       win = -1;
       if (lane == 0) {
         Desc dw{};
-        for (int i = 0; i <= nD; i++) {
-          Desc di;
-          if (i < nD) {
-            if (w.headj[i] >= k || ord64(w.headsc[i]) != m) continue;
-            di = Desc{w.headsc[i], w.e1[i], w.stok[w.headj[i]], 0};
-          } else {
-            if (sp_ptr >= nS || w.spkey[sp_ptr] != m) continue;
-            di = spec_desc(w, w.spord[sp_ptr]);
-          }
+        for (int i = 0; i < nH; i++) {
+          if (keyof(head_sc(i)) != mk) continue;
+          Desc di = i < nD ? Desc{w.headsc[i], w.e1[i], w.stok[w.headj[i]], 0} : spec_desc(w, w.spord[sp_ptr]);
           if (win < 0 || precedes(w, di, dw)) { win = i; dw = di; }
         }
       }
       win = __shfl_sync(FULL, win, 0);
     }
-    double sc = win < nD ? w.headsc[win] : w.spsc[w.spord[sp_ptr]];
-    if (r == 0) best = sc;
-    if (sc == -INFINITY) break;
-    if (!P.threshold_inf && sc < best - P.beam_threshold) break;
+    const double sc = head_sc(win);
     if (lane == 0) {
       if (win < nD) {
         int a = w.e1[win], j = w.headj[win], c = w.stok[j];
@@ -518,6 +559,7 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
     if (win == nD) sp_ptr++;
     Hn = r + 1;
     __syncwarp();
+    if ((win & 31) == lane) rescan();
   }
   // reset the token -> S rank map for the next frame
   for (int j = lane; j < k; j += 32) w.pos[w.stok[j]] = 0xffff;

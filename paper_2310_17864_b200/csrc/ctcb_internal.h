@@ -108,9 +108,9 @@ struct WarpLayout {
   size_t first, dpi, pd, dp_e1, dp_e2, excl, head_j, head_sc;
   size_t skey, sval, stok, pos;
   size_t sp_sc, sp_key, sp_ord, sp_base, sp_x, sp_flag, sp_src, sp_tok;
-  size_t hist, misc, tc_h, tc_r;
+  size_t hist, misc, tc_h, tc_r, htk, htf, hslot;
   size_t total;
-  int kw, sp_cap, sp_pad;
+  int kw, sp_cap, sp_pad, ts;
 };
 
 __host__ __device__ inline int pow2_at_least(int x) {
@@ -169,6 +169,10 @@ __host__ __device__ inline WarpLayout make_layout(int beam, int kpad, int V, int
   L.misc = take(4 * 16, 4);
   L.tc_h = take(2 * kTieCache * 8, 8);
   L.tc_r = take((kTieCache + 1) * 4, 4);
+  L.ts = pow2_at_least(2 * beam);
+  L.htk = take(8 * (size_t)L.ts, 8);
+  L.htf = take(4 * (size_t)L.ts, 4);
+  L.hslot = take(4 * (size_t)beam, 4);
   L.pos = take(2 * (size_t)V, 2);
   L.total = align_up(o, 128);
   return L;

@@ -1,0 +1,62 @@
+"""The ctcforge-shaped GPU entry points against the reference's
+own outputs (golden vectors), with full Hypothesis fields incl. timesteps."""
+
+import numpy as np
+import pytest
+
+from paper_2310_17864_b200.ctcforge_api import DecoderOptions
+
+
+def test_options_validation_matches_reference():
+    # decoder.py:54-66 (test_decoder.py:314-324)
+    for kw, msg in (({"beam_size": 0}, "beam_size"), ({"n_best": 5, "beam_size": 2}, "n_best"),
+                    ({"blank_skip_threshold": 0.0}, "blank_skip_threshold"), ({"merge_mode": "sum"}, "merge_mode"),
+                    ({"beam_threshold": 0.0}, "beam_threshold")):
+        with pytest.raises(ValueError, match=msg):
+            DecoderOptions(**kw)
+
+
+@pytest.mark.gpu
+def test_shim_matches_reference_golden(golden):
+    from paper_2310_17864_b200.ctcforge_api import beam_search_decode, decode_batch
+
+    cases = [c for c in golden["small"] if c["dtype"] == "float32" and c["merge"] == "logadd" and c["k"] is None]
+    assert cases
+    for c in cases:
+        lp = np.array(c["lp"], dtype=np.float64)
+        v = lp.shape[1]
+        tokens = ["-"] + [f"t{i}" for i in range(1, v)]
+        opts = DecoderOptions(beam_size=c["beam"], n_best=c["n_best"], blank_skip_threshold=c["thr"],
+                              beam_threshold=c["beam_threshold"])
+        nb = beam_search_decode(lp, tokens, opts)
+        assert [h.tokens for h in nb] == c["tokens"]
+        assert [h.timesteps for h in nb] == c["timesteps"]
+        for h, s in zip(nb, c["scores"]):
+            assert h.score == pytest.approx(s, abs=1e-9)
+            assert h.am_score == h.score and h.lm_score == 0.0 and h.words == []
+    # batch == per-utterance, order preserved
+    lps = [np.array(c["lp"], dtype=np.float64) for c in cases if len(c["lp"][0]) == 5][:6]
+    if lps:
+        tokens = ["-"] + [f"t{i}" for i in range(1, 5)]
+        opts = DecoderOptions(beam_size=4, n_best=2)
+        batch = decode_batch(lps, tokens, opts)
+        single = [beam_search_decode(lp, tokens, opts) for lp in lps]
+        assert [[h.tokens for h in x] for x in batch] == [[h.tokens for h in x] for x in single]
+
+
+@pytest.mark.gpu
+def test_shim_errors():
+    from paper_2310_17864_b200.ctcforge_api import beam_search_decode, decode_batch
+
+    tokens = ["-", "a", "b"]
+    with pytest.raises(ValueError, match="empty"):
+        beam_search_decode(np.zeros((0, 3)), tokens)
+    with pytest.raises(ValueError, match="columns"):
+        beam_search_decode(np.log(np.full((2, 4), 0.25)), tokens)
+    with pytest.raises(ValueError, match="full-vocabulary"):
+        beam_search_decode(np.log(np.full((2, 3), 1 / 3)), tokens, DecoderOptions(beam_size_token=2))
+    with pytest.raises(ValueError, match="logadd"):
+        beam_search_decode(np.log(np.full((2, 3), 1 / 3)), tokens, DecoderOptions(merge_mode="max"))
+    good = np.log(np.full((3, 3), 1 / 3))
+    with pytest.raises(ValueError, match="utterance 1: empty emissions"):
+        decode_batch([good, np.zeros((0, 3))], tokens)
