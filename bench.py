@@ -173,7 +173,7 @@ def run_reference(args, cfg, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "batch": cfg.batch, "vocab": cfg.vocab, "beam": cfg.beam,
                    "nbest": cfg.nbest, "blank_skip_threshold": cfg.threshold, "sample": sample},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample},
@@ -194,6 +194,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--beam", type=int, default=None, help="override the config's beam (cfg2 sweep: 1/10/50/100)")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the config's fixed batch over the ranks (BASELINE configs[4]); "
+                         "default is weak scaling: N x batch utterances, ~batch per rank")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -228,7 +231,14 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    # -- this rank's shard (LPT on length), generated straight into pinned memory
+    # -- this rank's shard (LPT on length), generated straight into pinned memory.
+    #    Weak scaling (default): the job is world x batch independent utterances
+    #    (global utterance index -> its own seed), LPT-sharded so each rank
+    #    holds ~batch; strong: the config's batch is split.
+    import dataclasses
+
+    if not args.strong and world > 1:
+        cfg = dataclasses.replace(cfg, batch=cfg.batch * world)
     lens_all = synth.lengths(cfg)
     shard = lpt_shards(lens_all, world)[rank]
     t_pad = int(lens_all[shard].max())
@@ -338,9 +348,10 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "batch": cfg.batch, "vocab": cfg.vocab, "beam": cfg.beam,
+            "config": {"workload": cfg.name, "batch": cfg.batch, "batch_per_rank": len(shard), "vocab": cfg.vocab, "beam": cfg.beam,
                        "nbest": cfg.nbest, "blank_skip_threshold": cfg.threshold, "t_range": [cfg.t_min, cfg.t_max],
                        "frames": int(frames_all), "parallelism": f"lpt-shard x{world}",
                        "l2": f"inputs larger than L2 ({host.numel() * 4 / 1e9:.1f} GB per rank), no flush"},
