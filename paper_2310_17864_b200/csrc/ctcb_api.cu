@@ -14,6 +14,8 @@
 namespace ctcb {
 __global__ void ctcb_decode_generic_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_framemap_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_topk_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter);
 __global__ void ctcb_debug_kernel(const __grid_constant__ Params P, int32_t* out_topk_tok, float* out_topk_val,
                                   float* out_blank);
@@ -22,6 +24,10 @@ __global__ void ctcb_validate_kernel(const float* lp, long long sb, long long st
 __global__ void ctcb_validate_decode_kernel(const unsigned long long* key, int T, int V, int64_t* out);
 }  // namespace ctcb
 
+struct ctcb_handle;
+namespace {
+bool use_fast(const ctcb_handle* h);
+}
 struct ctcb_handle {
   int V, blank, beam, nbest, k, kpad, device;
   float cutoff;
@@ -37,6 +43,8 @@ namespace {
 
 thread_local std::string g_last_error;
 
+bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
+
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -50,8 +58,20 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
   } while (0)
 
+bool use_fast(const ctcb_handle* h);
+// Precomputed-top-k mode for small batches (fewer utterances than ~2 per SM),
+// where one warp per utterance leaves the GPU latency-bound.
+// CTCB_TOPK_MODE=fused|precomp overrides.
+bool use_precomp(const ctcb_handle* h, int B) {
+  if (!use_fast(h)) return false;
+  const char* m = getenv("CTCB_TOPK_MODE");
+  if (m && strcmp(m, "fused") == 0) return false;
+  if (m && strcmp(m, "precomp") == 0) return true;
+  return B <= 2 * h->num_sms;
+}
+
 struct WsLayout {
-  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, total;
+  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, total;
 };
 WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   WsLayout w{};
@@ -68,6 +88,9 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   w.counter = take(4);
   w.seqbuf = take((size_t)B * 3 * (T + 1) * 4);
   w.anc = take((size_t)B * ((T + ctcb::kChunk - 1) / ctcb::kChunk) * 16);
+  const size_t ntk = use_precomp(h, B) ? (size_t)B * T * h->k : 0;
+  w.topk_tok = take(ntk * 4);
+  w.topk_val = take(ntk * 4);
   w.total = ctcb::align_up(o, 256);
   return w;
 }
@@ -120,13 +143,14 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.seqbuf = (int32_t*)(base + L.seqbuf);
   P.anc = (uint8_t*)(base + L.anc);
   P.n_chunks = (T + ctcb::kChunk - 1) / ctcb::kChunk;
+  P.topk_tok = (int32_t*)(base + L.topk_tok);
+  P.topk_val = (float*)(base + L.topk_val);
   P.row_bytes = (int)ctcb::align_up((size_t)h->V * 4, 16);
   P.ring = ring_for(P.row_bytes);
   P.bulk_ok = ((uintptr_t)lp % 16 == 0) && ((h->V * 4) % 16 == 0) && ((st * 4) % 16 == 0) && ((sb * 4) % 16 == 0);
   return CTCB_OK;
 }
 
-bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
 
 // Choose the row-ring depth and warps per block: shared memory per warp must
 // fit, then maximise resident warps per SM (occupancy API), and spread small
@@ -301,6 +325,20 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   int need = (B + P.warps_per_block - 1) / P.warps_per_block;
   int grid = h->num_sms * blocks_per_sm;
   if (grid > need) grid = need;
+  if (fast && use_precomp(h, B)) {
+    // frame maps -> top-k of every kept frame (frame-parallel) -> beam walk
+    P.precomp = 1;
+    ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
+    CTCB_CUDA(cudaGetLastError());
+    ctcb::Params Q = P;
+    Q.smem_per_warp = (int)ctcb::align_up((size_t)P.row_bytes + 64 * 8 + 256 * 4, 128);
+    const size_t tsmem = (size_t)Q.smem_per_warp * 8;
+    CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+    int tbps = 0;
+    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_kernel, 256, tsmem));
+    ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 256, tsmem, s>>>(Q);
+    CTCB_CUDA(cudaGetLastError());
+  }
   if (fast)
     ctcb::ctcb_decode_fast_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
   else

@@ -269,6 +269,94 @@ __device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k
 
 }  // namespace
 
+// Blank-skip compaction of one utterance by one warp: ballot + prefix
+// popcount over the blank column (emissions.py:298-306).  Returns the kept count.
+__device__ __forceinline__ int frame_map_warp(const Params& P, const float* ubase, int len_u, int32_t* fmap, int lane) {
+  int kept = 0;
+  for (int t0 = 0; t0 < len_u; t0 += 32) {
+    int t = t0 + lane;
+    bool keep = t < len_u;
+    if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
+    unsigned bal = __ballot_sync(FULL, keep);
+    if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
+    kept += __popc(bal);
+  }
+  return kept;
+}
+
+// Top-k of one staged row (blank and padding hold kSentinel): threshold = k-th
+// largest lane maximum (>= k elements reach it), compaction of the <= 64
+// elements above it, register bitonic sort of (log-prob desc, index asc)
+// keys.  Returns this lane's key of S (lanes < k).
+__device__ __forceinline__ uint64_t topk_key(const FastSmem& S, const float* row, int V, int k, int lane, bool small_v,
+                                             int nch4, unsigned long long* dbg) {
+  // threshold = k-th largest lane maximum (>= k elements reach it);
+  // compaction of the <= 64 elements above it; register bitonic sort of
+  // (log-prob desc, index asc) keys.
+  const float4* row4 = (const float4*)row;
+  float lmax = __uint_as_float(kSentinel);
+  for (int c = lane; c < nch4; c += 32) {
+    float4 q = row4[c];
+    lmax = fmaxf(lmax, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+  }
+  const uint32_t t0 = __shfl_sync(FULL, sort_desc32(isnan(lmax) ? 0u : okey(lmax), lane), k - 1);
+  const float tf = t0 == 0u ? -INFINITY : unord32(t0);
+  uint32_t pm = 0u;  // predicate bits (V <= 1024: chunk j of this lane -> bits 4j..4j+3)
+  int cl = 0;
+  if (small_v) {
+    int j = 0;
+    for (int c = lane; c < nch4; c += 32, j += 4) {
+      float4 q = row4[c];
+      pm |= ((uint32_t)(q.x >= tf) | ((uint32_t)(q.y >= tf) << 1) | ((uint32_t)(q.z >= tf) << 2) |
+             ((uint32_t)(q.w >= tf) << 3)) << j;
+    }
+    cl = __popc(pm);
+  } else {
+    for (int c = lane; c < nch4; c += 32) {
+      float4 q = row4[c];
+      cl += (q.x >= tf) + (q.y >= tf) + (q.z >= tf) + (q.w >= tf);
+    }
+  }
+  const int cnt = __reduce_add_sync(FULL, cl);
+  uint64_t skey;
+  if (cnt <= 64) {
+    int off = warp_incl_scan(cl, lane) - cl;
+    if (small_v) {
+      while (pm) {
+        const int bt = __ffs(pm) - 1;
+        pm &= pm - 1u;
+        const int e = 4 * (lane + 32 * (bt >> 2)) + (bt & 3);
+        S.cand[off++] = ((uint64_t)okey(row[e]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)e);
+      }
+    } else {
+      for (int c = lane; c < nch4; c += 32) {
+        float4 q = row4[c];
+        float vv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int z = 0; z < 4; z++)
+          if (vv[z] >= tf)
+            S.cand[off++] = ((uint64_t)okey(vv[z]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)(4 * c + z));
+      }
+    }
+    __syncwarp();
+    uint64_t a = lane < cnt ? S.cand[lane] : 0ull;
+    uint64_t b = lane + 32 < cnt ? S.cand[lane + 32] : 0ull;
+    __syncwarp();
+    a = sort_desc64(a, lane);
+    if (cnt > 32) {
+      b = sort_desc64(b, lane);
+      uint64_t br = shfl64(b, 31 - lane);
+      a = a > br ? a : br;
+      a = merge_desc64(a, lane);
+    }
+    skey = a;
+  } else {
+    if (lane == 0 && dbg) atomicAdd(&dbg[kDbgRadix], 1ull);
+    skey = topk_radix(S, row, V, k, lane);
+  }
+  return skey;
+}
+
 #ifndef CTCB_FAST_MIN_BLOCKS
 #define CTCB_FAST_MIN_BLOCKS 4
 #endif
@@ -337,18 +425,24 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
     const float* ubase = P.lp + (size_t)u * P.stride_b;
     int32_t* fmap = P.frame_map + (size_t)u * P.T_max;
 
-    // -- A. blank-skip compaction: ballot + prefix popcount (emissions.py:298-306)
+    // -- A. blank-skip compaction (emissions.py:298-306); in precomputed-top-k
+    //    mode ctcb_framemap_kernel already did it
     int kept = 0;
-    for (int t0 = 0; t0 < len_u; t0 += 32) {
-      int t = t0 + lane;
-      bool keep = t < len_u;
-      if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
-      unsigned bal = __ballot_sync(FULL, keep);
-      if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
-      kept += __popc(bal);
+    if (P.precomp) {
+      kept = P.kept[u];
+    } else {
+      kept = frame_map_warp(P, ubase, len_u, fmap, lane);
+      if (lane == 0) P.kept[u] = kept;
+      __syncwarp();
     }
-    if (lane == 0) P.kept[u] = kept;
-    __syncwarp();
+    // precomputed top-k lists, prefetched one frame ahead
+    const size_t tk_base = (size_t)u * P.T_max * k;
+    int pre_st = 0;
+    float pre_sv = 0.0f;
+    if (P.precomp && kept > 0 && lane < k) {
+      pre_st = P.topk_tok[tk_base + lane];
+      pre_sv = P.topk_val[tk_base + lane];
+    }
 
     auto issue = [&](int i) {
       uint32_t slot = n_issue % (uint32_t)P.ring;
@@ -388,80 +482,22 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       }
       const double eb = (double)row[P.blank];
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0 && !P.precomp) {
         ((uint32_t*)row)[P.blank] = kSentinel;
         for (int c = V; c < 4 * nch4; c++) ((uint32_t*)row)[c] = kSentinel;
       }
       __syncwarp();
 
       // ================= top-k (k <= 32) =================
-      // threshold = k-th largest lane maximum (>= k elements reach it);
-      // compaction of the <= 64 elements above it; register bitonic sort of
-      // (log-prob desc, index asc) keys.
-      const float4* row4 = (const float4*)row;
-      float lmax = __uint_as_float(kSentinel);
-      for (int c = lane; c < nch4; c += 32) {
-        float4 q = row4[c];
-        lmax = fmaxf(lmax, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
-      }
-      const uint32_t t0 = __shfl_sync(FULL, sort_desc32(isnan(lmax) ? 0u : okey(lmax), lane), k - 1);
-      const float tf = t0 == 0u ? -INFINITY : unord32(t0);
-      uint32_t pm = 0u;  // predicate bits (V <= 1024: chunk j of this lane -> bits 4j..4j+3)
-      int cl = 0;
-      if (small_v) {
-        int j = 0;
-        for (int c = lane; c < nch4; c += 32, j += 4) {
-          float4 q = row4[c];
-          pm |= ((uint32_t)(q.x >= tf) | ((uint32_t)(q.y >= tf) << 1) | ((uint32_t)(q.z >= tf) << 2) |
-                 ((uint32_t)(q.w >= tf) << 3)) << j;
-        }
-        cl = __popc(pm);
-      } else {
-        for (int c = lane; c < nch4; c += 32) {
-          float4 q = row4[c];
-          cl += (q.x >= tf) + (q.y >= tf) + (q.z >= tf) + (q.w >= tf);
-        }
-      }
-      const int cnt = __reduce_add_sync(FULL, cl);
-      uint64_t skey;
-      if (cnt <= 64) {
-        int off = warp_incl_scan(cl, lane) - cl;
-        if (small_v) {
-          while (pm) {
-            const int bt = __ffs(pm) - 1;
-            pm &= pm - 1u;
-            const int e = 4 * (lane + 32 * (bt >> 2)) + (bt & 3);
-            S.cand[off++] = ((uint64_t)okey(row[e]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)e);
-          }
-        } else {
-          for (int c = lane; c < nch4; c += 32) {
-            float4 q = row4[c];
-            float vv[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-            for (int z = 0; z < 4; z++)
-              if (vv[z] >= tf)
-                S.cand[off++] = ((uint64_t)okey(vv[z]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)(4 * c + z));
-          }
-        }
-        __syncwarp();
-        uint64_t a = lane < cnt ? S.cand[lane] : 0ull;
-        uint64_t b = lane + 32 < cnt ? S.cand[lane + 32] : 0ull;
-        __syncwarp();
-        a = sort_desc64(a, lane);
-        if (cnt > 32) {
-          b = sort_desc64(b, lane);
-          uint64_t br = shfl64(b, 31 - lane);
-          a = a > br ? a : br;
-          a = merge_desc64(a, lane);
-        }
-        skey = a;
-      } else {
-        if (lane == 0) atomicAdd(&P.dbg[kDbgRadix], 1ull);
-        skey = topk_radix(S, row, V, k, lane);
-      }
-      const int st = lane < k ? (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu)) : 0;
-      const float sv = lane < k ? row[st] : 0.0f;
+      uint64_t skey = 0ull;
+      if (!P.precomp) skey = topk_key(S, row, V, k, lane, small_v, nch4, P.dbg);
+      const int st = P.precomp ? pre_st : (lane < k ? (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu)) : 0);
+      const float sv = P.precomp ? pre_sv : (lane < k ? row[st] : 0.0f);
       if (lane < k) { S.sval[lane] = sv; S.stok[lane] = st; S.posmap[st] = (uint8_t)lane; }
+      if (P.precomp && i + 1 < kept && lane < k) {
+        pre_st = P.topk_tok[tk_base + (size_t)(i + 1) * k + lane];
+        pre_sv = P.topk_val[tk_base + (size_t)(i + 1) * k + lane];
+      }
       __syncwarp();
 
       // ================= merge structure =================
@@ -839,6 +875,61 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       if (lane == 0) { P.out_count[u] = nOut; P.status[u] = kUttOk; }
       __syncwarp();
     }
+  }
+}
+
+
+// Precomputed-top-k mode (small batches, where one warp per utterance leaves
+// the GPU latency-bound): frame maps first, then the top-k of every kept frame
+// of every utterance in parallel, then the beam kernel walks the frames with
+// the top-k lists prefetched.
+__global__ void __launch_bounds__(256) ctcb_framemap_kernel(const __grid_constant__ Params P) {
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u >= P.B) return;
+  int len_u = P.lens[u];
+  if (len_u < 0 || len_u > P.T_max) len_u = 0;
+  const int kept = frame_map_warp(P, P.lp + (size_t)u * P.stride_b, len_u, P.frame_map + (size_t)u * P.T_max, lane);
+  if (lane == 0) P.kept[u] = kept;
+}
+
+__global__ void __launch_bounds__(256) ctcb_topk_kernel(const __grid_constant__ Params P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint8_t* wbase = smem + (size_t)wid * P.smem_per_warp;
+  FastSmem S{};
+  S.rows = wbase;
+  S.cand = (uint64_t*)(wbase + P.row_bytes);
+  S.hist = (uint32_t*)(wbase + P.row_bytes + 64 * 8);
+  const int V = P.V, k = P.k, nch4 = (V + 3) >> 2;
+  const bool small_v = nch4 <= 256;
+  float* row = (float*)S.rows;
+  const long long total = (long long)P.B * P.T_max;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + wid; g < total; g += nwarps) {
+    const int u = (int)(g / P.T_max), i = (int)(g % P.T_max);
+    if (i >= P.kept[u]) continue;
+    const float* src = P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
+    if (P.bulk_ok) {
+      const float4* s4 = (const float4*)src;
+      for (int c = lane; c < nch4; c += 32) ((float4*)row)[c] = __ldg(s4 + c);
+    } else {
+      for (int c = lane; c < V; c += 32) row[c] = __ldg(src + c);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      ((uint32_t*)row)[P.blank] = kSentinel;
+      for (int c = V; c < 4 * nch4; c++) ((uint32_t*)row)[c] = kSentinel;
+    }
+    __syncwarp();
+    const uint64_t skey = topk_key(S, row, V, k, lane, small_v, nch4, nullptr);
+    if (lane < k) {
+      const int st = (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu));
+      const size_t o = ((size_t)u * P.T_max + i) * k + lane;
+      P.topk_tok[o] = st;
+      P.topk_val[o] = __ldg(src + st);
+    }
+    __syncwarp();
   }
 }
 

@@ -50,6 +50,9 @@ struct Params {
   int smem_per_warp;
   int n_chunks;         // ceil(T_max / kChunk)
   unsigned long long* dbg;  // [8] debug counters (kDbg*)
+  int precomp;              // top-k lists precomputed by ctcb_topk_kernel
+  int32_t* topk_tok;        // [B, T_max, k] (precomp mode)
+  float* topk_val;          // [B, T_max, k]
 };
 
 enum DbgCounter { kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5 };

@@ -243,7 +243,7 @@ class CUCTCDecoder:
         out_len = torch.zeros((B, nb), dtype=torch.int32, device=dev)
         out_score = torch.zeros((B, nb), dtype=torch.float64, device=dev)
         out_count = torch.zeros(B, dtype=torch.int32, device=dev)
-        out_status = torch.zeros(B, dtype=torch.int32, device=dev)
+        out_status = torch.full((B,), -1, dtype=torch.int32, device=dev)  # -1: not processed
         ws = self._workspace(B, T)
         vp = ctypes.c_void_p
         _lib.check(lib.ctcb_decode(
@@ -258,6 +258,8 @@ class CUCTCDecoder:
         errors for failed utterances.  Returns numpy arrays
         (tokens [B, nbest, Lmax], timesteps or None, lengths, scores, counts)."""
         status = out.status.cpu().numpy()
+        if (status < 0).any():
+            raise _lib.CtcbError(f"ctcb_decode left {(status < 0).sum()} utterance(s) unprocessed (kernel did not run)")
         bad = np.flatnonzero(status != _lib.UTT_OK)
         if bad.size:
             b = int(bad[0])

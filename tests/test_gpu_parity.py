@@ -285,3 +285,18 @@ def test_fast_and_generic_kernels_agree(monkeypatch):
         for x, y in zip(a, b):
             assert x["tokens"] == y["tokens"] and x["timesteps"] == y["timesteps"]
             assert np.allclose(x["scores"], y["scores"], atol=1e-9, rtol=0)
+
+
+def test_fused_and_precomputed_topk_modes_agree(monkeypatch):
+    """Small batches precompute the top-k of every frame in a frame-parallel
+    kernel; large batches fuse it into the beam walk.  Both must agree."""
+    cases = []
+    for cfg_id, idx in ((0, range(4)), (1, range(16)), (3, range(2))):
+        cfg = synth.CONFIGS[cfg_id]
+        lp, lens = synth.batch(cfg, indices=idx)
+        cases.append((lp, lens, cfg.beam, cfg.nbest, cfg.threshold))
+    monkeypatch.setenv("CTCB_TOPK_MODE", "precomp")
+    pre = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
+    monkeypatch.setenv("CTCB_TOPK_MODE", "fused")
+    fus = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
+    assert pre == fus
