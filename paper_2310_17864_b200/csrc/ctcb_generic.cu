@@ -45,7 +45,9 @@ struct Warp {
   uint64_t* tc_h;
   int* tc_r;
   uint64_t* htk;
-  int *htf, *hslot;
+  int *htf, *hslot, *rec, *rec2;
+  uint32_t* hkey;
+  double* lA;
   int kw, ts;
 
   __device__ void swap_state() {
@@ -103,6 +105,10 @@ __device__ void carve(Warp& w, uint8_t* base, const Params& P) {
   w.htk = (uint64_t*)(base + L.htk);
   w.htf = (int*)(base + L.htf);
   w.hslot = (int*)(base + L.hslot);
+  w.rec = (int*)(base + L.rec);
+  w.rec2 = (int*)(base + L.rec2);
+  w.hkey = (uint32_t*)(base + L.hkey);
+  w.lA = (double*)(base + L.lA);
   w.kw = L.kw;
   w.ts = L.ts;
 }
@@ -466,27 +472,22 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   __syncwarp();
   bitonic_pairs(w.spkey, w.spord, sp_pad, lane);
   fix_tie_runs(w, nS);
-  // -- generic list heads
+  // -- append-list heads.  Lists are ranked by A(R) + v with A = logaddexp of
+  //    R's entries (a few ulps from the exact per-candidate fold); exact
+  //    scores are computed for key ties and, in parallel, for the winners.
   for (int d = lane; d < nD; d += 32) {
-    int j = next_valid(w, d, -1);
-    w.headj[d] = j;
-    w.headsc[d] = j < k ? gen_score(w, d, j) : -INFINITY;
+    const int a = w.e1[d], b = w.e2[d];
+    w.lA[d] = b >= 0 ? np_logaddexp(w.cs[a], w.cs[b]) : w.cs[a];
+    w.headj[d] = next_valid(w, d, -1);
   }
   __syncwarp();
-
-  // -- k-way merge under the reference order, with the beam_threshold cut.
-  //    Heads are ranked by 32-bit fixed-point keys of their exact scores over
-  //    [best - R, best]; each lane caches the best key of the heads it owns
-  //    (i = lane + 32 j) and only the winner's lane rescans; equal keys are
-  //    resolved exactly (score, token sequence, flag).
-  int sp_ptr = 0, Hn = 0;
-  const int nH = nD + 1;
-  auto head_sc = [&](int i) -> double {
-    if (i < nD) return w.headj[i] < k ? w.headsc[i] : -INFINITY;
-    return sp_ptr < nS ? w.spsc[w.spord[sp_ptr]] : -INFINITY;
+  const int nH = nD + 1;  // lists 0..nD-1, then the sorted specials
+  auto head_approx = [&](int i, int sp) -> double {
+    if (i < nD) return w.headj[i] < k ? w.lA[i] + (double)w.sval[w.headj[i]] : -INFINITY;
+    return sp < nS ? w.spsc[w.spord[sp]] : -INFINITY;
   };
   double lbest = -INFINITY;
-  for (int i = lane; i < nH; i += 32) lbest = fmax(lbest, head_sc(i));
+  for (int i = lane; i < nH; i += 32) lbest = fmax(lbest, head_approx(i, 0));
   const uint64_t ok64 = lbest > -INFINITY ? ord64(lbest) : 0ull;
   const uint32_t mhi = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32));
   const uint32_t mlo = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32) == mhi ? (uint32_t)ok64 : 0u);
@@ -502,17 +503,26 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
     const uint32_t t = (uint32_t)__double_as_longlong(__dadd_rz(z, 4503599627370496.0));
     return sc >= lo_thr ? 1u + t : 0u;
   };
+  for (int i = lane; i < nH; i += 32) w.hkey[i] = keyof(head_approx(i, 0));
+  __syncwarp();
+
+  // -- k-way merge under the reference order (decoder.py:651-681): one
+  //    redux per round; each lane keeps the best key of the heads it owns
+  //    (i = lane + 32 j); the winner's lane pops and rescans its own heads.
+  int sp_ptr = 0;  // owned by lane (nD & 31); mirrored to misc[1] for the tie path
+  if (lane == 0) w.misc[1] = 0;
   uint32_t lk = 0u;
   int li = -1, lcnt = 0;
   auto rescan = [&]() {
     lk = 0u; li = -1; lcnt = 0;
     for (int i = lane; i < nH; i += 32) {
-      const uint32_t kk = keyof(head_sc(i));
+      const uint32_t kk = w.hkey[i];
       if (kk > lk) { lk = kk; li = i; lcnt = 1; }
       else if (kk == lk && kk != 0u) lcnt++;
     }
   };
   rescan();
+  int Hn = 0;
   for (int r = 0; r < beam; r++) {
     const uint32_t mk = __reduce_max_sync(FULL, lk);
     if (mk == 0u) break;
@@ -523,43 +533,72 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
     if ((tl & (tl - 1)) == 0u && cnt0 == 1) {
       win = __shfl_sync(FULL, li, first_lane);
     } else {
+      // equal keys: exact scores, then token sequence, then flag
       win = -1;
+      __syncwarp();
       if (lane == 0) {
+        const int sp = w.misc[1];
         Desc dw{};
         for (int i = 0; i < nH; i++) {
-          if (keyof(head_sc(i)) != mk) continue;
-          Desc di = i < nD ? Desc{w.headsc[i], w.e1[i], w.stok[w.headj[i]], 0} : spec_desc(w, w.spord[sp_ptr]);
+          if (w.hkey[i] != mk) continue;
+          Desc di = i < nD ? Desc{gen_score(w, i, w.headj[i]), w.e1[i], w.stok[w.headj[i]], 0}
+                           : spec_desc(w, w.spord[sp]);
           if (win < 0 || precedes(w, di, dw)) { win = i; dw = di; }
         }
       }
       win = __shfl_sync(FULL, win, 0);
     }
-    const double sc = head_sc(win);
-    if (lane == 0) {
+    if ((win & 31) == lane) {
       if (win < nD) {
-        int a = w.e1[win], j = w.headj[win], c = w.stok[j];
-        w.ns[r] = sc; w.nh[r] = child_hash(w.ch[a], c); w.nph[r] = w.ch[a];
-        w.nl[r] = c; w.nn[r] = w.cn[a] + 1; w.nf[r] = 0; w.ntrel[r] = pack_trel(a, c);
-        int jn = next_valid(w, win, j);
+        const int j = w.headj[win];
+        w.rec[r] = (win << 12) | j;
+        const int jn = next_valid(w, win, j);
         w.headj[win] = jn;
-        w.headsc[win] = jn < k ? gen_score(w, win, jn) : -INFINITY;
+        w.hkey[win] = jn < k ? keyof(w.lA[win] + (double)w.sval[jn]) : 0u;
       } else {
-        int s = w.spord[sp_ptr];
-        int a = w.spbase[s], x = w.spx[s];
-        w.ns[r] = sc;
-        if (x >= 0) {
-          w.nh[r] = child_hash(w.ch[a], x); w.nph[r] = w.ch[a]; w.nl[r] = x; w.nn[r] = w.cn[a] + 1;
-        } else {
-          w.nh[r] = w.ch[a]; w.nph[r] = w.cph[a]; w.nl[r] = w.cl[a]; w.nn[r] = w.cn[a];
-        }
-        w.nf[r] = w.spflag[s];
-        w.ntrel[r] = pack_trel(w.spsrc[s], w.sptok[s]);
+        w.rec[r] = (win << 12) | 0xfff;
+        w.rec2[r] = sp_ptr;
+        sp_ptr++;
+        w.misc[1] = sp_ptr;
+        w.hkey[win] = sp_ptr < nS ? keyof(w.spsc[w.spord[sp_ptr]]) : 0u;
       }
+      rescan();
     }
-    if (win == nD) sp_ptr++;
     Hn = r + 1;
-    __syncwarp();
-    if ((win & 31) == lane) rescan();
+  }
+  __syncwarp();
+  // -- new entries in parallel (exact scores: fold of R's entries in rank order)
+  for (int r = lane; r < Hn; r += 32) {
+    const int win = w.rec[r] >> 12, j = w.rec[r] & 0xfff;
+    if (win < nD) {
+      const int a = w.e1[win], c = w.stok[j];
+      w.ns[r] = gen_score(w, win, j); w.nh[r] = child_hash(w.ch[a], c); w.nph[r] = w.ch[a];
+      w.nl[r] = c; w.nn[r] = w.cn[a] + 1; w.nf[r] = 0; w.ntrel[r] = pack_trel(a, c);
+    } else {
+      const int s = w.spord[w.rec2[r]];
+      const int a = w.spbase[s], x = w.spx[s];
+      w.ns[r] = w.spsc[s];
+      if (x >= 0) {
+        w.nh[r] = child_hash(w.ch[a], x); w.nph[r] = w.ch[a]; w.nl[r] = x; w.nn[r] = w.cn[a] + 1;
+      } else {
+        w.nh[r] = w.ch[a]; w.nph[r] = w.cph[a]; w.nl[r] = w.cl[a]; w.nn[r] = w.cn[a];
+      }
+      w.nf[r] = w.spflag[s];
+      w.ntrel[r] = pack_trel(w.spsrc[s], w.sptok[s]);
+    }
+  }
+  // threshold on exact scores (winners are in exact rank order): drop a tail
+  // whose exact score falls below best_exact - beam_threshold
+  __syncwarp();
+  if (Hn > 0 && !P.threshold_inf) {
+    const double bex = w.ns[0];
+    int keepn = 0;
+    for (int r0 = 0; r0 < Hn; r0 += 32) {
+      const int r = r0 + lane;
+      const bool ok = r < Hn && w.ns[r] >= bex - P.beam_threshold && w.ns[r] > -INFINITY;
+      keepn += __popc(__ballot_sync(FULL, ok));
+    }
+    Hn = keepn;
   }
   // reset the token -> S rank map for the next frame
   for (int j = lane; j < k; j += 32) w.pos[w.stok[j]] = 0xffff;

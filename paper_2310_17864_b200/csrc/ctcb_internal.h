@@ -111,7 +111,7 @@ struct WarpLayout {
   size_t first, dpi, pd, dp_e1, dp_e2, excl, head_j, head_sc;
   size_t skey, sval, stok, pos;
   size_t sp_sc, sp_key, sp_ord, sp_base, sp_x, sp_flag, sp_src, sp_tok;
-  size_t hist, misc, tc_h, tc_r, htk, htf, hslot;
+  size_t hist, misc, tc_h, tc_r, htk, htf, hslot, rec, rec2, hkey, lA;
   size_t total;
   int kw, sp_cap, sp_pad, ts;
 };
@@ -176,6 +176,10 @@ __host__ __device__ inline WarpLayout make_layout(int beam, int kpad, int V, int
   L.htk = take(8 * (size_t)L.ts, 8);
   L.htf = take(4 * (size_t)L.ts, 4);
   L.hslot = take(4 * (size_t)beam, 4);
+  L.rec = take(4 * (size_t)beam, 4);
+  L.rec2 = take(4 * (size_t)beam, 4);
+  L.hkey = take(4 * ((size_t)beam + 1), 4);
+  L.lA = take(8 * (size_t)beam, 8);
   L.pos = take(2 * (size_t)V, 2);
   L.total = align_up(o, 128);
   return L;
