@@ -93,6 +93,15 @@ int ctcb_decode(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t str
                 int32_t* out_tokens, int32_t* out_timesteps, int32_t* out_len, double* out_score,
                 int32_t* out_count, int32_t* out_status);
 
+/* Decode from HOST memory (the e2e path a host-side binding uses): copies the
+ * valid frames of each utterance host->device (pinned memory makes the copies
+ * asynchronous DMA), decodes, copies the results back and synchronises
+ * `stream`.  Same layouts as ctcb_decode with host pointers throughout;
+ * lens are read on the host.  Device staging is cached in the handle. */
+int ctcb_decode_host(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
+                     int batch, int t_max, void* stream, int32_t* out_tokens, int32_t* out_timesteps,
+                     int32_t* out_len, double* out_score, int32_t* out_count, int32_t* out_status);
+
 /* Debug / minimum slice: blank-skip compaction and per-frame top-k only.
  * Replaces blank_collapse (emissions.py:284-306) and the token selection of
  * _BeamSearch._step (decoder.py:431-460, :440):

@@ -20,7 +20,7 @@ UTT_OK, UTT_EMPTY, UTT_BAD_LEN, UTT_BEAM_DIED = 0, 1, 2, 3
 # every symbol include/ctcb.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
     "ctcb_create", "ctcb_destroy", "ctcb_skip_cutoff", "ctcb_topk_size", "ctcb_workspace_bytes",
-    "ctcb_decode", "ctcb_debug_frames", "ctcb_validate", "ctcb_debug_counters", "ctcb_status_string",
+    "ctcb_decode", "ctcb_decode_host", "ctcb_debug_frames", "ctcb_validate", "ctcb_debug_counters", "ctcb_status_string",
     "ctcb_last_error",
 )
 
@@ -60,6 +60,7 @@ def load():
     lib.ctcb_workspace_bytes.argtypes = [vp, c_int, c_int, ctypes.POINTER(c_size_t)]
     lib.ctcb_decode.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, c_size_t, vp,
                                 vp, vp, vp, vp, vp, vp]
+    lib.ctcb_decode_host.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp]
     lib.ctcb_debug_frames.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp]
     lib.ctcb_validate.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, c_int, vp, vp]
     lib.ctcb_debug_counters.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]

@@ -37,6 +37,9 @@ struct ctcb_handle {
   unsigned long long* dbg;  // device [8] debug counters
   void* ws;
   size_t ws_bytes;
+  // ctcb_decode_host staging (device): input, lens, outputs
+  void* hbuf;
+  size_t hbuf_bytes;
 };
 
 namespace {
@@ -250,6 +253,8 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   h->ws = nullptr;
   h->ws_bytes = 0;
   h->dbg = nullptr;
+  h->hbuf = nullptr;
+  h->hbuf_bytes = 0;
   {
     const char* fg = getenv("CTCB_FORCE_GENERIC");
     h->force_generic = (fg && fg[0] == '1') ? 1 : 0;
@@ -268,6 +273,7 @@ int ctcb_destroy(ctcb_t* h) {
   if (!h) return CTCB_OK;
   if (h->ws) cudaFree(h->ws);
   if (h->dbg) cudaFree(h->dbg);
+  if (h->hbuf) cudaFree(h->hbuf);
   delete h;
   return CTCB_OK;
 }
@@ -344,6 +350,64 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   else
     ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
   CTCB_CUDA(cudaGetLastError());
+  return CTCB_OK;
+}
+
+int ctcb_decode_host(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
+                     void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len, double* out_score,
+                     int32_t* out_count, int32_t* out_status) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  if (!lp || !lens || !out_tokens || !out_len || !out_score || !out_count || !out_status)
+    return fail(CTCB_ERR_ARG, "host pointers must not be NULL (out_timesteps may be)");
+  if (B <= 0) return CTCB_OK;
+  if (T < 0) return fail(CTCB_ERR_ARG, "t_max must be >= 0");
+  if (st < h->V || sb < (int64_t)st * (T > 0 ? T : 1))
+    return fail(CTCB_ERR_ARG, "strides must describe a [batch, t_max, vocab] layout with unit vocab stride");
+  CTCB_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int Tp = T > 0 ? T : 1;
+  const size_t V = (size_t)h->V, nb = (size_t)h->nbest;
+  // device staging: dense [B, T, V] input (valid frames only are copied), lens, outputs
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = ctcb::align_up(o, 256); o = r + bytes; return r; };
+  const size_t o_in = take((size_t)B * Tp * V * 4), o_lens = take((size_t)B * 4),
+               o_tok = take((size_t)B * nb * Tp * 4), o_ts = take(out_ts ? (size_t)B * nb * Tp * 4 : 0),
+               o_len = take((size_t)B * nb * 4), o_sc = take((size_t)B * nb * 8), o_cnt = take((size_t)B * 4),
+               o_st = take((size_t)B * 4);
+  if (h->hbuf_bytes < o) {
+    if (h->hbuf) cudaFree(h->hbuf);
+    h->hbuf = nullptr;
+    h->hbuf_bytes = 0;
+    CTCB_CUDA(cudaMalloc(&h->hbuf, o));
+    h->hbuf_bytes = o;
+  }
+  char* d = (char*)h->hbuf;
+  float* din = (float*)(d + o_in);
+  // H2D: each utterance's valid frames (a dense [len, V] block when stride_t == V)
+  for (int b = 0; b < B; b++) {
+    int n = lens[b];
+    if (n <= 0) continue;
+    if (n > T) n = T;
+    const float* src = lp + (size_t)b * sb;
+    float* dst = din + (size_t)b * Tp * V;
+    if (st == (int64_t)V)
+      CTCB_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * V * 4, cudaMemcpyHostToDevice, s));
+    else
+      CTCB_CUDA(cudaMemcpy2DAsync(dst, V * 4, src, (size_t)st * 4, V * 4, (size_t)n, cudaMemcpyHostToDevice, s));
+  }
+  CTCB_CUDA(cudaMemcpyAsync(d + o_lens, lens, (size_t)B * 4, cudaMemcpyHostToDevice, s));
+  int rc = ctcb_decode(h, din, (int64_t)Tp * V, (int64_t)V, (const int32_t*)(d + o_lens), B, T, nullptr, 0, stream,
+                       (int32_t*)(d + o_tok), out_ts ? (int32_t*)(d + o_ts) : nullptr, (int32_t*)(d + o_len),
+                       (double*)(d + o_sc), (int32_t*)(d + o_cnt), (int32_t*)(d + o_st));
+  if (rc) return rc;
+  // D2H of the results
+  CTCB_CUDA(cudaMemcpyAsync(out_tokens, d + o_tok, (size_t)B * nb * Tp * 4, cudaMemcpyDeviceToHost, s));
+  if (out_ts) CTCB_CUDA(cudaMemcpyAsync(out_ts, d + o_ts, (size_t)B * nb * Tp * 4, cudaMemcpyDeviceToHost, s));
+  CTCB_CUDA(cudaMemcpyAsync(out_len, d + o_len, (size_t)B * nb * 4, cudaMemcpyDeviceToHost, s));
+  CTCB_CUDA(cudaMemcpyAsync(out_score, d + o_sc, (size_t)B * nb * 8, cudaMemcpyDeviceToHost, s));
+  CTCB_CUDA(cudaMemcpyAsync(out_count, d + o_cnt, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+  CTCB_CUDA(cudaMemcpyAsync(out_status, d + o_st, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+  CTCB_CUDA(cudaStreamSynchronize(s));
   return CTCB_OK;
 }
 

@@ -139,6 +139,7 @@ class CUCTCDecoder:
         if cuda_stream is not None and not isinstance(cuda_stream, torch.cuda.Stream):
             raise TypeError("cuda_stream must be torch.cuda.Stream")
         self.vocab_list = vocab_list
+        self._vocab_np = np.array(vocab_list, dtype=object)
         self.blank_id = blank_id
         self.beam_size = beam_size
         self.nbest = nbest
@@ -177,7 +178,7 @@ class CUCTCDecoder:
         if log_prob.dtype != torch.float32:
             raise ValueError(f"log_prob must be float32, got {log_prob.dtype}")
         if not log_prob.is_cuda:
-            raise ValueError("log_prob must be a CUDA tensor")
+            raise ValueError("log_prob must be a CUDA tensor (CPU tensors: use __call__ or decode_host)")
         B, T, V = log_prob.shape
         if V != len(self.vocab_list):
             raise ValueError(f"emissions have {V} columns but the token dictionary has "
@@ -258,6 +259,55 @@ class CUCTCDecoder:
         errors for failed utterances.  Returns numpy arrays
         (tokens [B, nbest, Lmax], timesteps or None, lengths, scores, counts)."""
         status = out.status.cpu().numpy()
+        self._raise_status(status, out.tokens.shape[2])
+        counts = out.counts.cpu().numpy()
+        lengths = out.lengths.cpu().numpy()
+        scores = out.scores.cpu().numpy()
+        lmax = int(lengths.max()) if lengths.size else 0
+        tokens = out.tokens[:, :, :lmax].cpu().numpy()
+        ts = out.timesteps[:, :, :lmax].cpu().numpy() if out.timesteps is not None else None
+        return tokens, ts, lengths, scores, counts
+
+    def decode_host(self, log_prob: torch.Tensor, encoder_out_lens, timesteps: bool = False):
+        """Host-buffer path through ``ctcb_decode_host``: ``log_prob`` a CPU
+        float32 [B, T, V] tensor (pin it for asynchronous DMA); only each
+        utterance's valid frames cross PCIe.  Returns numpy (tokens, timesteps
+        or None, lengths, scores, counts) like :meth:`to_host`."""
+        if not isinstance(log_prob, torch.Tensor) or log_prob.dim() != 3 or log_prob.is_cuda:
+            raise ValueError("decode_host expects a 3-D CPU tensor [batch, frames, tokens]")
+        if log_prob.dtype != torch.float32:
+            raise ValueError(f"log_prob must be float32, got {log_prob.dtype}")
+        B, T, V = log_prob.shape
+        if V != len(self.vocab_list):
+            raise ValueError(f"emissions have {V} columns but the token dictionary has "
+                             f"{len(self.vocab_list)} tokens")
+        if log_prob.stride(2) != 1:
+            log_prob = log_prob.contiguous()
+        lens = np.ascontiguousarray(np.asarray(encoder_out_lens.cpu() if isinstance(encoder_out_lens, torch.Tensor)
+                                               else encoder_out_lens, dtype=np.int32))
+        if lens.shape != (B,):
+            raise ValueError("encoder_out_lens must be a 1-D tensor with one length per utterance")
+        st = log_prob.stride(1) if T > 1 else V
+        sb = log_prob.stride(0) if B > 1 else st * max(T, 1)
+        nb, Tp = self.nbest, max(T, 1)
+        tok = np.empty((B, nb, Tp), dtype=np.int32)
+        ts = np.empty((B, nb, Tp), dtype=np.int32) if timesteps else None
+        ln = np.zeros((B, nb), dtype=np.int32)
+        sc = np.zeros((B, nb), dtype=np.float64)
+        cnt = np.zeros(B, dtype=np.int32)
+        status = np.full(B, -1, dtype=np.int32)
+        vp = ctypes.c_void_p
+        lib = _lib.load()
+        _lib.check(lib.ctcb_decode_host(self._h, vp(log_prob.data_ptr()), sb, st, vp(lens.ctypes.data), B, T,
+                                        self._stream(), vp(tok.ctypes.data), vp(ts.ctypes.data) if ts is not None else None,
+                                        vp(ln.ctypes.data), vp(sc.ctypes.data), vp(cnt.ctypes.data),
+                                        vp(status.ctypes.data)), "ctcb_decode_host")
+        self._raise_status(status, T)
+        lmax = int(ln.max()) if ln.size else 0
+        return tok[:, :, :lmax], (ts[:, :, :lmax] if ts is not None else None), ln, sc, cnt
+
+    @staticmethod
+    def _raise_status(status: np.ndarray, T: int) -> None:
         if (status < 0).any():
             raise _lib.CtcbError(f"ctcb_decode left {(status < 0).sum()} utterance(s) unprocessed (kernel did not run)")
         bad = np.flatnonzero(status != _lib.UTT_OK)
@@ -267,29 +317,31 @@ class CUCTCDecoder:
                 raise ValueError(f"utterance {b}: empty emissions")
             if status[b] == _lib.UTT_BEAM_DIED:
                 raise ValueError(f"utterance {b}: beam died: no extension survives")
-            raise ValueError(f"utterance {b}: length out of range [1, {out.tokens.shape[2]}]")
-        counts = out.counts.cpu().numpy()
-        lengths = out.lengths.cpu().numpy()
-        scores = out.scores.cpu().numpy()
-        lmax = int(lengths.max()) if lengths.size else 0
-        tokens = out.tokens[:, :, :lmax].cpu().numpy()
-        ts = out.timesteps[:, :, :lmax].cpu().numpy() if out.timesteps is not None else None
-        return tokens, ts, lengths, scores, counts
+            raise ValueError(f"utterance {b}: length out of range [1, {T}]")
 
     def __call__(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor) -> List[List[CUCTCHypothesis]]:
-        """Decode a batch: ``log_prob`` CUDA float32 [B, T, V] (log-softmax
-        output), ``encoder_out_lens`` [B] valid frames per utterance.  Returns
-        the sorted n-best per utterance (fewer than ``nbest`` when fewer
-        distinct prefixes survive, decoder.py:801)."""
-        out = self.decode(log_prob, encoder_out_lens)
-        tokens, _, lengths, scores, counts = self.to_host(out)
-        vocab = self.vocab_list
+        """Decode a batch: ``log_prob`` float32 [B, T, V] (log-softmax output),
+        ``encoder_out_lens`` [B] valid frames per utterance.  CUDA tensors are
+        decoded in place (TorchAudio's contract); CPU tensors go through the
+        host-buffer path (``ctcb_decode_host``).  Returns the sorted n-best per
+        utterance (fewer than ``nbest`` when fewer distinct prefixes survive,
+        decoder.py:801)."""
+        if isinstance(log_prob, torch.Tensor) and not log_prob.is_cuda:
+            tokens, _, lengths, scores, counts = self.decode_host(log_prob, encoder_out_lens)
+        else:
+            out = self.decode(log_prob, encoder_out_lens)
+            tokens, _, lengths, scores, counts = self.to_host(out)
+        return self._hypotheses(tokens, lengths, scores, counts)
+
+    def _hypotheses(self, tokens, lengths, scores, counts) -> List[List[CUCTCHypothesis]]:
+        # one tolist() per hypothesis; words through an object-array gather
+        vocab = self._vocab_np
         result = []
         for b in range(tokens.shape[0]):
             hyps = []
             for j in range(int(counts[b])):
-                t = tokens[b, j, : lengths[b, j]].tolist()
-                hyps.append(CUCTCHypothesis(tokens=t, words=[vocab[i] for i in t], score=float(scores[b, j])))
+                t = tokens[b, j, : lengths[b, j]]
+                hyps.append(CUCTCHypothesis(tokens=t.tolist(), words=vocab[t].tolist(), score=float(scores[b, j])))
             result.append(hyps)
         return result
 

@@ -300,3 +300,17 @@ def test_fused_and_precomputed_topk_modes_agree(monkeypatch):
     monkeypatch.setenv("CTCB_TOPK_MODE", "fused")
     fus = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
     assert pre == fus
+
+
+def test_host_buffer_path_matches_device_path():
+    """ctcb_decode_host (CPU tensors, valid frames copied) == device path."""
+    cfg = synth.CONFIGS[1]
+    lp, lens = synth.batch(cfg, indices=range(12))
+    dec = cuda_ctc_decoder(vocab(cfg.vocab), nbest=3, beam_size=10, blank_skip_threshold=cfg.threshold)
+    dev = dec(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+    host = dec(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens))
+    assert dev == host
+    lens2 = lens.copy()
+    lens2[3] = 0
+    with pytest.raises(ValueError, match="utterance 3: empty emissions"):
+        dec(torch.from_numpy(lp), torch.from_numpy(lens2))
