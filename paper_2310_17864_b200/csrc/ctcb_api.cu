@@ -40,6 +40,9 @@ struct ctcb_handle {
   // ctcb_decode_host staging (device): input, lens, outputs
   void* hbuf;
   size_t hbuf_bytes;
+  cudaStream_t cstreams[4];  // H2D copy streams of ctcb_decode_host (lazy)
+  cudaEvent_t cev[5];
+  int have_cstreams;
 };
 
 namespace {
@@ -255,6 +258,7 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   h->dbg = nullptr;
   h->hbuf = nullptr;
   h->hbuf_bytes = 0;
+  h->have_cstreams = 0;
   {
     const char* fg = getenv("CTCB_FORCE_GENERIC");
     h->force_generic = (fg && fg[0] == '1') ? 1 : 0;
@@ -274,6 +278,10 @@ int ctcb_destroy(ctcb_t* h) {
   if (h->ws) cudaFree(h->ws);
   if (h->dbg) cudaFree(h->dbg);
   if (h->hbuf) cudaFree(h->hbuf);
+  if (h->have_cstreams) {
+    for (int i = 0; i < 4; i++) cudaStreamDestroy(h->cstreams[i]);
+    for (int i = 0; i < 5; i++) cudaEventDestroy(h->cev[i]);
+  }
   delete h;
   return CTCB_OK;
 }
@@ -383,17 +391,31 @@ int ctcb_decode_host(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const i
   }
   char* d = (char*)h->hbuf;
   float* din = (float*)(d + o_in);
-  // H2D: each utterance's valid frames (a dense [len, V] block when stride_t == V)
+  // H2D: each utterance's valid frames (a dense [len, V] block when
+  // stride_t == V), spread over four copy streams ordered after `stream`'s
+  // prior work and joined back before the decode
+  if (!h->have_cstreams) {
+    for (int i = 0; i < 4; i++) CTCB_CUDA(cudaStreamCreateWithFlags(&h->cstreams[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 5; i++) CTCB_CUDA(cudaEventCreateWithFlags(&h->cev[i], cudaEventDisableTiming));
+    h->have_cstreams = 1;
+  }
+  CTCB_CUDA(cudaEventRecord(h->cev[4], s));
+  for (int i = 0; i < 4; i++) CTCB_CUDA(cudaStreamWaitEvent(h->cstreams[i], h->cev[4], 0));
   for (int b = 0; b < B; b++) {
     int n = lens[b];
     if (n <= 0) continue;
     if (n > T) n = T;
     const float* src = lp + (size_t)b * sb;
     float* dst = din + (size_t)b * Tp * V;
+    cudaStream_t cs = h->cstreams[b & 3];
     if (st == (int64_t)V)
-      CTCB_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * V * 4, cudaMemcpyHostToDevice, s));
+      CTCB_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * V * 4, cudaMemcpyHostToDevice, cs));
     else
-      CTCB_CUDA(cudaMemcpy2DAsync(dst, V * 4, src, (size_t)st * 4, V * 4, (size_t)n, cudaMemcpyHostToDevice, s));
+      CTCB_CUDA(cudaMemcpy2DAsync(dst, V * 4, src, (size_t)st * 4, V * 4, (size_t)n, cudaMemcpyHostToDevice, cs));
+  }
+  for (int i = 0; i < 4; i++) {
+    CTCB_CUDA(cudaEventRecord(h->cev[i], h->cstreams[i]));
+    CTCB_CUDA(cudaStreamWaitEvent(s, h->cev[i], 0));
   }
   CTCB_CUDA(cudaMemcpyAsync(d + o_lens, lens, (size_t)B * 4, cudaMemcpyHostToDevice, s));
   int rc = ctcb_decode(h, din, (int64_t)Tp * V, (int64_t)V, (const int32_t*)(d + o_lens), B, T, nullptr, 0, stream,
