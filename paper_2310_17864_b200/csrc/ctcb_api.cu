@@ -14,6 +14,7 @@
 namespace ctcb {
 __global__ void ctcb_decode_generic_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_decode_fast_pre_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_framemap_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_topk_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter);
@@ -151,7 +152,9 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.n_chunks = (T + ctcb::kChunk - 1) / ctcb::kChunk;
   P.topk_tok = (int32_t*)(base + L.topk_tok);
   P.topk_val = (float*)(base + L.topk_val);
-  P.row_bytes = (int)ctcb::align_up((size_t)h->V * 4, 16);
+  // rows of V <= 512 are padded to 512 floats: the fast top-k reads 4 float4
+  // chunks per lane without bounds checks (padding holds the sentinel)
+  P.row_bytes = (int)ctcb::align_up((size_t)(h->V <= 512 ? 512 : h->V) * 4, 16);
   P.ring = ring_for(P.row_bytes);
   P.bulk_ok = ((uintptr_t)lp % 16 == 0) && ((h->V * 4) % 16 == 0) && ((st * 4) % 16 == 0) && ((sb * 4) % 16 == 0);
   return CTCB_OK;
@@ -333,6 +336,9 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   size_t smem = (size_t)P.smem_per_warp * P.warps_per_block;
   const void* kfn = fast ? (const void*)ctcb::ctcb_decode_fast_kernel : (const void*)ctcb::ctcb_decode_generic_kernel;
   CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (fast)
+    CTCB_CUDA(cudaFuncSetAttribute((const void*)ctcb::ctcb_decode_fast_pre_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
   CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, 32 * P.warps_per_block, smem));
   if (blocks_per_sm < 1) blocks_per_sm = 1;
@@ -345,7 +351,7 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
     ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
     CTCB_CUDA(cudaGetLastError());
     ctcb::Params Q = P;
-    Q.smem_per_warp = (int)ctcb::align_up((size_t)P.row_bytes + 64 * 8 + 256 * 4, 128);
+    Q.smem_per_warp = (int)ctcb::align_up((size_t)P.row_bytes + 64 * 8 + 256 * 4 + 64 * 4 + 64 * 2, 128);
     const size_t tsmem = (size_t)Q.smem_per_warp * 8;
     CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
     int tbps = 0;
@@ -353,7 +359,9 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
     ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 256, tsmem, s>>>(Q);
     CTCB_CUDA(cudaGetLastError());
   }
-  if (fast)
+  if (fast && P.precomp)
+    ctcb::ctcb_decode_fast_pre_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
+  else if (fast)
     ctcb::ctcb_decode_fast_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
   else
     ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);

@@ -110,6 +110,9 @@ struct FastSmem {
   int* dlane;
   double* dA;
   uint32_t* dgv;
+  long long* wp;
+  uint32_t* ckey;
+  uint16_t* cidx;
 };
 
 // Token sequence of current entry `e` (length len) through the global trellis.
@@ -284,15 +287,13 @@ __device__ __forceinline__ int frame_map_warp(const Params& P, const float* ubas
   return kept;
 }
 
-// Top-k of one staged row (blank and padding hold kSentinel): threshold = k-th
-// largest lane maximum (>= k elements reach it), compaction of the <= 64
-// elements above it, register bitonic sort of (log-prob desc, index asc)
-// keys.  Returns this lane's key of S (lanes < k).
+// Top-k of one staged row (blank and padding hold kSentinel), general path:
+// threshold = k-th largest lane maximum (>= k elements reach it),
+// compaction of the <= 64 elements above it, register bitonic sort of
+// (log-prob desc, index asc) 64-bit keys; > 64 survivors take the radix
+// select.  Returns this lane's key of S (lanes < k).
 __device__ __forceinline__ uint64_t topk_key(const FastSmem& S, const float* row, int V, int k, int lane, bool small_v,
                                              int nch4, unsigned long long* dbg) {
-  // threshold = k-th largest lane maximum (>= k elements reach it);
-  // compaction of the <= 64 elements above it; register bitonic sort of
-  // (log-prob desc, index asc) keys.
   const float4* row4 = (const float4*)row;
   float lmax = __uint_as_float(kSentinel);
   for (int c = lane; c < nch4; c += 32) {
@@ -356,11 +357,136 @@ __device__ __forceinline__ uint64_t topk_key(const FastSmem& S, const float* row
   }
   return skey;
 }
+__device__ __forceinline__ int skey_tok(uint64_t skey) { return (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu)); }
+
+// Sort a bitonic sequence of 32-bit keys descending.
+__device__ __forceinline__ uint32_t merge_desc32(uint32_t x, int lane) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    uint32_t y = __shfl_xor_sync(FULL, x, j);
+    x = ((lane & j) == 0) ? max(x, y) : min(x, y);
+  }
+  return x;
+}
+
+// Top-k of one staged row for V <= 512 (<= 4 float4 chunks per lane) and
+// k <= 31, with 32-bit sort keys.  The chunks stay in registers between the
+// lane-maximum pass and the predicate pass; survivors (>= threshold) are
+// compacted in token-index order (per-chunk counts packed into one scan), so a
+// survivor's slot q orders ties by index.  Sort key = (order key with its low
+// 6 bits cleared) | (63 - q): value desc, then index asc, exact unless two
+// values collide after truncation; adjacent collisions in the top k+1 take the
+// exact 64-bit path (~1-2 % of rows).  Returns the token of rank `lane`
+// (lanes < k).
+__device__ __forceinline__ int topk_small(const FastSmem& S, const float* row, int V, int k, int lane, int nch4,
+                                          unsigned long long* dbg) {
+  const float4* row4 = (const float4*)row;
+  const float sent = __uint_as_float(kSentinel);
+  float4 q[4];
+  float lmax = sent;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    q[j] = row4[lane + 32 * j];  // rows are padded to 512 floats
+    lmax = fmaxf(lmax, fmaxf(fmaxf(q[j].x, q[j].y), fmaxf(q[j].z, q[j].w)));
+  }
+  const uint32_t t0 = __shfl_sync(FULL, sort_desc32(isnan(lmax) ? 0u : okey(lmax), lane), k - 1);
+  const float tf = t0 == 0u ? -INFINITY : unord32(t0);
+  uint32_t pm = 0u, packed = 0u;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const uint32_t nib = (uint32_t)(q[j].x >= tf) | ((uint32_t)(q[j].y >= tf) << 1) |
+                         ((uint32_t)(q[j].z >= tf) << 2) | ((uint32_t)(q[j].w >= tf) << 3);
+    pm |= nib << (4 * j);
+    packed |= (uint32_t)__popc(nib) << (8 * j);
+  }
+  const int cnt = __reduce_add_sync(FULL, __popc(pm));
+  if (cnt > 64) {
+    if (lane == 0 && dbg) atomicAdd(&dbg[kDbgRadix], 1ull);
+    const uint64_t sk = topk_radix(S, row, V, k, lane);
+    return skey_tok(sk);
+  }
+  // per-chunk exclusive offsets: chunk j of lane l starts after all survivors
+  // of chunks < j (every lane) and of chunk j in lanes < l
+  uint32_t incl = packed;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t tot = __shfl_sync(FULL, incl, 31);
+  uint32_t offs = tot * 0x01010100u + (incl - packed);
+  uint32_t* ckey = S.ckey;
+  uint16_t* cidx = S.cidx;
+  while (pm) {
+    const int bt = __ffs(pm) - 1;
+    pm &= pm - 1u;
+    const int sh = 8 * (bt >> 2);
+    const uint32_t off = (offs >> sh) & 0xffu;
+    offs += 1u << sh;
+    const int e = 4 * (lane + 32 * (bt >> 2)) + (bt & 3);
+    ckey[off] = (okey(row[e]) & ~63u) | (63u - off);
+    cidx[off] = (uint16_t)e;
+  }
+  __syncwarp();
+  uint32_t a = lane < cnt ? ckey[lane] : 0u;
+  a = sort_desc32(a, lane);
+  if (cnt > 32) {
+    uint32_t b = lane + 32 < cnt ? ckey[lane + 32] : 0u;
+    b = sort_desc32(b, lane);
+    a = max(a, __shfl_sync(FULL, b, 31 - lane));
+    a = merge_desc32(a, lane);
+  }
+  // exactness: keys that differ after truncation are ordered exactly
+  const uint32_t an = __shfl_down_sync(FULL, a, 1);
+  const bool bad = lane < k && a != 0u && (a >> 6) == (an >> 6);
+  int tok;
+  if (__any_sync(FULL, bad)) {
+    if (lane == 0 && dbg) atomicAdd(&dbg[kDbgTopkFix], 1ull);
+    const int ia = lane < cnt ? cidx[lane] : 0, ib = lane + 32 < cnt ? cidx[lane + 32] : 0;
+    uint64_t x = lane < cnt ? (((uint64_t)okey(row[ia]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)ia)) : 0ull;
+    x = sort_desc64(x, lane);
+    if (cnt > 32) {
+      uint64_t y = lane + 32 < cnt ? (((uint64_t)okey(row[ib]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)ib)) : 0ull;
+      y = sort_desc64(y, lane);
+      const uint64_t yr = shfl64(y, 31 - lane);
+      x = x > yr ? x : yr;
+      x = merge_desc64(x, lane);
+    }
+    tok = skey_tok(x);
+  } else {
+    tok = cidx[63u - (a & 63u)];
+  }
+  __syncwarp();
+  return tok;
+}
 
 #ifndef CTCB_FAST_MIN_BLOCKS
 #define CTCB_FAST_MIN_BLOCKS 4
 #endif
-__global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_kernel(const __grid_constant__ Params P) {
+
+// Rank keys are 32-bit fixed point: key(x) ~ (x - (best - R)) * 2^32 / R,
+// R = beam_threshold (2^20 when infinite); 0 = dropped (-inf), 1 = at or below
+// the floor.  Append keys are the clamped sum of a per-list term floor((A -
+// base) * 2^32/R) and a per-position term floor(v * 2^32/R) (64-bit integer
+// add instead of fp64 per candidate), so a key can be off by up to 2 units:
+// heads within kTol of the maximum are resolved exactly (fp64 fold, then
+// token-sequence order), as are keys within kTol of the floor (the exact
+// threshold test, decoder.py:621-623).
+constexpr uint32_t kTol = 3u;
+
+__device__ __forceinline__ uint32_t f2u_sat(double z) {
+  uint32_t r;
+  asm("cvt.rzi.u32.f64 %0, %1;" : "=r"(r) : "d"(z));  // saturating: < 0 -> 0, >= 2^32 -> 2^32 - 1
+  return r;
+}
+__device__ __forceinline__ long long f2ll_floor(double z) {
+  long long r;
+  asm("cvt.rmi.s64.f64 %0, %1;" : "=l"(r) : "d"(z));  // saturating; -inf -> INT64_MIN
+  return r;
+}
+
+template <bool PRE>
+__device__ __forceinline__ void fast_decode(const Params& P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int me = lane & 15;
@@ -383,28 +509,35 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
   S.posmap = wbase + L.posmap;
   S.tc_h = (uint64_t*)(wbase + L.tc_h);
   S.tc_r = (int*)(wbase + L.tc_r);
-  S.gkey = (uint32_t*)(wbase + L.gkey);
   S.hsc = (double*)(wbase + L.hsc);
   S.hp2 = (int*)(wbase + L.hp2);
   S.dlane = (int*)(wbase + L.dlane);
   S.dA = (double*)(wbase + L.dA);
   S.dgv = (uint32_t*)(wbase + L.dgv);
+  S.wp = (long long*)(wbase + L.wp);
+  S.ckey = (uint32_t*)(wbase + L.ckey);
+  S.cidx = (uint16_t*)(wbase + L.cidx);
   for (int i = lane; i < 2 * kTieCache; i += 32) S.tc_h[i] = 0ull;
   for (int i = lane; i <= kTieCache; i += 32) S.tc_r[i] = 0;
 
-  const int V = P.V, k = P.k, beam = P.beam;
+  const int V = P.V, k = P.k, beam = P.beam, ring = P.ring;
   const int nch4 = (V + 3) >> 2;
-  const bool small_v = nch4 <= 256;  // <= 8 float4 chunks per lane: predicate bits fit one register
+  const bool small_v = nch4 <= 256;               // general path: predicate bits fit one register
+  const bool tiny_v = nch4 <= 128 && k <= 31;     // topk_small: <= 4 chunks per lane
   const uint32_t fullk = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
   const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
-  const double kScale = 4294967294.0 / kR;
+  const double kScale = 4294967296.0 / kR;
 
   if (lane == 0)
-    for (int s = 0; s < P.ring; s++) mbar_init(&S.mbar[s], 1);
+    for (int s = 0; s < ring; s++) mbar_init(&S.mbar[s], 1);
   for (int c = lane; c < V; c += 32) S.posmap[c] = 0xff;
+  // padding beyond V is never written by the row copies: sentinel it once
+  for (int s = 0; s < ring; s++)
+    for (int c = V + lane; c < P.row_bytes / 4; c += 32) ((uint32_t*)(S.rows + (size_t)s * P.row_bytes))[c] = kSentinel;
   fence_mbar_init();
   __syncwarp();
-  uint32_t n_issue = 0, n_cons = 0;
+  int slot_i = 0, slot_c = 0;     // ring slots of the next issue / consume
+  uint32_t par_c = 0u;            // mbarrier phase parity of the consume slot
   const uint32_t row_copy = (uint32_t)V * 4u;
 
   for (;;) {
@@ -428,7 +561,7 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
     // -- A. blank-skip compaction (emissions.py:298-306); in precomputed-top-k
     //    mode ctcb_framemap_kernel already did it
     int kept = 0;
-    if (P.precomp) {
+    if (PRE) {
       kept = P.kept[u];
     } else {
       kept = frame_map_warp(P, ubase, len_u, fmap, lane);
@@ -439,24 +572,33 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
     const size_t tk_base = (size_t)u * P.T_max * k;
     int pre_st = 0;
     float pre_sv = 0.0f;
-    if (P.precomp && kept > 0 && lane < k) {
+    if (PRE && kept > 0 && lane < k) {
       pre_st = P.topk_tok[tk_base + lane];
       pre_sv = P.topk_val[tk_base + lane];
     }
 
-    auto issue = [&](int i) {
-      uint32_t slot = n_issue % (uint32_t)P.ring;
-      if (lane == 0) {
-        const float* src = ubase + (size_t)fmap[i] * P.stride_t;
-        fence_proxy_async();
-        mbar_arrive_expect_tx(&S.mbar[slot], row_copy);
-        tma_bulk_g2s(S.rows + (size_t)slot * P.row_bytes, src, row_copy, &S.mbar[slot]);
+    // row staging: lane 0 issues the bulk copy of kept frame `idx`; frame-map
+    // entries are read 32 at a time into registers
+    int fm_blk = -1, fm_reg = 0;
+    auto issue = [&](int idx) {
+      if ((idx >> 5) != fm_blk) {
+        fm_blk = idx >> 5;
+        const int t = (fm_blk << 5) + lane;
+        fm_reg = t < kept ? fmap[t] : 0;
       }
-      n_issue++;
+      const int fr = __shfl_sync(FULL, fm_reg, idx & 31);
+      if (lane == 0) {
+        const float* src = ubase + (size_t)fr * P.stride_t;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&S.mbar[slot_i], row_copy);
+        tma_bulk_g2s(S.rows + (size_t)slot_i * P.row_bytes, src, row_copy, &S.mbar[slot_i]);
+      }
+      slot_i = slot_i + 1 == ring ? 0 : slot_i + 1;
     };
+    int n_out = 0;  // issued, not yet consumed
     if (P.bulk_ok) {
-      const int pre = kept < P.ring - 1 ? kept : P.ring - 1;
-      for (int i = 0; i < pre; i++) issue(i);
+      const int pre = kept < ring - 1 ? kept : ring - 1;
+      for (int i = 0; i < pre; i++) { issue(i); n_out++; }
     }
 
     // beam state (decoder.py:358-370): the empty prefix, blank flag set, score 0
@@ -469,11 +611,12 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
     for (int i = 0; i < kept; i++) {
       float* row;
       if (P.bulk_ok) {
-        if (i + P.ring - 1 < kept) issue(i + P.ring - 1);
-        uint32_t slot = n_cons % (uint32_t)P.ring;
-        mbar_wait(&S.mbar[slot], (n_cons / (uint32_t)P.ring) & 1u);
-        n_cons++;
-        row = (float*)(S.rows + (size_t)slot * P.row_bytes);
+        if (i + ring - 1 < kept) { issue(i + ring - 1); n_out++; }
+        mbar_wait(&S.mbar[slot_c], par_c);
+        row = (float*)(S.rows + (size_t)slot_c * P.row_bytes);
+        n_out--;
+        slot_c++;
+        if (slot_c == ring) { slot_c = 0; par_c ^= 1u; }
       } else {
         row = (float*)S.rows;
         const float* src = ubase + (size_t)fmap[i] * P.stride_t;
@@ -482,21 +625,33 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       }
       const double eb = (double)row[P.blank];
       __syncwarp();
-      if (lane == 0 && !P.precomp) {
-        ((uint32_t*)row)[P.blank] = kSentinel;
-        for (int c = V; c < 4 * nch4; c++) ((uint32_t*)row)[c] = kSentinel;
+      if (!PRE) {
+        if (lane == 0) ((uint32_t*)row)[P.blank] = kSentinel;
+        __syncwarp();
       }
-      __syncwarp();
 
       // ================= top-k (k <= 32) =================
-      uint64_t skey = 0ull;
-      if (!P.precomp) skey = topk_key(S, row, V, k, lane, small_v, nch4, P.dbg);
-      const int st = P.precomp ? pre_st : (lane < k ? (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu)) : 0);
-      const float sv = P.precomp ? pre_sv : (lane < k ? row[st] : 0.0f);
-      if (lane < k) { S.sval[lane] = sv; S.stok[lane] = st; S.posmap[st] = (uint8_t)lane; }
-      if (P.precomp && i + 1 < kept && lane < k) {
-        pre_st = P.topk_tok[tk_base + (size_t)(i + 1) * k + lane];
-        pre_sv = P.topk_val[tk_base + (size_t)(i + 1) * k + lane];
+      int st;
+      float sv;
+      if (PRE) {
+        st = pre_st;
+        sv = pre_sv;
+        if (i + 1 < kept && lane < k) {
+          pre_st = P.topk_tok[tk_base + (size_t)(i + 1) * k + lane];
+          pre_sv = P.topk_val[tk_base + (size_t)(i + 1) * k + lane];
+        }
+      } else {
+        if (tiny_v) st = topk_small(S, row, V, k, lane, nch4, P.dbg);
+        else st = skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, P.dbg));
+        st = lane < k ? st : 0;
+        sv = lane < k ? row[st] : 0.0f;
+      }
+      // per-position key term: floor(v_p * 2^32 / R) (64-bit)
+      if (lane < k) {
+        S.sval[lane] = sv;
+        S.stok[lane] = st;
+        S.posmap[st] = (uint8_t)lane;
+        S.wp[lane] = f2ll_floor((double)sv * kScale);
       }
       __syncwarp();
 
@@ -574,6 +729,7 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
         double t = q1; q1 = q2; q2 = t; int x = k1; k1 = k2; k2 = x;
         if (q1 > q0) { t = q0; q0 = q1; q1 = t; x = k0; k0 = k1; k1 = x; }
       }
+      const int kpack = k0 | (k1 << 2) | (k2 << 4);
 
       // ================= append lists (lanes 16..16+nD) =================
       // first lanes publish (lane, A, valid positions) at their distinct index
@@ -589,9 +745,10 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       const int gsrc = gen ? S.dlane[me] : lane;
       const double gA = gen ? S.dA[me] : 0.0;
       uint32_t gv = gen ? S.dgv[me] : 0u;
+      const int gf = gv ? __ffs(gv) - 1 : 0;  // first valid position of the list
 
       // frame best (approximate append scores A + v; exact on key ties)
-      const double hsc0 = lane < 16 ? q0 : (gv ? gA + (double)S.sval[__ffs(gv) - 1] : -INFINITY);
+      const double hsc0 = lane < 16 ? q0 : (gv ? gA + (double)S.sval[gf] : -INFINITY);
       const uint64_t ok64 = hsc0 > -INFINITY ? ord64(hsc0) : 0ull;
       const uint32_t mhi = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32));
       const uint32_t mlo = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32) == mhi ? (uint32_t)ok64 : 0u);
@@ -600,72 +757,80 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       const double best = unord64(bk);
       // keep iff score >= best - beam_threshold and score > -inf (decoder.py:621-623)
       const double lo_thr = P.threshold_inf ? -DBL_MAX : best - P.beam_threshold;
-      const double koff = -(best - kR) * kScale;
-      // 32-bit fixed-point rank key: 0 = dropped, order-preserving above the cut
-      // (truncation via the 2^52 magic add: the low word of z + 2^52 rounded
-      // toward zero is floor(z) for 0 <= z < 2^32, no F2I conversion needed)
+      const double kbase = best - kR;
       auto keyof = [&](double sc) -> uint32_t {
-        const double z = fmin(fmax(fma(sc, kScale, koff), 0.0), 4294967294.0);
-        const uint32_t t = (uint32_t)__double_as_longlong(__dadd_rz(z, 4503599627370496.0));
-        return sc >= lo_thr ? 1u + t : 0u;
+        if (!(sc > -INFINITY)) return 0u;
+        const uint32_t t = f2u_sat((sc - kbase) * kScale);
+        return t > 1u ? t : 1u;
       };
+      // list keys: 64-bit fixed point (A - base) + v, both floored, clamped to
+      // [1, 2^32 - 1] for a live list (A > -inf), 0 otherwise
+      const long long gG = gv ? f2ll_floor((gA - kbase) * kScale) : 0ll;
+      const uint32_t gLow = (gv && gA > -INFINITY) ? 1u : 0u;
       // rank-key queues: each lane pops its candidates in order.  Lanes < 16
       // queue their <= 3 special groups (items 0..2 = local sorted order);
       // lanes 16.. queue the next four valid positions of their append list
-      // (item = S position), refilled on demand.
-      uint32_t kq[4];
-      uint32_t items;
+      // (gq = queued positions), refilled on demand.
+      uint32_t kq0, kq1, kq2, kq3;
+      uint32_t gq = 0u;
+      int npop = 0;
       auto refill = [&]() {
-        items = 0xffffffffu;
+        uint32_t kk[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-          kq[q] = 0u;
+          kk[q] = 0u;
           if (gv) {
             const int p = __ffs(gv) - 1;
             gv &= gv - 1u;
-            kq[q] = keyof(gA + (double)S.sval[p]);
-            items = (items & ~(0xffu << (8 * q))) | ((uint32_t)p << (8 * q));
+            gq |= 1u << p;
+            const long long t = gG + S.wp[p];
+            kk[q] = t < 1ll ? gLow : (t > 0xffffffffll ? 0xffffffffu : (uint32_t)t);
           }
         }
+        kq0 = kk[0]; kq1 = kk[1]; kq2 = kk[2]; kq3 = kk[3];
       };
       if (lane < 16) {
-        kq[0] = keyof(q0); kq[1] = keyof(q1); kq[2] = keyof(q2); kq[3] = 0u;
-        items = 0xff020100u;
+        kq0 = keyof(q0); kq1 = keyof(q1); kq2 = keyof(q2); kq3 = 0u;
       } else {
         refill();
       }
-      const int kpack = k0 | (k1 << 2) | (k2 << 4);
 
       // ================= k-way merge (decoder.py:651-681) =================
       int Hn = 0;
       for (int r = 0; r < beam; r++) {
-        const uint32_t mk = __reduce_max_sync(FULL, kq[0]);
+        const uint32_t mk = __reduce_max_sync(FULL, kq0);
         if (mk == 0u) break;
-        const unsigned tied = __ballot_sync(FULL, kq[0] == mk);
-        int w = __ffs(tied) - 1;
-        if (tied & (tied - 1)) {
-          // exact resolution: fp64 score, then token sequence, then flag
+        // the unique head within kTol of the maximum wins outright (predicated
+        // pop below); several such heads, or a head near the floor, take the
+        // exact path
+        bool win = kq0 != 0u && mk - kq0 <= kTol;
+        const unsigned tied = __ballot_sync(FULL, win);
+        if ((tied & (tied - 1)) || mk <= kTol + 1u) {
+          int w = __ffs(tied) - 1;
+          // exact resolution: fp64 score, then token sequence, then flag;
+          // near the floor also the exact threshold test
           if (tied & (1u << lane)) {
-            const int it = (int)(items & 0xffu);
             double esc;
-            int eb_, ex, ef;
+            int eb_, ex, ef, pos;
             if (lane < 16) {
-              const int kind = (kpack >> (2 * it)) & 3;
-              esc = it == 0 ? q0 : (it == 1 ? q1 : q2);
+              const int kind = (kpack >> (2 * npop)) & 3;
+              esc = npop == 0 ? q0 : (npop == 1 ? q1 : q2);
               eb_ = lane;
               ex = kind == 2 ? last : -1;
               ef = kind == 0 ? 1 : 0;
+              pos = -1;
             } else {
-              esc = gA + (double)S.sval[it];  // replaced by the exact fold below
+              pos = __ffs(gq) - 1;
+              esc = 0.0;  // exact fold below
               eb_ = gsrc;
-              ex = S.stok[it];
+              ex = S.stok[pos];
               ef = 0;
             }
             S.tie_sc[lane] = esc;
             S.tie_i[lane * 4 + 0] = eb_;
             S.tie_i[lane * 4 + 1] = ex;
             S.tie_i[lane * 4 + 2] = ef;
-            S.tie_i[lane * 4 + 3] = lane < 16 ? -1 : it;
+            S.tie_i[lane * 4 + 3] = pos;
           }
           if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; S.hsc[lane] = s; S.hp2[lane] = p2; }
           __syncwarp();
@@ -693,15 +858,25 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
                                 S.tie_sc[w], S.tie_i[w * 4], S.tie_i[w * 4 + 1], S.tie_i[w * 4 + 2]))
                 w = c;
             }
+            const double wsc = S.tie_sc[w];
+            if (!(wsc > -INFINITY) || !(wsc >= lo_thr)) w = -1;  // below the threshold: the beam is complete
           }
           w = __shfl_sync(FULL, w, 0);
           __syncwarp();
+          if (w < 0) break;
+          win = lane == w;
         }
-        if (lane == w) {
-          S.rec_i[r] = lane | (int)((items & 0xffu) << 8);
-          items = (items >> 8) | 0xff000000u;
-          kq[0] = kq[1]; kq[1] = kq[2]; kq[2] = kq[3]; kq[3] = 0u;
-          if (kq[0] == 0u && gv) refill();
+        const int it = lane < 16 ? npop : __ffs(gq) - 1;
+        if (win) S.rec_i[r] = lane | (it << 8);
+        npop += (win && lane < 16) ? 1 : 0;
+        gq = (win && lane >= 16) ? (gq & (gq - 1u)) : gq;
+        kq0 = win ? kq1 : kq0;
+        kq1 = win ? kq2 : kq1;
+        kq2 = win ? kq3 : kq2;
+        kq3 = win ? 0u : kq3;
+        const bool need = win && kq0 == 0u && gv != 0u;
+        if (__any_sync(FULL, need)) {
+          if (need) refill();
         }
         Hn = r + 1;
       }
@@ -712,7 +887,7 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       // lane r builds new entry r from the winning lane's registers
       const bool nent = lane < Hn;
       const int rec = S.rec_i[nent ? lane : 0];
-      const int wl = nent ? (rec & 0xff) : lane, item = rec >> 8;
+      const int wl = nent ? (rec & 0xff) : lane, item2 = rec >> 8;
       const int wk = __shfl_sync(FULL, kpack, wl);
       const double w_q0 = __shfl_sync(FULL, q0, wl), w_q1 = __shfl_sync(FULL, q1, wl), w_q2 = __shfl_sync(FULL, q2, wl);
       const int w_src = __shfl_sync(FULL, rep_src | (single_src << 8), wl);
@@ -727,14 +902,14 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       double nsc;
       int x, src, tok, nfl;
       if (wgen) {  // append group (R+c,0): exact fold of R's entries in rank order
-        const int c = S.stok[item];
-        const double v = (double)S.sval[item];
+        const int c = S.stok[item2];
+        const double v = (double)S.sval[item2];
         nsc = b_s1 + v;
         if (b_p2 >= 0) nsc = np_logaddexp(nsc, b_s2 + v);
         x = c; src = base; tok = c; nfl = 0;
       } else {
-        const int kind = (wk >> (2 * item)) & 3;
-        nsc = item == 0 ? w_q0 : (item == 1 ? w_q1 : w_q2);
+        const int kind = (wk >> (2 * item2)) & 3;
+        nsc = item2 == 0 ? w_q0 : (item2 == 1 ? w_q1 : w_q2);
         if (kind == 0) { x = -1; src = wl; tok = -1; nfl = 1; }                  // blank group
         else if (kind == 1) { x = -1; src = w_src & 0xff; tok = w_rtok; nfl = 0; }  // repeat group
         else { x = blast; src = w_src >> 8; tok = blast; nfl = 0; }               // last-token append
@@ -767,10 +942,11 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
     }
 
     if (died) {
-      while (n_cons < n_issue) {
-        uint32_t slot = n_cons % (uint32_t)P.ring;
-        mbar_wait(&S.mbar[slot], (n_cons / (uint32_t)P.ring) & 1u);
-        n_cons++;
+      while (n_out > 0) {
+        mbar_wait(&S.mbar[slot_c], par_c);
+        n_out--;
+        slot_c++;
+        if (slot_c == ring) { slot_c = 0; par_c ^= 1u; }
       }
       for (int c = lane; c < V; c += 32) S.posmap[c] = 0xff;
       if (lane == 0) { P.status[u] = kUttBeamDied; P.out_count[u] = 0; }
@@ -790,9 +966,9 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
       // order groups: (score desc, lane asc) by register sort, then exact tie runs
       uint64_t key = isf ? ord64(gsc) : 0ull;
       int pay = lane;
-#pragma unroll
+#pragma unroll 1
       for (int size = 2; size <= 32; size <<= 1)
-#pragma unroll
+#pragma unroll 1
         for (int j = size >> 1; j > 0; j >>= 1) {
           uint64_t ky = shflx64(key, j);
           int py = __shfl_xor_sync(FULL, pay, j);
@@ -878,6 +1054,13 @@ __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_ke
   }
 }
 
+__global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_kernel(const __grid_constant__ Params P) {
+  fast_decode<false>(P);
+}
+__global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS)
+    ctcb_decode_fast_pre_kernel(const __grid_constant__ Params P) {
+  fast_decode<true>(P);
+}
 
 // Precomputed-top-k mode (small batches, where one warp per utterance leaves
 // the GPU latency-bound): frame maps first, then the top-k of every kept frame
@@ -901,9 +1084,13 @@ __global__ void __launch_bounds__(256) ctcb_topk_kernel(const __grid_constant__ 
   S.rows = wbase;
   S.cand = (uint64_t*)(wbase + P.row_bytes);
   S.hist = (uint32_t*)(wbase + P.row_bytes + 64 * 8);
+  S.ckey = (uint32_t*)(wbase + P.row_bytes + 64 * 8 + 256 * 4);
+  S.cidx = (uint16_t*)(wbase + P.row_bytes + 64 * 8 + 256 * 4 + 64 * 4);
   const int V = P.V, k = P.k, nch4 = (V + 3) >> 2;
   const bool small_v = nch4 <= 256;
+  const bool tiny_v = nch4 <= 128 && k <= 31;
   float* row = (float*)S.rows;
+  for (int c = V + lane; c < P.row_bytes / 4; c += 32) ((uint32_t*)row)[c] = kSentinel;
   const long long total = (long long)P.B * P.T_max;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + wid; g < total; g += nwarps) {
@@ -912,19 +1099,16 @@ __global__ void __launch_bounds__(256) ctcb_topk_kernel(const __grid_constant__ 
     const float* src = P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
     if (P.bulk_ok) {
       const float4* s4 = (const float4*)src;
-      for (int c = lane; c < nch4; c += 32) ((float4*)row)[c] = __ldg(s4 + c);
+      for (int c = lane; c < V / 4; c += 32) ((float4*)row)[c] = __ldg(s4 + c);
     } else {
       for (int c = lane; c < V; c += 32) row[c] = __ldg(src + c);
     }
     __syncwarp();
-    if (lane == 0) {
-      ((uint32_t*)row)[P.blank] = kSentinel;
-      for (int c = V; c < 4 * nch4; c++) ((uint32_t*)row)[c] = kSentinel;
-    }
+    if (lane == 0) ((uint32_t*)row)[P.blank] = kSentinel;
     __syncwarp();
-    const uint64_t skey = topk_key(S, row, V, k, lane, small_v, nch4, nullptr);
+    int st = tiny_v ? topk_small(S, row, V, k, lane, nch4, nullptr)
+                    : skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, nullptr));
     if (lane < k) {
-      const int st = (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu));
       const size_t o = ((size_t)u * P.T_max + i) * k + lane;
       P.topk_tok[o] = st;
       P.topk_val[o] = __ldg(src + st);

@@ -55,7 +55,9 @@ struct Params {
   float* topk_val;          // [B, T_max, k]
 };
 
-enum DbgCounter { kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5 };
+enum DbgCounter {
+  kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5, kDbgTopkFix = 6
+};
 
 // Fast path (beam <= kFastBeam): trellis checkpoint interval.
 constexpr int kFastBeam = 16;
@@ -64,7 +66,8 @@ constexpr int kTieCache = 32;
 
 // Byte offsets of the per-warp shared memory of the fast decode kernel.
 struct FastLayout {
-  size_t rows, mbar, cand, sval, stok, excl, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, gkey, hsc, hp2, dlane, dA, dgv, ring, hist, posmap, total;
+  size_t rows, mbar, cand, sval, stok, excl, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, gkey, hsc, hp2, dlane, dA, dgv, ring, hist,
+      posmap, wp, ckey, cidx, total;
 };
 __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_bytes) {
   FastLayout L{};
@@ -88,14 +91,17 @@ __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_
   L.hl = take(16 * 4, 4);          // entry lengths (tie slow path)
   L.tc_h = take(2 * kTieCache * 8, 8);  // tie-order cache: (seq hash a, seq hash b)
   L.tc_r = take((kTieCache + 1) * 4, 4);  // cached order (-1/+1) + replacement cursor
-  L.gkey = take(16 * 32 * 4, 4);   // append-group rank keys [distinct prefix][S position]
+  L.gkey = take(256 * 4, 4);       // radix-select histogram (fallback only)
   L.hsc = take(16 * 8, 8);         // entry scores (tie slow path)
   L.hp2 = take(16 * 4, 4);         // partner entry of each first entry (tie slow path)
   L.dA = take(16 * 8, 8);          // per distinct prefix: A = logaddexp of its entries
   L.dlane = take(16 * 4, 4);       // per distinct prefix: its first entry lane
   L.dgv = take(16 * 4, 4);         // per distinct prefix: valid append positions in S
   L.ring = take((size_t)kChunk * 16 * 4, 4);
-  L.hist = L.gkey;                 // radix-select histogram (fallback only) aliases the key matrix
+  L.hist = L.gkey;
+  L.wp = take(32 * 8, 8);          // per S position: floor(v * 2^32 / R)
+  L.ckey = take(64 * 4, 4);        // top-k survivors: 32-bit sort keys
+  L.cidx = take(64 * 2, 2);        //                  token indices (index order)
   L.posmap = take((size_t)V, 1);
   L.total = (o + 127) / 128 * 128;
   return L;
