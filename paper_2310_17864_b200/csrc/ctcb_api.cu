@@ -15,6 +15,8 @@ namespace ctcb {
 __global__ void ctcb_decode_generic_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_pre_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_decode_fast_small_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_decode_fast_pre_small_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_framemap_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_topk_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter);
@@ -51,6 +53,13 @@ namespace {
 thread_local std::string g_last_error;
 
 bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
+// Fast kernel variant: compile-time layout when V <= kSmallV (ring 2, 2048-B rows).
+bool fast_small(const ctcb::Params& P) { return P.V <= ctcb::kSmallV && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes; }
+const void* fast_kernel_fn(const ctcb::Params& P, bool pre) {
+  const bool sm = fast_small(P);
+  if (pre) return sm ? (const void*)ctcb::ctcb_decode_fast_pre_small_kernel : (const void*)ctcb::ctcb_decode_fast_pre_kernel;
+  return sm ? (const void*)ctcb::ctcb_decode_fast_small_kernel : (const void*)ctcb::ctcb_decode_fast_kernel;
+}
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -165,15 +174,15 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
 // fit, then maximise resident warps per SM (occupancy API), and spread small
 // batches over all SMs (at most ceil(B / num_sms) warps per block).
 int launch_config(ctcb_handle* h, ctcb::Params& P, int B, bool fast) {
-  const void* kfn = fast ? (const void*)ctcb::ctcb_decode_fast_kernel : (const void*)ctcb::ctcb_decode_generic_kernel;
   for (;;) {
-    size_t total = fast ? ctcb::make_fast_layout(P.V, P.ring, P.row_bytes).total
+    size_t total = fast ? ctcb::make_fast_layout(fast_small(P) ? ctcb::kSmallV : P.V, P.ring, P.row_bytes).total
                         : ctcb::make_layout(P.beam, P.kpad, P.V, P.ring, P.row_bytes).total;
     P.smem_per_warp = (int)total;
     if ((int)total <= h->max_smem_optin) break;
     if (P.ring > 1) { P.ring--; continue; }
     return fail(CTCB_ERR_UNSUPPORTED, "beam/vocabulary too large for one warp's shared memory");
   }
+  const void* kfn = fast ? fast_kernel_fn(P, use_precomp(h, B)) : (const void*)ctcb::ctcb_decode_generic_kernel;
   int max_wpb = h->max_smem_optin / P.smem_per_warp;
   max_wpb = max_wpb < 1 ? 1 : (max_wpb > 8 ? 8 : max_wpb);
   if (fast && max_wpb > 4) max_wpb = 4;  // fast kernel: __launch_bounds__(128, 6)
@@ -334,18 +343,16 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   ctcb::ctcb_order_kernel<<<1, 1024, order_smem, s>>>(lens, B, P.order, P.counter);
   CTCB_CUDA(cudaGetLastError());
   size_t smem = (size_t)P.smem_per_warp * P.warps_per_block;
-  const void* kfn = fast ? (const void*)ctcb::ctcb_decode_fast_kernel : (const void*)ctcb::ctcb_decode_generic_kernel;
+  const bool pre = fast && use_precomp(h, B);
+  const void* kfn = fast ? fast_kernel_fn(P, pre) : (const void*)ctcb::ctcb_decode_generic_kernel;
   CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (fast)
-    CTCB_CUDA(cudaFuncSetAttribute((const void*)ctcb::ctcb_decode_fast_pre_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
   CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, 32 * P.warps_per_block, smem));
   if (blocks_per_sm < 1) blocks_per_sm = 1;
   int need = (B + P.warps_per_block - 1) / P.warps_per_block;
   int grid = h->num_sms * blocks_per_sm;
   if (grid > need) grid = need;
-  if (fast && use_precomp(h, B)) {
+  if (pre) {
     // frame maps -> top-k of every kept frame (frame-parallel) -> beam walk
     P.precomp = 1;
     ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
@@ -359,11 +366,10 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
     ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 256, tsmem, s>>>(Q);
     CTCB_CUDA(cudaGetLastError());
   }
-  if (fast && P.precomp)
-    ctcb::ctcb_decode_fast_pre_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
-  else if (fast)
-    ctcb::ctcb_decode_fast_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
-  else
+  if (fast) {
+    void* args[] = {(void*)&P};
+    CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
+  } else
     ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
   CTCB_CUDA(cudaGetLastError());
   return CTCB_OK;

@@ -113,6 +113,8 @@ struct FastSmem {
   long long* wp;
   uint32_t* ckey;
   uint16_t* cidx;
+  int* slot_rec;
+  long long* dG;
 };
 
 // Token sequence of current entry `e` (length len) through the global trellis.
@@ -415,7 +417,6 @@ __device__ __forceinline__ int topk_small(const FastSmem& S, const float* row, i
   }
   const uint32_t tot = __shfl_sync(FULL, incl, 31);
   uint32_t offs = tot * 0x01010100u + (incl - packed);
-  uint32_t* ckey = S.ckey;
   uint16_t* cidx = S.cidx;
   while (pm) {
     const int bt = __ffs(pm) - 1;
@@ -423,15 +424,14 @@ __device__ __forceinline__ int topk_small(const FastSmem& S, const float* row, i
     const int sh = 8 * (bt >> 2);
     const uint32_t off = (offs >> sh) & 0xffu;
     offs += 1u << sh;
-    const int e = 4 * (lane + 32 * (bt >> 2)) + (bt & 3);
-    ckey[off] = (okey(row[e]) & ~63u) | (63u - off);
-    cidx[off] = (uint16_t)e;
+    cidx[off] = (uint16_t)(4 * (lane + 32 * (bt >> 2)) + (bt & 3));
   }
   __syncwarp();
-  uint32_t a = lane < cnt ? ckey[lane] : 0u;
+  // slot q holds the q-th survivor in index order: key = truncated value | 63 - q
+  uint32_t a = lane < cnt ? ((okey(row[cidx[lane]]) & ~63u) | (uint32_t)(63 - lane)) : 0u;
   a = sort_desc32(a, lane);
   if (cnt > 32) {
-    uint32_t b = lane + 32 < cnt ? ckey[lane + 32] : 0u;
+    uint32_t b = lane + 32 < cnt ? ((okey(row[cidx[lane + 32]]) & ~63u) | (uint32_t)(31 - lane)) : 0u;
     b = sort_desc32(b, lane);
     a = max(a, __shfl_sync(FULL, b, 31 - lane));
     a = merge_desc32(a, lane);
@@ -485,13 +485,15 @@ __device__ __forceinline__ long long f2ll_floor(double z) {
   return r;
 }
 
-template <bool PRE>
+// SMALL: V <= 512, ring 2, rows of 2048 B -- the shared-memory layout is a
+// compile-time constant (immediate offsets from one base register).
+template <bool PRE, bool SMALL>
 __device__ __forceinline__ void fast_decode(const Params& P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int me = lane & 15;
-  const FastLayout L = make_fast_layout(P.V, P.ring, P.row_bytes);
-  uint8_t* wbase = smem + (size_t)wid * P.smem_per_warp;
+  const FastLayout L = SMALL ? make_fast_layout(kSmallV, 2, kSmallRowBytes) : make_fast_layout(P.V, P.ring, P.row_bytes);
+  uint8_t* wbase = smem + (size_t)wid * (SMALL ? L.total : (size_t)P.smem_per_warp);
   FastSmem S;
   S.rows = wbase + L.rows;
   S.mbar = (uint64_t*)(wbase + L.mbar);
@@ -517,23 +519,33 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
   S.wp = (long long*)(wbase + L.wp);
   S.ckey = (uint32_t*)(wbase + L.ckey);
   S.cidx = (uint16_t*)(wbase + L.cidx);
+  S.slot_rec = (int*)(wbase + L.slot_rec);
+  S.dG = (long long*)(wbase + L.dG);
   for (int i = lane; i < 2 * kTieCache; i += 32) S.tc_h[i] = 0ull;
   for (int i = lane; i <= kTieCache; i += 32) S.tc_r[i] = 0;
 
-  const int V = P.V, k = P.k, beam = P.beam, ring = P.ring;
+  const int V = P.V, k = P.k, beam = P.beam, ring = SMALL ? 2 : P.ring;
+  const int row_bytes = SMALL ? kSmallRowBytes : P.row_bytes;
   const int nch4 = (V + 3) >> 2;
   const bool small_v = nch4 <= 256;               // general path: predicate bits fit one register
-  const bool tiny_v = nch4 <= 128 && k <= 31;     // topk_small: <= 4 chunks per lane
+  const bool tiny_v = SMALL && k <= 31;            // topk_small: <= 4 chunks per lane
   const uint32_t fullk = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
   const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
   const double kScale = 4294967296.0 / kR;
+  // one-shot selection quota table: append slot `lane` -> (prefix d, j-th valid position)
+  int ldj = 0xff;
+  for (int d = 0, off = 0; d < beam && beam <= 10; d++) {
+    const int q = beam / (d + 1);
+    if (lane >= off && lane < off + q) ldj = d | ((lane - off) << 4);
+    off += q;
+  }
 
   if (lane == 0)
     for (int s = 0; s < ring; s++) mbar_init(&S.mbar[s], 1);
   for (int c = lane; c < V; c += 32) S.posmap[c] = 0xff;
   // padding beyond V is never written by the row copies: sentinel it once
   for (int s = 0; s < ring; s++)
-    for (int c = V + lane; c < P.row_bytes / 4; c += 32) ((uint32_t*)(S.rows + (size_t)s * P.row_bytes))[c] = kSentinel;
+    for (int c = V + lane; c < row_bytes / 4; c += 32) ((uint32_t*)(S.rows + (size_t)s * row_bytes))[c] = kSentinel;
   fence_mbar_init();
   __syncwarp();
   int slot_i = 0, slot_c = 0;     // ring slots of the next issue / consume
@@ -591,7 +603,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         const float* src = ubase + (size_t)fr * P.stride_t;
         fence_proxy_async();
         mbar_arrive_expect_tx(&S.mbar[slot_i], row_copy);
-        tma_bulk_g2s(S.rows + (size_t)slot_i * P.row_bytes, src, row_copy, &S.mbar[slot_i]);
+        tma_bulk_g2s(S.rows + (size_t)slot_i * row_bytes, src, row_copy, &S.mbar[slot_i]);
       }
       slot_i = slot_i + 1 == ring ? 0 : slot_i + 1;
     };
@@ -613,7 +625,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       if (P.bulk_ok) {
         if (i + ring - 1 < kept) { issue(i + ring - 1); n_out++; }
         mbar_wait(&S.mbar[slot_c], par_c);
-        row = (float*)(S.rows + (size_t)slot_c * P.row_bytes);
+        row = (float*)(S.rows + (size_t)slot_c * row_bytes);
         n_out--;
         slot_c++;
         if (slot_c == ring) { slot_c = 0; par_c ^= 1u; }
@@ -767,13 +779,73 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // [1, 2^32 - 1] for a live list (A > -inf), 0 otherwise
       const long long gG = gv ? f2ll_floor((gA - kbase) * kScale) : 0ll;
       const uint32_t gLow = (gv && gA > -INFINITY) ? 1u : 0u;
+      int Hn = 0;
+      // ---- one-shot selection (beam <= 10): when the distinct prefixes are
+      // ordered by A with a margin, append (d, j) (j-th valid S position of
+      // the d-th prefix) is beaten by the (d+1)(j+1)-1 appends (d' <= d,
+      // j' <= j), so only j < beam/(d+1) can enter the beam: <= 27 append
+      // slots + <= 30 specials, one 64-key sort.  Keys carry the slot in their
+      // low 6 bits; adjacent keys within 2 truncated units, or keys near the
+      // floor, fall back to the exact k-way merge below.
+      bool oneshot = beam <= 10;
+      if (oneshot) {
+        const double gA_prev = __shfl_up_sync(FULL, gA, 1);
+        const bool unsorted = gen && me > 0 && !(gA_prev > gA + 1e-9 * (1.0 + fabs(gA)));
+        oneshot = !__any_sync(FULL, unsorted);
+      }
+      if (oneshot) {
+        if (gen) S.dG[me] = gG;
+        // specials -> slots [0, nS) in lane order
+        const uint32_t s0 = lane < 16 ? keyof(q0) : 0u, s1 = lane < 16 ? keyof(q1) : 0u,
+                       s2 = lane < 16 ? keyof(q2) : 0u;
+        const int cS = (s0 != 0u) + (s1 != 0u) + (s2 != 0u);  // q0 >= q1 >= q2: a prefix
+        const int incl = warp_incl_scan(cS, lane);
+        const int sb = incl - cS;
+        const int nS = __shfl_sync(FULL, incl, 31);
+        bool nearfloor = (s0 != 0u && s0 < 128u) || (s1 != 0u && s1 < 128u) || (s2 != 0u && s2 < 128u);
+        if (cS > 0) { S.ckey[sb] = (s0 & ~63u) | (uint32_t)(63 - sb); S.slot_rec[sb] = lane; }
+        if (cS > 1) { S.ckey[sb + 1] = (s1 & ~63u) | (uint32_t)(62 - sb); S.slot_rec[sb + 1] = lane | (1 << 8); }
+        if (cS > 2) { S.ckey[sb + 2] = (s2 & ~63u) | (uint32_t)(61 - sb); S.slot_rec[sb + 2] = lane | (2 << 8); }
+        __syncwarp();
+        // append slot 32 + lane: (d, j) from the quota table
+        uint32_t bkey = 0u;
+        const int qd = ldj & 15, qj = ldj >> 4;
+        if (ldj != 0xff && qd < nD) {
+          uint32_t m = S.dgv[qd];
+          for (int t = 0; t < qj; t++) m &= m - 1u;
+          if (m) {
+            const int pp = __ffs(m) - 1;
+            const long long t = S.dG[qd] + S.wp[pp];
+            const uint32_t kk = t < 1ll ? 1u : (t > 0xffffffffll ? 0xffffffffu : (uint32_t)t);
+            const bool live = S.dA[qd] > -INFINITY;
+            nearfloor |= live && kk < 128u;
+            bkey = live ? ((kk & ~63u) | (uint32_t)(31 - lane)) : 0u;
+            S.slot_rec[32 + lane] = (16 + qd) | (pp << 8);
+          }
+        }
+        uint32_t akey = lane < nS ? S.ckey[lane] : 0u;
+        akey = sort_desc32(akey, lane);
+        bkey = sort_desc32(bkey, lane);
+        akey = max(akey, __shfl_sync(FULL, bkey, 31 - lane));
+        akey = merge_desc32(akey, lane);
+        const uint32_t nxt = __shfl_down_sync(FULL, akey, 1);
+        const bool close = lane < beam && akey != 0u && nxt != 0u && (akey >> 6) - (nxt >> 6) <= 1u;
+        if (__any_sync(FULL, close || nearfloor)) {
+          oneshot = false;
+          if (lane == 0) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
+        } else {
+          Hn = __popc(__ballot_sync(FULL, lane < beam && akey != 0u));
+          if (lane < Hn) S.rec_i[lane] = S.slot_rec[63 - (int)(akey & 63u)];
+        }
+        __syncwarp();
+      }
+      if (!oneshot) {
       // rank-key queues: each lane pops its candidates in order.  Lanes < 16
       // queue their <= 3 special groups (items 0..2 = local sorted order);
       // lanes 16.. queue the next four valid positions of their append list
       // (gq = queued positions), refilled on demand.
       uint32_t kq0, kq1, kq2, kq3;
-      uint32_t gq = 0u;
-      int npop = 0;
+      uint32_t gq = 0u;  // queued items (specials: local ranks 0..2; lists: S positions)
       auto refill = [&]() {
         uint32_t kk[4];
 #pragma unroll
@@ -791,12 +863,13 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       };
       if (lane < 16) {
         kq0 = keyof(q0); kq1 = keyof(q1); kq2 = keyof(q2); kq3 = 0u;
+        gq = 7u;
       } else {
         refill();
       }
+      int recw = lane | ((__ffs(gq) - 1) << 8);  // record of the queue head
 
       // ================= k-way merge (decoder.py:651-681) =================
-      int Hn = 0;
       for (int r = 0; r < beam; r++) {
         const uint32_t mk = __reduce_max_sync(FULL, kq0);
         if (mk == 0u) break;
@@ -813,6 +886,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
             double esc;
             int eb_, ex, ef, pos;
             if (lane < 16) {
+              const int npop = __ffs(gq) - 1;
               const int kind = (kpack >> (2 * npop)) & 3;
               esc = npop == 0 ? q0 : (npop == 1 ? q1 : q2);
               eb_ = lane;
@@ -866,20 +940,25 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
           if (w < 0) break;
           win = lane == w;
         }
-        const int it = lane < 16 ? npop : __ffs(gq) - 1;
-        if (win) S.rec_i[r] = lane | (it << 8);
-        npop += (win && lane < 16) ? 1 : 0;
-        gq = (win && lane >= 16) ? (gq & (gq - 1u)) : gq;
+        // pop: the record of the head (lane | item << 8) goes to the new rank;
+        // losers write their own scratch slot instead of branching
+        S.rec_i[win ? r : 16 + lane] = recw;
+        gq = win ? (gq & (gq - 1u)) : gq;
+        recw = lane | ((__ffs(gq) - 1) << 8);
         kq0 = win ? kq1 : kq0;
         kq1 = win ? kq2 : kq1;
         kq2 = win ? kq3 : kq2;
         kq3 = win ? 0u : kq3;
         const bool need = win && kq0 == 0u && gv != 0u;
         if (__any_sync(FULL, need)) {
-          if (need) refill();
+          if (need) {
+            refill();
+            recw = lane | ((__ffs(gq) - 1) << 8);
+          }
         }
         Hn = r + 1;
       }
+      }  // !oneshot
       __syncwarp();
       if (Hn == 0) { died = true; break; }
 
@@ -1055,11 +1134,19 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
 }
 
 __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS) ctcb_decode_fast_kernel(const __grid_constant__ Params P) {
-  fast_decode<false>(P);
+  fast_decode<false, false>(P);
+}
+__global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS)
+    ctcb_decode_fast_small_kernel(const __grid_constant__ Params P) {
+  fast_decode<false, true>(P);
 }
 __global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS)
     ctcb_decode_fast_pre_kernel(const __grid_constant__ Params P) {
-  fast_decode<true>(P);
+  fast_decode<true, false>(P);
+}
+__global__ void __launch_bounds__(128, CTCB_FAST_MIN_BLOCKS)
+    ctcb_decode_fast_pre_small_kernel(const __grid_constant__ Params P) {
+  fast_decode<true, true>(P);
 }
 
 // Precomputed-top-k mode (small batches, where one warp per utterance leaves

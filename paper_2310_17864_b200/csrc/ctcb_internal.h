@@ -56,20 +56,23 @@ struct Params {
 };
 
 enum DbgCounter {
-  kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5, kDbgTopkFix = 6
+  kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5, kDbgTopkFix = 6, kDbgOneshotFallback = 7
 };
 
 // Fast path (beam <= kFastBeam): trellis checkpoint interval.
 constexpr int kFastBeam = 16;
 constexpr int kChunk = 16;
 constexpr int kTieCache = 32;
+// Fast path with a compile-time shared-memory layout: V <= kSmallV, ring 2.
+constexpr int kSmallV = 512;
+constexpr int kSmallRowBytes = kSmallV * 4;
 
 // Byte offsets of the per-warp shared memory of the fast decode kernel.
 struct FastLayout {
   size_t rows, mbar, cand, sval, stok, excl, rec_i, tie_sc, tie_i, hs, hl, tc_h, tc_r, gkey, hsc, hp2, dlane, dA, dgv, ring, hist,
-      posmap, wp, ckey, cidx, total;
+      posmap, wp, ckey, cidx, slot_rec, dG, total;
 };
-__host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_bytes) {
+__host__ __device__ constexpr inline FastLayout make_fast_layout(int V, int ring, int row_bytes) {
   FastLayout L{};
   size_t o = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -86,7 +89,7 @@ __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_
   L.sval = take(32 * 4, 4);
   L.stok = take(32 * 4, 4);
   L.excl = take(16 * 4, 4);
-  L.rec_i = take(16 * 4, 4);       // merge record per new entry: winning lane | item << 8
+  L.rec_i = take(48 * 4, 4);       // merge record per new entry: winning lane | item << 8 (+32 scratch)
   L.tie_i = take(32 * 4 * 4, 4);   // 4 ints per tie candidate
   L.hl = take(16 * 4, 4);          // entry lengths (tie slow path)
   L.tc_h = take(2 * kTieCache * 8, 8);  // tie-order cache: (seq hash a, seq hash b)
@@ -102,6 +105,8 @@ __host__ __device__ inline FastLayout make_fast_layout(int V, int ring, int row_
   L.wp = take(32 * 8, 8);          // per S position: floor(v * 2^32 / R)
   L.ckey = take(64 * 4, 4);        // top-k survivors: 32-bit sort keys
   L.cidx = take(64 * 2, 2);        //                  token indices (index order)
+  L.slot_rec = take(64 * 4, 4);    // one-shot selection: merge record per candidate slot
+  L.dG = take(16 * 8, 8);          // per distinct prefix: floor((A - base) * 2^32 / R)
   L.posmap = take((size_t)V, 1);
   L.total = (o + 127) / 128 * 128;
   return L;
