@@ -124,8 +124,17 @@ int ctcb_validate(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t s
 
 /* Diagnostics of the last ctcb_decode on this handle (synchronising read):
  * {key ties resolved exactly, exact fp64 score ties, token-sequence
- *  materialisations, trellis steps walked by them, radix top-k fallbacks, 0, 0, 0}. */
+ *  materialisations, trellis steps walked by them, radix top-k fallbacks, 0,
+ *  truncated-key top-k fixups, one-shot selection fallbacks to the k-way merge}. */
 int ctcb_debug_counters(ctcb_t* h, uint64_t* out8);
+
+/* Kernel timing for measurement: while enabled, every ctcb_decode records a
+ * CUDA event pair around its beam-search kernel on the decode stream (up to 64
+ * launches; enabling resets the list).  ctcb_kernel_time synchronises on the
+ * last pair and returns the summed kernel time, the number of timed launches
+ * and the name of the last kernel launched (static storage). */
+int ctcb_kernel_timing(ctcb_t* h, int enable);
+int ctcb_kernel_time(ctcb_t* h, double* total_ms, int* launches, const char** kernel);
 
 const char* ctcb_status_string(int status);
 /* Message of the last error on this host thread. */

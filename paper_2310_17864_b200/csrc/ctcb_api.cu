@@ -46,6 +46,12 @@ struct ctcb_handle {
   cudaStream_t cstreams[4];  // H2D copy streams of ctcb_decode_host (lazy)
   cudaEvent_t cev[5];
   int have_cstreams;
+  // ctcb_kernel_timing: CUDA events around the beam kernel of each decode
+  int timing;
+  int n_timed;
+  cudaEvent_t tev[2 * 64];
+  int have_tev;
+  const char* last_kernel;
 };
 
 namespace {
@@ -285,8 +291,38 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   return CTCB_OK;
 }
 
+int ctcb_kernel_timing(ctcb_t* h, int enable) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  CTCB_CUDA(cudaSetDevice(h->device));
+  if (enable && !h->have_tev) {
+    for (int i = 0; i < 2 * 64; i++) CTCB_CUDA(cudaEventCreate(&h->tev[i]));
+    h->have_tev = 1;
+  }
+  h->timing = enable ? 1 : 0;
+  h->n_timed = 0;
+  return CTCB_OK;
+}
+
+int ctcb_kernel_time(ctcb_t* h, double* total_ms, int* launches, const char** kernel) {
+  if (!h || !total_ms || !launches) return fail(CTCB_ERR_ARG, "NULL argument");
+  *total_ms = 0.0;
+  *launches = h->n_timed;
+  if (kernel) *kernel = h->last_kernel ? h->last_kernel : "";
+  if (!h->n_timed) return CTCB_OK;
+  CTCB_CUDA(cudaSetDevice(h->device));
+  CTCB_CUDA(cudaEventSynchronize(h->tev[2 * h->n_timed - 1]));
+  for (int i = 0; i < h->n_timed; i++) {
+    float ms = 0.f;
+    CTCB_CUDA(cudaEventElapsedTime(&ms, h->tev[2 * i], h->tev[2 * i + 1]));
+    *total_ms += ms;
+  }
+  return CTCB_OK;
+}
+
 int ctcb_destroy(ctcb_t* h) {
   if (!h) return CTCB_OK;
+  if (h->have_tev)
+    for (int i = 0; i < 2 * 64; i++) cudaEventDestroy(h->tev[i]);
   if (h->ws) cudaFree(h->ws);
   if (h->dbg) cudaFree(h->dbg);
   if (h->hbuf) cudaFree(h->hbuf);
@@ -366,12 +402,22 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
     ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 256, tsmem, s>>>(Q);
     CTCB_CUDA(cudaGetLastError());
   }
+  const bool timed = h->timing && h->n_timed < 64;
+  if (timed) CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed], s));
   if (fast) {
     void* args[] = {(void*)&P};
     CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
-  } else
+    h->last_kernel = !fast_small(P) ? (pre ? "ctcb_decode_fast_pre_kernel" : "ctcb_decode_fast_kernel")
+                                    : (pre ? "ctcb_decode_fast_pre_small_kernel" : "ctcb_decode_fast_small_kernel");
+  } else {
     ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
+    h->last_kernel = "ctcb_decode_generic_kernel";
+  }
   CTCB_CUDA(cudaGetLastError());
+  if (timed) {
+    CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed + 1], s));
+    h->n_timed++;
+  }
   return CTCB_OK;
 }
 

@@ -345,12 +345,26 @@ class CUCTCDecoder:
             result.append(hyps)
         return result
 
+    def kernel_timing(self, enable: bool = True) -> None:
+        """Record CUDA events around the beam-search kernel of every following
+        decode (measurement only; see ctcb_kernel_timing)."""
+        _lib.check(_lib.load().ctcb_kernel_timing(self._h, 1 if enable else 0), "ctcb_kernel_timing")
+
+    def kernel_time(self) -> tuple[float, int, str]:
+        """(summed kernel ms, timed launches, last kernel name) since kernel_timing()."""
+        lib = _lib.load()
+        ms, n, name = ctypes.c_double(), ctypes.c_int(), ctypes.c_char_p()
+        _lib.check(lib.ctcb_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(name)),
+                   "ctcb_kernel_time")
+        return ms.value, n.value, (name.value or b"").decode()
+
     def debug_counters(self) -> dict:
         """Slow-path counters of the last decode (see include/ctcb.h)."""
         lib = _lib.load()
         arr = (ctypes.c_uint64 * 8)()
         _lib.check(lib.ctcb_debug_counters(self._h, arr), "ctcb_debug_counters")
-        names = ("key_ties", "exact_ties", "materializations", "materialize_steps", "radix_fallbacks")
+        names = ("key_ties", "exact_ties", "materializations", "materialize_steps", "radix_fallbacks", "frames",
+                 "topk_fixups", "oneshot_fallbacks")
         return {n: int(arr[i]) for i, n in enumerate(names)}
 
     def debug_frames(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor):
