@@ -336,7 +336,7 @@ def main():
         d2h = int(len(lens) * (nb * (t_pad * 4 + 4 + 8) + 8))
         e2e = {"value": frames_all / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s, "steps": e2e_steps,
-               "path": "CUCTCDecoder.__call__(pinned CPU tensor) -> ctcb_decode_host (C ABI, host buffers) "
+               "path": "CUCTCDecoder.__call__(pinned CPU tensor) -> ctcb_decode_host_async (C ABI, host buffers, zero-copy gather + decode + D2H per utterance range, hypotheses built while later ranges run) "
                        "-> CUCTCHypothesis lists"}
         del hyps
 

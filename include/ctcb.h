@@ -102,6 +102,20 @@ int ctcb_decode_host(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_
                      int batch, int t_max, void* stream, int32_t* out_tokens, int32_t* out_timesteps,
                      int32_t* out_len, double* out_score, int32_t* out_count, int32_t* out_status);
 
+/* Chunked, asynchronous form of ctcb_decode_host for pipelined callers:
+ * splits the batch into `nchunks` (<= 64) consecutive utterance ranges and
+ * enqueues, per range, the H2D copies of its valid frames, its decode and the
+ * D2H of its results into the host output buffers (pinned memory keeps the
+ * copies asynchronous), then returns without synchronising; *chunks_out is
+ * the number of ranges.  The H2D copies of range c+1 overlap the decode of c.
+ * ctcb_decode_host_wait blocks until range `chunk` is on the host and reports
+ * it as [*b0, *b1).  Host buffers must stay valid until the last wait. */
+int ctcb_decode_host_async(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t,
+                           const int32_t* lens, int batch, int t_max, int nchunks, void* stream,
+                           int32_t* out_tokens, int32_t* out_timesteps, int32_t* out_len, double* out_score,
+                           int32_t* out_count, int32_t* out_status, int* chunks_out);
+int ctcb_decode_host_wait(ctcb_t* h, int chunk, int* b0, int* b1);
+
 /* Debug / minimum slice: blank-skip compaction and per-frame top-k only.
  * Replaces blank_collapse (emissions.py:284-306) and the token selection of
  * _BeamSearch._step (decoder.py:431-460, :440):

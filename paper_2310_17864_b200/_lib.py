@@ -21,7 +21,7 @@ UTT_OK, UTT_EMPTY, UTT_BAD_LEN, UTT_BEAM_DIED = 0, 1, 2, 3
 SYMBOLS = (
     "ctcb_create", "ctcb_destroy", "ctcb_skip_cutoff", "ctcb_topk_size", "ctcb_workspace_bytes",
     "ctcb_decode", "ctcb_decode_host", "ctcb_debug_frames", "ctcb_validate", "ctcb_debug_counters", "ctcb_status_string",
-    "ctcb_last_error", "ctcb_kernel_timing", "ctcb_kernel_time",
+    "ctcb_last_error", "ctcb_kernel_timing", "ctcb_kernel_time", "ctcb_decode_host_async", "ctcb_decode_host_wait",
 )
 
 _lib = None
@@ -64,6 +64,9 @@ def load():
     lib.ctcb_debug_frames.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp]
     lib.ctcb_validate.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, c_int, vp, vp]
     lib.ctcb_debug_counters.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+    lib.ctcb_decode_host_async.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp,
+                                           vp, ctypes.POINTER(c_int)]
+    lib.ctcb_decode_host_wait.argtypes = [vp, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]
     lib.ctcb_kernel_timing.argtypes = [vp, c_int]
     lib.ctcb_kernel_time.argtypes = [vp, ctypes.POINTER(c_double), ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_char_p)]
     lib.ctcb_status_string.argtypes = [c_int]

@@ -27,6 +27,42 @@ __global__ void ctcb_validate_kernel(const float* lp, long long sb, long long st
 __global__ void ctcb_validate_decode_kernel(const unsigned long long* key, int T, int V, int64_t* out);
 }  // namespace ctcb
 
+namespace ctcb {
+// Zero-copy H2D gather for the host-buffer path: warps copy each utterance's
+// valid frames straight from page-locked host memory (mapped into the device
+// address space) into the dense device staging [B, T, V].  One launch per
+// utterance range replaces one cudaMemcpyAsync per utterance (whose host-side
+// enqueue cost, ~20 us each, bounded the copy rate); PCIe reads reach ~51 GB/s.
+__global__ void __launch_bounds__(256) ctcb_gather_kernel(const float* __restrict__ src, long long sb, long long st,
+                                                          const int32_t* __restrict__ lens, int b0, int b1, int T,
+                                                          int Tp, int V, float* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const bool vec = st == V && (V & 3) == 0 && (sb & 3) == 0 && (((uintptr_t)src) & 15) == 0;
+  for (int b = b0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); b < b1; b += nw) {
+    int n = lens[b];
+    if (n <= 0) continue;
+    if (n > T) n = T;
+    const float* s = src + (size_t)b * sb;
+    float* d = dst + (size_t)b * Tp * V;
+    if (vec) {
+      const float4* s4 = (const float4*)s;
+      float4* d4 = (float4*)d;
+      const long long m = (long long)n * V / 4;
+      long long i = lane;
+      for (; i + 96 < m; i += 128) {
+        const float4 x0 = s4[i], x1 = s4[i + 32], x2 = s4[i + 64], x3 = s4[i + 96];
+        d4[i] = x0; d4[i + 32] = x1; d4[i + 64] = x2; d4[i + 96] = x3;
+      }
+      for (; i < m; i += 32) d4[i] = s4[i];
+    } else {
+      for (int t = 0; t < n; t++)
+        for (int v = lane; v < V; v += 32) d[(size_t)t * V + v] = s[(size_t)t * st + v];
+    }
+  }
+}
+}  // namespace ctcb
+
 struct ctcb_handle;
 namespace {
 bool use_fast(const ctcb_handle* h);
@@ -46,6 +82,10 @@ struct ctcb_handle {
   cudaStream_t cstreams[4];  // H2D copy streams of ctcb_decode_host (lazy)
   cudaEvent_t cev[5];
   int have_cstreams;
+  // ctcb_decode_host_async: per-chunk completion events and utterance ranges
+  cudaEvent_t chunk_ev[64];
+  int chunk_b0[64], chunk_b1[64];
+  int n_chunks;
   // ctcb_kernel_timing: CUDA events around the beam kernel of each decode
   int timing;
   int n_timed;
@@ -57,6 +97,7 @@ struct ctcb_handle {
 namespace {
 
 thread_local std::string g_last_error;
+constexpr int kMaxChunks = 64;
 
 bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
 // Fast kernel variant: compile-time layout when V <= kSmallV (ring 2, 2048-B rows).
@@ -329,6 +370,7 @@ int ctcb_destroy(ctcb_t* h) {
   if (h->have_cstreams) {
     for (int i = 0; i < 4; i++) cudaStreamDestroy(h->cstreams[i]);
     for (int i = 0; i < 5; i++) cudaEventDestroy(h->cev[i]);
+    for (int i = 0; i < kMaxChunks; i++) cudaEventDestroy(h->chunk_ev[i]);
   }
   delete h;
   return CTCB_OK;
@@ -421,16 +463,24 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   return CTCB_OK;
 }
 
-int ctcb_decode_host(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
-                     void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len, double* out_score,
-                     int32_t* out_count, int32_t* out_status) {
+// Host-buffer decode, enqueued in `nchunks` consecutive utterance ranges: per
+// chunk the valid frames of each utterance go H2D on four copy streams, the
+// decode stream joins them, decodes the chunk and copies its results D2H, then
+// records the chunk's event.  Copies of chunk c+1 overlap the decode of c.
+static int host_enqueue(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
+                        int nchunks, void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len,
+                        double* out_score, int32_t* out_count, int32_t* out_status) {
   if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
   if (!lp || !lens || !out_tokens || !out_len || !out_score || !out_count || !out_status)
     return fail(CTCB_ERR_ARG, "host pointers must not be NULL (out_timesteps may be)");
+  h->n_chunks = 0;
   if (B <= 0) return CTCB_OK;
   if (T < 0) return fail(CTCB_ERR_ARG, "t_max must be >= 0");
   if (st < h->V || sb < (int64_t)st * (T > 0 ? T : 1))
     return fail(CTCB_ERR_ARG, "strides must describe a [batch, t_max, vocab] layout with unit vocab stride");
+  if (nchunks < 1) nchunks = 1;
+  if (nchunks > kMaxChunks) nchunks = kMaxChunks;
+  if (nchunks > B) nchunks = B;
   CTCB_CUDA(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int Tp = T > 0 ? T : 1;
@@ -443,7 +493,10 @@ int ctcb_decode_host(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const i
                o_len = take((size_t)B * nb * 4), o_sc = take((size_t)B * nb * 8), o_cnt = take((size_t)B * 4),
                o_st = take((size_t)B * 4);
   if (h->hbuf_bytes < o) {
-    if (h->hbuf) cudaFree(h->hbuf);
+    if (h->hbuf) {
+      CTCB_CUDA(cudaDeviceSynchronize());
+      cudaFree(h->hbuf);
+    }
     h->hbuf = nullptr;
     h->hbuf_bytes = 0;
     CTCB_CUDA(cudaMalloc(&h->hbuf, o));
@@ -451,45 +504,104 @@ int ctcb_decode_host(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const i
   }
   char* d = (char*)h->hbuf;
   float* din = (float*)(d + o_in);
-  // H2D: each utterance's valid frames (a dense [len, V] block when
-  // stride_t == V), spread over four copy streams ordered after `stream`'s
-  // prior work and joined back before the decode
+  int32_t* dlens = (int32_t*)(d + o_lens);
+  int32_t *dtok = (int32_t*)(d + o_tok), *dts = out_ts ? (int32_t*)(d + o_ts) : nullptr, *dln = (int32_t*)(d + o_len);
+  double* dsc = (double*)(d + o_sc);
+  int32_t *dcnt = (int32_t*)(d + o_cnt), *dst_ = (int32_t*)(d + o_st);
   if (!h->have_cstreams) {
     for (int i = 0; i < 4; i++) CTCB_CUDA(cudaStreamCreateWithFlags(&h->cstreams[i], cudaStreamNonBlocking));
     for (int i = 0; i < 5; i++) CTCB_CUDA(cudaEventCreateWithFlags(&h->cev[i], cudaEventDisableTiming));
+    for (int i = 0; i < kMaxChunks; i++) CTCB_CUDA(cudaEventCreateWithFlags(&h->chunk_ev[i], cudaEventDisableTiming));
     h->have_cstreams = 1;
   }
+  // page-locked input mapped into the device address space: gather it with a
+  // kernel (one launch per range) instead of per-utterance DMA calls
+  const float* mapped = nullptr;
+  {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, lp) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      mapped = (const float*)pa.devicePointer;
+    cudaGetLastError();
+  }
+  // copies are ordered after `stream`'s prior work
   CTCB_CUDA(cudaEventRecord(h->cev[4], s));
   for (int i = 0; i < 4; i++) CTCB_CUDA(cudaStreamWaitEvent(h->cstreams[i], h->cev[4], 0));
-  for (int b = 0; b < B; b++) {
-    int n = lens[b];
-    if (n <= 0) continue;
-    if (n > T) n = T;
-    const float* src = lp + (size_t)b * sb;
-    float* dst = din + (size_t)b * Tp * V;
-    cudaStream_t cs = h->cstreams[b & 3];
-    if (st == (int64_t)V)
-      CTCB_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * V * 4, cudaMemcpyHostToDevice, cs));
-    else
-      CTCB_CUDA(cudaMemcpy2DAsync(dst, V * 4, src, (size_t)st * 4, V * 4, (size_t)n, cudaMemcpyHostToDevice, cs));
+  CTCB_CUDA(cudaMemcpyAsync(dlens, lens, (size_t)B * 4, cudaMemcpyHostToDevice, s));
+  if (mapped) {
+    CTCB_CUDA(cudaEventRecord(h->cev[4], s));  // lens on the device
+    CTCB_CUDA(cudaStreamWaitEvent(h->cstreams[0], h->cev[4], 0));
   }
-  for (int i = 0; i < 4; i++) {
-    CTCB_CUDA(cudaEventRecord(h->cev[i], h->cstreams[i]));
-    CTCB_CUDA(cudaStreamWaitEvent(s, h->cev[i], 0));
+  for (int c = 0; c < nchunks; c++) {
+    const int b0 = (int)((int64_t)B * c / nchunks), b1 = (int)((int64_t)B * (c + 1) / nchunks);
+    if (mapped) {
+      ctcb::ctcb_gather_kernel<<<2 * h->num_sms, 256, 0, h->cstreams[0]>>>(mapped, sb, st, dlens, b0, b1, T, Tp, (int)V, din);
+      CTCB_CUDA(cudaGetLastError());
+    }
+    for (int b = b0; b < b1 && !mapped; b++) {
+      int n = lens[b];
+      if (n <= 0) continue;
+      if (n > T) n = T;
+      const float* src = lp + (size_t)b * sb;
+      float* dst = din + (size_t)b * Tp * V;
+      cudaStream_t cs = h->cstreams[b & 3];
+      if (st == (int64_t)V)
+        CTCB_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * V * 4, cudaMemcpyHostToDevice, cs));
+      else
+        CTCB_CUDA(cudaMemcpy2DAsync(dst, V * 4, src, (size_t)st * 4, V * 4, (size_t)n, cudaMemcpyHostToDevice, cs));
+    }
+    for (int i = 0; i < 4; i++) {
+      CTCB_CUDA(cudaEventRecord(h->cev[i], h->cstreams[i]));
+      CTCB_CUDA(cudaStreamWaitEvent(s, h->cev[i], 0));
+    }
+    const int Bc = b1 - b0;
+    const size_t r0 = (size_t)b0 * nb;
+    int rc = ctcb_decode(h, din + (size_t)b0 * Tp * V, (int64_t)Tp * V, (int64_t)V, dlens + b0, Bc, T, nullptr, 0,
+                         stream, dtok + r0 * Tp, dts ? dts + r0 * Tp : nullptr, dln + r0, dsc + r0, dcnt + b0, dst_ + b0);
+    if (rc) return rc;
+    // D2H of the chunk's results
+    CTCB_CUDA(cudaMemcpyAsync(out_tokens + r0 * Tp, dtok + r0 * Tp, (size_t)Bc * nb * Tp * 4, cudaMemcpyDeviceToHost, s));
+    if (out_ts)
+      CTCB_CUDA(cudaMemcpyAsync(out_ts + r0 * Tp, dts + r0 * Tp, (size_t)Bc * nb * Tp * 4, cudaMemcpyDeviceToHost, s));
+    CTCB_CUDA(cudaMemcpyAsync(out_len + r0, dln + r0, (size_t)Bc * nb * 4, cudaMemcpyDeviceToHost, s));
+    CTCB_CUDA(cudaMemcpyAsync(out_score + r0, dsc + r0, (size_t)Bc * nb * 8, cudaMemcpyDeviceToHost, s));
+    CTCB_CUDA(cudaMemcpyAsync(out_count + b0, dcnt + b0, (size_t)Bc * 4, cudaMemcpyDeviceToHost, s));
+    CTCB_CUDA(cudaMemcpyAsync(out_status + b0, dst_ + b0, (size_t)Bc * 4, cudaMemcpyDeviceToHost, s));
+    CTCB_CUDA(cudaEventRecord(h->chunk_ev[c], s));
+    h->chunk_b0[c] = b0;
+    h->chunk_b1[c] = b1;
+    h->n_chunks = c + 1;
   }
-  CTCB_CUDA(cudaMemcpyAsync(d + o_lens, lens, (size_t)B * 4, cudaMemcpyHostToDevice, s));
-  int rc = ctcb_decode(h, din, (int64_t)Tp * V, (int64_t)V, (const int32_t*)(d + o_lens), B, T, nullptr, 0, stream,
-                       (int32_t*)(d + o_tok), out_ts ? (int32_t*)(d + o_ts) : nullptr, (int32_t*)(d + o_len),
-                       (double*)(d + o_sc), (int32_t*)(d + o_cnt), (int32_t*)(d + o_st));
+  return CTCB_OK;
+}
+
+int ctcb_decode_host(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
+                     void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len, double* out_score,
+                     int32_t* out_count, int32_t* out_status) {
+  int rc = host_enqueue(h, lp, sb, st, lens, B, T, 1, stream, out_tokens, out_ts, out_len, out_score, out_count,
+                        out_status);
   if (rc) return rc;
-  // D2H of the results
-  CTCB_CUDA(cudaMemcpyAsync(out_tokens, d + o_tok, (size_t)B * nb * Tp * 4, cudaMemcpyDeviceToHost, s));
-  if (out_ts) CTCB_CUDA(cudaMemcpyAsync(out_ts, d + o_ts, (size_t)B * nb * Tp * 4, cudaMemcpyDeviceToHost, s));
-  CTCB_CUDA(cudaMemcpyAsync(out_len, d + o_len, (size_t)B * nb * 4, cudaMemcpyDeviceToHost, s));
-  CTCB_CUDA(cudaMemcpyAsync(out_score, d + o_sc, (size_t)B * nb * 8, cudaMemcpyDeviceToHost, s));
-  CTCB_CUDA(cudaMemcpyAsync(out_count, d + o_cnt, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
-  CTCB_CUDA(cudaMemcpyAsync(out_status, d + o_st, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
-  CTCB_CUDA(cudaStreamSynchronize(s));
+  CTCB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return CTCB_OK;
+}
+
+int ctcb_decode_host_async(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
+                           int nchunks, void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len,
+                           double* out_score, int32_t* out_count, int32_t* out_status, int* chunks_out) {
+  if (!chunks_out) return fail(CTCB_ERR_ARG, "chunks_out must not be NULL");
+  *chunks_out = 0;
+  int rc = host_enqueue(h, lp, sb, st, lens, B, T, nchunks, stream, out_tokens, out_ts, out_len, out_score,
+                        out_count, out_status);
+  if (h) *chunks_out = h->n_chunks;
+  return rc;
+}
+
+int ctcb_decode_host_wait(ctcb_t* h, int chunk, int* b0, int* b1) {
+  if (!h || !b0 || !b1) return fail(CTCB_ERR_ARG, "NULL argument");
+  if (chunk < 0 || chunk >= h->n_chunks) return fail(CTCB_ERR_ARG, "chunk out of range");
+  CTCB_CUDA(cudaSetDevice(h->device));
+  CTCB_CUDA(cudaEventSynchronize(h->chunk_ev[chunk]));
+  *b0 = h->chunk_b0[chunk];
+  *b1 = h->chunk_b1[chunk];
   return CTCB_OK;
 }
 

@@ -28,6 +28,7 @@ arguments, allocates through PyTorch's caching allocator and converts results.
 from __future__ import annotations
 
 import ctypes
+import gc
 from typing import List, NamedTuple, Optional, Union
 
 import numpy as np
@@ -306,6 +307,62 @@ class CUCTCDecoder:
         lmax = int(ln.max()) if ln.size else 0
         return tok[:, :, :lmax], (ts[:, :, :lmax] if ts is not None else None), ln, sc, cnt
 
+    def _pinned_outputs(self, B: int, Tp: int):
+        """Page-locked host output buffers (cached per shape) so the D2H copies of
+        the chunked host path are asynchronous DMA."""
+        key = (B, Tp)
+        if getattr(self, "_pin_key", None) != key:
+            nb = self.nbest
+            mk = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True)
+            self._pin = (mk((B, nb, Tp), torch.int32), mk((B, nb), torch.int32), mk((B, nb), torch.float64),
+                         mk((B,), torch.int32), mk((B,), torch.int32))
+            self._pin_key = key
+        return [t.numpy() for t in self._pin]
+
+    def _decode_host_chunks(self, log_prob: torch.Tensor, encoder_out_lens, chunks: int):
+        """Pipelined host path (``ctcb_decode_host_async``): yields
+        (b0, b1, tokens, lengths, scores, counts) per utterance range as soon as
+        that range's results are on the host, while later ranges are still
+        being copied and decoded."""
+        if not isinstance(log_prob, torch.Tensor) or log_prob.dim() != 3 or log_prob.is_cuda:
+            raise ValueError("expected a 3-D CPU tensor [batch, frames, tokens]")
+        if log_prob.dtype != torch.float32:
+            raise ValueError(f"log_prob must be float32, got {log_prob.dtype}")
+        B, T, V = log_prob.shape
+        if V != len(self.vocab_list):
+            raise ValueError(f"emissions have {V} columns but the token dictionary has "
+                             f"{len(self.vocab_list)} tokens")
+        if log_prob.stride(2) != 1:
+            log_prob = log_prob.contiguous()
+        lens = np.ascontiguousarray(np.asarray(encoder_out_lens.cpu() if isinstance(encoder_out_lens, torch.Tensor)
+                                               else encoder_out_lens, dtype=np.int32))
+        if lens.shape != (B,):
+            raise ValueError("encoder_out_lens must be a 1-D tensor with one length per utterance")
+        st = log_prob.stride(1) if T > 1 else V
+        sb = log_prob.stride(0) if B > 1 else st * max(T, 1)
+        Tp = max(T, 1)
+        tok, ln, sc, cnt, status = self._pinned_outputs(B, Tp)
+        status.fill(-1)
+        vp = ctypes.c_void_p
+        lib = _lib.load()
+        n = ctypes.c_int()
+        _lib.check(lib.ctcb_decode_host_async(self._h, vp(log_prob.data_ptr()), sb, st, vp(lens.ctypes.data), B, T,
+                                              chunks, self._stream(), vp(tok.ctypes.data), None, vp(ln.ctypes.data),
+                                              vp(sc.ctypes.data), vp(cnt.ctypes.data), vp(status.ctypes.data),
+                                              ctypes.byref(n)), "ctcb_decode_host_async")
+        b0, b1 = ctypes.c_int(), ctypes.c_int()
+        for c in range(n.value):
+            _lib.check(lib.ctcb_decode_host_wait(self._h, c, ctypes.byref(b0), ctypes.byref(b1)),
+                       "ctcb_decode_host_wait")
+            lo, hi = b0.value, b1.value
+            if (status[lo:hi] != _lib.UTT_OK).any():
+                _lib.check(lib.ctcb_decode_host_wait(self._h, n.value - 1, ctypes.byref(b0), ctypes.byref(b1)),
+                           "ctcb_decode_host_wait")  # drain before raising
+                err = status.copy()
+                err[:lo] = _lib.UTT_OK
+                self._raise_status(err, T)
+            yield lo, hi, tok[lo:hi], ln[lo:hi], sc[lo:hi], cnt[lo:hi]
+
     @staticmethod
     def _raise_status(status: np.ndarray, T: int) -> None:
         if (status < 0).any():
@@ -327,22 +384,38 @@ class CUCTCDecoder:
         utterance (fewer than ``nbest`` when fewer distinct prefixes survive,
         decoder.py:801)."""
         if isinstance(log_prob, torch.Tensor) and not log_prob.is_cuda:
-            tokens, _, lengths, scores, counts = self.decode_host(log_prob, encoder_out_lens)
+            # pipelined: hypotheses of range c are built while c+1.. are copied/decoded
+            B = log_prob.shape[0] if log_prob.dim() == 3 else 0
+            chunks = max(1, min(16, B // 256))
+            result = []
+            for _, _, tokens, lengths, scores, counts in self._decode_host_chunks(log_prob, encoder_out_lens, chunks):
+                result.extend(self._hypotheses(tokens, lengths, scores, counts))
+            return result
         else:
             out = self.decode(log_prob, encoder_out_lens)
             tokens, _, lengths, scores, counts = self.to_host(out)
         return self._hypotheses(tokens, lengths, scores, counts)
 
     def _hypotheses(self, tokens, lengths, scores, counts) -> List[List[CUCTCHypothesis]]:
-        # one tolist() per hypothesis; words through an object-array gather
+        # one tolist() per hypothesis; words through an object-array gather.
+        # The cyclic garbage collector is paused while the (acyclic) result is
+        # built: its generation scans over the growing list otherwise double
+        # the cost for a few thousand utterances.
         vocab = self._vocab_np
         result = []
-        for b in range(tokens.shape[0]):
-            hyps = []
-            for j in range(int(counts[b])):
-                t = tokens[b, j, : lengths[b, j]]
-                hyps.append(CUCTCHypothesis(tokens=t.tolist(), words=vocab[t].tolist(), score=float(scores[b, j])))
-            result.append(hyps)
+        paused = gc.isenabled()
+        if paused:
+            gc.disable()
+        try:
+            for b in range(tokens.shape[0]):
+                hyps = []
+                for j in range(int(counts[b])):
+                    t = tokens[b, j, : lengths[b, j]]
+                    hyps.append(CUCTCHypothesis(tokens=t.tolist(), words=vocab[t].tolist(), score=float(scores[b, j])))
+                result.append(hyps)
+        finally:
+            if paused:
+                gc.enable()
         return result
 
     def kernel_timing(self, enable: bool = True) -> None:

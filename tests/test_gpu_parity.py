@@ -6,6 +6,7 @@ top-1/top-2 gap exceeds 1e-3; scores within 1e-4 absolute (fp64 device math
 typically agrees to ~1e-12); blank-skip frame maps bit-exact.
 """
 
+import dataclasses
 import hashlib
 
 import numpy as np
@@ -314,3 +315,20 @@ def test_host_buffer_path_matches_device_path():
     lens2[3] = 0
     with pytest.raises(ValueError, match="utterance 3: empty emissions"):
         dec(torch.from_numpy(lp), torch.from_numpy(lens2))
+
+
+def test_host_buffer_chunked_pipeline():
+    """The pipelined host path (ctcb_decode_host_async, several utterance ranges)
+    == device path, and an error in a later range names the right utterance."""
+    cfg = dataclasses.replace(synth.CONFIGS[0], batch=600)
+    lp, lens = synth.batch(cfg)
+    dec = cuda_ctc_decoder(vocab(cfg.vocab), nbest=2, beam_size=10, blank_skip_threshold=cfg.threshold)
+    dev = dec(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+    host = dec(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens))
+    assert len(host) == 600 and dev == host
+    lens2 = lens.copy()
+    lens2[450] = 0
+    with pytest.raises(ValueError, match="utterance 450: empty emissions"):
+        dec(torch.from_numpy(lp), torch.from_numpy(lens2))
+    # the handle is reusable after the error
+    assert dec(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens)) == dev
