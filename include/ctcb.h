@@ -61,6 +61,11 @@ int ctcb_create(int vocab, int blank, int beam, int nbest, float skip_cutoff, do
                 int device, ctcb_t** out);
 int ctcb_destroy(ctcb_t* h);
 
+/* Candidate merge rule (DecoderOptions.merge_mode, decoder.py:52-53, :610-613,
+ * :789-791): 0 = "logadd" (default: numpy's logaddexp fold), 1 = "max"
+ * (group maximum; flag variants also combined by max at finalisation). */
+int ctcb_set_merge_mode(ctcb_t* h, int max_mode);
+
 /* fp32 cutoff c(thr) such that, for every finite fp32 x,
  *   x >= c  <=>  exp((double)x) >= thr - 1e-12
  * i.e. ctcforge's skip rule (emissions.py:300-301, BLANK_SKIP_EPS :29).

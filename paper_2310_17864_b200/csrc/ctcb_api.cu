@@ -72,6 +72,7 @@ struct ctcb_handle {
   float cutoff;
   double beam_threshold;
   int num_sms, max_smem_optin;
+  int merge_max;      // ctcb_set_merge_mode
   int force_generic;  // CTCB_FORCE_GENERIC=1: use the generic kernel for every beam (testing)
   unsigned long long* dbg;  // device [8] debug counters
   void* ws;
@@ -198,6 +199,7 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.skip = std::isfinite(h->cutoff) || h->cutoff < 0 ? 1 : 0;
   P.beam_threshold = h->beam_threshold;
   P.threshold_inf = std::isinf(h->beam_threshold) ? 1 : 0;
+  P.merge_max = h->merge_max;
   P.frame_map = (int32_t*)(base + L.frame_map);
   P.kept = (int32_t*)(base + L.kept);
   P.trellis = (uint32_t*)(base + L.trellis);
@@ -329,6 +331,13 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   h->num_sms = prop.multiProcessorCount;
   h->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
   *out = h;
+  return CTCB_OK;
+}
+
+int ctcb_set_merge_mode(ctcb_t* h, int max_mode) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  if (max_mode != 0 && max_mode != 1) return fail(CTCB_ERR_ARG, "merge mode must be 0 (logadd) or 1 (max)");
+  h->merge_max = max_mode;
   return CTCB_OK;
 }
 

@@ -90,6 +90,12 @@ __device__ __forceinline__ double np_logaddexp(double x, double y) {
   return tmp;
 }
 
+// Candidate merge of the reference (decoder.py:610-613, :789-791): logadd
+// (numpy's left fold) or max (merge_mode="max").
+__device__ __forceinline__ double merge2(double x, double y, bool mx) {
+  return mx ? (x > y ? x : y) : np_logaddexp(x, y);
+}
+
 // ---------------------------------------------------------------- prefixes
 // Content-defined prefix identity: a chained 64-bit hash of the token
 // sequence (plus its length, compared alongside).  The reference interns

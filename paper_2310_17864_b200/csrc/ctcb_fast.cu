@@ -525,6 +525,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
   for (int i = lane; i <= kTieCache; i += 32) S.tc_r[i] = 0;
 
   const int V = P.V, k = P.k, beam = P.beam, ring = SMALL ? 2 : P.ring;
+  const bool MX = P.merge_max != 0;  // merge_mode="max" (decoder.py:610-613)
   const int row_bytes = SMALL ? kSmallRowBytes : P.row_bytes;
   const int nch4 = (V + 3) >> 2;
   const bool small_v = nch4 <= 256;               // general path: predicate bits fit one register
@@ -709,19 +710,19 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       int rep_src = lane, rep_tok = -1, single_src = lane;
       if (isfirst) {  // blank group (R,1): entries of R in rank order (decoder.py:513-521)
         c_blank = s + eb;
-        if (p2 >= 0) c_blank = np_logaddexp(c_blank, s_p2 + eb);
+        if (p2 >= 0) c_blank = merge2(c_blank, s_p2 + eb, MX);
       }
       if (ent && fl == 0) {  // repeat group (R',0): repeat first, then parent appends (:522-543)
         const double ec = (double)row[last];
         double sc = s + ec, bst = sc;
         if (pa >= 0 && !(fl_pa == 0 && last_pa == last)) {
           double x = s_pa + ec;
-          sc = np_logaddexp(sc, x);
+          sc = merge2(sc, x, MX);
           if (x > bst) { bst = x; rep_src = pa; rep_tok = last; }
         }
         if (pb >= 0 && !(fl_pb == 0 && last_pb == last)) {
           double x = s_pb + ec;
-          sc = np_logaddexp(sc, x);
+          sc = merge2(sc, x, MX);
           if (x > bst) { bst = x; rep_src = pb; rep_tok = last; }
         }
         c_rep = sc;
@@ -745,7 +746,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
 
       // ================= append lists (lanes 16..16+nD) =================
       // first lanes publish (lane, A, valid positions) at their distinct index
-      const double A = isfirst ? (p2 >= 0 ? np_logaddexp(s, s_p2) : s) : 0.0;
+      const double A = isfirst ? (p2 >= 0 ? merge2(s, s_p2, MX) : s) : 0.0;
       if (isfirst) {
         const int d = __popc(firstmask & lanemask_lt());
         S.dlane[d] = lane;
@@ -920,7 +921,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
                 const int f = S.tie_i[c * 4];
                 const double v = (double)S.sval[pos];
                 double e = S.hsc[f] + v;
-                if (S.hp2[f] >= 0) e = np_logaddexp(e, S.hsc[S.hp2[f]] + v);
+                if (S.hp2[f] >= 0) e = merge2(e, S.hsc[S.hp2[f]] + v, MX);
                 S.tie_sc[c] = e;
               }
             }
@@ -984,7 +985,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         const int c = S.stok[item2];
         const double v = (double)S.sval[item2];
         nsc = b_s1 + v;
-        if (b_p2 >= 0) nsc = np_logaddexp(nsc, b_s2 + v);
+        if (b_p2 >= 0) nsc = merge2(nsc, b_s2 + v, MX);
         x = c; src = base; tok = c; nfl = 0;
       } else {
         const int kind = (wk >> (2 * item2)) & 3;
@@ -1041,7 +1042,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       const unsigned pm = fm & ~(1u << lane);
       const int p2 = (ent && pm) ? __ffs(pm) - 1 : -1;
       const double s_p2 = __shfl_sync(FULL, s, p2 >= 0 ? p2 : lane);
-      const double gsc = isf ? (p2 >= 0 ? np_logaddexp(s, s_p2) : s) : -INFINITY;
+      const double gsc = isf ? (p2 >= 0 ? merge2(s, s_p2, MX) : s) : -INFINITY;
       // order groups: (score desc, lane asc) by register sort, then exact tie runs
       uint64_t key = isf ? ord64(gsc) : 0ull;
       int pay = lane;

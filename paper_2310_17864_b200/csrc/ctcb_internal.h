@@ -27,6 +27,7 @@ struct Params {
   int skip;                  // cutoff finite
   double beam_threshold;
   int threshold_inf;
+  int merge_max;             // merge_mode="max": group max instead of the logadd fold
   // workspace
   int32_t* frame_map;   // [B, T_max]
   int32_t* kept;        // [B]

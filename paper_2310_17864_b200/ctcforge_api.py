@@ -16,9 +16,9 @@ merge_mode`` (a ``DecoderOptions`` here or ctcforge's own).  They return
 score, timesteps)`` exactly like decoder.py:69-99, decoded by libctcb.so.
 
 What the CUDA path implements: the full-vocabulary (``beam_size_token`` None
-or >= V) logadd search.  Other option values raise ``ValueError`` here — the
-reference's LM / lexicon / max-merge paths are not on the CUDA decoder path
-(DESIGN.md §7).  fp64 emissions are rounded to fp32 (the decoder's input
+or >= V) search with ``merge_mode`` "logadd" or "max".  ``beam_size_token < V``
+raises ``ValueError`` here, as do lexicon / LM arguments — the reference's LM
+and lexicon paths are not on the CUDA decoder path.  fp64 emissions are rounded to fp32 (the decoder's input
 dtype) before decoding.
 """
 
@@ -114,14 +114,14 @@ _DECODERS: dict = {}
 def _decoder(vocab, blank, opts, device) -> CUCTCDecoder:
     if opts.beam_size_token is not None and opts.beam_size_token < len(vocab):
         raise ValueError("the CUDA decoder implements full-vocabulary search (beam_size_token None or >= V)")
-    if opts.merge_mode != "logadd":
-        raise ValueError('the CUDA decoder implements merge_mode="logadd"')
-    key = (tuple(vocab), blank, opts.beam_size, opts.n_best, opts.blank_skip_threshold, opts.beam_threshold, device)
+    key = (tuple(vocab), blank, opts.beam_size, opts.n_best, opts.blank_skip_threshold, opts.beam_threshold,
+           opts.merge_mode, device)
     dec = _DECODERS.get(key)
     if dec is None:
         dec = CUCTCDecoder(vocab, blank_id=blank, beam_size=opts.beam_size, nbest=opts.n_best,
                            blank_skip_threshold=opts.blank_skip_threshold, beam_threshold=opts.beam_threshold,
                            device=device)
+        dec.set_merge_mode(opts.merge_mode)
         _DECODERS[key] = dec
     return dec
 

@@ -418,6 +418,14 @@ class CUCTCDecoder:
                 gc.enable()
         return result
 
+    def set_merge_mode(self, mode: str) -> None:
+        """``"logadd"`` (default) or ``"max"``: how candidates sharing a merge key
+        and the two blank-flag variants of a prefix combine (DecoderOptions.merge_mode,
+        decoder.py:610-613, :789-791)."""
+        if mode not in ("logadd", "max"):
+            raise ValueError('merge_mode must be one of ("logadd", "max")')
+        _lib.check(_lib.load().ctcb_set_merge_mode(self._h, 1 if mode == "max" else 0), "ctcb_set_merge_mode")
+
     def kernel_timing(self, enable: bool = True) -> None:
         """Record CUDA events around the beam-search kernel of every following
         decode (measurement only; see ctcb_kernel_timing)."""

@@ -20,14 +20,14 @@ def test_options_validation_matches_reference():
 def test_shim_matches_reference_golden(golden):
     from paper_2310_17864_b200.ctcforge_api import beam_search_decode, decode_batch
 
-    cases = [c for c in golden["small"] if c["dtype"] == "float32" and c["merge"] == "logadd" and c["k"] is None]
+    cases = [c for c in golden["small"] if c["dtype"] == "float32" and c["k"] is None]
     assert cases
     for c in cases:
         lp = np.array(c["lp"], dtype=np.float64)
         v = lp.shape[1]
         tokens = ["-"] + [f"t{i}" for i in range(1, v)]
         opts = DecoderOptions(beam_size=c["beam"], n_best=c["n_best"], blank_skip_threshold=c["thr"],
-                              beam_threshold=c["beam_threshold"])
+                              beam_threshold=c["beam_threshold"], merge_mode=c["merge"])
         nb = beam_search_decode(lp, tokens, opts)
         assert [h.tokens for h in nb] == c["tokens"]
         assert [h.timesteps for h in nb] == c["timesteps"]
@@ -45,6 +45,25 @@ def test_shim_matches_reference_golden(golden):
 
 
 @pytest.mark.gpu
+def test_shim_merge_max_matches_oracle(golden):
+    """merge_mode="max" through the shim against the oracle on fp32-rounded inputs
+    (the golden max-merge cases are fp64; the decoder's input dtype is fp32)."""
+    import oracle
+    from paper_2310_17864_b200.ctcforge_api import beam_search_decode
+
+    for c in [c for c in golden["small"] if c["merge"] == "max"][:12]:
+        lp = np.array(c["lp"], dtype=np.float32).astype(np.float64)
+        tokens = ["-"] + [f"t{i}" for i in range(1, lp.shape[1])]
+        opts = DecoderOptions(beam_size=c["beam"], n_best=c["n_best"], blank_skip_threshold=c["thr"],
+                              beam_threshold=c["beam_threshold"], merge_mode="max")
+        nb = beam_search_decode(lp, tokens, opts)
+        ref = oracle.decode(lp, beam_size=c["beam"], n_best=c["n_best"], blank_skip_threshold=c["thr"],
+                            beam_threshold=c["beam_threshold"], merge_mode="max")
+        assert [h.tokens for h in nb] == ref.tokens and [h.timesteps for h in nb] == ref.timesteps
+        assert np.allclose([h.score for h in nb], ref.scores, atol=1e-9, rtol=0)
+
+
+@pytest.mark.gpu
 def test_shim_errors():
     from paper_2310_17864_b200.ctcforge_api import beam_search_decode, decode_batch
 
@@ -55,8 +74,6 @@ def test_shim_errors():
         beam_search_decode(np.log(np.full((2, 4), 0.25)), tokens)
     with pytest.raises(ValueError, match="full-vocabulary"):
         beam_search_decode(np.log(np.full((2, 3), 1 / 3)), tokens, DecoderOptions(beam_size_token=2))
-    with pytest.raises(ValueError, match="logadd"):
-        beam_search_decode(np.log(np.full((2, 3), 1 / 3)), tokens, DecoderOptions(merge_mode="max"))
     good = np.log(np.full((3, 3), 1 / 3))
     with pytest.raises(ValueError, match="utterance 1: empty emissions"):
         decode_batch([good, np.zeros((0, 3))], tokens)

@@ -7,6 +7,8 @@ typically agrees to ~1e-12); blank-skip frame maps bit-exact.
 """
 
 import dataclasses
+import json
+import os
 import hashlib
 
 import numpy as np
@@ -27,9 +29,10 @@ def vocab(v):
     return ["-"] + [f"t{i}" for i in range(1, v)]
 
 
-def run(lp, lens, beam, nbest=1, thr=1.0, bthr=50.0, timesteps=False):
+def run(lp, lens, beam, nbest=1, thr=1.0, bthr=50.0, timesteps=False, merge="logadd"):
     dec = CUCTCDecoder(vocab(lp.shape[2]), beam_size=beam, nbest=nbest, blank_skip_threshold=thr,
                        beam_threshold=bthr)
+    dec.set_merge_mode(merge)
     out = dec.decode(torch.from_numpy(np.ascontiguousarray(lp)).cuda(), torch.from_numpy(np.asarray(lens, np.int32)).cuda(),
                      timesteps=timesteps)
     tokens, ts, lengths, scores, counts = dec.to_host(out)
@@ -332,3 +335,28 @@ def test_host_buffer_chunked_pipeline():
         dec(torch.from_numpy(lp), torch.from_numpy(lens2))
     # the handle is reusable after the error
     assert dec(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens)) == dev
+
+
+@pytest.mark.parametrize("force_generic", ["0", "1"])
+def test_merge_mode_max_matches_oracle(monkeypatch, force_generic):
+    """merge_mode="max" (decoder.py:610-613, :789-791) on both kernels against the
+    oracle (fp32 inputs): the golden fp64 max-merge cases rounded to fp32, and
+    config-shaped batches."""
+    monkeypatch.setenv("CTCB_FORCE_GENERIC", force_generic)
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+    for c in [c for c in g["small"] if c["merge"] == "max"]:
+        lp = np.array(c["lp"], dtype=np.float32)[None]
+        thr = c["beam_threshold"]
+        thr = np.inf if thr == "inf" else thr
+        ref = oracle.decode(lp[0], beam_size=c["beam"], n_best=c["n_best"], blank_skip_threshold=c["thr"],
+                            beam_threshold=thr, merge_mode="max")
+        got = run(lp, [lp.shape[1]], c["beam"], c["n_best"], c["thr"], thr, timesteps=True, merge="max")[0]
+        assert_same(got, ref.tokens, ref.scores, ref.timesteps, ctx=f"seed {c['seed']}")
+    for cfg_id, idx in ((0, range(4)), (1, range(8))):
+        cfg = synth.CONFIGS[cfg_id]
+        lp, lens = synth.batch(cfg, indices=idx)
+        got = run(lp, lens, cfg.beam, 3, cfg.threshold, merge="max")
+        for b in range(len(lens)):
+            ref = oracle.decode(lp[b, : lens[b]], beam_size=cfg.beam, n_best=3, blank_skip_threshold=cfg.threshold,
+                                merge_mode="max")
+            assert_same(got[b], ref.tokens, ref.scores, ctx=f"cfg{cfg_id} utt {b}")
