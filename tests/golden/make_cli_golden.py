@@ -1,0 +1,89 @@
+"""Generate the CLI golden corpus by running the REFERENCE ``ctcforge decode``
+command (imported from /root/reference in the build container; it does not exist
+on the GPU box):
+
+    python tests/golden/make_cli_golden.py
+
+Writes ``tests/golden/cli/``: ``tokens.txt``, ``corpus/*.ctce|*.tsv`` (seeded
+peaky posteriors, float32-exact; plus a wrong-width file and a non-normalized
+file that fail per utterance), and for each option set in RUNS the reference's
+JSON-lines output, its ``.meta`` failed list and exit code (``expected.json``).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import shutil
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(HERE, "cli")
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from ctcforge import cli as ref_cli  # noqa: E402
+from ctcforge.emissions import EmissionMatrix, write_emissions  # noqa: E402
+
+V = 12
+TOKENS = ["<blank>"] + [f"u{i}" for i in range(1, V)]
+RUNS = {
+    "default": [],
+    "beam5_nbest3_skip": ["--beam-size", "5", "--nbest", "3", "--blank-skip-threshold", "0.9"],
+    "max_merge": ["--merge", "max", "--beam-size", "8", "--nbest", "2", "--beam-threshold", "6.0"],
+    "nonstrict": ["--no-strict-validation", "--beam-size", "4"],
+}
+
+
+def utterance(rng, t):
+    logits = rng.normal(0.0, 1.0, size=(t, V))
+    for i in range(t):
+        if rng.random() < 0.55:
+            logits[i, 0] += rng.uniform(4, 9)
+        else:
+            logits[i, rng.integers(1, V)] += rng.uniform(3, 7)
+    lp = logits - np.log(np.exp(logits - logits.max(1, keepdims=True)).sum(1, keepdims=True)) - logits.max(1, keepdims=True)
+    return lp.astype(np.float32)
+
+
+def main():
+    shutil.rmtree(OUT, ignore_errors=True)
+    corpus = os.path.join(OUT, "corpus")
+    os.makedirs(corpus)
+    with open(os.path.join(OUT, "tokens.txt"), "w", encoding="utf-8") as fh:
+        fh.write("\n".join(TOKENS) + "\n")
+    rng = np.random.default_rng(20261019)
+    for i in range(9):
+        lp = utterance(rng, int(rng.integers(8, 48)))
+        write_emissions(EmissionMatrix(lp.astype(np.float64)), os.path.join(corpus, f"utt{i:02d}.ctce"))
+    lp = utterance(rng, 20)
+    with open(os.path.join(corpus, "utt09.tsv"), "w", encoding="utf-8") as fh:
+        for row in lp:
+            fh.write("\t".join(repr(float(x)) for x in row) + "\n")
+    # per-utterance failures: wrong width, and a row that does not normalise
+    write_emissions(EmissionMatrix(utterance(rng, 6)[:, :V - 1].astype(np.float64), strict=False),
+                    os.path.join(corpus, "bad_width.ctce"))
+    lp = utterance(rng, 10)
+    lp[3] -= 0.5
+    write_emissions(EmissionMatrix(lp.astype(np.float64), strict=False), os.path.join(corpus, "unnormalized.ctce"))
+    expected = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, flags in RUNS.items():
+            out = os.path.join(tmp, name + ".jsonl")
+            rc = ref_cli.main(["decode", "--emissions", corpus, "--tokens", os.path.join(OUT, "tokens.txt"),
+                               "--out", out] + flags)
+            with open(out, encoding="utf-8") as fh:
+                records = [json.loads(line) for line in fh]
+            with open(out + ".meta", encoding="utf-8") as fh:
+                meta = json.load(fh)
+            expected[name] = {"flags": flags, "exit_code": rc, "records": records, "failed": meta["failed"],
+                              "options": meta["options"]}
+    with open(os.path.join(OUT, "expected.json"), "w", encoding="utf-8") as fh:
+        json.dump(expected, fh, sort_keys=True, indent=1)
+    print({k: (v["exit_code"], len(v["records"]), v["failed"]) for k, v in expected.items()})
+
+
+if __name__ == "__main__":
+    main()
