@@ -812,10 +812,17 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         uint32_t bkey = 0u;
         const int qd = ldj & 15, qj = ldj >> 4;
         if (ldj != 0xff && qd < nD) {
-          uint32_t m = S.dgv[qd];
-          for (int t = 0; t < qj; t++) m &= m - 1u;
-          if (m) {
-            const int pp = __ffs(m) - 1;
+          // j-th valid position: j plus the excluded positions at or below it
+          // (exclusions are the few flag-0 children and last(R))
+          uint32_t ex = ~S.dgv[qd] & fullk;
+          int pp = qj;
+          while (ex) {
+            const int e = __ffs(ex) - 1;
+            if (e > pp) break;
+            pp++;
+            ex &= ex - 1u;
+          }
+          if (pp < k) {
             const long long t = S.dG[qd] + S.wp[pp];
             const uint32_t kk = t < 1ll ? 1u : (t > 0xffffffffll ? 0xffffffffu : (uint32_t)t);
             const bool live = S.dA[qd] > -INFINITY;
