@@ -42,7 +42,8 @@ enum {
   CTCB_UTT_OK = 0,
   CTCB_UTT_EMPTY = 1,      /* len == 0: "empty emissions" (decoder.py:117-118) */
   CTCB_UTT_BAD_LEN = 2,    /* len < 0 or len > t_max */
-  CTCB_UTT_BEAM_DIED = 3,  /* no finite extension survives (decoder.py:616-620) */
+  CTCB_UTT_BEAM_DIED = 3,  /* no finite extension survives (decoder.py:616-620); out_len[b][0] = the
+                              kept-frame index where it died */
 };
 
 /* Create a decoder.  Replaces DecoderOptions (decoder.py:34-66) + the
@@ -65,6 +66,14 @@ int ctcb_destroy(ctcb_t* h);
  * :789-791): 0 = "logadd" (default: numpy's logaddexp fold), 1 = "max"
  * (group maximum; flag variants also combined by max at finalisation). */
 int ctcb_set_merge_mode(ctcb_t* h, int max_mode);
+
+/* Token selection DecoderOptions.beam_size_token (decoder.py:440-458): per
+ * frame only the K best tokens of the row, blank included, by (log-prob desc,
+ * index asc) are candidates; blank groups need the blank selected, repeat
+ * groups and last-token appends need the last token selected.  K <= 0 or
+ * K == V: full vocabulary (the default); K > V: CTCB_ERR_ARG
+ * ("beam_size_token K exceeds vocabulary size V", decoder.py:124-128). */
+int ctcb_set_beam_size_token(ctcb_t* h, int K);
 
 /* fp32 cutoff c(thr) such that, for every finite fp32 x,
  *   x >= c  <=>  exp((double)x) >= thr - 1e-12

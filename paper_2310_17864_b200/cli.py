@@ -5,7 +5,7 @@ outputs and exit codes, decoding every utterance of a corpus in batched
 
     python -m paper_2310_17864_b200 decode --emissions DIR|FILE --tokens FILE --out OUT.jsonl
         [--config JSON] [--beam-size N] [--beam-threshold X] [--blank-skip-threshold P]
-        [--nbest N] [--merge logadd|max] [--blank-token T] [--silence-token T]
+        [--nbest N] [--merge logadd|max] [--beam-size-token K] [--blank-token T] [--silence-token T]
         [--no-strict-validation] [--workers N] [--gpu-batch N] [--device D]
 
 Inputs (emissions.py:181-253): one utterance per ``.ctce`` / ``.bin`` / ``.tsv``
@@ -23,13 +23,12 @@ ensure_ascii=False``, plus ``OUT.meta`` (total time, per-utterance times, failed
 ids, decoder options).  Exit codes: 0 success, 1 when any utterance failed
 (the others are still written), 2 on configuration errors.
 
-What differs from the CPU command: the decoder is the lexicon-free, LM-free,
-full-vocabulary CUDA search, so ``--lexicon`` / ``--lm`` / ``--beam-size-token``
-below V / a silence token with a non-zero ``--sil-score`` are configuration
-errors (exit 2); TSV values are rounded to float32, the decoder's input dtype
-(CTCE files are float32 already, so their decode is bit-identical to the CPU
-command's); per-utterance times in the meta file are the utterance's share of
-its batch (load + decode).
+What differs from the CPU command: the decoder is the lexicon-free, LM-free
+CUDA search, so ``--lexicon`` / ``--lm`` / a silence token with a non-zero
+``--sil-score`` are configuration errors (exit 2); TSV values are rounded to
+float32, the decoder's input dtype (CTCE files are float32 already, so their
+decode is bit-identical to the CPU command's); per-utterance times in the meta
+file are the utterance's share of its batch (load + decode).
 """
 
 from __future__ import annotations
@@ -251,8 +250,6 @@ def cmd_decode(cfg: dict) -> int:
                                            silence_token=cfg["silence_token"])
     except ValueError as exc:
         raise ConfigError(f"--tokens: {exc}") from exc
-    if opts.beam_size_token is not None and opts.beam_size_token < len(tokens):
-        raise ConfigError("the CUDA decoder implements full-vocabulary search (--beam-size-token None or >= V)")
     if tokens.silence_index is not None and opts.sil_score != 0.0:
         raise ConfigError("the CUDA decoder has no silence score (--sil-score must be 0 with --silence-token)")
     batch = int(cfg["gpu_batch"])
@@ -269,6 +266,9 @@ def cmd_decode(cfg: dict) -> int:
                        nbest=opts.n_best, blank_skip_threshold=opts.blank_skip_threshold,
                        beam_threshold=opts.beam_threshold, device=int(cfg["device"]))
     dec.set_merge_mode(opts.merge_mode)
+    too_wide = opts.beam_size_token is not None and opts.beam_size_token > len(tokens)
+    if opts.beam_size_token is not None and not too_wide:
+        dec.set_beam_size_token(opts.beam_size_token)
     strict = bool(cfg["strict_validation"])
     records, failed, times = [], [], {}
     for i0 in range(0, len(utts), batch):
@@ -281,7 +281,10 @@ def cmd_decode(cfg: dict) -> int:
                 ids.append(utt_id)
             except ValueError as exc:
                 errors[utt_id] = str(exc)
-        if lps:
+        if lps and too_wide:  # decoder.py:124-128, per utterance
+            for utt_id in ids:
+                errors[utt_id] = f"beam_size_token {opts.beam_size_token} exceeds vocabulary size {len(tokens)}"
+        elif lps:
             recs, errs = _decode_group(dec, tokens, ids, lps, strict, torch, _lib)
             records.extend(recs)
             errors.update(errs)
@@ -360,7 +363,9 @@ def _decode_group(dec, tokens, ids, lps, strict, torch, _lib):
         if ids[b] in errors:
             continue
         if status[b] == _lib.UTT_BEAM_DIED:
-            errors[ids[b]] = "beam died: no extension survives"
+            K = dec.beam_size_token or V
+            errors[ids[b]] = (f"beam died at frame {int(lengths[b, 0])}: no extension survives "
+                              f"(beam_size_token={K} may be too small)")
             continue
         nbest = []
         for r in range(int(counts[b])):

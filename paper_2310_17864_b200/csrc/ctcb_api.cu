@@ -73,6 +73,7 @@ struct ctcb_handle {
   double beam_threshold;
   int num_sms, max_smem_optin;
   int merge_max;      // ctcb_set_merge_mode
+  int tok_k;          // ctcb_set_beam_size_token (0: full vocabulary)
   int force_generic;  // CTCB_FORCE_GENERIC=1: use the generic kernel for every beam (testing)
   unsigned long long* dbg;  // device [8] debug counters
   void* ws;
@@ -200,6 +201,7 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.beam_threshold = h->beam_threshold;
   P.threshold_inf = std::isinf(h->beam_threshold) ? 1 : 0;
   P.merge_max = h->merge_max;
+  P.tokK = h->tok_k;
   P.frame_map = (int32_t*)(base + L.frame_map);
   P.kept = (int32_t*)(base + L.kept);
   P.trellis = (uint32_t*)(base + L.trellis);
@@ -338,6 +340,14 @@ int ctcb_set_merge_mode(ctcb_t* h, int max_mode) {
   if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
   if (max_mode != 0 && max_mode != 1) return fail(CTCB_ERR_ARG, "merge mode must be 0 (logadd) or 1 (max)");
   h->merge_max = max_mode;
+  return CTCB_OK;
+}
+
+int ctcb_set_beam_size_token(ctcb_t* h, int K) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  if (K > h->V)
+    return fail(CTCB_ERR_ARG, "beam_size_token " + std::to_string(K) + " exceeds vocabulary size " + std::to_string(h->V));
+  h->tok_k = (K <= 0 || K >= h->V) ? 0 : K;
   return CTCB_OK;
 }
 

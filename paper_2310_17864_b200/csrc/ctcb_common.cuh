@@ -128,6 +128,73 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// ---------------------------------------------------------------- token selection
+// beam_size_token = K < V (decoder.py:440-458): the K best tokens of the whole
+// row, blank included, by (log-prob desc, index asc).  kth_token finds the
+// K-th of them as (order key tv, index ti) with an 8-bit radix select on
+// ord32 keys (hist: 256 words of shared memory) followed by an index-ordered
+// scan of the ties; token c is selected iff ord32(v_c) > tv, or == tv and
+// c <= ti.  `row` may hold a sentinel at `blank`: its value is passed as ebf.
+// Whole warp, FULL mask.
+__device__ __forceinline__ void kth_token(const float* row, int V, int blank, float ebf, int K, uint32_t* hist,
+                                          int lane, uint32_t& tv, int& ti) {
+  uint32_t prefix = 0, pmask = 0;
+  int need = K;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (int c = lane; c < V; c += 32) {
+      const uint32_t key = ord32(c == blank ? ebf : row[c]);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t h[8], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) { h[q] = hist[lane * 8 + q]; sum += h[q]; }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t v = __shfl_down_sync(FULL, incl, off);
+      if (lane + off < 32) incl += v;
+    }
+    uint32_t cum = incl - sum;  // tokens in digits owned by higher lanes
+    int found = -1;
+    uint32_t cgt = 0;
+#pragma unroll
+    for (int q = 7; q >= 0; q--) {
+      if (found < 0 && cum < (uint32_t)need && cum + h[q] >= (uint32_t)need) { found = lane * 8 + q; cgt = cum; }
+      cum += h[q];
+    }
+    const unsigned bal = __ballot_sync(FULL, found >= 0);
+    const int src = __ffs(bal) - 1;
+    const int digit = __shfl_sync(FULL, found, src);
+    cgt = __shfl_sync(FULL, cgt, src);
+    need -= (int)cgt;
+    prefix |= (uint32_t)digit << shift;
+    pmask |= 0xffu << shift;
+    __syncwarp();
+  }
+  tv = prefix;
+  // the need-th token (index order) among those with key == tv
+  ti = V - 1;
+  for (int c0 = 0; c0 < V; c0 += 32) {
+    const int c = c0 + lane;
+    const bool eq = c < V && ord32(c == blank ? ebf : row[c]) == tv;
+    const unsigned beq = __ballot_sync(FULL, eq);
+    const int n = __popc(beq);
+    if (need <= n) {
+      unsigned m = beq;
+      for (int i = 1; i < need; i++) m &= m - 1u;
+      ti = c0 + __ffs(m) - 1;
+      break;
+    }
+    need -= n;
+  }
+}
+__device__ __forceinline__ bool token_selected(uint32_t key, int c, uint32_t tv, int ti) {
+  return key > tv || (key == tv && c <= ti);
+}
+
 // ---------------------------------------------------------------- TMA bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

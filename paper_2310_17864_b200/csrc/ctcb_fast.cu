@@ -620,6 +620,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
     int last = -1, len = 0, fl = 1;
     int H = 1;
     bool died = false;
+    int died_at = 0;
 
     for (int i = 0; i < kept; i++) {
       float* row;
@@ -667,6 +668,27 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         S.wp[lane] = f2ll_floor((double)sv * kScale);
       }
       __syncwarp();
+      // beam_size_token = K < V (decoder.py:440-458): the selected non-blank
+      // tokens are a prefix (mS) of S when K <= k; otherwise all of S plus
+      // tokens beyond it, tested against the K-th key (kth_token)
+      uint32_t selk = fullk;
+      bool has_blank = true, wide = false;
+      int mS = k;
+      uint32_t tv = 0u;
+      int ti = 0;
+      if (P.tokK) {
+        const uint32_t kb = ord32((float)eb);
+        if (P.tokK <= k) {
+          const bool above = lane < k && (ord32(sv) > kb || (ord32(sv) == kb && st < P.blank));
+          has_blank = __popc(__ballot_sync(FULL, above)) < P.tokK;
+          mS = has_blank ? P.tokK - 1 : P.tokK;
+          selk = mS >= 32 ? 0xffffffffu : ((1u << mS) - 1u);
+        } else {
+          kth_token(row, V, P.blank, (float)eb, P.tokK, S.hist, lane, tv, ti);
+          has_blank = token_selected(kb, P.blank, tv, ti);
+          wide = true;
+        }
+      }
 
       // ================= merge structure =================
       const bool ent = lane < H;
@@ -696,6 +718,9 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       if (ent && fl == 0 && pa >= 0 && mybit) atomicOr(&S.excl[pa], mybit);
       __syncwarp();
       const uint32_t childx = lane < 16 ? S.excl[lane] : 0u;
+      // last(R) selected this frame (repeat groups and the last-token append need it)
+      const bool mem_last = !P.tokK || (ent && last >= 0 &&
+                                        (wide ? token_selected(ord32(row[last]), last, tv, ti) : mypos < mS));
 
       // ================= special groups (lanes < 16) =================
       const unsigned pr2 = parents & (parents - 1);
@@ -708,11 +733,11 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       const int last_pb = __shfl_sync(FULL, last, pb >= 0 ? pb : lane);
       double c_blank = -INFINITY, c_rep = -INFINITY, c_single = -INFINITY;
       int rep_src = lane, rep_tok = -1, single_src = lane;
-      if (isfirst) {  // blank group (R,1): entries of R in rank order (decoder.py:513-521)
+      if (isfirst && has_blank) {  // blank group (R,1): entries of R in rank order (decoder.py:513-521)
         c_blank = s + eb;
         if (p2 >= 0) c_blank = merge2(c_blank, s_p2 + eb, MX);
       }
-      if (ent && fl == 0) {  // repeat group (R',0): repeat first, then parent appends (:522-543)
+      if (ent && fl == 0 && mem_last) {  // repeat group (R',0): repeat first, then parent appends (:522-543)
         const double ec = (double)row[last];
         double sc = s + ec, bst = sc;
         if (pa >= 0 && !(fl_pa == 0 && last_pa == last)) {
@@ -727,7 +752,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         }
         c_rep = sc;
       }
-      if (isfirst && mybit && !(childx & mybit)) {  // (R+last(R),0) from (R,1) only (blocked repeat)
+      if (isfirst && mybit && mem_last && !(childx & mybit)) {  // (R+last(R),0) from (R,1) only (blocked repeat)
         const int f1 = fl == 1 ? lane : ((p2 >= 0 && fl_p2 == 1) ? p2 : -1);
         if (f1 >= 0) {
           c_single = (f1 == lane ? s : s_p2) + (double)S.sval[mypos];
@@ -751,7 +776,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         const int d = __popc(firstmask & lanemask_lt());
         S.dlane[d] = lane;
         S.dA[d] = A;
-        S.dgv[d] = fullk & ~(childx | mybit);
+        S.dgv[d] = selk & ~(childx | mybit);
       }
       __syncwarp();
       const bool gen = lane >= 16 && me < nD;
@@ -766,7 +791,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       const uint32_t mhi = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32));
       const uint32_t mlo = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32) == mhi ? (uint32_t)ok64 : 0u);
       const uint64_t bk = ((uint64_t)mhi << 32) | mlo;
-      if (bk == 0ull) { died = true; break; }  // every extension is -inf (decoder.py:616-620)
+      if (bk == 0ull) { died = true; died_at = i; break; }  // every extension is -inf (decoder.py:616-620)
       const double best = unord64(bk);
       // keep iff score >= best - beam_threshold and score > -inf (decoder.py:621-623)
       const double lo_thr = P.threshold_inf ? -DBL_MAX : best - P.beam_threshold;
@@ -968,7 +993,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       }
       }  // !oneshot
       __syncwarp();
-      if (Hn == 0) { died = true; break; }
+      if (Hn == 0) { died = true; died_at = i; break; }
 
       // ================= commit (decoder.py:683-744) =================
       // lane r builds new entry r from the winning lane's registers
@@ -1036,7 +1061,11 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         if (slot_c == ring) { slot_c = 0; par_c ^= 1u; }
       }
       for (int c = lane; c < V; c += 32) S.posmap[c] = 0xff;
-      if (lane == 0) { P.status[u] = kUttBeamDied; P.out_count[u] = 0; }
+      if (lane == 0) {  // the dying frame (kept-frame index) goes to out_len[u][0]
+        P.status[u] = kUttBeamDied;
+        P.out_count[u] = 0;
+        P.out_len[(size_t)u * P.nbest] = died_at;
+      }
       __syncwarp();
       continue;
     }

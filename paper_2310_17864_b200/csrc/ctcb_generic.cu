@@ -32,6 +32,7 @@ namespace {
 struct Warp {
   const Params* P;
   int lane, u, steps_done;
+  int keff;  // valid top-k positions this frame (beam_size_token: the selected prefix of S)
   uint8_t* rows;
   uint64_t* mbar;
   double *cs, *ns, *headsc, *spsc;
@@ -341,7 +342,7 @@ __device__ __forceinline__ bool excl_bit(const Warp& w, int d, int j) {
   return (w.excl[d * w.kw + (j >> 5)] >> (j & 31)) & 1u;
 }
 __device__ __forceinline__ int next_valid(const Warp& w, int d, int j) {
-  const int k = w.P->k;
+  const int k = w.keff;
   for (++j; j < k; ++j)
     if (!excl_bit(w, d, j)) break;
   return j;
@@ -360,8 +361,39 @@ __device__ __forceinline__ double gen_score(const Warp& w, int d, int j) {
 // row `row`.  Returns the new beam size (0: beam died).
 __device__ int beam_step(Warp& w, const float* row, int H) {
   const Params& P = *w.P;
-  const int lane = w.lane, k = P.k, beam = P.beam;
+  const int lane = w.lane, beam = P.beam;
   const double eb = (double)row[P.blank];
+  // beam_size_token = K < V (decoder.py:440-458): blank / repeats / appends
+  // only for selected tokens; the selected non-blank tokens are a prefix of S
+  // when K <= k, else every S token plus those above the K-th key
+  int k = P.k;
+  bool has_blank = true, wide = false;
+  uint32_t tv = 0u;
+  int ti = 0;
+  if (P.tokK) {
+    const uint32_t kb = ord32((float)eb);
+    if (P.tokK <= P.k) {
+      int above = 0;
+      for (int j = lane; j < P.k; j += 32) {
+        const uint32_t kv = ord32(w.sval[j]);
+        above += (kv > kb || (kv == kb && w.stok[j] < P.blank)) ? 1 : 0;
+      }
+      above = __reduce_add_sync(FULL, above);
+      has_blank = above < P.tokK;
+      k = has_blank ? P.tokK - 1 : P.tokK;
+    } else {
+      kth_token(row, P.V, P.blank, (float)eb, P.tokK, w.hist, lane, tv, ti);
+      has_blank = token_selected(kb, P.blank, tv, ti);
+      wide = true;
+    }
+  }
+  w.keff = k;
+  auto selected = [&](int c) -> bool {
+    if (!P.tokK) return true;
+    if (wide) return token_selected(ord32(row[c]), c, tv, ti);
+    const int j = w.pos[c];
+    return j != 0xffff && j < k;
+  };
 
   // -- prefix grouping: entries sharing a token sequence (flag 0 / flag 1),
   //    through a shared-memory hash table keyed by (prefix hash, length)
@@ -423,16 +455,18 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   // -- specials: blank groups, repeat groups, last-token appends
   for (int d = lane; d < nD; d += 32) {
     int a = w.e1[d], b = w.e2[d];
-    double sc = w.cs[a] + eb;
-    if (b >= 0) sc = merge2(sc, w.cs[b] + eb, w.P->merge_max != 0);
-    int s = atomicAdd(&w.misc[0], 1);
-    w.spsc[s] = sc; w.spbase[s] = a; w.spx[s] = -1; w.spflag[s] = 1; w.spsrc[s] = a; w.sptok[s] = -1;
+    if (has_blank) {
+      double sc = w.cs[a] + eb;
+      if (b >= 0) sc = merge2(sc, w.cs[b] + eb, w.P->merge_max != 0);
+      int s = atomicAdd(&w.misc[0], 1);
+      w.spsc[s] = sc; w.spbase[s] = a; w.spx[s] = -1; w.spflag[s] = 1; w.spsrc[s] = a; w.sptok[s] = -1;
+    }
     int c = w.cl[a];
     if (c >= 0) {
       int j = w.pos[c];
       if (j != 0xffff && !excl_bit(w, d, j)) {
         int f = w.cf[a] == 1 ? a : ((b >= 0 && w.cf[b] == 1) ? b : -1);
-        if (f >= 0) {
+        if (f >= 0 && selected(c)) {
           int s2 = atomicAdd(&w.misc[0], 1);
           w.spsc[s2] = w.cs[f] + (double)w.sval[j];
           w.spbase[s2] = a; w.spx[s2] = c; w.spflag[s2] = 0; w.spsrc[s2] = f; w.sptok[s2] = c;
@@ -444,6 +478,7 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   for (int e = lane; e < H; e += 32) {
     if (w.cf[e] != 0) continue;
     int c = w.cl[e];
+    if (!selected(c)) continue;  // no repeat and no parent append of an unselected token
     double ec = (double)row[c];
     double sc = w.cs[e] + ec, best = sc;  // repeat candidate comes first (decoder.py:522-530)
     int src = e, tok = -1;
@@ -601,7 +636,7 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
     Hn = keepn;
   }
   // reset the token -> S rank map for the next frame
-  for (int j = lane; j < k; j += 32) w.pos[w.stok[j]] = 0xffff;
+  for (int j = lane; j < P.k; j += 32) w.pos[w.stok[j]] = 0xffff;
   __syncwarp();
   return Hn;
 }
@@ -764,7 +799,11 @@ __global__ void __launch_bounds__(256) ctcb_decode_generic_kernel(const __grid_c
         mbar_wait(&w.mbar[slot], (n_cons / (uint32_t)P.ring) & 1u);
         n_cons++;
       }
-      if (lane == 0) { P.status[u] = kUttBeamDied; P.out_count[u] = 0; }
+      if (lane == 0) {  // the dying frame (kept-frame index) goes to out_len[u][0]
+        P.status[u] = kUttBeamDied;
+        P.out_count[u] = 0;
+        P.out_len[(size_t)u * P.nbest] = w.steps_done;
+      }
       __syncwarp();
       continue;
     }

@@ -28,6 +28,7 @@ struct Params {
   double beam_threshold;
   int threshold_inf;
   int merge_max;             // merge_mode="max": group max instead of the logadd fold
+  int tokK;                  // beam_size_token K (0: full vocabulary; else 1 <= K < V)
   // workspace
   int32_t* frame_map;   // [B, T_max]
   int32_t* kept;        // [B]

@@ -15,10 +15,11 @@ merge_mode`` (a ``DecoderOptions`` here or ctcforge's own).  They return
 ``NBestList``s of ``Hypothesis(tokens, words=[], am_score, lm_score=0.0,
 score, timesteps)`` exactly like decoder.py:69-99, decoded by libctcb.so.
 
-What the CUDA path implements: the full-vocabulary (``beam_size_token`` None
-or >= V) search with ``merge_mode`` "logadd" or "max".  ``beam_size_token < V``
-raises ``ValueError`` here, as do lexicon / LM arguments — the reference's LM
-and lexicon paths are not on the CUDA decoder path.  fp64 emissions are rounded to fp32 (the decoder's input
+What the CUDA path implements: the lexicon-free, LM-free search with any
+``beam_size_token`` (None / V: full vocabulary; K < V: per-frame top-K token
+selection, decoder.py:440-458) and ``merge_mode`` "logadd" or "max".  Lexicon /
+LM arguments raise ``ValueError`` — the reference's LM and lexicon paths are
+not on the CUDA decoder path.  fp64 emissions are rounded to fp32 (the decoder's input
 dtype) before decoding.
 """
 
@@ -112,16 +113,16 @@ _DECODERS: dict = {}
 
 
 def _decoder(vocab, blank, opts, device) -> CUCTCDecoder:
-    if opts.beam_size_token is not None and opts.beam_size_token < len(vocab):
-        raise ValueError("the CUDA decoder implements full-vocabulary search (beam_size_token None or >= V)")
     key = (tuple(vocab), blank, opts.beam_size, opts.n_best, opts.blank_skip_threshold, opts.beam_threshold,
-           opts.merge_mode, device)
+           opts.merge_mode, opts.beam_size_token, device)
     dec = _DECODERS.get(key)
     if dec is None:
         dec = CUCTCDecoder(vocab, blank_id=blank, beam_size=opts.beam_size, nbest=opts.n_best,
                            blank_skip_threshold=opts.blank_skip_threshold, beam_threshold=opts.beam_threshold,
                            device=device)
         dec.set_merge_mode(opts.merge_mode)
+        if opts.beam_size_token is not None and opts.beam_size_token <= len(vocab):
+            dec.set_beam_size_token(opts.beam_size_token)
         _DECODERS[key] = dec
     return dec
 
@@ -141,6 +142,8 @@ def decode_batch(emissions, tokens, opts=None, lexicon=None, lm=None, workers: i
                              f"dictionary has {len(vocab)} tokens")
     if not lps:
         return []
+    if opts.beam_size_token is not None and opts.beam_size_token > len(vocab):  # decoder.py:124-128
+        raise ValueError(f"utterance 0: beam_size_token {opts.beam_size_token} exceeds vocabulary size {len(vocab)}")
     dec = _decoder(vocab, blank, opts, device)
     T = max(lp.shape[0] for lp in lps)
     x = torch.zeros((len(lps), max(T, 1), len(vocab)), dtype=torch.float32)

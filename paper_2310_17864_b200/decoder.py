@@ -140,6 +140,7 @@ class CUCTCDecoder:
         if cuda_stream is not None and not isinstance(cuda_stream, torch.cuda.Stream):
             raise TypeError("cuda_stream must be torch.cuda.Stream")
         self.vocab_list = vocab_list
+        self.beam_size_token: Optional[int] = None  # full vocabulary (set_beam_size_token)
         self._vocab_np = np.array(vocab_list, dtype=object)
         self.blank_id = blank_id
         self.beam_size = beam_size
@@ -260,9 +261,9 @@ class CUCTCDecoder:
         errors for failed utterances.  Returns numpy arrays
         (tokens [B, nbest, Lmax], timesteps or None, lengths, scores, counts)."""
         status = out.status.cpu().numpy()
-        self._raise_status(status, out.tokens.shape[2])
         counts = out.counts.cpu().numpy()
         lengths = out.lengths.cpu().numpy()
+        self._raise_status(status, out.tokens.shape[2], lengths)
         scores = out.scores.cpu().numpy()
         lmax = int(lengths.max()) if lengths.size else 0
         tokens = out.tokens[:, :, :lmax].cpu().numpy()
@@ -303,7 +304,7 @@ class CUCTCDecoder:
                                         self._stream(), vp(tok.ctypes.data), vp(ts.ctypes.data) if ts is not None else None,
                                         vp(ln.ctypes.data), vp(sc.ctypes.data), vp(cnt.ctypes.data),
                                         vp(status.ctypes.data)), "ctcb_decode_host")
-        self._raise_status(status, T)
+        self._raise_status(status, T, ln)
         lmax = int(ln.max()) if ln.size else 0
         return tok[:, :, :lmax], (ts[:, :, :lmax] if ts is not None else None), ln, sc, cnt
 
@@ -360,11 +361,10 @@ class CUCTCDecoder:
                            "ctcb_decode_host_wait")  # drain before raising
                 err = status.copy()
                 err[:lo] = _lib.UTT_OK
-                self._raise_status(err, T)
+                self._raise_status(err, T, ln)
             yield lo, hi, tok[lo:hi], ln[lo:hi], sc[lo:hi], cnt[lo:hi]
 
-    @staticmethod
-    def _raise_status(status: np.ndarray, T: int) -> None:
+    def _raise_status(self, status: np.ndarray, T: int, lengths=None) -> None:
         if (status < 0).any():
             raise _lib.CtcbError(f"ctcb_decode left {(status < 0).sum()} utterance(s) unprocessed (kernel did not run)")
         bad = np.flatnonzero(status != _lib.UTT_OK)
@@ -373,7 +373,11 @@ class CUCTCDecoder:
             if status[b] == _lib.UTT_EMPTY:
                 raise ValueError(f"utterance {b}: empty emissions")
             if status[b] == _lib.UTT_BEAM_DIED:
-                raise ValueError(f"utterance {b}: beam died: no extension survives")
+                # decoder.py:616-620; the kernel leaves the kept-frame index in lengths[b, 0]
+                t = int(np.asarray(lengths)[b, 0]) if lengths is not None else "?"
+                K = self.beam_size_token or len(self.vocab_list)
+                raise ValueError(f"utterance {b}: beam died at frame {t}: no extension survives "
+                                 f"(beam_size_token={K} may be too small)")
             raise ValueError(f"utterance {b}: length out of range [1, {T}]")
 
     def __call__(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor) -> List[List[CUCTCHypothesis]]:
@@ -425,6 +429,16 @@ class CUCTCDecoder:
         if mode not in ("logadd", "max"):
             raise ValueError('merge_mode must be one of ("logadd", "max")')
         _lib.check(_lib.load().ctcb_set_merge_mode(self._h, 1 if mode == "max" else 0), "ctcb_set_merge_mode")
+
+    def set_beam_size_token(self, k: Optional[int]) -> None:
+        """``DecoderOptions.beam_size_token``: None (default) or V searches the
+        full vocabulary; K < V restricts each frame's candidates to its K best
+        tokens, blank included (decoder.py:440-458)."""
+        if k is not None and k < 1:
+            raise ValueError("beam_size_token must be >= 1")
+        _lib.check(_lib.load().ctcb_set_beam_size_token(self._h, 0 if k is None else int(k)),
+                   "ctcb_set_beam_size_token")
+        self.beam_size_token = None if k is None or k >= len(self.vocab_list) else int(k)
 
     def kernel_timing(self, enable: bool = True) -> None:
         """Record CUDA events around the beam-search kernel of every following

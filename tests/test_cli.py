@@ -82,8 +82,6 @@ def test_config_errors_exit_2(tmp_path, capsys):
     lm = tmp_path / "x.arpa"
     lm.write_text("\\data\\\n")
     assert cli.main(base + ["--out", out, "--lm", str(lm)]) == 2 and "LM-free" in capsys.readouterr().err
-    assert cli.main(base + ["--out", out, "--beam-size-token", "3"]) == 2
-    assert "full-vocabulary" in capsys.readouterr().err
     assert cli.main(base + ["--out", out, "--nbest", "20"]) == 2 and "n_best" in capsys.readouterr().err
     cfg = tmp_path / "c.json"
     cfg.write_text(json.dumps({"bogus": 1}))

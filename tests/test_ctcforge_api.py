@@ -64,6 +64,33 @@ def test_shim_merge_max_matches_oracle(golden):
 
 
 @pytest.mark.gpu
+def test_shim_beam_size_token_matches_reference_golden(golden):
+    """beam_size_token < V through the shim against the oracle on fp32-rounded
+    golden inputs (the golden K=2 cases are fp64)."""
+    import oracle
+    from paper_2310_17864_b200.ctcforge_api import beam_search_decode
+
+    cases = [c for c in golden["small"] if c["k"] is not None]
+    assert cases
+    for c in cases:
+        lp = np.array(c["lp"], dtype=np.float32).astype(np.float64)
+        tokens = ["-"] + [f"t{i}" for i in range(1, lp.shape[1])]
+        opts = DecoderOptions(beam_size=c["beam"], n_best=c["n_best"], blank_skip_threshold=c["thr"],
+                              beam_threshold=c["beam_threshold"], beam_size_token=c["k"], merge_mode=c["merge"])
+        try:
+            ref = oracle.decode(lp, beam_size=c["beam"], n_best=c["n_best"], blank_skip_threshold=c["thr"],
+                                beam_threshold=c["beam_threshold"], beam_size_token=c["k"], merge_mode=c["merge"])
+        except oracle.OracleError as exc:
+            with pytest.raises(ValueError, match="beam died"):
+                beam_search_decode(lp, tokens, opts)
+            assert "beam died" in str(exc)
+            continue
+        nb = beam_search_decode(lp, tokens, opts)
+        assert [h.tokens for h in nb] == ref.tokens and [h.timesteps for h in nb] == ref.timesteps
+        assert np.allclose([h.score for h in nb], ref.scores, atol=1e-9, rtol=0)
+
+
+@pytest.mark.gpu
 def test_shim_errors():
     from paper_2310_17864_b200.ctcforge_api import beam_search_decode, decode_batch
 
@@ -72,8 +99,8 @@ def test_shim_errors():
         beam_search_decode(np.zeros((0, 3)), tokens)
     with pytest.raises(ValueError, match="columns"):
         beam_search_decode(np.log(np.full((2, 4), 0.25)), tokens)
-    with pytest.raises(ValueError, match="full-vocabulary"):
-        beam_search_decode(np.log(np.full((2, 3), 1 / 3)), tokens, DecoderOptions(beam_size_token=2))
+    with pytest.raises(ValueError, match="^beam_size_token 4 exceeds vocabulary size 3$"):
+        beam_search_decode(np.log(np.full((2, 3), 1 / 3)), tokens, DecoderOptions(beam_size_token=4))
     good = np.log(np.full((3, 3), 1 / 3))
     with pytest.raises(ValueError, match="utterance 1: empty emissions"):
         decode_batch([good, np.zeros((0, 3))], tokens)

@@ -29,10 +29,11 @@ def vocab(v):
     return ["-"] + [f"t{i}" for i in range(1, v)]
 
 
-def run(lp, lens, beam, nbest=1, thr=1.0, bthr=50.0, timesteps=False, merge="logadd"):
+def run(lp, lens, beam, nbest=1, thr=1.0, bthr=50.0, timesteps=False, merge="logadd", K=None):
     dec = CUCTCDecoder(vocab(lp.shape[2]), beam_size=beam, nbest=nbest, blank_skip_threshold=thr,
                        beam_threshold=bthr)
     dec.set_merge_mode(merge)
+    dec.set_beam_size_token(K)
     out = dec.decode(torch.from_numpy(np.ascontiguousarray(lp)).cuda(), torch.from_numpy(np.asarray(lens, np.int32)).cuda(),
                      timesteps=timesteps)
     tokens, ts, lengths, scores, counts = dec.to_host(out)
@@ -360,3 +361,28 @@ def test_merge_mode_max_matches_oracle(monkeypatch, force_generic):
             ref = oracle.decode(lp[b, : lens[b]], beam_size=cfg.beam, n_best=3, blank_skip_threshold=cfg.threshold,
                                 merge_mode="max")
             assert_same(got[b], ref.tokens, ref.scores, ctx=f"cfg{cfg_id} utt {b}")
+
+
+@pytest.mark.parametrize("force_generic", ["0", "1"])
+def test_beam_size_token_matches_oracle(monkeypatch, force_generic):
+    """beam_size_token = K < V (decoder.py:440-458) on both kernels against the
+    oracle: K below, at and above the kept top-k size (k = 2 beam), so the
+    selected tokens are a prefix of the top-k list or need the K-th key of the
+    whole row; blank selected or not; a repeat's token selected or not."""
+    monkeypatch.setenv("CTCB_FORCE_GENERIC", force_generic)
+    plans = ((0, range(4), 10, (1, 2, 5, 19, 20, 21, 25, 31, 32)), (1, range(6), 10, (3, 15, 21, 60, 499)),
+             (1, range(3), 16, (7, 31, 32, 33, 40)), (3, range(2), 10, (4, 20, 22, 200)))
+    for cfg_id, idx, beam, Ks in plans:
+        cfg = synth.CONFIGS[cfg_id]
+        lp, lens = synth.batch(cfg, indices=idx)
+        nb = min(3, beam)
+        for K in Ks:
+            got = run(lp, lens, beam, nb, cfg.threshold, timesteps=True, K=K)
+            for b in range(len(lens)):
+                ref = oracle.decode(lp[b, : lens[b]], beam_size=beam, n_best=nb, blank_skip_threshold=cfg.threshold,
+                                    beam_size_token=K)
+                assert_same(got[b], ref.tokens, ref.scores, ref.timesteps, ctx=f"cfg{cfg_id} beam {beam} K {K} utt {b}")
+    # K == V is the full vocabulary
+    cfg = synth.CONFIGS[0]
+    lp, lens = synth.batch(cfg)
+    assert run(lp, lens, 10, 2, cfg.threshold, K=cfg.vocab) == run(lp, lens, 10, 2, cfg.threshold)
