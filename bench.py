@@ -65,7 +65,9 @@ def algorithmic_bytes(lp: np.ndarray, lens: np.ndarray, cutoff: float) -> tuple[
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons, sampled every 50 ms from before
+    the warm-up (so nvidia-smi's own start-up, which can hold driver locks, is
+    outside the timed region); summary() keeps the samples taken inside it."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -73,8 +75,9 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
-        self.lines: list[str] = []
+        self.lines: list = []
         self.proc = None
+        self.window = None
 
     def __enter__(self):
         try:
@@ -89,7 +92,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def wait_ready(self, timeout: float = 10.0):
+        t_end = time.monotonic() + timeout
+        while self.proc is not None and not self.lines and time.monotonic() < t_end:
+            time.sleep(0.02)
+
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -101,9 +112,15 @@ class ClockSampler:
         return False
 
     def summary(self):
+        lines = self.lines
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [x for x in lines if t0 <= x[0] <= t1 + 0.05]
+            after = [x for x in lines if x[0] > t1]
+            lines = inside or after[:1]
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        for _, line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
                 continue
@@ -259,20 +276,24 @@ def main():
 
     # -- device-timed decode
     stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local_dev).__enter__()
     for _ in range(args.warmup):
         dec.decode(lp_dev, lens_dev)
     torch.cuda.synchronize(dev)
+    clocks.wait_ready()
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dec.kernel_timing(True)  # event pair around the beam kernel of each step (same stream)
-    with ClockSampler(local_dev) as clocks:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            out = dec.decode(lp_dev, lens_dev)
-        ev1.record(stream)
-        torch.cuda.synchronize(dev)
+    t_mark = time.monotonic()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        out = dec.decode(lp_dev, lens_dev)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.mark(t_mark, time.monotonic())
+    clocks.__exit__(None, None, None)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)

@@ -164,6 +164,34 @@ int ctcb_debug_counters(ctcb_t* h, uint64_t* out8);
 int ctcb_kernel_timing(ctcb_t* h, int enable);
 int ctcb_kernel_time(ctcb_t* h, double* total_ms, int* launches, const char** kernel);
 
+/* ---- CTC forced alignment (ctcforge align.py:46-123) ----------------------
+ * Viterbi over each utterance's blank-interleaved targets, one warp per
+ * utterance, fp64 path scores with the reference's tie-breaking (stay over
+ * advance-1 over advance-2; the final blank over the final token):
+ *   log_probs        device fp32 [batch, t_max, vocab] (strides as ctcb_decode)
+ *   lens             device int32 [batch] frames per utterance
+ *   targets          device int32, all utterances' target tokens concatenated
+ *   target_offsets   device int32 [batch + 1] (utterance b: [off[b], off[b+1]))
+ *   s_max            >= 2 * max targets + 1
+ *   workspace        device >= ctcb_align_workspace_bytes(batch, t_max, s_max)
+ * Outputs (device): out_labels int32 [batch, t_max] token per frame (blank
+ * allowed), out_scores fp32 [batch, t_max] its log-prob, out_status int32
+ * [batch] CTCB_ALIGN_*.  Enqueued on `stream` (on the current device). */
+enum {
+  CTCB_ALIGN_OK = 0,
+  CTCB_ALIGN_EMPTY_TARGETS = 1,  /* "targets must be non-empty" (align.py:62-63) */
+  CTCB_ALIGN_BLANK_TARGET = 2,   /* "targets must not contain the blank token" (:64-66) */
+  CTCB_ALIGN_RANGE = 3,          /* "target token t out of range [0, V)" (:67-68) */
+  CTCB_ALIGN_INFEASIBLE = 4,     /* T < L + adjacent repeats (:69-75) */
+  CTCB_ALIGN_NO_PATH = 5,        /* "no feasible alignment path" (:108-110) */
+  CTCB_ALIGN_BAD_LEN = 6,        /* length outside [0, t_max] or targets beyond s_max */
+};
+int ctcb_align_workspace_bytes(int batch, int t_max, int s_max, size_t* bytes);
+int ctcb_align(const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
+               const int32_t* targets, const int32_t* target_offsets, int batch, int t_max, int vocab, int blank,
+               int s_max, void* workspace, size_t workspace_bytes, void* stream, int32_t* out_labels,
+               float* out_scores, int32_t* out_status);
+
 const char* ctcb_status_string(int status);
 /* Message of the last error on this host thread. */
 const char* ctcb_last_error(void);

@@ -30,4 +30,12 @@ int ctco_blank_keep(const double* lp, int64_t T, int64_t V, int64_t blank, doubl
 int ctco_decode(const double* lp, int64_t T, int64_t V, const ctco_opts* opts,
                 int32_t* out_count, int32_t* out_len, int32_t* out_tokens, int32_t* out_ts,
                 double* out_score, int32_t* out_frame_map, int64_t* out_n_kept, int64_t* err_frame);
+/* CTC forced alignment (align.py:46-123), ctc_align.c. */
+#define CTCO_ALIGN_EMPTY 11       /* "targets must be non-empty" */
+#define CTCO_ALIGN_BLANK 12       /* "targets must not contain the blank token" */
+#define CTCO_ALIGN_RANGE 13       /* "target token t out of range [0, V)" */
+#define CTCO_ALIGN_INFEASIBLE 14  /* "infeasible alignment: ..." */
+#define CTCO_ALIGN_NO_PATH 15     /* "no feasible alignment path" */
+int ctco_align(const double* lp, int64_t T, int64_t V, int64_t blank, const int32_t* targets, int64_t L,
+               int32_t* frame_labels);
 #endif

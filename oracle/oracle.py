@@ -41,7 +41,8 @@ def build(force: bool = False) -> str:
     """Compile the oracle with gcc (oracle/Makefile)."""
     path = lib_path()
     src = os.path.join(_HERE, "ctc_oracle.c")
-    if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+    srcs = [src, os.path.join(_HERE, "ctc_align.c")]
+    if force or not os.path.exists(path) or os.path.getmtime(path) < max(os.path.getmtime(x) for x in srcs):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return path
 
@@ -65,6 +66,9 @@ def _lib():
             ctypes.c_double, p(ctypes.c_int32), p(ctypes.c_int64),
         ]
         lib.ctco_blank_keep.restype = ctypes.c_int
+        lib.ctco_align.argtypes = [p(ctypes.c_double), ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                   p(ctypes.c_int32), ctypes.c_int64, p(ctypes.c_int32)]
+        lib.ctco_align.restype = ctypes.c_int
         _LIB = lib
     return _LIB
 
@@ -161,3 +165,28 @@ def decode_batch(log_probs: np.ndarray, lens, threads: int | None = None, **kw) 
 
 
 INF = math.inf
+
+
+def align(lp: np.ndarray, targets, blank: int = 0) -> np.ndarray:
+    """CTC forced alignment of one utterance (align.py:46-123): per-frame labels.
+    Raises OracleError with the reference's messages."""
+    lp = np.ascontiguousarray(lp, dtype=np.float64)
+    T, V = lp.shape
+    tg = np.ascontiguousarray(np.asarray(list(targets), dtype=np.int32))
+    labels = np.zeros(max(T, 1), dtype=np.int32)
+    rc = _lib().ctco_align(_ptr(lp, ctypes.c_double), T, V, blank, _ptr(tg, ctypes.c_int32), len(tg),
+                           _ptr(labels, ctypes.c_int32))
+    if rc == 11:
+        raise OracleError("targets must be non-empty")
+    if rc == 12:
+        raise OracleError("targets must not contain the blank token")
+    if rc == 13:
+        bad = next(int(t) for t in tg if not 0 <= t < V)
+        raise OracleError(f"target token {bad} out of range [0, {V})")
+    if rc == 14:
+        reps = int(sum(a == b for a, b in zip(tg[:-1], tg[1:])))
+        raise OracleError(f"infeasible alignment: {T} frames cannot fit {len(tg)} targets "
+                          f"with {reps} adjacent repeats (need at least {len(tg) + reps})")
+    if rc == 15:
+        raise OracleError("no feasible alignment path")
+    return labels[:T]

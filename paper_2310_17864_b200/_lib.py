@@ -22,7 +22,7 @@ SYMBOLS = (
     "ctcb_create", "ctcb_destroy", "ctcb_skip_cutoff", "ctcb_topk_size", "ctcb_workspace_bytes",
     "ctcb_decode", "ctcb_decode_host", "ctcb_debug_frames", "ctcb_validate", "ctcb_debug_counters", "ctcb_status_string",
     "ctcb_last_error", "ctcb_kernel_timing", "ctcb_kernel_time", "ctcb_decode_host_async", "ctcb_decode_host_wait",
-    "ctcb_set_merge_mode", "ctcb_set_beam_size_token",
+    "ctcb_set_merge_mode", "ctcb_set_beam_size_token", "ctcb_align", "ctcb_align_workspace_bytes",
 )
 
 _lib = None
@@ -70,6 +70,9 @@ def load():
     lib.ctcb_decode_host_wait.argtypes = [vp, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]
     lib.ctcb_kernel_timing.argtypes = [vp, c_int]
     lib.ctcb_set_merge_mode.argtypes = [vp, c_int]
+    lib.ctcb_align_workspace_bytes.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_size_t)]
+    lib.ctcb_align.argtypes = [vp, c_int64, c_int64, vp, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, c_size_t, vp,
+                               vp, vp, vp]
     lib.ctcb_set_beam_size_token.argtypes = [vp, c_int]
     lib.ctcb_kernel_time.argtypes = [vp, ctypes.POINTER(c_double), ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_char_p)]
     lib.ctcb_status_string.argtypes = [c_int]

@@ -103,7 +103,9 @@ constexpr int kMaxChunks = 64;
 
 bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
 // Fast kernel variant: compile-time layout when V <= kSmallV (ring 2, 2048-B rows).
-bool fast_small(const ctcb::Params& P) { return P.V <= ctcb::kSmallV && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes; }
+bool fast_small(const ctcb::Params& P) {
+  return P.V <= ctcb::kSmallV && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes && P.tokK == 0;
+}
 const void* fast_kernel_fn(const ctcb::Params& P, bool pre) {
   const bool sm = fast_small(P);
   if (pre) return sm ? (const void*)ctcb::ctcb_decode_fast_pre_small_kernel : (const void*)ctcb::ctcb_decode_fast_pre_kernel;

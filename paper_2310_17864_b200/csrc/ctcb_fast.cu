@@ -526,6 +526,9 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
 
   const int V = P.V, k = P.k, beam = P.beam, ring = SMALL ? 2 : P.ring;
   const bool MX = P.merge_max != 0;  // merge_mode="max" (decoder.py:610-613)
+  // beam_size_token < V runs on the general-layout kernels only (the host never
+  // picks a SMALL variant for it), so its code is compiled out of SMALL
+  const int tokK = SMALL ? 0 : P.tokK;
   const int row_bytes = SMALL ? kSmallRowBytes : P.row_bytes;
   const int nch4 = (V + 3) >> 2;
   const bool small_v = nch4 <= 256;               // general path: predicate bits fit one register
@@ -676,15 +679,15 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       int mS = k;
       uint32_t tv = 0u;
       int ti = 0;
-      if (P.tokK) {
+      if (tokK) {
         const uint32_t kb = ord32((float)eb);
-        if (P.tokK <= k) {
+        if (tokK <= k) {
           const bool above = lane < k && (ord32(sv) > kb || (ord32(sv) == kb && st < P.blank));
-          has_blank = __popc(__ballot_sync(FULL, above)) < P.tokK;
-          mS = has_blank ? P.tokK - 1 : P.tokK;
+          has_blank = __popc(__ballot_sync(FULL, above)) < tokK;
+          mS = has_blank ? tokK - 1 : tokK;
           selk = mS >= 32 ? 0xffffffffu : ((1u << mS) - 1u);
         } else {
-          kth_token(row, V, P.blank, (float)eb, P.tokK, S.hist, lane, tv, ti);
+          kth_token(row, V, P.blank, (float)eb, tokK, S.hist, lane, tv, ti);
           has_blank = token_selected(kb, P.blank, tv, ti);
           wide = true;
         }
@@ -719,7 +722,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       __syncwarp();
       const uint32_t childx = lane < 16 ? S.excl[lane] : 0u;
       // last(R) selected this frame (repeat groups and the last-token append need it)
-      const bool mem_last = !P.tokK || (ent && last >= 0 &&
+      const bool mem_last = !tokK || (ent && last >= 0 &&
                                         (wide ? token_selected(ord32(row[last]), last, tv, ti) : mypos < mS));
 
       // ================= special groups (lanes < 16) =================
