@@ -19,6 +19,7 @@ __global__ void ctcb_decode_fast_small_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_pre_small_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_framemap_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_topk_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_rowoff_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter);
 __global__ void ctcb_debug_kernel(const __grid_constant__ Params P, int32_t* out_topk_tok, float* out_topk_val,
                                   float* out_blank);
@@ -138,7 +139,7 @@ bool use_precomp(const ctcb_handle* h, int B) {
 }
 
 struct WsLayout {
-  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, total;
+  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, rowoff, total;
 };
 WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   WsLayout w{};
@@ -158,6 +159,7 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   const size_t ntk = use_precomp(h, B) ? (size_t)B * T * h->k : 0;
   w.topk_tok = take(ntk * 4);
   w.topk_val = take(ntk * 4);
+  w.rowoff = take(ntk ? ((size_t)B + 1) * 4 : 0);
   w.total = ctcb::align_up(o, 256);
   return w;
 }
@@ -214,6 +216,7 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.n_chunks = (T + ctcb::kChunk - 1) / ctcb::kChunk;
   P.topk_tok = (int32_t*)(base + L.topk_tok);
   P.topk_val = (float*)(base + L.topk_val);
+  P.rowoff = (int32_t*)(base + L.rowoff);
   // rows of V <= 512 are padded to 512 floats: the fast top-k reads 4 float4
   // chunks per lane without bounds checks (padding holds the sentinel)
   P.row_bytes = (int)ctcb::align_up((size_t)(h->V <= 512 ? 512 : h->V) * 4, 16);
@@ -456,13 +459,17 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
     P.precomp = 1;
     ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
     CTCB_CUDA(cudaGetLastError());
+    ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
+    CTCB_CUDA(cudaGetLastError());
     ctcb::Params Q = P;
-    Q.smem_per_warp = (int)ctcb::align_up((size_t)P.row_bytes + 64 * 8 + 256 * 4 + 64 * 4 + 64 * 2, 128);
-    const size_t tsmem = (size_t)Q.smem_per_warp * 8;
+    Q.smem_per_warp = (int)ctcb::align_up((size_t)ctcb::kTopkRing * P.row_bytes + 64 + 64 * 8 + 256 * 4 + 64 * 4 + 64 * 2, 128);
+    int twpb = h->max_smem_optin / Q.smem_per_warp;
+    twpb = twpb < 1 ? 1 : (twpb > 8 ? 8 : twpb);
+    const size_t tsmem = (size_t)Q.smem_per_warp * twpb;
     CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
     int tbps = 0;
-    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_kernel, 256, tsmem));
-    ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 256, tsmem, s>>>(Q);
+    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_kernel, 32 * twpb, tsmem));
+    ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 32 * twpb, tsmem, s>>>(Q);
     CTCB_CUDA(cudaGetLastError());
   }
   const bool timed = h->timing && h->n_timed < 64;

@@ -1203,44 +1203,130 @@ __global__ void __launch_bounds__(256) ctcb_framemap_kernel(const __grid_constan
   if (lane == 0) P.kept[u] = kept;
 }
 
-__global__ void __launch_bounds__(256) ctcb_topk_kernel(const __grid_constant__ Params P) {
+// Exclusive prefix sums of the kept-frame counts (one block): row offsets of
+// the flattened (utterance, kept frame) space the top-k kernel splits evenly.
+__global__ void __launch_bounds__(1024) ctcb_rowoff_kernel(const __grid_constant__ Params P) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < P.B; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const int v = b < P.B ? P.kept[b] : 0;
+    const int incl = warp_incl_scan(v, lane);
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const int t = warp_tot[lane];
+      warp_tot[lane] = warp_incl_scan(t, lane) - t;
+    }
+    __syncthreads();
+    if (b < P.B) P.rowoff[b] = carry + warp_tot[wid] + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += warp_tot[31] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) P.rowoff[P.B] = carry;
+}
+
+// Frame-parallel top-k (precomputed mode): the kept rows of all utterances,
+// flattened and split evenly over the warps; rows are staged by TMA bulk
+// copies into a per-warp 3-deep ring two rows ahead of use.
+#ifndef CTCB_TOPK_MIN_BLOCKS
+#define CTCB_TOPK_MIN_BLOCKS 4
+#endif
+#ifndef CTCB_TOPK_RING
+#define CTCB_TOPK_RING 2
+#endif
+__global__ void __launch_bounds__(256, CTCB_TOPK_MIN_BLOCKS) ctcb_topk_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int kRing = CTCB_TOPK_RING;
   uint8_t* wbase = smem + (size_t)wid * P.smem_per_warp;
   FastSmem S{};
   S.rows = wbase;
-  S.cand = (uint64_t*)(wbase + P.row_bytes);
-  S.hist = (uint32_t*)(wbase + P.row_bytes + 64 * 8);
-  S.ckey = (uint32_t*)(wbase + P.row_bytes + 64 * 8 + 256 * 4);
-  S.cidx = (uint16_t*)(wbase + P.row_bytes + 64 * 8 + 256 * 4 + 64 * 4);
+  uint64_t* mbar = (uint64_t*)(wbase + (size_t)kRing * P.row_bytes);
+  S.cand = (uint64_t*)(wbase + (size_t)kRing * P.row_bytes + 64);
+  S.hist = (uint32_t*)((uint8_t*)S.cand + 64 * 8);
+  S.ckey = (uint32_t*)((uint8_t*)S.hist + 256 * 4);
+  S.cidx = (uint16_t*)((uint8_t*)S.ckey + 64 * 4);
   const int V = P.V, k = P.k, nch4 = (V + 3) >> 2;
   const bool small_v = nch4 <= 256;
   const bool tiny_v = nch4 <= 128 && k <= 31;
-  float* row = (float*)S.rows;
-  for (int c = V + lane; c < P.row_bytes / 4; c += 32) ((uint32_t*)row)[c] = kSentinel;
-  const long long total = (long long)P.B * P.T_max;
-  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + wid; g < total; g += nwarps) {
-    const int u = (int)(g / P.T_max), i = (int)(g % P.T_max);
-    if (i >= P.kept[u]) continue;
-    const float* src = P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
+  const uint32_t sdir = 0u;
+  (void)sdir;
+  for (int r = 0; r < kRing; r++)
+    for (int c = V + lane; c < P.row_bytes / 4; c += 32) ((uint32_t*)(S.rows + (size_t)r * P.row_bytes))[c] = kSentinel;
+  if (lane == 0)
+    for (int r = 0; r < kRing; r++) mbar_init(&mbar[r], 1);
+  fence_mbar_init();
+  fence_proxy_async();
+  __syncwarp();
+  const long long total = P.rowoff[P.B];
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
+  const long long g0 = total * w / nw, g1 = total * (w + 1) / nw;
+  if (g0 >= g1) return;
+  // utterance of the first row: last u with rowoff[u] <= g0
+  int lo = 0, hi = P.B - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.rowoff[mid] <= g0) lo = mid; else hi = mid - 1;
+  }
+  // (utterance, frame) cursors for issue and consume
+  int iu = lo, ii = (int)(g0 - P.rowoff[lo]);
+  int cu = iu, ci = ii;
+  const uint32_t row_copy = (uint32_t)V * 4u;
+  auto advance = [&](int& u, int& i) {
+    i++;
+    while (u < P.B && i >= P.kept[u]) { u++; i = 0; }
+  };
+  auto src_of = [&](int u, int i) -> const float* {
+    return P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
+  };
+  while (iu < P.B && ii >= P.kept[iu]) { iu++; ii = 0; }
+  cu = iu; ci = ii;
+  const long long n = g1 - g0;
+  int slot_i = 0, slot_c = 0;
+  uint32_t par = 0u;
+  long long issued = 0;
+  auto issue = [&]() {
     if (P.bulk_ok) {
-      const float4* s4 = (const float4*)src;
-      for (int c = lane; c < V / 4; c += 32) ((float4*)row)[c] = __ldg(s4 + c);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&mbar[slot_i], row_copy);
+        tma_bulk_g2s(S.rows + (size_t)slot_i * P.row_bytes, src_of(iu, ii), row_copy, &mbar[slot_i]);
+      }
+    }
+    slot_i = slot_i + 1 == kRing ? 0 : slot_i + 1;
+    issued++;
+    advance(iu, ii);
+  };
+  for (int r = 0; r < kRing - 1 && issued < n; r++) issue();
+  for (long long g = 0; g < n; g++) {
+    if (issued < n) issue();
+    float* row = (float*)(S.rows + (size_t)slot_c * P.row_bytes);
+    const float* src = src_of(cu, ci);
+    if (P.bulk_ok) {
+      mbar_wait(&mbar[slot_c], par);
     } else {
       for (int c = lane; c < V; c += 32) row[c] = __ldg(src + c);
     }
     __syncwarp();
     if (lane == 0) ((uint32_t*)row)[P.blank] = kSentinel;
     __syncwarp();
-    int st = tiny_v ? topk_small(S, row, V, k, lane, nch4, nullptr)
-                    : skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, nullptr));
+    const int st = tiny_v ? topk_small(S, row, V, k, lane, nch4, nullptr)
+                          : skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, nullptr));
     if (lane < k) {
-      const size_t o = ((size_t)u * P.T_max + i) * k + lane;
+      const size_t o = ((size_t)cu * P.T_max + ci) * k + lane;
       P.topk_tok[o] = st;
-      P.topk_val[o] = __ldg(src + st);
+      P.topk_val[o] = row[st];
     }
     __syncwarp();
+    fence_proxy_async();  // generic writes to the slot (blank sentinel) before it is refilled by TMA
+    slot_c++;
+    if (slot_c == kRing) { slot_c = 0; par ^= 1u; }
+    advance(cu, ci);
   }
 }
 

@@ -55,6 +55,7 @@ struct Params {
   int precomp;              // top-k lists precomputed by ctcb_topk_kernel
   int32_t* topk_tok;        // [B, T_max, k] (precomp mode)
   float* topk_val;          // [B, T_max, k]
+  int32_t* rowoff;          // [B + 1] exclusive prefix sums of kept (precomp mode)
 };
 
 enum DbgCounter {
@@ -68,6 +69,10 @@ constexpr int kTieCache = 32;
 // Fast path with a compile-time shared-memory layout: V <= kSmallV, ring 2.
 constexpr int kSmallV = 512;
 constexpr int kSmallRowBytes = kSmallV * 4;
+#ifndef CTCB_TOPK_RING
+#define CTCB_TOPK_RING 2
+#endif
+constexpr int kTopkRing = CTCB_TOPK_RING;  // row ring depth of ctcb_topk_kernel
 
 // Byte offsets of the per-warp shared memory of the fast decode kernel.
 struct FastLayout {
