@@ -818,8 +818,11 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // floor, fall back to the exact k-way merge below.
       bool oneshot = beam <= 10;
       if (oneshot) {
+        // the dominance count needs every list to hold >= beam valid positions
+        // (true with k = 2 beam <= V-1 and the full vocabulary; small V or
+        // beam_size_token can leave shorter lists)
         const double gA_prev = __shfl_up_sync(FULL, gA, 1);
-        const bool unsorted = gen && me > 0 && !(gA_prev > gA + 1e-9 * (1.0 + fabs(gA)));
+        const bool unsorted = gen && ((me > 0 && !(gA_prev > gA + 1e-9 * (1.0 + fabs(gA)))) || __popc(gv) < beam);
         oneshot = !__any_sync(FULL, unsorted);
       }
       if (oneshot) {

@@ -386,3 +386,18 @@ def test_beam_size_token_matches_oracle(monkeypatch, force_generic):
     cfg = synth.CONFIGS[0]
     lp, lens = synth.batch(cfg)
     assert run(lp, lens, 10, 2, cfg.threshold, K=cfg.vocab) == run(lp, lens, 10, 2, cfg.threshold)
+
+
+@pytest.mark.parametrize("force_generic", ["0", "1"])
+def test_regression_short_append_lists(monkeypatch, force_generic):
+    """Found by tools/fuzz_parity.py: V=5, beam 8, beam_size_token 3 leaves
+    append lists shorter than the beam, where the one-shot selection's
+    dominance count does not hold; the kernel must fall back to the exact
+    merge (the candidate [2, 1] was dropped at the second kept frame)."""
+    monkeypatch.setenv("CTCB_FORCE_GENERIC", force_generic)
+    u = np.load(os.path.join(os.path.dirname(__file__), "golden", "regress_short_lists.npy"))
+    for T in (7, u.shape[0]):
+        for K in (3, None):
+            got = run(u[None, :T], [T], 8, 8, 0.8, timesteps=True, K=K)[0]
+            ref = oracle.decode(u[:T], beam_size=8, n_best=8, blank_skip_threshold=0.8, beam_size_token=K)
+            assert_same(got, ref.tokens, ref.scores, ref.timesteps, ctx=f"T {T} K {K}")
