@@ -536,7 +536,10 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   auto keyof = [&](double sc) -> uint32_t {
     const double z = fmin(fmax(fma(sc, kScale, koff), 0.0), 4294967294.0);
     const uint32_t t = (uint32_t)__double_as_longlong(__dadd_rz(z, 4503599627370496.0));
-    return sc >= lo_thr ? 1u + t : 0u;
+    // approximate list scores may sit an ulp below the threshold: keep a
+    // margin here, the exact post-filter below applies decoder.py:621-623
+    if (!(sc > -INFINITY)) return 0u;
+    return (P.threshold_inf || sc >= lo_thr - 1e-9 * (1.0 + fabs(lo_thr))) ? 1u + t : 0u;
   };
   for (int i = lane; i < nH; i += 32) w.hkey[i] = keyof(head_approx(i, 0));
   __syncwarp();
@@ -546,36 +549,39 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   //    (i = lane + 32 j); the winner's lane pops and rescans its own heads.
   int sp_ptr = 0;  // owned by lane (nD & 31); mirrored to misc[1] for the tie path
   if (lane == 0) w.misc[1] = 0;
-  uint32_t lk = 0u;
-  int li = -1, lcnt = 0;
+  uint32_t lk = 0u, lk2 = 0u;  // best and second-best key of the heads this lane owns
+  int li = -1;
   auto rescan = [&]() {
-    lk = 0u; li = -1; lcnt = 0;
+    lk = 0u; lk2 = 0u; li = -1;
     for (int i = lane; i < nH; i += 32) {
       const uint32_t kk = w.hkey[i];
-      if (kk > lk) { lk = kk; li = i; lcnt = 1; }
-      else if (kk == lk && kk != 0u) lcnt++;
+      if (kk > lk) { lk2 = lk; lk = kk; li = i; }
+      else if (kk > lk2) lk2 = kk;
     }
   };
   rescan();
   int Hn = 0;
+  // list keys come from A + v, a few ulps from the exact fold, and every key
+  // is floored: heads within kTolG units of the maximum are resolved exactly
+  constexpr uint32_t kTolG = 2u;
   for (int r = 0; r < beam; r++) {
     const uint32_t mk = __reduce_max_sync(FULL, lk);
     if (mk == 0u) break;
-    const unsigned tl = __ballot_sync(FULL, lk == mk);
+    const unsigned tl = __ballot_sync(FULL, mk - lk <= kTolG);
     const int first_lane = __ffs(tl) - 1;
-    const int cnt0 = __shfl_sync(FULL, lcnt, first_lane);
+    const uint32_t second = __shfl_sync(FULL, lk2, first_lane);
     int win;
-    if ((tl & (tl - 1)) == 0u && cnt0 == 1) {
+    if ((tl & (tl - 1)) == 0u && (second == 0u || mk - second > kTolG)) {
       win = __shfl_sync(FULL, li, first_lane);
     } else {
-      // equal keys: exact scores, then token sequence, then flag
+      // (near-)equal keys: exact scores, then token sequence, then flag
       win = -1;
       __syncwarp();
       if (lane == 0) {
         const int sp = w.misc[1];
         Desc dw{};
         for (int i = 0; i < nH; i++) {
-          if (w.hkey[i] != mk) continue;
+          if (w.hkey[i] == 0u || mk - w.hkey[i] > kTolG) continue;
           Desc di = i < nD ? Desc{gen_score(w, i, w.headj[i]), w.e1[i], w.stok[w.headj[i]], 0}
                            : spec_desc(w, w.spord[sp]);
           if (win < 0 || precedes(w, di, dw)) { win = i; dw = di; }
