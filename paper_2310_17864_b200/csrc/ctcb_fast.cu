@@ -824,6 +824,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         const double gA_prev = __shfl_up_sync(FULL, gA, 1);
         const bool unsorted = gen && ((me > 0 && !(gA_prev > gA + 1e-9 * (1.0 + fabs(gA)))) || __popc(gv) < beam);
         oneshot = !__any_sync(FULL, unsorted);
+        if (!oneshot && lane == 0) atomicAdd(&P.dbg[kDbgFrames], 1ull);  // diagnostics: fallback by order/length
       }
       if (oneshot) {
         if (gen) S.dG[me] = gG;

@@ -458,8 +458,8 @@ class CUCTCDecoder:
         lib = _lib.load()
         arr = (ctypes.c_uint64 * 8)()
         _lib.check(lib.ctcb_debug_counters(self._h, arr), "ctcb_debug_counters")
-        names = ("key_ties", "exact_ties", "materializations", "materialize_steps", "radix_fallbacks", "frames",
-                 "topk_fixups", "oneshot_fallbacks")
+        names = ("key_ties", "exact_ties", "materializations", "materialize_steps", "radix_fallbacks",
+                 "oneshot_unordered", "topk_fixups", "oneshot_fallbacks")
         return {n: int(arr[i]) for i, n in enumerate(names)}
 
     def debug_frames(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor):
