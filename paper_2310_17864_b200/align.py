@@ -83,9 +83,11 @@ def _log_probs(e) -> np.ndarray:
     return lp
 
 
-def forced_align_batch(emissions, targets, tokens=None, device: int = 0) -> list:
+def forced_align_batch(emissions, targets, tokens=None, device: int = 0, raise_errors: bool = True) -> list:
     """Align a batch in one ``ctcb_align`` launch; ``tokens`` is a
-    TokenDictionary-like object (``blank_index``), a blank index, or None (0)."""
+    TokenDictionary-like object (``blank_index``), a blank index, or None (0).
+    With ``raise_errors=False`` a failing utterance yields its error message
+    (str) in place of an AlignmentResult."""
     blank = _blank_of(tokens)
     lps = [_log_probs(e) for e in emissions]
     tgs = [[int(t) for t in tg] for tg in targets]
@@ -103,7 +105,7 @@ def forced_align_batch(emissions, targets, tokens=None, device: int = 0) -> list
     dev = torch.device("cuda", device)
     x = torch.zeros((B, T, V), dtype=torch.float32)
     for b, lp in enumerate(lps):
-        x[b, : lp.shape[0]] = torch.from_numpy(np.ascontiguousarray(lp, dtype=np.float32))
+        x[b, : lp.shape[0]] = torch.from_numpy(np.array(lp, dtype=np.float32))
     x = x.to(dev)
     lens = torch.tensor([lp.shape[0] for lp in lps], dtype=torch.int32, device=dev)
     offs = np.zeros(B + 1, dtype=np.int32)
@@ -131,7 +133,11 @@ def forced_align_batch(emissions, targets, tokens=None, device: int = 0) -> list
     for b in range(B):
         Tb = lps[b].shape[0]
         if st[b] != ALIGN_OK:
-            raise ValueError(f"utterance {b}: " + _message(int(st[b]), tgs[b], Tb, V))
+            msg = _message(int(st[b]), tgs[b], Tb, V)
+            if raise_errors:
+                raise ValueError(f"utterance {b}: " + msg)
+            out.append(msg)
+            continue
         fl = lab[b, :Tb].astype(np.int64)
         fs = sco[b, :Tb].astype(np.float64)
         out.append(AlignmentResult(frame_labels=fl, frame_scores=fs, spans=_spans_from_labels(fl, fs, blank)))
@@ -165,3 +171,36 @@ def forced_align(emissions, targets, tokens=None, device: int = 0) -> AlignmentR
     except ValueError as exc:
         msg = str(exc)
         raise ValueError(msg.split(": ", 1)[1] if msg.startswith("utterance 0: ") else msg) from None
+
+
+@dataclass(frozen=True)
+class WordSpan:
+    word: str
+    start_frame: int
+    end_frame: int  # exclusive
+    score: float
+
+
+def align_words(result: AlignmentResult, tokens, transcript: list, lexicon) -> list:
+    """Group token spans into word spans (align.py:168-212); ``lexicon.entries``
+    maps word -> list of spellings (tuples of token indices)."""
+    spellings = []
+    for word in transcript:
+        variants = lexicon.entries.get(word)
+        if not variants:
+            raise ValueError(f"word {word!r} is not in the lexicon")
+        spellings.append(variants[0])
+    flat = [tok for sp in spellings for tok in sp]
+    aligned = [span.token for span in result.spans]
+    if flat != aligned:
+        raise ValueError("concatenated transcript spellings do not match the aligned targets")
+    out = []
+    pos = 0
+    for word, spelling in zip(transcript, spellings):
+        group = result.spans[pos: pos + len(spelling)]
+        pos += len(spelling)
+        frames = sum(sp.end_frame - sp.start_frame for sp in group)
+        total = sum(float(result.frame_scores[sp.start_frame: sp.end_frame].sum()) for sp in group)
+        out.append(WordSpan(word=word, start_frame=group[0].start_frame, end_frame=group[-1].end_frame,
+                            score=total / frames))
+    return out

@@ -1,7 +1,11 @@
-"""``decode`` command on the GPU: the reference's CLI caller of the decoder path
-(ctcforge cli.py:262-312) with the same inputs, flags,
-outputs and exit codes, decoding every utterance of a corpus in batched
-``ctcb_decode`` launches instead of one CPU process per utterance.
+"""``decode`` and ``align`` commands on the GPU: the reference's CLI callers of
+the decoder and alignment paths (ctcforge cli.py:262-388, SURVEY.md §8(f1),
+(f4)) with the same inputs, flags, outputs and exit codes, processing a corpus
+in batched ``ctcb_decode`` / ``ctcb_align`` launches instead of one CPU call per
+utterance.
+
+    python -m paper_2310_17864_b200 align --emissions DIR|FILE --tokens FILE --refs REFS
+        [--lexicon LEX] [--out OUT.jsonl] [--attribute-blanks] [--no-strict-validation]
 
     python -m paper_2310_17864_b200 decode --emissions DIR|FILE --tokens FILE --out OUT.jsonl
         [--config JSON] [--beam-size N] [--beam-threshold X] [--blank-skip-threshold P]
@@ -60,7 +64,7 @@ DEFAULTS = {  # cli.py:41-65
     "beam_size": 10, "beam_size_token": None, "beam_threshold": 50.0, "lm_weight": 2.0,
     "word_score": 0.0, "sil_score": 0.0, "blank_skip_threshold": 1.0, "nbest": 1, "merge": "logadd",
     "workers": 1, "strict_validation": True, "blank_token": None, "silence_token": None,
-    "gpu_batch": 1024, "device": 0,
+    "gpu_batch": 1024, "device": 0, "refs": None, "attribute_blanks": False,
 }
 
 
@@ -188,6 +192,75 @@ def write_emissions(log_probs: np.ndarray, path) -> None:
         fh.write(lp.astype("<f4").tobytes())
 
 
+# --------------------------------------------------------------------------- lexicon / transcripts
+class LexiconFormatError(ValueError):
+    """A lexicon file line is malformed (lexicon.py:14-15)."""
+
+
+@dataclasses.dataclass
+class Lexicon:
+    words: list
+    entries: dict  # word -> list of spellings (tuples of token indices)
+
+
+def parse_lexicon(path, tokens: TokenDictionary) -> Lexicon:
+    """"word token token ..." lines, '#' comments, variants per word
+    (lexicon.py:87-122)."""
+    path = Path(path)
+    index = {tok: i for i, tok in enumerate(tokens.tokens)}
+    words, entries = [], {}
+    for lineno, raw in enumerate(path.read_text(encoding="utf-8").splitlines(), 1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        fields = line.split()
+        word, spelling_toks = fields[0], fields[1:]
+        if not spelling_toks:
+            raise LexiconFormatError(f"{path}: line {lineno}: empty spelling")
+        spelling = []
+        for tok in spelling_toks:
+            if tok not in index:
+                raise LexiconFormatError(f"{path}: line {lineno}: unknown spelling token {tok!r}")
+            spelling.append(index[tok])
+        spelling = tuple(spelling)
+        if word not in entries:
+            entries[word] = []
+            words.append(word)
+        if spelling in entries[word]:
+            raise LexiconFormatError(f"{path}: line {lineno}: duplicate spelling for {word!r}")
+        entries[word].append(spelling)
+    return Lexicon(words=words, entries=entries)
+
+
+def read_refs(path) -> dict:
+    """One utterance per line: "utt_id<TAB>word word word" (cli.py:182-195)."""
+    refs = {}
+    for lineno, line in enumerate(Path(path).read_text(encoding="utf-8").splitlines(), 1):
+        if not line.strip():
+            continue
+        utt_id, sep, rest = line.partition("\t")
+        if not utt_id or not sep:
+            raise ConfigError(f"--refs: line {lineno}: expected 'utt_id<TAB>words'")
+        refs[utt_id.strip()] = rest.split()
+    return refs
+
+
+def check_emission_matrix(lp: np.ndarray, strict: bool) -> None:
+    """EmissionMatrix.__post_init__ checks (emissions.py:128-150) on the host."""
+    lp = lp.astype(np.float64)
+    if lp.size and lp.max() > MAX_LOG_PROB:
+        t, v = np.argwhere(lp > MAX_LOG_PROB)[0]
+        raise ValueError(f"log-probability above 0 at frame {t}, token {v}: {lp[t, v]:.6g}")
+    if strict and lp.size:
+        m = lp.max(axis=1)
+        norms = m + np.log(np.exp(lp - m[:, None]).sum(axis=1))
+        off = np.abs(norms) > ROW_NORM_TOL
+        if off.any():
+            t = int(np.argmax(off))
+            raise ValueError(f"frame {t} is not normalized: log-sum-exp = {norms[t]:.6g} "
+                             f"(tolerance {ROW_NORM_TOL}); pass strict=False to skip this check")
+
+
 # --------------------------------------------------------------------------- config
 def _merge_config(args: argparse.Namespace) -> dict:
     """CLI > --config JSON > defaults (cli.py:130-148)."""
@@ -201,7 +274,7 @@ def _merge_config(args: argparse.Namespace) -> dict:
         if not isinstance(file_values, dict):
             raise ConfigError("--config: expected a JSON object")
         for key, value in file_values.items():
-            if key not in DEFAULTS and key not in ("refs", "hyps", "figure", "attribute_blanks", "json"):
+            if key not in DEFAULTS and key not in ("hyps", "figure", "json"):
                 raise ConfigError(f"--config: unknown key {key!r}")
             merged[key] = value
     for key in DEFAULTS:
@@ -378,6 +451,96 @@ def _decode_group(dec, tokens, ids, lps, strict, torch, _lib):
     return records, errors
 
 
+# --------------------------------------------------------------------------- align
+def cmd_align(cfg: dict) -> int:
+    """Force-align transcripts to emissions (cli.py:327-388) with one
+    ``ctcb_align`` launch per batch of utterances; records in utterance order,
+    an ``{"utt", "error"}`` record per failed utterance."""
+    for name in ("emissions", "tokens", "refs"):
+        if cfg[name] is None:
+            raise ConfigError(f"--{name.replace('_', '-')} is required")
+    for name in ("emissions", "tokens", "refs", "lexicon"):
+        if cfg[name] is not None and not Path(cfg[name]).exists():
+            raise ConfigError(f"--{name.replace('_', '-')}: file not found: {cfg[name]}")
+    try:
+        tokens = TokenDictionary.from_file(cfg["tokens"], blank_token=cfg["blank_token"],
+                                           silence_token=cfg["silence_token"])
+    except ValueError as exc:
+        raise ConfigError(f"--tokens: {exc}") from exc
+    lexicon = parse_lexicon(cfg["lexicon"], tokens) if cfg["lexicon"] else None
+    refs = read_refs(cfg["refs"])
+    utts = _discover_utterances(cfg["emissions"])
+    from . import align as galign
+
+    strict = bool(cfg["strict_validation"])
+    batch = int(cfg["gpu_batch"])
+    failed = 0
+    out = sys.stdout if cfg["out"] is None else open(cfg["out"], "w", encoding="utf-8")
+    index = {t: i for i, t in enumerate(tokens.tokens)}
+    try:
+        for i0 in range(0, len(utts), batch):
+            group = utts[i0:i0 + batch]
+            prepared, results = [], {}
+            for utt_id, path in group:
+                try:
+                    if utt_id not in refs:
+                        raise ValueError(f"no transcript for {utt_id} in --refs")
+                    transcript = refs[utt_id]
+                    lp = parse_emissions(path, len(tokens))
+                    check_emission_matrix(lp, strict)
+                    if lexicon is not None:
+                        targets = []
+                        for word in transcript:
+                            variants = lexicon.entries.get(word)
+                            if not variants:
+                                raise ValueError(f"word {word!r} is not in the lexicon")
+                            targets.extend(variants[0])
+                    else:
+                        targets = []
+                        for tok in transcript:  # TokenDictionary.index (emissions.py:69-73)
+                            if tok not in index:
+                                raise KeyError(f"unknown token: {tok!r}")
+                            targets.append(index[tok])
+                    prepared.append((utt_id, transcript, lp, targets))
+                except Exception as exc:  # noqa: BLE001 - per-utterance failure, as cli.py:339-344
+                    results[utt_id] = str(exc)
+            if prepared:
+                aligned = galign.forced_align_batch([p[2] for p in prepared], [p[3] for p in prepared], tokens,
+                                                    device=int(cfg["device"]), raise_errors=False)
+                for (utt_id, transcript, _, _), r in zip(prepared, aligned):
+                    results[utt_id] = (transcript, r) if not isinstance(r, str) else r
+            for utt_id, _ in group:
+                r = results[utt_id]
+                try:
+                    if isinstance(r, str):
+                        raise ValueError(r)
+                    records = _align_records(cfg, tokens, lexicon, utt_id, *r, galign)
+                except Exception as exc:  # noqa: BLE001
+                    out.write(json.dumps({"utt": utt_id, "error": str(exc)}, sort_keys=True, ensure_ascii=False) + "\n")
+                    log.error("utterance %s failed: %s", utt_id, exc)
+                    failed += 1
+                    continue
+                for record in records:
+                    out.write(json.dumps(record, sort_keys=True, ensure_ascii=False) + "\n")
+    finally:
+        if out is not sys.stdout:
+            out.close()
+    return 1 if failed else 0
+
+
+def _align_records(cfg, tokens, lexicon, utt_id, transcript, result, galign) -> list:
+    import math
+
+    spans = galign.attribute_blanks(result) if cfg["attribute_blanks"] else result.spans
+    records = [{"utt": utt_id, "token": tokens.tokens[sp.token], "start": sp.start_frame, "end": sp.end_frame,
+                "score": sp.score, "prob": math.exp(sp.score)} for sp in spans]
+    if lexicon is not None:
+        for ws in galign.align_words(result, tokens, transcript, lexicon):
+            records.append({"utt": utt_id, "word": ws.word, "start": ws.start_frame, "end": ws.end_frame,
+                            "score": ws.score, "prob": math.exp(ws.score)})
+    return records
+
+
 # --------------------------------------------------------------------------- argparse
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_2310_17864_b200",
@@ -407,6 +570,22 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--workers", type=int, default=_UNSET, help="accepted for compatibility (the GPU batches)")
     p.add_argument("--gpu-batch", type=int, default=_UNSET, dest="gpu_batch", help="utterances per launch")
     p.add_argument("--device", type=int, default=_UNSET)
+
+    p = sub.add_parser("align", help="force-align transcripts to emissions")
+    p.add_argument("--config", default=_UNSET, help="JSON config file")
+    p.add_argument("--tokens", default=_UNSET, help="token file, one token per line")
+    p.add_argument("--blank-token", default=_UNSET, dest="blank_token")
+    p.add_argument("--silence-token", default=_UNSET, dest="silence_token")
+    p.add_argument("--strict-validation", action=argparse.BooleanOptionalAction, default=_UNSET,
+                   dest="strict_validation")
+    p.add_argument("--emissions", default=_UNSET, help="emission file or directory")
+    p.add_argument("--refs", default=_UNSET, help="transcripts: utt_id<TAB>words")
+    p.add_argument("--lexicon", default=_UNSET, help="word mode: spell transcript words through this lexicon")
+    p.add_argument("--out", default=_UNSET, help="output JSON-lines path (default: stdout)")
+    p.add_argument("--attribute-blanks", action=argparse.BooleanOptionalAction, default=_UNSET,
+                   dest="attribute_blanks", help="widen spans so blanks attach to the preceding token")
+    p.add_argument("--gpu-batch", type=int, default=_UNSET, dest="gpu_batch", help="utterances per launch")
+    p.add_argument("--device", type=int, default=_UNSET)
     return parser
 
 
@@ -417,7 +596,10 @@ def main(argv=None) -> int:
     logging.basicConfig(level=level, format="%(levelname)s %(name)s: %(message)s")
     args = build_parser().parse_args(argv)
     try:
-        return cmd_decode(_merge_config(args))
+        cfg = _merge_config(args)
+        if args.command == "align":
+            return cmd_align(cfg)
+        return cmd_decode(cfg)
     except ConfigError as exc:
         print(f"ctcforge {args.command}: {exc}", file=sys.stderr)
         return 2

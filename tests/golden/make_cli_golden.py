@@ -80,9 +80,57 @@ def main():
                 meta = json.load(fh)
             expected[name] = {"flags": flags, "exit_code": rc, "records": records, "failed": meta["failed"],
                               "options": meta["options"]}
+    # align: transcripts = the reference's own best decodes (feasible), in token
+    # and word form, plus per-utterance failures (missing transcript, unknown
+    # token / word, infeasible length)
+    best = {r["utt"]: r["nbest"][0]["tokens"] for r in expected["default"]["records"]}
+    tok_lines, word_lines, lex = [], [], {}
+    for utt, toks in sorted(best.items()):
+        if utt == "utt05":
+            continue  # no transcript
+        t = list(toks) if toks else ["u1"]
+        if utt == "utt06":
+            t = t + ["zz"]  # unknown token
+        if utt == "utt07":
+            t = t * 40  # infeasible
+        tok_lines.append(utt + "\t" + " ".join(t))
+        # words: consecutive token pairs
+        words = []
+        for i in range(0, len(toks), 2):
+            w = "w" + "_".join(toks[i:i + 2])
+            lex.setdefault(w, toks[i:i + 2])
+            words.append(w)
+        if utt == "utt08":
+            words.append("notaword")
+        word_lines.append(utt + "\t" + " ".join(words or ["wu1"]))
+    lex.setdefault("wu1", ["u1"])
+    tok_lines.append("bad_width\tu1")
+    tok_lines.append("unnormalized\tu1 u2")
+    word_lines.append("unnormalized\twu1")
+    with open(os.path.join(OUT, "refs_tokens.txt"), "w", encoding="utf-8") as fh:
+        fh.write("\n".join(tok_lines) + "\n")
+    with open(os.path.join(OUT, "refs_words.txt"), "w", encoding="utf-8") as fh:
+        fh.write("\n".join(word_lines) + "\n")
+    with open(os.path.join(OUT, "lexicon.txt"), "w", encoding="utf-8") as fh:
+        fh.write("# word spelling\n" + "\n".join(f"{w} {' '.join(sp)}" for w, sp in lex.items()) + "\n")
+    ALIGN_RUNS = {
+        "align_tokens": ["--refs", os.path.join(OUT, "refs_tokens.txt")],
+        "align_tokens_tiled": ["--refs", os.path.join(OUT, "refs_tokens.txt"), "--attribute-blanks"],
+        "align_tokens_nonstrict": ["--refs", os.path.join(OUT, "refs_tokens.txt"), "--no-strict-validation"],
+        "align_words": ["--refs", os.path.join(OUT, "refs_words.txt"), "--lexicon", os.path.join(OUT, "lexicon.txt")],
+    }
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, flags in ALIGN_RUNS.items():
+            out = os.path.join(tmp, name + ".jsonl")
+            rc = ref_cli.main(["align", "--emissions", corpus, "--tokens", os.path.join(OUT, "tokens.txt"),
+                               "--out", out] + flags)
+            with open(out, encoding="utf-8") as fh:
+                records = [json.loads(line) for line in fh]
+            expected[name] = {"flags": [os.path.basename(f) if os.sep in f else f for f in flags],
+                              "exit_code": rc, "records": records}
     with open(os.path.join(OUT, "expected.json"), "w", encoding="utf-8") as fh:
         json.dump(expected, fh, sort_keys=True, indent=1)
-    print({k: (v["exit_code"], len(v["records"]), v["failed"]) for k, v in expected.items()})
+    print({k: (v["exit_code"], len(v["records"]), v.get("failed")) for k, v in expected.items()})
 
 
 if __name__ == "__main__":

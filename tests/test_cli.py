@@ -136,3 +136,30 @@ def test_decode_single_file_and_small_batches(tmp_path):
         rec = [json.loads(line) for line in fh]
     ref = [r for r in exp["records"] if r["utt"] == "utt03"]
     assert [r["nbest"][0]["token_ids"] for r in rec] == [r["nbest"][0]["token_ids"] for r in ref]
+
+
+def _norm_paths(records):
+    # error texts carry the emission file path of the machine that ran the command
+    out = []
+    for r in records:
+        r = dict(r)
+        if "error" in r:
+            r["error"] = r["error"].replace(os.path.abspath(CORPUS) + os.sep, "").replace(
+                "/root/repo/tests/golden/cli/corpus/", "")
+        out.append(r)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("run", ["align_tokens", "align_tokens_tiled", "align_tokens_nonstrict", "align_words"])
+def test_align_matches_reference_command(tmp_path, run):
+    """The GPU align command (token and word modes, tiled spans, per-utterance
+    error records) against the reference `ctcforge align` output."""
+    exp = expected()[run]
+    flags = [os.path.join(GOLD, f) if f.endswith(".txt") else f for f in exp["flags"]]
+    out = str(tmp_path / "a.jsonl")
+    rc = cli.main(["align", "--emissions", CORPUS, "--tokens", TOKENS, "--out", out] + flags)
+    assert rc == exp["exit_code"]
+    with open(out, encoding="utf-8") as fh:
+        got = [json.loads(line) for line in fh]
+    assert _norm_paths(got) == _norm_paths(exp["records"])
