@@ -16,4 +16,5 @@ from .decoder import (  # noqa: F401
     cuda_ctc_decoder,
     skip_cutoff,
 )
-from .shard import lpt_shards  # noqa: F401
+from .multi import MultiDeviceDecoder  # noqa: F401
+from .shard import balanced_ranges, lpt_shards  # noqa: F401

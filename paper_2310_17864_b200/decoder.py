@@ -27,6 +27,7 @@ arguments, allocates through PyTorch's caching allocator and converts results.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import gc
 from typing import List, NamedTuple, Optional, Union
@@ -174,6 +175,11 @@ class CUCTCDecoder:
         s = self.cuda_stream if self.cuda_stream is not None else torch.cuda.current_stream(self.device)
         return ctypes.c_void_p(s.cuda_stream)
 
+    def _on_stream(self):
+        # with an explicit cuda_stream, output allocation/initialisation, the
+        # launch and the result copies are all ordered on that stream
+        return torch.cuda.stream(self.cuda_stream) if self.cuda_stream is not None else contextlib.nullcontext()
+
     def _check_inputs(self, log_prob: torch.Tensor, lens: torch.Tensor):
         if not isinstance(log_prob, torch.Tensor) or log_prob.dim() != 3:
             raise ValueError("log_prob must be a 3-D tensor [batch, frames, tokens]")
@@ -209,7 +215,7 @@ class CUCTCDecoder:
             self._ws = torch.empty(max(n.value, 1), dtype=torch.uint8, device=self.device)
         return self._ws
 
-    def _validate(self, log_prob: torch.Tensor, lens: torch.Tensor) -> None:
+    def _validate(self, log_prob: torch.Tensor, lens: torch.Tensor, offset: int = 0) -> None:
         lib = _lib.load()
         B, T, _ = log_prob.shape
         err = torch.empty(4, dtype=torch.int64, device=self.device)
@@ -220,23 +226,30 @@ class CUCTCDecoder:
         if code == 0:
             return
         x = float(log_prob[b, t, v]) if v >= 0 else None
+        u = b + offset
         # EmissionMatrix.__post_init__ messages (emissions.py:133-150), tagged as decode_batch does
         if code == 1:
-            raise ValueError(f"utterance {b}: non-finite log-probability at frame {t}, token {v}")
+            raise ValueError(f"utterance {u}: non-finite log-probability at frame {t}, token {v}")
         if code == 2:
-            raise ValueError(f"utterance {b}: log-probability above 0 at frame {t}, token {v}: {x:.6g}")
+            raise ValueError(f"utterance {u}: log-probability above 0 at frame {t}, token {v}: {x:.6g}")
         row = log_prob[b, t].double()
         norm = float(torch.logsumexp(row, 0))
-        raise ValueError(f"utterance {b}: frame {t} is not normalized: log-sum-exp = {norm:.6g} "
+        raise ValueError(f"utterance {u}: frame {t} is not normalized: log-sum-exp = {norm:.6g} "
                          f"(tolerance 0.001); pass strict=False to skip this check")
 
     # ------------------------------------------------------------------ API
-    def decode(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor, timesteps: bool = False) -> DecodeOutput:
+    def decode(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor, timesteps: bool = False,
+               offset: int = 0) -> DecodeOutput:
         """Enqueue a decode on the decoder's stream and return device tensors
-        (no synchronisation)."""
+        (no synchronisation).  ``offset`` shifts the batch indices in error
+        messages (a range of a larger batch)."""
+        with self._on_stream():
+            return self._decode(log_prob, encoder_out_lens, timesteps, offset)
+
+    def _decode(self, log_prob, encoder_out_lens, timesteps: bool, offset: int) -> DecodeOutput:
         log_prob, lens = self._check_inputs(log_prob, encoder_out_lens)
         if self.validate:
-            self._validate(log_prob, lens)
+            self._validate(log_prob, lens, offset)
         lib = _lib.load()
         B, T, _ = log_prob.shape
         dev = self.device
@@ -256,14 +269,19 @@ class CUCTCDecoder:
             vp(out_score.data_ptr()), vp(out_count.data_ptr()), vp(out_status.data_ptr())), "ctcb_decode")
         return DecodeOutput(out_tok, out_ts, out_len, out_score, out_count, out_status)
 
-    def to_host(self, out: DecodeOutput):
+    def to_host(self, out: DecodeOutput, offset: int = 0):
         """Synchronise and copy results to the host; raise the reference's
-        errors for failed utterances.  Returns numpy arrays
-        (tokens [B, nbest, Lmax], timesteps or None, lengths, scores, counts)."""
+        errors for failed utterances (batch indices shifted by ``offset``).
+        Returns numpy arrays (tokens [B, nbest, Lmax], timesteps or None,
+        lengths, scores, counts)."""
+        with self._on_stream():
+            return self._to_host(out, offset)
+
+    def _to_host(self, out: DecodeOutput, offset: int):
         status = out.status.cpu().numpy()
         counts = out.counts.cpu().numpy()
         lengths = out.lengths.cpu().numpy()
-        self._raise_status(status, out.tokens.shape[2], lengths)
+        self._raise_status(status, out.tokens.shape[2], lengths, offset)
         scores = out.scores.cpu().numpy()
         lmax = int(lengths.max()) if lengths.size else 0
         tokens = out.tokens[:, :, :lmax].cpu().numpy()
@@ -320,7 +338,7 @@ class CUCTCDecoder:
             self._pin_key = key
         return [t.numpy() for t in self._pin]
 
-    def _decode_host_chunks(self, log_prob: torch.Tensor, encoder_out_lens, chunks: int):
+    def _decode_host_chunks(self, log_prob: torch.Tensor, encoder_out_lens, chunks: int, offset: int = 0):
         """Pipelined host path (``ctcb_decode_host_async``): yields
         (b0, b1, tokens, lengths, scores, counts) per utterance range as soon as
         that range's results are on the host, while later ranges are still
@@ -361,24 +379,26 @@ class CUCTCDecoder:
                            "ctcb_decode_host_wait")  # drain before raising
                 err = status.copy()
                 err[:lo] = _lib.UTT_OK
-                self._raise_status(err, T, ln)
+                self._raise_status(err, T, ln, offset)
             yield lo, hi, tok[lo:hi], ln[lo:hi], sc[lo:hi], cnt[lo:hi]
 
-    def _raise_status(self, status: np.ndarray, T: int, lengths=None) -> None:
+    def _raise_status(self, status: np.ndarray, T: int, lengths=None, offset: int = 0) -> None:
+        # ``offset``: batch index of status[0] in the caller's batch (multi-device ranges)
         if (status < 0).any():
             raise _lib.CtcbError(f"ctcb_decode left {(status < 0).sum()} utterance(s) unprocessed (kernel did not run)")
         bad = np.flatnonzero(status != _lib.UTT_OK)
         if bad.size:
             b = int(bad[0])
+            u = b + offset
             if status[b] == _lib.UTT_EMPTY:
-                raise ValueError(f"utterance {b}: empty emissions")
+                raise ValueError(f"utterance {u}: empty emissions")
             if status[b] == _lib.UTT_BEAM_DIED:
                 # decoder.py:616-620; the kernel leaves the kept-frame index in lengths[b, 0]
                 t = int(np.asarray(lengths)[b, 0]) if lengths is not None else "?"
                 K = self.beam_size_token or len(self.vocab_list)
-                raise ValueError(f"utterance {b}: beam died at frame {t}: no extension survives "
+                raise ValueError(f"utterance {u}: beam died at frame {t}: no extension survives "
                                  f"(beam_size_token={K} may be too small)")
-            raise ValueError(f"utterance {b}: length out of range [1, {T}]")
+            raise ValueError(f"utterance {u}: length out of range [1, {T}]")
 
     def __call__(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor) -> List[List[CUCTCHypothesis]]:
         """Decode a batch: ``log_prob`` float32 [B, T, V] (log-softmax output),
@@ -465,6 +485,10 @@ class CUCTCDecoder:
     def debug_frames(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor):
         """Minimum slice: (frame_map [B,T], kept [B], topk_tok [B,T,k],
         topk_val [B,T,k], blank [B,T]) device tensors after synchronisation."""
+        with self._on_stream():
+            return self._debug_frames(log_prob, encoder_out_lens)
+
+    def _debug_frames(self, log_prob, encoder_out_lens):
         log_prob, lens = self._check_inputs(log_prob, encoder_out_lens)
         lib = _lib.load()
         B, T, _ = log_prob.shape

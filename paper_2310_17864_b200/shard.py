@@ -32,6 +32,31 @@ def lpt_shards(lens, n_ranks: int) -> list[np.ndarray]:
     return [np.array(sorted(s), dtype=np.int64) for s in shards]
 
 
+def balanced_ranges(lens, n_parts: int) -> list[tuple[int, int]]:
+    """Split ``range(len(lens))`` into ``n_parts`` consecutive ranges with
+    balanced Σ max(len, 1): part k ends at the first index whose prefix load
+    reaches (k+1)/n of the total.  Consecutive ranges are views of a [B, T, V]
+    batch (no host gather), and each device's kernel orders its own range
+    longest-first, so only the per-range sums need balancing.  Empty ranges
+    appear when n_parts > len(lens)."""
+    lens = np.maximum(np.asarray(lens, dtype=np.int64), 1)
+    if n_parts < 1:
+        raise ValueError("n_parts must be >= 1")
+    B = len(lens)
+    pre = np.concatenate([[0], np.cumsum(lens)])
+    total = int(pre[-1])
+    cuts = [0]
+    for k in range(1, n_parts):
+        # smallest b with pre[b] >= k * total / n, rounded to the nearer side
+        target = total * k / n_parts
+        b = int(np.searchsorted(pre, target, side="left"))
+        if 0 < b <= B and target - pre[b - 1] < pre[b] - target:
+            b -= 1
+        cuts.append(min(max(b, cuts[-1]), B))
+    cuts.append(B)
+    return [(cuts[k], cuts[k + 1]) for k in range(n_parts)]
+
+
 def merge_shards(shards: list[np.ndarray], per_rank_results: list[list], n_total: int) -> list:
     """Reassemble per-rank result lists (in shard index order) into batch order."""
     out = [None] * n_total

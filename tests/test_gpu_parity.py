@@ -338,6 +338,36 @@ def test_host_buffer_chunked_pipeline():
     assert dec(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens)) == dev
 
 
+def test_multi_device_decoder_matches_single():
+    """MultiDeviceDecoder (consecutive length-balanced ranges, one decoder and
+    stream per entry of ``devices``; [0, 0, 0] runs three on one GPU) ==
+    the single-device decoder for CPU (pinned and pageable) and CUDA inputs;
+    errors name the utterance's index in the whole batch."""
+    from paper_2310_17864_b200 import MultiDeviceDecoder
+    cfg = dataclasses.replace(synth.CONFIGS[0], batch=700)
+    lp, lens = synth.batch(cfg)
+    single = cuda_ctc_decoder(vocab(cfg.vocab), nbest=2, beam_size=10, blank_skip_threshold=cfg.threshold)
+    ref = single(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+    multi = MultiDeviceDecoder(vocab(cfg.vocab), devices=[0, 0, 0], nbest=2, beam_size=10,
+                               blank_skip_threshold=cfg.threshold)
+    assert multi(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens)) == ref
+    assert len(multi.last_ranges) == 3 and all(b1 > b0 for b0, b1 in multi.last_ranges)
+    assert multi(torch.from_numpy(lp), torch.from_numpy(lens)) == ref
+    assert multi(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda()) == ref
+    lens2 = lens.copy()
+    b_err = multi.last_ranges[2][0] + 5
+    lens2[b_err] = 0
+    for x in (torch.from_numpy(lp), torch.from_numpy(lp).cuda()):
+        with pytest.raises(ValueError, match=f"utterance {b_err}: empty emissions"):
+            multi(x, torch.from_numpy(lens2))
+    assert multi(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens)) == ref
+    # options reach every device's decoder
+    multi.set_merge_mode("max")
+    single.set_merge_mode("max")
+    assert multi(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda()) == \
+        single(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+
+
 @pytest.mark.parametrize("force_generic", ["0", "1"])
 def test_merge_mode_max_matches_oracle(monkeypatch, force_generic):
     """merge_mode="max" (decoder.py:610-613, :789-791) on both kernels against the

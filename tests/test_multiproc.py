@@ -17,7 +17,7 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_2310_17864_b200 import synth
-from paper_2310_17864_b200.shard import lpt_shards, merge_shards
+from paper_2310_17864_b200.shard import balanced_ranges, lpt_shards, merge_shards
 
 CFG = synth.CONFIGS[0]
 INDICES = np.arange(4)
@@ -59,6 +59,27 @@ def test_lpt_shards_balanced_and_disjoint():
         assert max(loads) - min(loads) <= int(lens.max())
     with pytest.raises(ValueError):
         lpt_shards(lens, 0)
+
+
+def test_balanced_ranges_cover_and_balance():
+    """Consecutive ranges (the single-process multi-device split): they tile
+    the batch in order and each range's load is within one utterance of the
+    even share."""
+    lens = synth.lengths(synth.CONFIGS[4])
+    for n in (1, 2, 3, 4, 8):
+        ranges = balanced_ranges(lens, n)
+        assert len(ranges) == n and ranges[0][0] == 0 and ranges[-1][1] == len(lens)
+        assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+        share = lens.sum() / n
+        for b0, b1 in ranges:
+            assert abs(int(lens[b0:b1].sum()) - share) <= 2 * int(lens.max())
+    # more parts than utterances: empty ranges, still a tiling; zero lengths count as 1
+    r = balanced_ranges([5, 0, 7], 5)
+    assert r[0][0] == 0 and r[-1][1] == 3 and all(b0 <= b1 for b0, b1 in r)
+    assert sum(b1 - b0 for b0, b1 in r) == 3
+    assert balanced_ranges([], 3) == [(0, 0)] * 3
+    with pytest.raises(ValueError):
+        balanced_ranges([1, 2], 0)
 
 
 def test_sharded_decode_equals_unsharded(tmp_path):
