@@ -216,6 +216,21 @@ int ctco_blank_keep(const double* lp, int64_t T, int64_t V, int64_t blank, doubl
 int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o,
                 int32_t* out_count, int32_t* out_len, int32_t* out_tokens, int32_t* out_ts,
                 double* out_score, int32_t* out_frame_map, int64_t* out_n_kept, int64_t* err_frame) {
+  return ctco_decode_fused(lp_in, T_in, V, o, NULL, out_count, out_len, out_tokens, out_ts, out_score, NULL,
+                           out_frame_map, out_n_kept, err_frame);
+}
+
+/* With fusion (fu != NULL): token-level LM scores enter every append as
+ * (h + e_c) + w * L[state, c], then the silence bonus (decoder.py:467-473,
+ * :485-486); hypotheses carry their LM context and LM total (payload of the
+ * group's best member); finalize adds w * finish(state) (decoder.py:770-777). */
+int ctco_decode_fused(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o, const ctco_fusion* fu,
+                      int32_t* out_count, int32_t* out_len, int32_t* out_tokens, int32_t* out_ts,
+                      double* out_score, double* out_lm, int32_t* out_frame_map, int64_t* out_n_kept,
+                      int64_t* err_frame) {
+  const int use_lm = fu && fu->lm_score;
+  const int64_t sil = fu ? fu->sil : -1;
+  const double wlm = use_lm ? fu->lm_weight : 0.0;
   if (T_in == 0) return CTCO_ERR_EMPTY; /* decoder.py:117-118 */
   if (o->beam < 1 || o->n_best < 1 || o->n_best > o->beam || !(o->beam_threshold > 0) ||
       !(o->skip_threshold > 0.0 && o->skip_threshold <= 1.0) || o->blank < 0 || o->blank >= V)
@@ -251,6 +266,11 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
           *n_last = (int64_t*)malloc((size_t)Hcap * sizeof(int64_t)), *n_flag = (int64_t*)malloc((size_t)Hcap * sizeof(int64_t)),
           *n_ts = (int64_t*)malloc((size_t)Hcap * sizeof(int64_t));
   h_score[0] = 0.0; h_prefix[0] = 0; h_parent[0] = -1; h_last[0] = -1; h_flag[0] = 1; h_ts[0] = -1;
+  int64_t* h_state = (int64_t*)calloc((size_t)Hcap, sizeof(int64_t));
+  int64_t* n_state = (int64_t*)calloc((size_t)Hcap, sizeof(int64_t));
+  double* h_lm = (double*)calloc((size_t)Hcap, sizeof(double));
+  double* n_lm = (double*)calloc((size_t)Hcap, sizeof(double));
+  h_state[0] = use_lm ? fu->lm_start : 0;
 
   int64_t* ck = (int64_t*)malloc((size_t)V * sizeof(int64_t));
   int64_t* order = (int64_t*)malloc((size_t)V * sizeof(int64_t));
@@ -261,6 +281,8 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
   int64_t* c_flg = (int64_t*)malloc((size_t)ncand_cap * sizeof(int64_t));
   int64_t* c_src = (int64_t*)malloc((size_t)ncand_cap * sizeof(int64_t));
   double* c_score = (double*)malloc((size_t)ncand_cap * sizeof(double));
+  double* c_lm = (double*)malloc((size_t)ncand_cap * sizeof(double));
+  int64_t* c_st = (int64_t*)malloc((size_t)ncand_cap * sizeof(int64_t));
   group_t* grp = (group_t*)malloc((size_t)ncand_cap * sizeof(group_t));
   double* gtmp = (double*)malloc((size_t)ncand_cap * sizeof(double));
   int64_t* gidx = (int64_t*)malloc((size_t)ncand_cap * sizeof(int64_t));
@@ -290,11 +312,13 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
     if (has_blank)
       for (int64_t h = 0; h < H; h++) {
         c_par[n] = h_parent[h]; c_tok[n] = h_last[h]; c_flg[n] = 1; c_src[n] = h;
+        c_lm[n] = h_lm[h]; c_st[n] = h_state[h];
         c_score[n] = h_score[h] + em[blank]; n++;
       }
     for (int64_t h = 0; h < H; h++) {
       if (!h_flag[h] && h_last[h] >= 0 && selset[h_last[h]]) {
         c_par[n] = h_parent[h]; c_tok[n] = h_last[h]; c_flg[n] = 0; c_src[n] = h;
+        c_lm[n] = h_lm[h]; c_st[n] = h_state[h];
         c_score[n] = h_score[h] + em[h_last[h]]; n++;
       }
     }
@@ -304,7 +328,18 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
         int64_t c = ck[j];
         int blocked = (c == h_last[h]) && !h_flag[h]; /* decoder.py:495-496 */
         c_par[n] = h_prefix[h]; c_tok[n] = c; c_flg[n] = 0; c_src[n] = h;
-        c_score[n] = blocked ? -INFINITY : h_score[h] + em[c]; n++;
+        double sc = h_score[h] + em[c];
+        if (use_lm) {
+          const double d = fu->lm_score[h_state[h] * V + c];
+          sc = sc + wlm * d;
+          c_lm[n] = h_lm[h] + d;
+          c_st[n] = fu->lm_next[h_state[h] * V + c];
+        } else {
+          c_lm[n] = h_lm[h];
+          c_st[n] = h_state[h];
+        }
+        if (c == sil) sc = sc + fu->sil_score;
+        c_score[n] = blocked ? -INFINITY : sc; n++;
       }
 
     /* merge on the packed key (decoder.py:595-613, :634-646): left fold in
@@ -374,6 +409,7 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
       }
       n_score[r] = g->score; n_prefix[r] = pid; n_parent[r] = p; n_last[r] = c;
       n_flag[r] = c_flg[w]; n_ts[r] = ts;
+      n_lm[r] = c_lm[w]; n_state[r] = c_st[w];
     }
     H = Hn;
     memcpy(h_score, n_score, (size_t)H * sizeof(double));
@@ -382,6 +418,8 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
     memcpy(h_last, n_last, (size_t)H * sizeof(int64_t));
     memcpy(h_flag, n_flag, (size_t)H * sizeof(int64_t));
     memcpy(h_ts, n_ts, (size_t)H * sizeof(int64_t));
+    memcpy(h_lm, n_lm, (size_t)H * sizeof(double));
+    memcpy(h_state, n_state, (size_t)H * sizeof(int64_t));
   }
 
   if (rc == CTCO_OK) {
@@ -391,14 +429,20 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
     double* fbest = gtmp;
     int64_t F = 0;
     for (int64_t h = 0; h < H; h++) {
+      double sh = h_score[h];
+      if (use_lm) { /* decoder.py:770-777 */
+        const double fz = fu->lm_fin[h_state[h]];
+        sh += wlm * fz;
+        h_lm[h] += fz;
+      }
       int64_t f = -1;
       for (int64_t j = 0; j < F; j++) if (fin[j].par == h_prefix[h]) { f = j; break; }
       if (f < 0) {
-        fin[F].score = h_score[h]; fin[F].par = h_prefix[h]; fin[F].tok = -1; fin[F].flg = 0;
-        fin[F].winner = h; fin[F].key = 0; fbest[F] = h_score[h]; F++;
+        fin[F].score = sh; fin[F].par = h_prefix[h]; fin[F].tok = -1; fin[F].flg = 0;
+        fin[F].winner = h; fin[F].key = 0; fbest[F] = sh; F++;
       } else {
-        fin[f].score = logadd ? np_logaddexp(fin[f].score, h_score[h]) : (h_score[h] > fin[f].score ? h_score[h] : fin[f].score);
-        if (h_score[h] > fbest[f]) { fbest[f] = h_score[h]; fin[f].winner = h; }
+        fin[f].score = logadd ? np_logaddexp(fin[f].score, sh) : (sh > fin[f].score ? sh : fin[f].score);
+        if (sh > fbest[f]) { fbest[f] = sh; fin[f].winner = h; }
       }
     }
     /* express prefix id p as (parent, token) so group_cmp's sequence order applies */
@@ -414,6 +458,7 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
     for (int64_t r = 0; r < nb; r++) {
       const group_t* g = &fin[gidx[r]];
       out_score[r] = g->score;
+      if (out_lm) out_lm[r] = h_lm[g->winner];
       /* tokens and timesteps from the best variant's ts chain (decoder.py:407-415) */
       int64_t len = 0;
       for (int64_t ts = h_ts[g->winner]; ts >= 0; ts = s.ts_parent.d[ts]) len++;
@@ -433,5 +478,6 @@ int ctco_decode(const double* lp_in, int64_t T_in, int64_t V, const ctco_opts* o
   free(n_score); free(n_prefix); free(n_parent); free(n_last); free(n_flag); free(n_ts);
   free(ck); free(order); free(selset); free(c_par); free(c_tok); free(c_flg); free(c_src); free(c_score);
   free(grp); free(gtmp); free(gidx); free(gtmp2); hm_free(&gmap);
+  free(h_state); free(n_state); free(h_lm); free(n_lm); free(c_lm); free(c_st);
   return rc;
 }

@@ -30,6 +30,40 @@ int ctco_blank_keep(const double* lp, int64_t T, int64_t V, int64_t blank, doubl
 int ctco_decode(const double* lp, int64_t T, int64_t V, const ctco_opts* opts,
                 int32_t* out_count, int32_t* out_len, int32_t* out_tokens, int32_t* out_ts,
                 double* out_score, int32_t* out_frame_map, int64_t* out_n_kept, int64_t* err_frame);
+/* Backoff n-gram LM, flattened (paper_2310_17864_b200.lm.flatten), and the
+ * dense (context x token) tables of token-level fusion (ctc_lm.c). */
+typedef struct {
+  int32_t order;
+  int64_t n;               /* n-grams */
+  const int32_t* words;    /* [n, order], -1 padded */
+  const int32_t* lengths;  /* [n] */
+  const double* logprob;   /* [n] natural log */
+  const double* backoff;   /* [n] */
+  const int32_t* start;    /* start context ids */
+  int32_t start_len;
+  int32_t eos;             /* word id of "</s>" (or <unk>), -1: OOV */
+} ctco_lm;
+int ctco_lm_tables(const ctco_lm* lm, const int32_t* token_word, int64_t V, double** score, int32_t** next,
+                   double** fin, int64_t* n_states, int32_t* start_state);
+void ctco_lm_free(double* score, int32_t* next, double* fin);
+
+/* Fusion options of the lexicon-free search (decoder.py:467-473, :531-543,
+ * :753-817): token-level LM (dense tables from ctco_lm_tables, or none) and
+ * the silence bonus. */
+typedef struct {
+  const double* lm_score;  /* [S, V] or NULL: no LM */
+  const int32_t* lm_next;  /* [S, V] */
+  const double* lm_fin;    /* [S] */
+  int32_t lm_start;
+  double lm_weight;
+  int64_t sil;             /* silence token, < 0: none */
+  double sil_score;
+} ctco_fusion;
+int ctco_decode_fused(const double* lp, int64_t T, int64_t V, const ctco_opts* opts, const ctco_fusion* fu,
+                      int32_t* out_count, int32_t* out_len, int32_t* out_tokens, int32_t* out_ts,
+                      double* out_score, double* out_lm, int32_t* out_frame_map, int64_t* out_n_kept,
+                      int64_t* err_frame);
+
 /* CTC forced alignment (align.py:46-123), ctc_align.c. */
 #define CTCO_ALIGN_EMPTY 11       /* "targets must be non-empty" */
 #define CTCO_ALIGN_BLANK 12       /* "targets must not contain the blank token" */

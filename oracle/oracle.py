@@ -33,6 +33,69 @@ class _Opts(ctypes.Structure):
     ]
 
 
+class _LM(ctypes.Structure):
+    _fields_ = [
+        ("order", ctypes.c_int32),
+        ("n", ctypes.c_int64),
+        ("words", ctypes.POINTER(ctypes.c_int32)),
+        ("lengths", ctypes.POINTER(ctypes.c_int32)),
+        ("logprob", ctypes.POINTER(ctypes.c_double)),
+        ("backoff", ctypes.POINTER(ctypes.c_double)),
+        ("start", ctypes.POINTER(ctypes.c_int32)),
+        ("start_len", ctypes.c_int32),
+        ("eos", ctypes.c_int32),
+    ]
+
+
+class _Fusion(ctypes.Structure):
+    _fields_ = [
+        ("lm_score", ctypes.POINTER(ctypes.c_double)),
+        ("lm_next", ctypes.POINTER(ctypes.c_int32)),
+        ("lm_fin", ctypes.POINTER(ctypes.c_double)),
+        ("lm_start", ctypes.c_int32),
+        ("lm_weight", ctypes.c_double),
+        ("sil", ctypes.c_int64),
+        ("sil_score", ctypes.c_double),
+    ]
+
+
+@dataclass
+class LMTables:
+    """Dense (context x token) fusion tables (ctc_lm.c; decoder.py:178-259)."""
+
+    score: np.ndarray   # float64 [S, V]
+    next: np.ndarray    # int32 [S, V]
+    fin: np.ndarray     # float64 [S]
+    start: int
+
+
+def lm_tables(flat, token_word) -> LMTables:
+    """Tables for a flattened model (paper_2310_17864_b200.lm.flatten) and a
+    per-token word map (paper_2310_17864_b200.lm.token_words)."""
+    tw = np.ascontiguousarray(token_word, dtype=np.int32)
+    words = np.ascontiguousarray(flat.words, dtype=np.int32)
+    lens = np.ascontiguousarray(flat.lengths, dtype=np.int32)
+    lp = np.ascontiguousarray(flat.logprob, dtype=np.float64)
+    bo = np.ascontiguousarray(flat.backoff, dtype=np.float64)
+    st = np.ascontiguousarray(flat.start, dtype=np.int32)
+    m = _LM(flat.order, len(lens), _ptr(words, ctypes.c_int32), _ptr(lens, ctypes.c_int32),
+            _ptr(lp, ctypes.c_double), _ptr(bo, ctypes.c_double), _ptr(st, ctypes.c_int32), flat.start_len, flat.eos)
+    ps, pn, pf = ctypes.POINTER(ctypes.c_double)(), ctypes.POINTER(ctypes.c_int32)(), ctypes.POINTER(ctypes.c_double)()
+    S = ctypes.c_int64()
+    start = ctypes.c_int32()
+    rc = _lib().ctco_lm_tables(ctypes.byref(m), _ptr(tw, ctypes.c_int32), len(tw), ctypes.byref(ps),
+                               ctypes.byref(pn), ctypes.byref(pf), ctypes.byref(S), ctypes.byref(start))
+    if rc != OK:
+        raise OracleError("LM too large for the oracle's exact tuple keys")
+    V = len(tw)
+    n = S.value
+    out = LMTables(np.ctypeslib.as_array(ps, shape=(n * V,)).reshape(n, V).copy(),
+                   np.ctypeslib.as_array(pn, shape=(n * V,)).reshape(n, V).copy(),
+                   np.ctypeslib.as_array(pf, shape=(n,)).copy(), start.value)
+    _lib().ctco_lm_free(ps, pn, pf)
+    return out
+
+
 def lib_path() -> str:
     return os.path.join(_HERE, "build", "libctc_oracle.so")
 
@@ -41,7 +104,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle with gcc (oracle/Makefile)."""
     path = lib_path()
     src = os.path.join(_HERE, "ctc_oracle.c")
-    srcs = [src, os.path.join(_HERE, "ctc_align.c")]
+    srcs = [src, os.path.join(_HERE, "ctc_align.c"), os.path.join(_HERE, "ctc_lm.c")]
     if force or not os.path.exists(path) or os.path.getmtime(path) < max(os.path.getmtime(x) for x in srcs):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return path
@@ -69,6 +132,18 @@ def _lib():
         lib.ctco_align.argtypes = [p(ctypes.c_double), ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                    p(ctypes.c_int32), ctypes.c_int64, p(ctypes.c_int32)]
         lib.ctco_align.restype = ctypes.c_int
+        lib.ctco_decode_fused.argtypes = [
+            p(ctypes.c_double), ctypes.c_int64, ctypes.c_int64, p(_Opts), p(_Fusion),
+            p(ctypes.c_int32), p(ctypes.c_int32), p(ctypes.c_int32), p(ctypes.c_int32),
+            p(ctypes.c_double), p(ctypes.c_double), p(ctypes.c_int32), p(ctypes.c_int64), p(ctypes.c_int64),
+        ]
+        lib.ctco_decode_fused.restype = ctypes.c_int
+        lib.ctco_lm_tables.argtypes = [p(_LM), p(ctypes.c_int32), ctypes.c_int64, p(p(ctypes.c_double)),
+                                       p(p(ctypes.c_int32)), p(p(ctypes.c_double)), p(ctypes.c_int64),
+                                       p(ctypes.c_int32)]
+        lib.ctco_lm_tables.restype = ctypes.c_int
+        lib.ctco_lm_free.argtypes = [p(ctypes.c_double), p(ctypes.c_int32), p(ctypes.c_double)]
+        lib.ctco_lm_free.restype = None
         _LIB = lib
     return _LIB
 
@@ -80,6 +155,7 @@ class OracleResult:
     tokens: list = field(default_factory=list)      # list[list[int]]
     scores: list = field(default_factory=list)      # list[float]
     timesteps: list = field(default_factory=list)   # list[list[int]]
+    lm_scores: list = field(default_factory=list)   # list[float] (fusion only)
     frame_map: np.ndarray | None = None             # kept original frames
 
     def __len__(self):
@@ -105,7 +181,8 @@ def blank_keep(lp: np.ndarray, threshold: float, blank: int = 0) -> np.ndarray:
 
 def decode(lp: np.ndarray, beam_size: int = 10, n_best: int = 1, blank_skip_threshold: float = 1.0,
            beam_threshold: float = 50.0, beam_size_token: int | None = None,
-           merge_mode: str = "logadd", blank: int = 0) -> OracleResult:
+           merge_mode: str = "logadd", blank: int = 0, lm: LMTables | None = None, lm_weight: float = 0.0,
+           sil: int | None = None, sil_score: float = 0.0) -> OracleResult:
     """Decode one utterance ``lp`` [T, V] (float32 is upcast exactly to float64,
     as EmissionMatrix does at emissions.py:129)."""
     lp = np.ascontiguousarray(lp, dtype=np.float64)
@@ -124,10 +201,24 @@ def decode(lp: np.ndarray, beam_size: int = 10, n_best: int = 1, blank_skip_thre
     out_ts = np.zeros((max(n_best, 1), tmax), dtype=np.int32)
     out_sc = np.zeros(max(n_best, 1), dtype=np.float64)
     fm = np.zeros(tmax, dtype=np.int32)
-    rc = _lib().ctco_decode(_ptr(lp, ctypes.c_double), t, v, ctypes.byref(opts), ctypes.byref(cnt),
-                            _ptr(out_len, ctypes.c_int32), _ptr(out_tok, ctypes.c_int32),
-                            _ptr(out_ts, ctypes.c_int32), _ptr(out_sc, ctypes.c_double),
-                            _ptr(fm, ctypes.c_int32), ctypes.byref(nk), ctypes.byref(ef))
+    out_lm = np.zeros(max(n_best, 1), dtype=np.float64)
+    if lm is None and sil is None:
+        rc = _lib().ctco_decode(_ptr(lp, ctypes.c_double), t, v, ctypes.byref(opts), ctypes.byref(cnt),
+                                _ptr(out_len, ctypes.c_int32), _ptr(out_tok, ctypes.c_int32),
+                                _ptr(out_ts, ctypes.c_int32), _ptr(out_sc, ctypes.c_double),
+                                _ptr(fm, ctypes.c_int32), ctypes.byref(nk), ctypes.byref(ef))
+    else:
+        fu = _Fusion(None, None, None, 0, float(lm_weight), -1 if sil is None else int(sil), float(sil_score))
+        if lm is not None:
+            fu.lm_score = _ptr(lm.score, ctypes.c_double)
+            fu.lm_next = _ptr(lm.next, ctypes.c_int32)
+            fu.lm_fin = _ptr(lm.fin, ctypes.c_double)
+            fu.lm_start = lm.start
+        rc = _lib().ctco_decode_fused(_ptr(lp, ctypes.c_double), t, v, ctypes.byref(opts), ctypes.byref(fu),
+                                      ctypes.byref(cnt), _ptr(out_len, ctypes.c_int32),
+                                      _ptr(out_tok, ctypes.c_int32), _ptr(out_ts, ctypes.c_int32),
+                                      _ptr(out_sc, ctypes.c_double), _ptr(out_lm, ctypes.c_double),
+                                      _ptr(fm, ctypes.c_int32), ctypes.byref(nk), ctypes.byref(ef))
     if rc == ERR_EMPTY:
         raise OracleError("empty emissions")
     if rc == ERR_ARG:
@@ -143,6 +234,7 @@ def decode(lp: np.ndarray, beam_size: int = 10, n_best: int = 1, blank_skip_thre
         res.tokens.append(out_tok[r, :n].tolist())
         res.timesteps.append(out_ts[r, :n].tolist())
         res.scores.append(float(out_sc[r]))
+        res.lm_scores.append(float(out_lm[r]))
     return res
 
 
