@@ -28,6 +28,7 @@ extern "C" {
 #endif
 
 typedef struct ctcb_handle ctcb_t;
+typedef struct ctcb_lm ctcb_lm_t;
 
 enum {
   CTCB_OK = 0,
@@ -44,6 +45,8 @@ enum {
   CTCB_UTT_BAD_LEN = 2,    /* len < 0 or len > t_max */
   CTCB_UTT_BEAM_DIED = 3,  /* no finite extension survives (decoder.py:616-620); out_len[b][0] = the
                               kept-frame index where it died */
+  CTCB_UTT_OVERFLOW = 4,   /* fused search (LM / silence bonus): more near-tied candidates at the
+                              beam cut than the kernel's window holds; out_len[b][0] = frame */
 };
 
 /* Create a decoder.  Replaces DecoderOptions (decoder.py:34-66) + the
@@ -191,6 +194,38 @@ int ctcb_align(const float* log_probs, int64_t stride_b, int64_t stride_t, const
                const int32_t* targets, const int32_t* target_offsets, int batch, int t_max, int vocab, int blank,
                int s_max, void* workspace, size_t workspace_bytes, void* stream, int32_t* out_labels,
                float* out_scores, int32_t* out_status);
+
+/* ---- Token-level LM fusion ---------------------------
+ * Replaces NGramLM + parse_arpa (lm.py:35-226) on the device and the
+ * lexicon-free fusion of _BeamSearch (decoder.py:178-259, :467-486, :753-817).
+ *
+ * ctcb_lm_create uploads a flattened backoff model: n-gram i has
+ * words[i * order .. + lengths[i]) (word ids >= 0), natural-log logprob[i] and
+ * backoff[i]; a repeated tuple keeps its last row.  `start` (start_len <=
+ * order - 1 words) is the start context (lm.py:229-233: "<s>" shrunk to a known
+ * context, or empty); `eos` the word id scored at the end ("</s>", else
+ * "<unk>", else -1 for the OOV penalty).  order <= 8. */
+int ctcb_lm_create(int order, int64_t n_ngrams, const int32_t* words, const int32_t* lengths, const double* logprob,
+                   const double* backoff, const int32_t* start, int start_len, int eos, int device,
+                   ctcb_lm_t** out);
+int ctcb_lm_destroy(ctcb_lm_t* lm);
+/* Attach a model to a decoder (NULL detaches): builds the dense context x
+ * token score / successor tables on the device.  token_word[c] (host, V
+ * entries): the LM word id of token c (its string, or "<unk>"), -1 when the
+ * string is out of vocabulary and the model has no "<unk>" (fixed penalty
+ * -20, context reset: lm.py:236-238), -2 for blank and the silence token
+ * (identity: no LM score, context kept).  weight: lm_weight.  beam <= 64. */
+int ctcb_set_lm(ctcb_t* h, const ctcb_lm_t* lm, const int32_t* token_word, double weight);
+/* Silence token (-1: none) and its per-emission bonus sil_score
+ * (decoder.py:485-486); a non-zero bonus selects the fused search (beam <= 64). */
+int ctcb_set_silence(ctcb_t* h, int silence_index, double sil_score);
+/* ctcb_decode plus out_lm: float64 [batch, nbest] LM total of each hypothesis
+ * (Hypothesis.lm_score, finish score included; decoder.py:770-777), or NULL.
+ * Scores include lm_weight * LM and the silence bonuses. */
+int ctcb_decode_lm(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
+                   int batch, int t_max, void* workspace, size_t workspace_bytes, void* stream,
+                   int32_t* out_tokens, int32_t* out_timesteps, int32_t* out_len, double* out_score,
+                   double* out_lm, int32_t* out_count, int32_t* out_status);
 
 const char* ctcb_status_string(int status);
 /* Message of the last error on this host thread. */

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CTCB_LIB") or os.path.join(_HERE, "libctcb.so")
 
 CTCB_OK, CTCB_ERR_ARG, CTCB_ERR_CUDA, CTCB_ERR_WORKSPACE, CTCB_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
-UTT_OK, UTT_EMPTY, UTT_BAD_LEN, UTT_BEAM_DIED = 0, 1, 2, 3
+UTT_OK, UTT_EMPTY, UTT_BAD_LEN, UTT_BEAM_DIED, UTT_OVERFLOW = 0, 1, 2, 3, 4
 
 # every symbol include/ctcb.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
@@ -23,6 +23,7 @@ SYMBOLS = (
     "ctcb_decode", "ctcb_decode_host", "ctcb_debug_frames", "ctcb_validate", "ctcb_debug_counters", "ctcb_status_string",
     "ctcb_last_error", "ctcb_kernel_timing", "ctcb_kernel_time", "ctcb_decode_host_async", "ctcb_decode_host_wait",
     "ctcb_set_merge_mode", "ctcb_set_beam_size_token", "ctcb_align", "ctcb_align_workspace_bytes",
+    "ctcb_lm_create", "ctcb_lm_destroy", "ctcb_set_lm", "ctcb_set_silence", "ctcb_decode_lm",
 )
 
 _lib = None
@@ -74,6 +75,12 @@ def load():
     lib.ctcb_align.argtypes = [vp, c_int64, c_int64, vp, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, c_size_t, vp,
                                vp, vp, vp]
     lib.ctcb_set_beam_size_token.argtypes = [vp, c_int]
+    lib.ctcb_lm_create.argtypes = [c_int, c_int64, vp, vp, vp, vp, vp, c_int, c_int, c_int, ctypes.POINTER(vp)]
+    lib.ctcb_lm_destroy.argtypes = [vp]
+    lib.ctcb_set_lm.argtypes = [vp, vp, vp, c_double]
+    lib.ctcb_set_silence.argtypes = [vp, c_int, c_double]
+    lib.ctcb_decode_lm.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, c_size_t, vp,
+                                   vp, vp, vp, vp, vp, vp, vp]
     lib.ctcb_kernel_time.argtypes = [vp, ctypes.POINTER(c_double), ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_char_p)]
     lib.ctcb_status_string.argtypes = [c_int]
     lib.ctcb_status_string.restype = ctypes.c_char_p

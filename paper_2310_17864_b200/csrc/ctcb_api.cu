@@ -95,6 +95,16 @@ struct ctcb_handle {
   cudaEvent_t tev[2 * 64];
   int have_tev;
   const char* last_kernel;
+  // fused search (ctcb_set_lm / ctcb_set_silence)
+  ctcb::LmTables lm;
+  int has_lm;
+  double lm_weight;
+  int sil;
+  double sil_score;
+};
+
+struct ctcb_lm {
+  ctcb::LmModel* m;
 };
 
 namespace {
@@ -102,7 +112,8 @@ namespace {
 thread_local std::string g_last_error;
 constexpr int kMaxChunks = 64;
 
-bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic; }
+bool use_fused(const ctcb_handle* h) { return h->has_lm || (h->sil >= 0 && h->sil_score != 0.0); }
+bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic && !use_fused(h); }
 // Fast kernel variant: compile-time layout when V <= kSmallV (ring 2, 2048-B rows).
 bool fast_small(const ctcb::Params& P) {
   return P.V <= ctcb::kSmallV && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes && P.tokK == 0;
@@ -230,17 +241,21 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
 // fit, then maximise resident warps per SM (occupancy API), and spread small
 // batches over all SMs (at most ceil(B / num_sms) warps per block).
 int launch_config(ctcb_handle* h, ctcb::Params& P, int B, bool fast) {
+  const bool fused = use_fused(h);
   for (;;) {
-    size_t total = fast ? ctcb::make_fast_layout(fast_small(P) ? ctcb::kSmallV : P.V, P.ring, P.row_bytes).total
-                        : ctcb::make_layout(P.beam, P.kpad, P.V, P.ring, P.row_bytes).total;
+    size_t total = fused ? ctcb::fused_smem_per_warp(P.beam, P.V, P.ring, P.row_bytes)
+                   : fast ? ctcb::make_fast_layout(fast_small(P) ? ctcb::kSmallV : P.V, P.ring, P.row_bytes).total
+                          : ctcb::make_layout(P.beam, P.kpad, P.V, P.ring, P.row_bytes).total;
     P.smem_per_warp = (int)total;
     if ((int)total <= h->max_smem_optin) break;
     if (P.ring > 1) { P.ring--; continue; }
     return fail(CTCB_ERR_UNSUPPORTED, "beam/vocabulary too large for one warp's shared memory");
   }
-  const void* kfn = fast ? fast_kernel_fn(P, use_precomp(h, B)) : (const void*)ctcb::ctcb_decode_generic_kernel;
+  const void* kfn = fused ? ctcb::fused_kernel_fn()
+                    : fast ? fast_kernel_fn(P, use_precomp(h, B)) : (const void*)ctcb::ctcb_decode_generic_kernel;
   int max_wpb = h->max_smem_optin / P.smem_per_warp;
   max_wpb = max_wpb < 1 ? 1 : (max_wpb > 8 ? 8 : max_wpb);
+  if (fused && max_wpb > 4) max_wpb = 4;  // __launch_bounds__(128)
   if (fast && max_wpb > 4) max_wpb = 4;  // fast kernel: __launch_bounds__(128, 6)
   int spread = (B + h->num_sms - 1) / h->num_sms;
   if (spread < 1) spread = 1;
@@ -327,6 +342,9 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   h->hbuf = nullptr;
   h->hbuf_bytes = 0;
   h->have_cstreams = 0;
+  h->has_lm = 0;
+  h->sil = -1;
+  h->sil_score = 0.0;
   {
     const char* fg = getenv("CTCB_FORCE_GENERIC");
     h->force_generic = (fg && fg[0] == '1') ? 1 : 0;
@@ -386,6 +404,10 @@ int ctcb_kernel_time(ctcb_t* h, double* total_ms, int* launches, const char** ke
 
 int ctcb_destroy(ctcb_t* h) {
   if (!h) return CTCB_OK;
+  if (h->has_lm) {
+    cudaSetDevice(h->device);
+    ctcb::lm_tables_free(&h->lm);
+  }
   if (h->have_tev)
     for (int i = 0; i < 2 * 64; i++) cudaEventDestroy(h->tev[i]);
   if (h->ws) cudaFree(h->ws);
@@ -413,9 +435,10 @@ int ctcb_workspace_bytes(const ctcb_t* h, int batch, int t_max, size_t* bytes) {
   return CTCB_OK;
 }
 
-int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T, void* ws,
-                size_t ws_bytes, void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len,
-                double* out_score, int32_t* out_count, int32_t* out_status) {
+static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T,
+                       void* ws, size_t ws_bytes, void* stream, int32_t* out_tokens, int32_t* out_ts,
+                       int32_t* out_len, double* out_score, int32_t* out_count, int32_t* out_status,
+                       double* out_lm) {
   if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
   if (!out_tokens || !out_len || !out_score || !out_count || !out_status)
     return fail(CTCB_ERR_ARG, "output pointers must not be NULL (out_timesteps may be)");
@@ -431,7 +454,18 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   P.out_len = out_len;
   P.out_score = out_score;
   P.out_count = out_count;
-  const bool fast = use_fast(h);
+  P.out_lm = out_lm;
+  const bool fast = use_fast(h), fused = use_fused(h);
+  if (fused) {
+    P.lm_score = h->has_lm ? h->lm.score : nullptr;
+    P.lm_next = h->lm.next;
+    P.lm_fin = h->lm.fin;
+    P.lm_wmax = h->lm.wmax;
+    P.lm_start = h->lm.start;
+    P.lm_weight = h->lm_weight;
+  }
+  P.sil = h->sil;
+  P.sil_score = h->sil_score;
   rc = launch_config(h, P, B, fast);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
@@ -446,7 +480,8 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   CTCB_CUDA(cudaGetLastError());
   size_t smem = (size_t)P.smem_per_warp * P.warps_per_block;
   const bool pre = fast && use_precomp(h, B);
-  const void* kfn = fast ? fast_kernel_fn(P, pre) : (const void*)ctcb::ctcb_decode_generic_kernel;
+  const void* kfn = fused ? ctcb::fused_kernel_fn()
+                    : fast ? fast_kernel_fn(P, pre) : (const void*)ctcb::ctcb_decode_generic_kernel;
   CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
   CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, 32 * P.warps_per_block, smem));
@@ -474,7 +509,11 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
   }
   const bool timed = h->timing && h->n_timed < 64;
   if (timed) CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed], s));
-  if (fast) {
+  if (fused) {
+    void* args[] = {(void*)&P};
+    CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
+    h->last_kernel = "ctcb_decode_fused_kernel";
+  } else if (fast) {
     void* args[] = {(void*)&P};
     CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
     h->last_kernel = !fast_small(P) ? (pre ? "ctcb_decode_fast_pre_kernel" : "ctcb_decode_fast_kernel")
@@ -488,6 +527,79 @@ int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_
     CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed + 1], s));
     h->n_timed++;
   }
+  return CTCB_OK;
+}
+
+int ctcb_decode(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T, void* ws,
+                size_t ws_bytes, void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len,
+                double* out_score, int32_t* out_count, int32_t* out_status) {
+  return decode_impl(h, lp, sb, st, lens, B, T, ws, ws_bytes, stream, out_tokens, out_ts, out_len, out_score,
+                     out_count, out_status, nullptr);
+}
+
+int ctcb_decode_lm(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int32_t* lens, int B, int T, void* ws,
+                   size_t ws_bytes, void* stream, int32_t* out_tokens, int32_t* out_ts, int32_t* out_len,
+                   double* out_score, double* out_lm, int32_t* out_count, int32_t* out_status) {
+  return decode_impl(h, lp, sb, st, lens, B, T, ws, ws_bytes, stream, out_tokens, out_ts, out_len, out_score,
+                     out_count, out_status, out_lm);
+}
+
+int ctcb_lm_create(int order, int64_t n_ngrams, const int32_t* words, const int32_t* lengths, const double* logprob,
+                   const double* backoff, const int32_t* start, int start_len, int eos, int device, ctcb_lm_t** out) {
+  if (!out) return fail(CTCB_ERR_ARG, "out must not be NULL");
+  *out = nullptr;
+  int ndev = 0;
+  CTCB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(CTCB_ERR_ARG, "invalid CUDA device " + std::to_string(device));
+  ctcb::LmModel* m = nullptr;
+  const char* err = "";
+  int rc = ctcb::lm_model_create(order, n_ngrams, words, lengths, logprob, backoff, start, start_len, eos, device, &m,
+                                 &err);
+  if (rc) return fail(rc, std::string("ctcb_lm_create: ") + err);
+  *out = new ctcb_lm{m};
+  return CTCB_OK;
+}
+
+int ctcb_lm_destroy(ctcb_lm_t* lm) {
+  if (!lm) return CTCB_OK;
+  ctcb::lm_model_destroy(lm->m);
+  delete lm;
+  return CTCB_OK;
+}
+
+int ctcb_set_lm(ctcb_t* h, const ctcb_lm_t* lm, const int32_t* token_word, double weight) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  CTCB_CUDA(cudaSetDevice(h->device));
+  if (h->has_lm) {
+    CTCB_CUDA(cudaDeviceSynchronize());
+    ctcb::lm_tables_free(&h->lm);
+    h->has_lm = 0;
+  }
+  if (!lm) return CTCB_OK;
+  if (!token_word) return fail(CTCB_ERR_ARG, "token_word must not be NULL");
+  if (!std::isfinite(weight)) return fail(CTCB_ERR_ARG, "lm_weight must be finite");
+  if (h->beam > ctcb::kFusedMaxBeam)
+    return fail(CTCB_ERR_UNSUPPORTED, "LM fusion supports beam_size <= " + std::to_string(ctcb::kFusedMaxBeam));
+  if (lm->m->device != h->device) return fail(CTCB_ERR_ARG, "LM and decoder are on different devices");
+  for (int c = 0; c < h->V; c++)
+    if (token_word[c] < -2) return fail(CTCB_ERR_ARG, "token_word entries must be >= -2");
+  const char* err = "";
+  int rc = ctcb::lm_tables_build(lm->m, token_word, h->V, weight, &h->lm, &err);
+  if (rc) return fail(rc, std::string("ctcb_set_lm: ") + err);
+  h->has_lm = 1;
+  h->lm_weight = weight;
+  return CTCB_OK;
+}
+
+int ctcb_set_silence(ctcb_t* h, int sil, double sil_score) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  if (sil >= h->V) return fail(CTCB_ERR_ARG, "silence_index " + std::to_string(sil) + " out of range");
+  if (sil == h->blank) return fail(CTCB_ERR_ARG, "silence_index must differ from blank_index");
+  if (!std::isfinite(sil_score)) return fail(CTCB_ERR_ARG, "sil_score must be finite");
+  if (sil >= 0 && sil_score != 0.0 && h->beam > ctcb::kFusedMaxBeam)
+    return fail(CTCB_ERR_UNSUPPORTED, "a silence bonus supports beam_size <= " + std::to_string(ctcb::kFusedMaxBeam));
+  h->sil = sil < 0 ? -1 : sil;
+  h->sil_score = sil < 0 ? 0.0 : sil_score;
   return CTCB_OK;
 }
 

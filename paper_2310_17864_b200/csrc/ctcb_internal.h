@@ -56,7 +56,50 @@ struct Params {
   int32_t* topk_tok;        // [B, T_max, k] (precomp mode)
   float* topk_val;          // [B, T_max, k]
   int32_t* rowoff;          // [B + 1] exclusive prefix sums of kept (precomp mode)
+  // fused search (ctcb_set_lm / ctcb_set_silence): token-level LM and silence bonus
+  const double* lm_score;   // [S, V] natural-log LM score of token c after context s, or null (no LM)
+  const int32_t* lm_next;   // [S, V] successor context
+  const double* lm_fin;     // [S] score of "</s>"
+  const double* lm_wmax;    // [S] max_c weight * lm_score[s, c] (pruning bound)
+  int lm_start;             // start context
+  double lm_weight;
+  int sil;                  // silence token (-1: none)
+  double sil_score;
+  double* out_lm;           // [B, nbest] LM total of each hypothesis, or null
 };
+
+// Fused search limits.
+constexpr int kFusedMaxBeam = 64;
+constexpr int kUttOverflow = 4;  // fused search: too many near-tied candidates at the beam cut
+
+// Device copy of a flattened backoff n-gram model (ctcb_lm_t).
+struct LmModel {
+  int order, device;
+  int64_t n, cap, n_states;
+  int32_t *words, *lengths;     // [n, order], [n]
+  double *logprob, *backoff;    // [n]
+  int32_t* slots;               // [cap] open-addressing table: entry index or -1
+  int32_t* state_entry;         // [n_states] entry of context state s (-1: the empty context)
+  int32_t* entry_state;         // [n] context state of an entry (-1: top-order n-gram)
+  int start_state, eos;
+};
+// Dense fusion tables of one handle: S x V scores / successors, finish scores, bounds.
+struct LmTables {
+  double* score;
+  int32_t* next;
+  double* fin;
+  double* wmax;
+  int64_t n_states;
+  int start;
+};
+int lm_model_create(int order, int64_t n, const int32_t* words, const int32_t* lengths, const double* logprob,
+                    const double* backoff, const int32_t* start, int start_len, int eos, int device, LmModel** out,
+                    const char** err);
+void lm_model_destroy(LmModel* m);
+int lm_tables_build(const LmModel* m, const int32_t* token_word, int V, double weight, LmTables* t, const char** err);
+void lm_tables_free(LmTables* t);
+size_t fused_smem_per_warp(int beam, int V, int ring, int row_bytes);
+const void* fused_kernel_fn();
 
 enum DbgCounter {
   kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5, kDbgTopkFix = 6, kDbgOneshotFallback = 7

@@ -15,12 +15,13 @@ merge_mode`` (a ``DecoderOptions`` here or ctcforge's own).  They return
 ``NBestList``s of ``Hypothesis(tokens, words=[], am_score, lm_score=0.0,
 score, timesteps)`` exactly like decoder.py:69-99, decoded by libctcb.so.
 
-What the CUDA path implements: the lexicon-free, LM-free search with any
+What the CUDA path implements: the lexicon-free search with any
 ``beam_size_token`` (None / V: full vocabulary; K < V: per-frame top-K token
-selection, decoder.py:440-458) and ``merge_mode`` "logadd" or "max".  Lexicon /
-LM arguments raise ``ValueError`` — the reference's LM and lexicon paths are
-not on the CUDA decoder path.  fp64 emissions are rounded to fp32 (the decoder's input
-dtype) before decoding.
+selection, decoder.py:440-458), ``merge_mode`` "logadd" or "max", token-level
+shallow fusion with a backoff n-gram ``lm`` (decoder.py:178-259, :467-473,
+:753-817; ``lm_weight``), and the silence token's ``sil_score`` bonus
+(decoder.py:485-486).  A lexicon raises ``ValueError``.  fp64
+emissions are rounded to fp32 (the decoder's input dtype) before decoding.
 """
 
 from __future__ import annotations
@@ -105,16 +106,19 @@ def _log_probs(e) -> np.ndarray:
 
 def _token_list(tokens):
     if hasattr(tokens, "tokens"):
-        return list(tokens.tokens), int(getattr(tokens, "blank_index", 0))
-    return list(tokens), 0
+        sil = getattr(tokens, "silence_index", None)
+        return list(tokens.tokens), int(getattr(tokens, "blank_index", 0)), (None if sil is None else int(sil))
+    return list(tokens), 0, None
 
 
 _DECODERS: dict = {}
 
 
-def _decoder(vocab, blank, opts, device) -> CUCTCDecoder:
+def _decoder(vocab, blank, opts, device, sil=None, lm=None) -> CUCTCDecoder:
+    sil_score = float(getattr(opts, "sil_score", 0.0)) if sil is not None else 0.0
     key = (tuple(vocab), blank, opts.beam_size, opts.n_best, opts.blank_skip_threshold, opts.beam_threshold,
-           opts.merge_mode, opts.beam_size_token, device)
+           opts.merge_mode, opts.beam_size_token, device, sil, sil_score, id(lm) if lm is not None else None,
+           float(opts.lm_weight) if lm is not None else None)
     dec = _DECODERS.get(key)
     if dec is None:
         dec = CUCTCDecoder(vocab, blank_id=blank, beam_size=opts.beam_size, nbest=opts.n_best,
@@ -123,6 +127,11 @@ def _decoder(vocab, blank, opts, device) -> CUCTCDecoder:
         dec.set_merge_mode(opts.merge_mode)
         if opts.beam_size_token is not None and opts.beam_size_token <= len(vocab):
             dec.set_beam_size_token(opts.beam_size_token)
+        if sil is not None:
+            dec.set_silence(sil, sil_score)
+        if lm is not None:
+            dec.set_lm(lm, float(opts.lm_weight))
+            dec._lm_ref = lm  # keeps id(lm) in the cache key unique while cached
         _DECODERS[key] = dec
     return dec
 
@@ -131,10 +140,10 @@ def decode_batch(emissions, tokens, opts=None, lexicon=None, lm=None, workers: i
     """GPU ``decode_batch`` (decoder.py:138-170): one launch for the batch;
     ``workers`` is accepted for signature compatibility (the GPU decodes all
     utterances concurrently).  Errors carry the utterance index."""
-    if lexicon is not None or lm is not None:
-        raise ValueError("the CUDA decoder has no lexicon / LM fusion")
+    if lexicon is not None:
+        raise ValueError("the CUDA decoder has no lexicon mode")
     opts = opts if opts is not None else DecoderOptions()
-    vocab, blank = _token_list(tokens)
+    vocab, blank, sil = _token_list(tokens)
     lps = [_log_probs(e) for e in emissions]
     for i, lp in enumerate(lps):
         if lp.shape[1] != len(vocab):
@@ -144,7 +153,7 @@ def decode_batch(emissions, tokens, opts=None, lexicon=None, lm=None, workers: i
         return []
     if opts.beam_size_token is not None and opts.beam_size_token > len(vocab):  # decoder.py:124-128
         raise ValueError(f"utterance 0: beam_size_token {opts.beam_size_token} exceeds vocabulary size {len(vocab)}")
-    dec = _decoder(vocab, blank, opts, device)
+    dec = _decoder(vocab, blank, opts, device, sil, lm)
     T = max(lp.shape[0] for lp in lps)
     x = torch.zeros((len(lps), max(T, 1), len(vocab)), dtype=torch.float32)
     for b, lp in enumerate(lps):
@@ -153,13 +162,21 @@ def decode_batch(emissions, tokens, opts=None, lexicon=None, lm=None, workers: i
     dev = torch.device("cuda", device)
     out = dec.decode(x.to(dev), lens.to(dev), timesteps=True)
     toks, ts, lengths, scores, counts = dec.to_host(out)
+    lms = out.lm.cpu().numpy() if out.lm is not None else None
+    sil_score = float(getattr(opts, "sil_score", 0.0))
+    w = float(opts.lm_weight)
     result = []
     for b in range(len(lps)):
         hyps = []
         for j in range(int(counts[b])):
             n = int(lengths[b, j])
             sc = float(scores[b, j])
-            hyps.append(Hypothesis(tokens=toks[b, j, :n].tolist(), words=[], am_score=sc, lm_score=0.0, score=sc,
+            tk = toks[b, j, :n].tolist()
+            lm_v = float(lms[b, j]) if lms is not None else 0.0
+            # decoder.py:805-812
+            bonuses = float(opts.word_score) * 0 + sil_score * (tk.count(sil) if sil is not None else 0)
+            lm_part = w * lm_v if lms is not None else 0.0
+            hyps.append(Hypothesis(tokens=tk, words=[], am_score=sc - lm_part - bonuses, lm_score=lm_v, score=sc,
                                    timesteps=ts[b, j, :n].tolist()))
         result.append(NBestList(hyps))
     return result

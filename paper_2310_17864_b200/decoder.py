@@ -61,6 +61,7 @@ class DecodeOutput(NamedTuple):
     scores: torch.Tensor      # float64 [B, nbest]
     counts: torch.Tensor      # int32 [B]
     status: torch.Tensor      # int32 [B]
+    lm: Optional[torch.Tensor] = None  # float64 [B, nbest] LM totals (decoder with an LM attached)
 
 
 def _read_vocab(path: str) -> list[str]:
@@ -163,12 +164,20 @@ class CUCTCDecoder:
         _lib.check(lib.ctcb_topk_size(h, ctypes.byref(k)), "ctcb_topk_size")
         self.topk = k.value
         self._ws = None
+        self._lm = None          # ctcb_lm_t of the attached model (set_lm)
+        self.lm_weight = 0.0
+        self.silence_index: Optional[int] = None
+        self.sil_score = 0.0
 
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib._lib is not None:
             _lib._lib.ctcb_destroy(h)
             self._h = None
+        m = getattr(self, "_lm", None)
+        if m is not None and m.value and _lib._lib is not None:
+            _lib._lib.ctcb_lm_destroy(m)
+            self._lm = None
 
     # ------------------------------------------------------------------ helpers
     def _stream(self):
@@ -262,6 +271,15 @@ class CUCTCDecoder:
         out_status = torch.full((B,), -1, dtype=torch.int32, device=dev)  # -1: not processed
         ws = self._workspace(B, T)
         vp = ctypes.c_void_p
+        if self._lm is not None:
+            out_lm = torch.zeros((B, nb), dtype=torch.float64, device=dev)
+            _lib.check(lib.ctcb_decode_lm(
+                self._h, vp(log_prob.data_ptr()), self._strides[0], self._strides[1], vp(lens.data_ptr()), B, T,
+                vp(ws.data_ptr()), ws.numel(), self._stream(), vp(out_tok.data_ptr()),
+                vp(out_ts.data_ptr()) if out_ts is not None else None, vp(out_len.data_ptr()),
+                vp(out_score.data_ptr()), vp(out_lm.data_ptr()), vp(out_count.data_ptr()),
+                vp(out_status.data_ptr())), "ctcb_decode_lm")
+            return DecodeOutput(out_tok, out_ts, out_len, out_score, out_count, out_status, out_lm)
         _lib.check(lib.ctcb_decode(
             self._h, vp(log_prob.data_ptr()), self._strides[0], self._strides[1], vp(lens.data_ptr()), B, T,
             vp(ws.data_ptr()), ws.numel(), self._stream(), vp(out_tok.data_ptr()),
@@ -392,6 +410,10 @@ class CUCTCDecoder:
             u = b + offset
             if status[b] == _lib.UTT_EMPTY:
                 raise ValueError(f"utterance {u}: empty emissions")
+            if status[b] == _lib.UTT_OVERFLOW:
+                t = int(np.asarray(lengths)[b, 0]) if lengths is not None else "?"
+                raise _lib.CtcbError(f"utterance {u}: frame {t}: more near-tied candidates at the beam cut than "
+                                     "the fused search window holds")
             if status[b] == _lib.UTT_BEAM_DIED:
                 # decoder.py:616-620; the kernel leaves the kept-frame index in lengths[b, 0]
                 t = int(np.asarray(lengths)[b, 0]) if lengths is not None else "?"
@@ -449,6 +471,56 @@ class CUCTCDecoder:
         if mode not in ("logadd", "max"):
             raise ValueError('merge_mode must be one of ("logadd", "max")')
         _lib.check(_lib.load().ctcb_set_merge_mode(self._h, 1 if mode == "max" else 0), "ctcb_set_merge_mode")
+
+    def set_lm(self, lm, lm_weight: float = 2.0) -> None:
+        """Token-level shallow fusion with a backoff n-gram model (lexicon-free
+        ``beam_search_decode(..., lm=lm)``, decoder.py:178-259, :467-473,
+        :753-817): ``lm`` is a :class:`paper_2310_17864_b200.lm.NGramLM` (or the
+        reference's, same fields), None to detach.  Token strings are looked up
+        in the model's vocabulary; blank and the silence token carry no LM
+        score.  Hypothesis scores then include ``lm_weight`` × LM and the
+        decode outputs carry the LM totals (``DecodeOutput.lm``)."""
+        from . import lm as _lmmod
+        lib = _lib.load()
+        vp = ctypes.c_void_p
+        if lm is None:
+            _lib.check(lib.ctcb_set_lm(self._h, None, None, 0.0), "ctcb_set_lm")
+            if self._lm is not None:
+                lib.ctcb_lm_destroy(self._lm)
+            self._lm = None
+            self.lm_weight = 0.0
+            return
+        flat = _lmmod.flatten(lm)
+        words = np.ascontiguousarray(flat.words, dtype=np.int32)
+        lens = np.ascontiguousarray(flat.lengths, dtype=np.int32)
+        lp = np.ascontiguousarray(flat.logprob, dtype=np.float64)
+        bo = np.ascontiguousarray(flat.backoff, dtype=np.float64)
+        st = np.ascontiguousarray(flat.start, dtype=np.int32)
+        m = ctypes.c_void_p()
+        _lib.check(lib.ctcb_lm_create(flat.order, len(lens), vp(words.ctypes.data), vp(lens.ctypes.data),
+                                      vp(lp.ctypes.data), vp(bo.ctypes.data), vp(st.ctypes.data), flat.start_len,
+                                      flat.eos, self.device.index, ctypes.byref(m)), "ctcb_lm_create")
+        tw = np.ascontiguousarray(_lmmod.token_words(lm, self.vocab_list, self.blank_id, self.silence_index),
+                                  dtype=np.int32)
+        rc = lib.ctcb_set_lm(self._h, m, vp(tw.ctypes.data), float(lm_weight))
+        if rc != _lib.CTCB_OK:
+            lib.ctcb_lm_destroy(m)
+            _lib.check(rc, "ctcb_set_lm")
+        if self._lm is not None:
+            lib.ctcb_lm_destroy(self._lm)
+        self._lm = m
+        self._lm_model = lm
+        self.lm_weight = float(lm_weight)
+
+    def set_silence(self, index: Optional[int], sil_score: float = 0.0) -> None:
+        """Silence token (TokenDictionary.silence_index) and its per-emission
+        bonus ``sil_score`` (decoder.py:485-486); it carries no LM score."""
+        _lib.check(_lib.load().ctcb_set_silence(self._h, -1 if index is None else int(index), float(sil_score)),
+                   "ctcb_set_silence")
+        self.silence_index = None if index is None else int(index)
+        self.sil_score = float(sil_score)
+        if self._lm is not None:  # the silence column of the LM tables is the identity
+            self.set_lm(self._lm_model, self.lm_weight)
 
     def set_beam_size_token(self, k: Optional[int]) -> None:
         """``DecoderOptions.beam_size_token``: None (default) or V searches the

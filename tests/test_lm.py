@@ -108,3 +108,132 @@ def test_oracle_tables_are_the_incremental_api():
                 assert tabs.score[s, c] == want
                 s = tabs.next[s, c]
             assert tabs.fin[s] == glm.lm_finish(lm, st)
+
+
+# ------------------------------------------------------------------ GPU
+class _Tokens:
+    def __init__(self, tokens, sil=None):
+        self.tokens = tuple(tokens)
+        self.blank_index = 0
+        self.silence_index = sil
+
+
+def _close(a, b):
+    return abs(a - b) <= 1e-9 * (1.0 + abs(b))
+
+
+@pytest.mark.gpu
+def test_fused_kernel_matches_reference_golden():
+    """ctcforge-shaped decode with lm= on the fused kernel == the reference's
+    n-best (tokens, timesteps exact; score / am_score / lm_score to 1e-9)."""
+    from paper_2310_17864_b200 import ctcforge_api as api
+    g = golden()
+    models = {m["name"]: m for m in g["models"]}
+    for k, case in enumerate(g["cases"]):
+        m = models[case["model"]]
+        lm = load_model(m)
+        opts = api.DecoderOptions(**case["opts"])
+        res = api.beam_search_decode(np.array(case["lp"]), _Tokens(m["tokens"], case["sil"]), opts, lm=lm)
+        exp = case["nbest"]
+        assert [h.tokens for h in res] == [h["tokens"] for h in exp], (k, case["model"], case["opts"])
+        assert [h.timesteps for h in res] == [h["timesteps"] for h in exp], k
+        for h, e in zip(res, exp):
+            assert _close(h.score, e["score"]) and _close(h.lm_score, e["lm_score"]), (k, h, e)
+            assert _close(h.am_score, e["am_score"]), (k, h, e)
+
+
+def random_arpa(path, rng, words, order, keep):
+    """Seeded synthetic backoff model (our generator, like make_lm_golden.py)."""
+    vocab = ["<s>", "</s>"] + list(words)
+    tables = {1: {(w,): (-99.0 if w == "<s>" else float(rng.uniform(-2.5, -0.3)),
+                         float(rng.uniform(-1.0, 0.3)) if order > 1 else None) for w in vocab}}
+    for n in range(2, order + 1):
+        tables[n] = {}
+        for ctx in list(tables[n - 1]):
+            if ctx[-1] == "</s>":
+                continue
+            for w in vocab[1:]:
+                if rng.random() < keep:
+                    tables[n][ctx + (w,)] = (float(rng.uniform(-2.2, -0.05)),
+                                             float(rng.uniform(-0.9, 0.2)) if n < order else None)
+    lines = ["\\data\\"] + [f"ngram {n}={len(tables[n])}" for n in range(1, order + 1)]
+    for n in range(1, order + 1):
+        lines += ["", f"\\{n}-grams:"]
+        for ng, (p, b) in sorted(tables[n].items()):
+            lines.append(f"{p:.5f}\t{' '.join(ng)}" + (f"\t{b:.5f}" if b is not None else ""))
+    lines += ["", "\\end\\", ""]
+    path.write_text("\n".join(lines))
+    return glm.parse_arpa(path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V,order,beam,T", [(40, 2, 10, 120), (40, 3, 16, 90), (120, 2, 8, 200), (500, 2, 10, 150),
+                                            (30, 2, 32, 60), (500, 1, 4, 80)])
+def test_fused_kernel_matches_oracle_batches(tmp_path, V, order, beam, T):
+    """Batches of ragged utterances through CUCTCDecoder.set_lm against the
+    oracle's fused search (same fp32 inputs)."""
+    import torch
+    from paper_2310_17864_b200 import CUCTCDecoder
+    rng = np.random.default_rng(V * 100 + order * 10 + beam)
+    toks = ["-"] + [f"w{i}" for i in range(1, V)]
+    lm = random_arpa(tmp_path / "m.arpa", rng, toks[1: V - 2], order, keep=min(0.5, 30.0 / V))  # 2 OOV tokens
+    B = 12
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    x = rng.normal(size=(B, T, V)) * float(rng.choice([1.0, 3.0]))
+    x = x - x.max(2, keepdims=True)
+    lp = (x - np.log(np.exp(x).sum(2, keepdims=True))).astype(np.float32)
+    for w, thr, merge in ((1.3, 0.95, "logadd"), (0.4, 1.0, "max"), (2.5, 0.99, "logadd")):
+        dec = CUCTCDecoder(toks, beam_size=beam, nbest=min(beam, 3), blank_skip_threshold=thr, beam_threshold=30.0)
+        dec.set_merge_mode(merge)
+        dec.set_lm(lm, w)
+        out = dec.decode(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+        tokens, _, lengths, scores, counts = dec.to_host(out)
+        lms = out.lm.cpu().numpy()
+        tabs = oracle.lm_tables(glm.flatten(lm), glm.token_words(lm, toks, 0))
+        for b in range(B):
+            ref = oracle.decode(lp[b, : lens[b]], beam_size=beam, n_best=min(beam, 3), blank_skip_threshold=thr,
+                                beam_threshold=30.0, merge_mode=merge, lm=tabs, lm_weight=w)
+            got = [tokens[b, j, : lengths[b, j]].tolist() for j in range(counts[b])]
+            assert got == ref.tokens, (b, w, thr, merge)
+            for j in range(counts[b]):
+                assert _close(scores[b, j], ref.scores[j]) and _close(lms[b, j], ref.lm_scores[j]), (b, j)
+
+
+@pytest.mark.gpu
+def test_silence_bonus_without_lm_matches_oracle():
+    import torch
+    from paper_2310_17864_b200 import CUCTCDecoder
+    rng = np.random.default_rng(77)
+    V, T, B = 24, 70, 8
+    toks = ["-"] + [f"t{i}" for i in range(1, V)]
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    x = rng.normal(size=(B, T, V)) * 2.0
+    x = x - x.max(2, keepdims=True)
+    lp = (x - np.log(np.exp(x).sum(2, keepdims=True))).astype(np.float32)
+    for sil_score in (1.5, -0.7):
+        dec = CUCTCDecoder(toks, beam_size=12, nbest=2)
+        dec.set_silence(V - 1, sil_score)
+        out = dec.decode(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+        tokens, _, lengths, scores, counts = dec.to_host(out)
+        for b in range(B):
+            ref = oracle.decode(lp[b, : lens[b]], beam_size=12, n_best=2, blank_skip_threshold=0.95,
+                                sil=V - 1, sil_score=sil_score)
+            assert [tokens[b, j, : lengths[b, j]].tolist() for j in range(counts[b])] == ref.tokens
+            assert all(_close(scores[b, j], ref.scores[j]) for j in range(counts[b]))
+
+
+@pytest.mark.gpu
+def test_fused_errors(tmp_path):
+    from paper_2310_17864_b200 import CUCTCDecoder
+    rng = np.random.default_rng(3)
+    toks = ["-", "a", "b", "c"]
+    lm = random_arpa(tmp_path / "e.arpa", rng, toks[1:], 2, 0.5)
+    dec = CUCTCDecoder(toks, beam_size=100)
+    with pytest.raises(ValueError, match="beam_size <= 64"):
+        dec.set_lm(lm, 1.0)
+    dec = CUCTCDecoder(toks, beam_size=4)
+    with pytest.raises(ValueError, match="silence_index must differ"):
+        dec.set_silence(0, 1.0)
+    dec.set_lm(lm, 1.0)
+    dec.set_lm(None)
+    assert dec._lm is None
