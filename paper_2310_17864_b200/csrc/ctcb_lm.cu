@@ -754,9 +754,74 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   }
   // a candidate this lane dropped may lie inside the window
   if (nc >= beam && dropmax >= lo_key) overflow = true;
-  if (__any_sync(FULL, overflow)) return -1;
   __syncwarp();
   if (nc == 0) return 0;
+  auto desc = [&](int i) -> FDesc {
+    const uint32_t id = w.c_id[i];
+    if (id & kSpecialBit) {
+      const int s = (int)(id & ~kSpecialBit);
+      return FDesc{w.c_sc[i], w.sp_base[s], w.sp_x[s], w.sp_flag[s]};
+    }
+    return FDesc{w.c_sc[i], w.e1[id / (uint32_t)V], (int)(id % (uint32_t)V), 0};
+  };
+  if (__any_sync(FULL, overflow)) {
+    // Near-ties wider than the lane lists: stream every candidate of the window
+    // [beam-th key - tol, ...) through lane 0's exactly ordered top-`beam` buffer.
+    atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
+    int nsel = 0;
+    auto offer = [&](uint32_t id) {  // lane 0
+      const CandOut o = exact_cand(w, id, row, use_lm);
+      if (!(o.sc > -INFINITY)) return;
+      FDesc dx;
+      if (id & kSpecialBit) {
+        const int s = (int)(id & ~kSpecialBit);
+        dx = FDesc{o.sc, w.sp_base[s], w.sp_x[s], w.sp_flag[s]};
+      } else {
+        dx = FDesc{o.sc, w.e1[id / (uint32_t)V], (int)(id % (uint32_t)V), 0};
+      }
+      if (nsel == beam && !fprecedes(w, dx, desc(beam - 1))) return;
+      int j = nsel < beam ? nsel++ : beam - 1;
+      while (j > 0 && fprecedes(w, dx, desc(j - 1))) {
+        w.c_id[j] = w.c_id[j - 1]; w.c_sc[j] = w.c_sc[j - 1]; w.c_lm[j] = w.c_lm[j - 1];
+        w.c_src[j] = w.c_src[j - 1]; w.c_st[j] = w.c_st[j - 1];
+        j--;
+      }
+      w.c_id[j] = id; w.c_sc[j] = o.sc; w.c_lm[j] = o.lm; w.c_src[j] = o.src; w.c_st[j] = o.st;
+    };
+    if (lane == 0)
+      for (int s = 0; s < nS; s++)
+        if (w.sp_sc[s] > -INFINITY && ord64(w.sp_sc[s]) >= lo_key) offer(kSpecialBit | (uint32_t)s);
+    uint32_t* stage = w.li;  // lane lists are no longer needed
+    for (int d = 0; d < nD; d++) {
+      const int a = w.e1[d];
+      const int lastc = w.cl[a];
+      for (int k = lane; k < nEx; k += 32)
+        if (w.exd[k] == d) atomicOr(&w.excl[w.exc[k] >> 5], 1u << (w.exc[k] & 31));
+      __syncwarp();
+      for (int c0 = 0; c0 < V; c0 += 32) {
+        const int c = c0 + lane;
+        bool in = false;
+        if (c < V && c != P.blank && c != lastc && !((w.excl[c >> 5] >> (c & 31)) & 1u) && selected(c)) {
+          double x = w.lA[d] + (double)row[c];
+          if (use_lm) x = x + P.lm_weight * P.lm_score[(size_t)w.cst[a] * V + c];
+          if (c == P.sil) x = x + P.sil_score;
+          in = x > -INFINITY && ord64(x) >= lo_key;
+        }
+        const unsigned bal = __ballot_sync(FULL, in);
+        if (in) stage[__popc(bal & lanemask_lt())] = (uint32_t)d * (uint32_t)V + (uint32_t)c;
+        __syncwarp();
+        if (lane == 0)
+          for (int q = 0; q < __popc(bal); q++) offer(stage[q]);
+        __syncwarp();
+      }
+      for (int k = lane; k < nEx; k += 32)
+        if (w.exd[k] == d) atomicAnd(&w.excl[w.exc[k] >> 5], ~(1u << (w.exc[k] & 31)));
+      __syncwarp();
+    }
+    nc = __shfl_sync(FULL, nsel, 0);
+    for (int i = lane; i < nc; i += 32) { w.c_ord[i] = i; w.c_key[i] = ord64(w.c_sc[i]); }
+    __syncwarp();
+  } else {
 
   // -- exact scores of the window, exact order
   const int npad = pow2_at_least(nc);
@@ -772,14 +837,6 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   }
   __syncwarp();
   fbitonic(w.c_key, w.c_ord, npad, lane);
-  auto desc = [&](int i) -> FDesc {
-    const uint32_t id = w.c_id[i];
-    if (id & kSpecialBit) {
-      const int s = (int)(id & ~kSpecialBit);
-      return FDesc{w.c_sc[i], w.sp_base[s], w.sp_x[s], w.sp_flag[s]};
-    }
-    return FDesc{w.c_sc[i], w.e1[id / (uint32_t)V], (int)(id % (uint32_t)V), 0};
-  };
   // runs of equal exact scores: token sequence, then flag (decoder.py:651-681)
   {
     bool run = false;
@@ -803,6 +860,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
       __syncwarp();
     }
   }
+  }  // exact window
   int valid = 0;
   for (int i0 = 0; i0 < nc; i0 += 32) valid += __popc(__ballot_sync(FULL, i0 + lane < nc && w.c_key[i0 + lane] != 0ull));
   int Hn = valid < beam ? valid : beam;
