@@ -134,11 +134,14 @@ __global__ void ctcb_lm_finish_kernel(NgView m, int eos, long long S, double* __
   }
 }
 
-// per context: max_c weight * score[s, c] (the products the search adds)
-__global__ void ctcb_lm_bound_kernel(const double* __restrict__ score, int V, double w, double* __restrict__ wmax) {
+// per context: max_c weight * score[s, c] over word tokens (the products the
+// search adds; blank and silence, identity columns, are handled separately)
+__global__ void ctcb_lm_bound_kernel(const double* __restrict__ score, const int32_t* __restrict__ token_word, int V,
+                                     double w, double* __restrict__ wmax) {
   const long long s = blockIdx.x;
   double mx = -INFINITY;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmax(mx, w * score[s * V + c]);
+  for (int c = threadIdx.x; c < V; c += blockDim.x)
+    if (token_word[c] != -2) mx = fmax(mx, w * score[s * V + c]);
   __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -276,7 +279,7 @@ int lm_tables_build(const LmModel* m, const int32_t* token_word, int V, double w
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) {
-      ctcb_lm_bound_kernel<<<(unsigned)S, 256>>>(t->score, V, weight, t->wmax);
+      ctcb_lm_bound_kernel<<<(unsigned)S, 256>>>(t->score, dtw, V, weight, t->wmax);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -307,7 +310,7 @@ struct FusedLayout {
   size_t rows, mbar, cs, clm, ch, cph, cn, cl, cf, cst, ns, nlm, nh, nph, nn, nl, nf, nst, ntrel;
   size_t first, dpi, e1, e2, f1, pd, lA, vmin, exd, exc;
   size_t sp_sc, sp_lm, sp_base, sp_x, sp_flag, sp_src, sp_tok, sp_st;
-  size_t lk, li, c_key, c_ord, c_id, c_sc, c_lm, c_src, c_st, excl, hist, misc;
+  size_t lk, li, c_key, c_ord, c_id, c_sc, c_lm, c_src, c_st, excl, plist, seed, hist, misc;
   size_t total;
   int cc, cc_pad, sp_cap, excl_words;
 };
@@ -350,6 +353,8 @@ __host__ __device__ inline FusedLayout make_fused_layout(int beam, int V, int ri
   L.c_src = take(4 * (size_t)L.cc, 4);
   L.c_st = take(4 * (size_t)L.cc, 4);
   L.excl = take(4 * (size_t)L.excl_words, 4);
+  L.plist = take(4 * (size_t)V, 4);
+  L.seed = take(4 * 32, 4);
   L.hist = take(4 * 256, 4);
   L.misc = take(4 * 16, 4);
   L.total = (o + 127) / 128 * 128;
@@ -367,7 +372,7 @@ struct FW {
   double *cs, *clm, *ns, *nlm, *lA, *vmin, *sp_sc, *sp_lm, *c_sc, *c_lm;
   uint64_t *ch, *cph, *nh, *nph, *lk, *c_key;
   int *cn, *cl, *cf, *cst, *nn, *nl, *nf, *nst, *first, *dpi, *e1, *e2, *f1, *pd, *exd, *exc;
-  int *sp_base, *sp_x, *sp_flag, *sp_src, *sp_tok, *sp_st, *c_ord, *c_src, *c_st, *misc;
+  int *sp_base, *sp_x, *sp_flag, *sp_src, *sp_tok, *sp_st, *c_ord, *c_src, *c_st, *misc, *seed, *plist;
   uint32_t *ntrel, *li, *c_id, *excl, *hist;
   int cc, cc_pad;
 
@@ -408,6 +413,8 @@ __device__ void fcarve(FW& w, uint8_t* base, const Params& P) {
   w.c_ord = (int*)(base + L.c_ord); w.c_id = (uint32_t*)(base + L.c_id);
   w.c_src = (int*)(base + L.c_src); w.c_st = (int*)(base + L.c_st);
   w.excl = (uint32_t*)(base + L.excl);
+  w.plist = (int*)(base + L.plist);
+  w.seed = (int*)(base + L.seed);
   w.hist = (uint32_t*)(base + L.hist);
   w.misc = (int*)(base + L.misc);
   w.cc = L.cc;
@@ -654,7 +661,9 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   uint32_t* myli = w.li + (size_t)lane * beam;
   int cnt = 0, minpos = 0;
   uint64_t minkey = 0ull, dropmax = 0ull;  // dropmax: best key this lane evicted or rejected
+  uint64_t lmax = 0ull;                    // best key in this lane's list
   auto insert = [&](uint64_t key, uint32_t id) {
+    lmax = key > lmax ? key : lmax;
     if (cnt < beam) {
       mylk[cnt] = key; myli[cnt] = id; cnt++;
       if (cnt == beam) {
@@ -673,46 +682,124 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   for (int s = lane; s < nS; s += 32)
     if (w.sp_sc[s] > -INFINITY) insert(ord64(w.sp_sc[s]), kSpecialBit | (uint32_t)s);
   // shared lower bound of the beam cut: any full lane list's minimum
+  // Lower bound of the beam cut: the beam-th largest lane maximum (beam
+  // candidates in distinct lanes reach it), or any full lane list's minimum.
+  // Prefix d scans token c in lane (c + d) mod 32, so the same strong token of
+  // different prefixes lands in different lanes.
   auto bound = [&]() -> double {
     const uint64_t m = cnt == beam ? minkey : 0ull;
-    const uint64_t g = warp_max64(m);
+    uint64_t g = warp_max64(m);
+    if (beam <= 32) {
+      uint64_t x = lmax;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(x >> 32), j) << 32) |
+                             __shfl_xor_sync(FULL, (uint32_t)x, j);
+          const bool take_max = ((lane & j) == 0) == ((lane & k) == 0);
+          x = take_max ? (x > y ? x : y) : (x < y ? x : y);
+        }
+      const uint64_t kth = ((uint64_t)__shfl_sync(FULL, (uint32_t)(x >> 32), beam - 1) << 32) |
+                           __shfl_sync(FULL, (uint32_t)x, beam - 1);
+      g = kth > g ? kth : g;
+    }
     return g ? unord64(g) : -INFINITY;
   };
+  // one tolerance per frame covers the rounding gap between approximate and exact scores
+  const double tolF = 1e-9 * (1.0 + fabs(w.cs[0])) + 1e-9;
   double theta = bound();
-  const double sil_up = (P.sil >= 0 && P.sil_score > 0.0) ? P.sil_score : 0.0;
-  // candidate (d, c) is scanned only if (lA + v) + wmax + sil_up can reach the cut
+  auto valid_pair = [&](int d, int c) -> bool {
+    if (c == P.blank || c == w.cl[w.e1[d]]) return false;  // the last token: a special or blocked
+    for (int k = 0; k < nEx; k++)
+      if (w.exd[k] == d && w.exc[k] == c) return false;  // merges into a child's repeat group
+    return true;
+  };
+  auto approx = [&](int d, int c, float vf) -> double {  // exact when the prefix has one entry
+    double x = w.lA[d] + (double)vf;
+    if (use_lm) x = x + P.lm_weight * P.lm_score[(size_t)w.cst[w.e1[d]] * V + c];
+    if (c == P.sil) x = x + P.sil_score;
+    return x;
+  };
+  auto offer = [&](int d, int c, double x) {
+    if (!(x > -INFINITY)) return;
+    const uint64_t key = ord64(x);
+    if (cnt < beam || key > minkey) insert(key, (uint32_t)d * (uint32_t)V + (uint32_t)c);
+    else dropmax = key > dropmax ? key : dropmax;
+  };
+  // (1) seeds: every lane's best selected token (of c = lane mod 32) appended to
+  //     every prefix, so the beam bound is strong before the full scan
+  float bv = -INFINITY;
+  int bc = -1;
+  for (int c = lane; c < V; c += 32) {
+    const float v = row[c];
+    if (c != P.blank && v > bv && selected(c)) { bv = v; bc = c; }
+  }
+  if (!use_lm) {
+    // without an LM the emission order is the score order: the row's best token suffices
+    const uint32_t bk = bc >= 0 ? ord32(bv) : 0u;
+    const uint32_t mk = __reduce_max_sync(FULL, bk);
+    const int c1 = (int)__reduce_min_sync(FULL, (mk && bk == mk) ? (uint32_t)bc : 0x7fffffffu);
+    bc = (mk && (c1 & 31) == lane) ? c1 : -1;
+  }
+  w.seed[lane] = bc;
+  if (bc >= 0)
+    for (int d = 0; d < nD; d++)
+      if (valid_pair(d, bc)) offer(d, bc, approx(d, bc, bv));
+  __syncwarp();
+  theta = bound();
+  for (int d = lane; d < nD; d += 32) {
+    const double wb = use_lm ? P.lm_wmax[w.cst[w.e1[d]]] : 0.0;
+    w.vmin[d] = w.lA[d] + wb;  // upper-bound offset of prefix d's appends (silence: lA)
+  }
+  __syncwarp();
+  auto fcut = [&](double th, double off) -> float {  // v < fcut  =>  off + v < th - tolF
+    if (!(th > -INFINITY)) return -INFINITY;
+    const double c = th - 2.0 * tolF - off;
+    float cf = (float)c;
+    if ((double)cf > c) cf = nextafterf(cf, -INFINITY);
+    return cf;
+  };
+  // (2) tokens whose emission can reach the cut for the most promising prefix
+  double amax = -INFINITY;
+  for (int d = lane; d < nD; d += 32) amax = fmax(amax, w.vmin[d]);
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(FULL, amax, o));
+  const float gcut = fcut(theta, amax);
+  int nP = 0;
+  for (int c0 = 0; c0 < V; c0 += 32) {
+    const int c = c0 + lane;
+    bool pass = false;
+    if (c < V) {
+      const float vf = row[c];
+      pass = (!(vf < gcut) || c == P.sil) && c != P.blank && c != w.seed[lane] && selected(c);
+    }
+    const unsigned bal = __ballot_sync(FULL, pass);
+    if (pass) w.plist[nP + __popc(bal & lanemask_lt())] = c;
+    nP += __popc(bal);
+  }
+  __syncwarp();
+  // (3) prefix-major over the listed tokens, each pair against its prefix's cut
   for (int d = 0; d < nD; d++) {
-    const int a = w.e1[d];
-    const double wb = use_lm ? P.lm_wmax[w.cst[a]] : 0.0;
-    const int lastc = w.cl[a];
-    for (int k = lane; k < nEx; k += 32)
-      if (w.exd[k] == d) atomicOr(&w.excl[w.exc[k] >> 5], 1u << (w.exc[k] & 31));
-    __syncwarp();
-    const double lAd = w.lA[d];
-    auto cut_of = [&](double th) -> float {
-      // v < cut  =>  (lA + v) + wb + sil_up < th - tol  (margin for rounding)
-      if (!(th > -INFINITY)) return -INFINITY;
-      const double tol = 1e-9 * (1.0 + fabs(th));
-      const double c = th - tol - lAd - wb - sil_up - tol;
-      float cf = (float)c;
-      if ((double)cf > c) cf = nextafterf(cf, -INFINITY);
-      return cf;
-    };
+    const int lastc = w.cl[w.e1[d]];
+    const double off = w.vmin[d];
     double mth = cnt == beam ? fmax(theta, unord64(minkey)) : theta;
-    float cut = cut_of(mth);
-    for (int c0 = 0; c0 < V; c0 += 32) {
-      const int c = c0 + lane;
-      if (c < V) {
-        const float vf = row[c];
-        if (!(vf < cut) && c != P.blank && c != lastc && !((w.excl[c >> 5] >> (c & 31)) & 1u) && selected(c)) {
-          double x = lAd + (double)vf;
-          if (use_lm) x = x + P.lm_weight * P.lm_score[(size_t)w.cst[a] * V + c];
-          if (c == P.sil) x = x + P.sil_score;
+    float cut = fcut(mth, off);
+    const int rot = d & 31;
+    for (int j0 = 0; j0 < nP; j0 += 32) {
+      int j = j0 + ((lane + rot) & 31);  // spread one token's pairs over lanes
+      if (j >= nP) continue;
+      const int c = w.plist[j];
+      const float vf = row[c];
+      if ((!(vf < cut) || c == P.sil) && c != lastc) {
+        bool ok = true;
+        for (int k = 0; k < nEx; k++) ok &= !(w.exd[k] == d && w.exc[k] == c);
+        if (ok) {
+          const double x = approx(d, c, vf);
           if (x > -INFINITY) {
             const uint64_t key = ord64(x);
             if (cnt < beam || key > minkey) {
               insert(key, (uint32_t)d * (uint32_t)V + (uint32_t)c);
-              if (cnt == beam) { mth = fmax(theta, unord64(minkey)); cut = cut_of(mth); }
+              if (cnt == beam) { mth = fmax(theta, unord64(minkey)); cut = fcut(mth, off); }
             } else {
               dropmax = key > dropmax ? key : dropmax;
             }
@@ -720,11 +807,9 @@ __device__ int fused_step(FW& w, const float* row, int H) {
         }
       }
     }
-    for (int k = lane; k < nEx; k += 32)
-      if (w.exd[k] == d) atomicAnd(&w.excl[w.exc[k] >> 5], ~(1u << (w.exc[k] & 31)));
-    theta = bound();
-    __syncwarp();
+    if (d < 2 || (d & 3) == 3) theta = bound();
   }
+  __syncwarp();
 
   // -- sort each lane list (descending) and extract the global top by k-way merge
   for (int i = 1; i < cnt; i++) {
@@ -747,10 +832,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
     const int win = __ffs(wl) - 1;
     if (lane == win) { w.c_id[nc] = myli[pos]; pos++; }
     nc++;
-    if (nc == beam) {
-      const double th = unord64(M);
-      lo_key = ord64(th - 1e-9 * (1.0 + fabs(th)));
-    }
+    if (nc == beam) lo_key = ord64(unord64(M) - tolF);
   }
   // a candidate this lane dropped may lie inside the window
   if (nc >= beam && dropmax >= lo_key) overflow = true;
