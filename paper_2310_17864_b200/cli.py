@@ -27,9 +27,10 @@ ensure_ascii=False``, plus ``OUT.meta`` (total time, per-utterance times, failed
 ids, decoder options).  Exit codes: 0 success, 1 when any utterance failed
 (the others are still written), 2 on configuration errors.
 
-What differs from the CPU command: the decoder is the lexicon-free, LM-free
-CUDA search, so ``--lexicon`` / ``--lm`` / a silence token with a non-zero
-``--sil-score`` are configuration errors (exit 2); TSV values are rounded to
+What differs from the CPU command: the decoder is the lexicon-free CUDA search
+(token-level ``--lm`` fusion and the ``--sil-score`` bonus included), so
+``--lexicon`` is a configuration error (exit 2), as is ``--lm`` with a beam
+above 64; TSV values are rounded to
 float32, the decoder's input dtype (CTCE files are float32 already, so their
 decode is bit-identical to the CPU command's); per-utterance times in the meta
 file are the utterance's share of its batch (load + decode).
@@ -316,15 +317,21 @@ def cmd_decode(cfg: dict) -> int:
         if cfg[name] is not None and not Path(cfg[name]).exists():
             raise ConfigError(f"--{name.replace('_', '-')}: file not found: {cfg[name]}")
     opts = _options(cfg)
-    if cfg["lexicon"] is not None or cfg["lm"] is not None:
-        raise ConfigError("the CUDA decoder is lexicon-free and LM-free: --lexicon / --lm are not supported")
+    if cfg["lexicon"] is not None:
+        raise ConfigError("the CUDA decoder is lexicon-free: --lexicon is not supported")
     try:
         tokens = TokenDictionary.from_file(cfg["tokens"], blank_token=cfg["blank_token"],
                                            silence_token=cfg["silence_token"])
     except ValueError as exc:
         raise ConfigError(f"--tokens: {exc}") from exc
-    if tokens.silence_index is not None and opts.sil_score != 0.0:
-        raise ConfigError("the CUDA decoder has no silence score (--sil-score must be 0 with --silence-token)")
+    lm = None
+    if cfg["lm"] is not None:  # cli.py:214-216: a malformed model is a configuration error
+        from .lm import parse_arpa
+
+        try:
+            lm = parse_arpa(cfg["lm"])
+        except ValueError as exc:
+            raise ConfigError(str(exc)) from exc
     batch = int(cfg["gpu_batch"])
     if batch < 1:
         raise ConfigError("--gpu-batch must be >= 1")
@@ -339,6 +346,13 @@ def cmd_decode(cfg: dict) -> int:
                        nbest=opts.n_best, blank_skip_threshold=opts.blank_skip_threshold,
                        beam_threshold=opts.beam_threshold, device=int(cfg["device"]))
     dec.set_merge_mode(opts.merge_mode)
+    try:
+        if tokens.silence_index is not None:
+            dec.set_silence(tokens.silence_index, opts.sil_score)
+        if lm is not None:
+            dec.set_lm(lm, opts.lm_weight)
+    except ValueError as exc:
+        raise ConfigError(str(exc)) from exc
     too_wide = opts.beam_size_token is not None and opts.beam_size_token > len(tokens)
     if opts.beam_size_token is not None and not too_wide:
         dec.set_beam_size_token(opts.beam_size_token)
@@ -358,7 +372,7 @@ def cmd_decode(cfg: dict) -> int:
             for utt_id in ids:
                 errors[utt_id] = f"beam_size_token {opts.beam_size_token} exceeds vocabulary size {len(tokens)}"
         elif lps:
-            recs, errs = _decode_group(dec, tokens, ids, lps, strict, torch, _lib)
+            recs, errs = _decode_group(dec, tokens, ids, lps, strict, torch, _lib, opts)
             records.extend(recs)
             errors.update(errs)
         share = (time.perf_counter() - t0) / max(len(group), 1)
@@ -379,7 +393,7 @@ def cmd_decode(cfg: dict) -> int:
     return 1 if failed else 0
 
 
-def _decode_group(dec, tokens, ids, lps, strict, torch, _lib):
+def _decode_group(dec, tokens, ids, lps, strict, torch, _lib, opts):
     """Validate (EmissionMatrix checks, emissions.py:128-150) and decode one
     batch on the GPU; returns (records, {utt_id: error})."""
     import ctypes
@@ -430,6 +444,8 @@ def _decode_group(dec, tokens, ids, lps, strict, torch, _lib):
     lmax = int(lengths.max()) if lengths.size else 0
     toks = out.tokens[:, :, :lmax].cpu().numpy()
     ts = out.timesteps[:, :, :lmax].cpu().numpy()
+    lms = out.lm.cpu().numpy() if out.lm is not None else None
+    sil = tokens.silence_index
     records = []
     names = tokens.tokens
     for b in range(B):
@@ -445,7 +461,11 @@ def _decode_group(dec, tokens, ids, lps, strict, torch, _lib):
             n = int(lengths[b, r])
             ti = toks[b, r, :n].tolist()
             sc = float(scores[b, r])
-            nbest.append({"rank": r, "score": sc, "am_score": sc, "lm_score": 0.0, "token_ids": ti,
+            lm_v = float(lms[b, r]) if lms is not None else 0.0
+            # am_score = score - lm_weight * lm - bonuses (decoder.py:805-812)
+            bonuses = opts.word_score * 0 + opts.sil_score * (ti.count(sil) if sil is not None else 0)
+            am = sc - (opts.lm_weight * lm_v if lms is not None else 0.0) - bonuses
+            nbest.append({"rank": r, "score": sc, "am_score": am, "lm_score": lm_v, "token_ids": ti,
                           "tokens": [names[i] for i in ti], "words": [], "timesteps": ts[b, r, :n].tolist()})
         records.append({"utt": ids[b], "nbest": nbest})
     return records, errors

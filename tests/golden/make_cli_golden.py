@@ -34,7 +34,29 @@ RUNS = {
     "beam5_nbest3_skip": ["--beam-size", "5", "--nbest", "3", "--blank-skip-threshold", "0.9"],
     "max_merge": ["--merge", "max", "--beam-size", "8", "--nbest", "2", "--beam-threshold", "6.0"],
     "nonstrict": ["--no-strict-validation", "--beam-size", "4"],
+    # token-level LM fusion (lm.arpa: seeded synthetic bigram over the token strings)
+    "lm_bigram": ["--lm", "lm.arpa", "--lm-weight", "1.5", "--beam-size", "6", "--nbest", "2"],
+    "lm_silence": ["--lm", "lm.arpa", "--lm-weight", "0.8", "--silence-token", "u11", "--sil-score", "0.7",
+                   "--nbest", "3", "--blank-skip-threshold", "0.95"],
 }
+
+
+def write_lm(path):
+    """Seeded synthetic bigram model over u1..u10 (u11 is out of vocabulary)."""
+    rng = np.random.default_rng(7)
+    vocab = ["<s>", "</s>"] + TOKENS[1:-1]
+    lines = ["\\data\\", f"ngram 1={len(vocab)}", "ngram 2=PLACEHOLDER", "", "\\1-grams:"]
+    for w in vocab:
+        p = -99.0 if w == "<s>" else rng.uniform(-2.0, -0.4)
+        lines.append(f"{p:.4f}\t{w}\t{rng.uniform(-0.7, 0.1):.4f}")
+    big = []
+    for a in vocab[:1] + vocab[2:]:
+        for b in vocab[1:]:
+            if rng.random() < 0.4:
+                big.append(f"{rng.uniform(-1.8, -0.05):.4f}\t{a} {b}")
+    lines += ["", "\\2-grams:"] + big + ["", "\\end\\", ""]
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("\n".join(lines).replace("PLACEHOLDER", str(len(big))))
 
 
 def utterance(rng, t):
@@ -68,12 +90,14 @@ def main():
     lp = utterance(rng, 10)
     lp[3] -= 0.5
     write_emissions(EmissionMatrix(lp.astype(np.float64), strict=False), os.path.join(corpus, "unnormalized.ctce"))
+    write_lm(os.path.join(OUT, "lm.arpa"))
     expected = {}
     with tempfile.TemporaryDirectory() as tmp:
         for name, flags in RUNS.items():
             out = os.path.join(tmp, name + ".jsonl")
+            full = [os.path.join(OUT, f) if f.endswith(".arpa") else f for f in flags]
             rc = ref_cli.main(["decode", "--emissions", corpus, "--tokens", os.path.join(OUT, "tokens.txt"),
-                               "--out", out] + flags)
+                               "--out", out] + full)
             with open(out, encoding="utf-8") as fh:
                 records = [json.loads(line) for line in fh]
             with open(out + ".meta", encoding="utf-8") as fh:

@@ -81,7 +81,8 @@ def test_config_errors_exit_2(tmp_path, capsys):
     assert "file not found" in capsys.readouterr().err
     lm = tmp_path / "x.arpa"
     lm.write_text("\\data\\\n")
-    assert cli.main(base + ["--out", out, "--lm", str(lm)]) == 2 and "LM-free" in capsys.readouterr().err
+    assert cli.main(base + ["--out", out, "--lm", str(lm)]) == 2 and "ngram N=count" in capsys.readouterr().err
+    assert cli.main(base + ["--out", out, "--lexicon", str(lm)]) == 2 and "lexicon-free" in capsys.readouterr().err
     assert cli.main(base + ["--out", out, "--nbest", "20"]) == 2 and "n_best" in capsys.readouterr().err
     cfg = tmp_path / "c.json"
     cfg.write_text(json.dumps({"bogus": 1}))
@@ -100,11 +101,13 @@ def test_config_precedence(tmp_path):
 
 # ------------------------------------------------------------------ GPU: full command
 @pytest.mark.gpu
-@pytest.mark.parametrize("run", ["default", "beam5_nbest3_skip", "max_merge", "nonstrict"])
+@pytest.mark.parametrize("run", ["default", "beam5_nbest3_skip", "max_merge", "nonstrict", "lm_bigram",
+                                 "lm_silence"])
 def test_decode_matches_reference_command(tmp_path, run):
     exp = expected()[run]
     out = str(tmp_path / "o.jsonl")
-    rc = cli.main(["decode", "--emissions", CORPUS, "--tokens", TOKENS, "--out", out] + exp["flags"])
+    flags = [os.path.join(GOLD, f) if f.endswith(".arpa") else f for f in exp["flags"]]
+    rc = cli.main(["decode", "--emissions", CORPUS, "--tokens", TOKENS, "--out", out] + flags)
     assert rc == exp["exit_code"]
     with open(out, encoding="utf-8") as fh:
         got = [json.loads(line) for line in fh]
@@ -116,8 +119,9 @@ def test_decode_matches_reference_command(tmp_path, run):
     for g, e in zip(got, exp["records"]):
         assert len(g["nbest"]) == len(e["nbest"]), g["utt"]
         for a, b in zip(g["nbest"], e["nbest"]):
-            for key in ("rank", "token_ids", "tokens", "words", "timesteps", "lm_score"):
+            for key in ("rank", "token_ids", "tokens", "words", "timesteps"):
                 assert a[key] == b[key], (g["utt"], key)
+            assert a["lm_score"] == pytest.approx(b["lm_score"], abs=1e-9)
             assert a["score"] == pytest.approx(b["score"], abs=1e-9)
             assert a["am_score"] == pytest.approx(b["am_score"], abs=1e-9)
 
