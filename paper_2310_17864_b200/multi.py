@@ -66,6 +66,16 @@ class MultiDeviceDecoder:
         for dec in self.decoders:
             dec.set_beam_size_token(k)
 
+    def set_silence(self, index: Optional[int], sil_score: float = 0.0) -> None:
+        for dec in self.decoders:
+            dec.set_silence(index, sil_score)
+
+    def set_lm(self, lm, lm_weight: float = 2.0) -> None:
+        """Attach a token-level n-gram model to every device's decoder (each
+        device builds its own context x token tables)."""
+        for dec in self.decoders:
+            dec.set_lm(lm, lm_weight)
+
     def _run_host(self, dec: CUCTCDecoder, lp: torch.Tensor, lens, b0: int):
         B = lp.shape[0]
         chunks = max(1, min(16, B // 256))

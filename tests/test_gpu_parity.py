@@ -366,6 +366,10 @@ def test_multi_device_decoder_matches_single():
     single.set_merge_mode("max")
     assert multi(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda()) == \
         single(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+    multi.set_silence(cfg.vocab - 1, 0.5)
+    single.set_silence(cfg.vocab - 1, 0.5)
+    assert multi(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens)) == \
+        single(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
 
 
 @pytest.mark.parametrize("force_generic", ["0", "1"])

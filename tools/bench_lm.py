@@ -52,7 +52,7 @@ def synthetic_lm(path, tokens, order, per_ctx, seed=7):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg1"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg1", "cfg3"])
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--orders", default="2,3")
@@ -65,7 +65,7 @@ def main():
     import oracle
     from paper_2310_17864_b200 import CUCTCDecoder
 
-    cfg = synth.CONFIGS[4 if args.workload == "cfg4" else 1]
+    cfg = synth.CONFIGS[int(args.workload[3:])]
     toks = synth.simple_tokens(cfg.vocab)
     lens_all = synth.lengths(cfg)
     T = int(lens_all.max())
