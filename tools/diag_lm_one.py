@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import numpy as np, torch
 from paper_2310_17864_b200 import synth, CUCTCDecoder
 from bench_lm import synthetic_lm
-cfg = synth.CONFIGS[1]
+cfg = synth.CONFIGS[int(sys.argv[2]) if len(sys.argv) > 2 else 1]
 toks = synth.simple_tokens(cfg.vocab)
 lens_all = synth.lengths(cfg); T = int(lens_all.max())
 host = np.zeros((cfg.batch, T, cfg.vocab), np.float32)
