@@ -659,25 +659,25 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   // -- per-lane top-`beam` lists of approximate keys (specials: exact)
   uint64_t* mylk = w.lk + (size_t)lane * beam;
   uint32_t* myli = w.li + (size_t)lane * beam;
-  int cnt = 0, minpos = 0;
+  int cnt = 0;
   uint64_t minkey = 0ull, dropmax = 0ull;  // dropmax: best key this lane evicted or rejected
   uint64_t lmax = 0ull;                    // best key in this lane's list
+  // lane list kept sorted descending: inserts near the cut shift few entries
   auto insert = [&](uint64_t key, uint32_t id) {
-    lmax = key > lmax ? key : lmax;
+    int j;
     if (cnt < beam) {
-      mylk[cnt] = key; myli[cnt] = id; cnt++;
-      if (cnt == beam) {
-        minkey = ~0ull;
-        for (int i = 0; i < beam; i++) if (mylk[i] < minkey) { minkey = mylk[i]; minpos = i; }
-      }
+      j = cnt++;
     } else if (key > minkey) {
       dropmax = minkey > dropmax ? minkey : dropmax;
-      mylk[minpos] = key; myli[minpos] = id;
-      minkey = ~0ull;
-      for (int i = 0; i < beam; i++) if (mylk[i] < minkey) { minkey = mylk[i]; minpos = i; }
+      j = beam - 1;
     } else {
       dropmax = key > dropmax ? key : dropmax;
+      return;
     }
+    while (j > 0 && mylk[j - 1] < key) { mylk[j] = mylk[j - 1]; myli[j] = myli[j - 1]; j--; }
+    mylk[j] = key; myli[j] = id;
+    if (cnt == beam) minkey = mylk[beam - 1];
+    lmax = key > lmax ? key : lmax;
   };
   for (int s = lane; s < nS; s += 32)
     if (w.sp_sc[s] > -INFINITY) insert(ord64(w.sp_sc[s]), kSpecialBit | (uint32_t)s);
@@ -811,14 +811,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   }
   __syncwarp();
 
-  // -- sort each lane list (descending) and extract the global top by k-way merge
-  for (int i = 1; i < cnt; i++) {
-    const uint64_t k = mylk[i];
-    const uint32_t id = myli[i];
-    int j = i;
-    while (j > 0 && mylk[j - 1] < k) { mylk[j] = mylk[j - 1]; myli[j] = myli[j - 1]; j--; }
-    mylk[j] = k; myli[j] = id;
-  }
+  // -- extract the global top from the sorted lane lists by k-way merge
   int pos = 0, nc = 0;
   uint64_t lo_key = 0ull;
   bool overflow = false;
