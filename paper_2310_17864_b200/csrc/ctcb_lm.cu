@@ -755,10 +755,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   __syncwarp();
   auto fcut = [&](double th, double off) -> float {  // v < fcut  =>  off + v < th - tolF
     if (!(th > -INFINITY)) return -INFINITY;
-    const double c = th - 2.0 * tolF - off;
-    float cf = (float)c;
-    if ((double)cf > c) cf = nextafterf(cf, -INFINITY);
-    return cf;
+    return __double2float_rd(th - 2.0 * tolF - off);  // rounded down: the cut stays conservative
   };
   // (2) tokens whose emission can reach the cut for the most promising prefix
   double amax = -INFINITY;
@@ -785,14 +782,19 @@ __device__ int fused_step(FW& w, const float* row, int H) {
     double mth = cnt == beam ? fmax(theta, unord64(minkey)) : theta;
     float cut = fcut(mth, off);
     const int rot = d & 31;
+    // this prefix's excluded tokens (children's repeat groups): two in registers, else the list
+    int ex0 = -1, ex1 = -1, nex = 0;
+    for (int k = 0; k < nEx; k++)
+      if (w.exd[k] == d) { if (nex == 0) ex0 = w.exc[k]; else if (nex == 1) ex1 = w.exc[k]; nex++; }
     for (int j0 = 0; j0 < nP; j0 += 32) {
       int j = j0 + ((lane + rot) & 31);  // spread one token's pairs over lanes
       if (j >= nP) continue;
       const int c = w.plist[j];
       const float vf = row[c];
       if ((!(vf < cut) || c == P.sil) && c != lastc) {
-        bool ok = true;
-        for (int k = 0; k < nEx; k++) ok &= !(w.exd[k] == d && w.exc[k] == c);
+        bool ok = c != ex0 && c != ex1;
+        if (nex > 2)
+          for (int k = 0; k < nEx; k++) ok &= !(w.exd[k] == d && w.exc[k] == c);
         if (ok) {
           const double x = approx(d, c, vf);
           if (x > -INFINITY) {
@@ -807,7 +809,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
         }
       }
     }
-    if (d < 2 || (d & 3) == 3) theta = bound();
+    if (d == 1 || (d & 7) == 7) theta = bound();
   }
   __syncwarp();
 
