@@ -237,3 +237,24 @@ def test_fused_errors(tmp_path):
     dec.set_lm(lm, 1.0)
     dec.set_lm(None)
     assert dec._lm is None
+
+
+@pytest.mark.gpu
+def test_fused_host_buffer_path_matches_device_path(tmp_path):
+    """__call__ with a pinned CPU tensor (ctcb_decode_host_async, chunked) and
+    with CUDA tensors give the same LM-fused hypotheses."""
+    import torch
+    from paper_2310_17864_b200 import CUCTCDecoder
+    rng = np.random.default_rng(12)
+    V, T, B = 50, 80, 600
+    toks = ["-"] + [f"w{i}" for i in range(1, V)]
+    lm = random_arpa(tmp_path / "h.arpa", rng, toks[1:], 2, 0.3)
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    x = rng.normal(size=(B, T, V)) * 2.0
+    x = x - x.max(2, keepdims=True)
+    lp = (x - np.log(np.exp(x).sum(2, keepdims=True))).astype(np.float32)
+    dec = CUCTCDecoder(toks, beam_size=8, nbest=2)
+    dec.set_lm(lm, 1.2)
+    dev = dec(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+    host = dec(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens))
+    assert dev == host and len(dev) == B
