@@ -285,6 +285,19 @@ def _merge_config(args: argparse.Namespace) -> dict:
     return merged
 
 
+def _device_index(dev) -> int:
+    """--device: an ordinal, "cuda" (device 0) or "cuda:N"."""
+    text = str(dev).strip().lower()
+    if text == "cuda":
+        return 0
+    if text.startswith("cuda:"):
+        text = text[5:]
+    try:
+        return int(text)
+    except ValueError:
+        raise ConfigError(f"--device: expected N, cuda or cuda:N, got {dev!r}") from None
+
+
 def _options(cfg: dict):
     from .ctcforge_api import DecoderOptions
 
@@ -344,7 +357,7 @@ def cmd_decode(cfg: dict) -> int:
 
     dec = CUCTCDecoder(list(tokens.tokens), blank_id=tokens.blank_index, beam_size=opts.beam_size,
                        nbest=opts.n_best, blank_skip_threshold=opts.blank_skip_threshold,
-                       beam_threshold=opts.beam_threshold, device=int(cfg["device"]))
+                       beam_threshold=opts.beam_threshold, device=_device_index(cfg["device"]))
     dec.set_merge_mode(opts.merge_mode)
     try:
         if tokens.silence_index is not None:
@@ -526,7 +539,7 @@ def cmd_align(cfg: dict) -> int:
                     results[utt_id] = str(exc)
             if prepared:
                 aligned = galign.forced_align_batch([p[2] for p in prepared], [p[3] for p in prepared], tokens,
-                                                    device=int(cfg["device"]), raise_errors=False)
+                                                    device=_device_index(cfg["device"]), raise_errors=False)
                 for (utt_id, transcript, _, _), r in zip(prepared, aligned):
                     results[utt_id] = (transcript, r) if not isinstance(r, str) else r
             for utt_id, _ in group:
@@ -589,7 +602,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--out", default=_UNSET, help="output JSON-lines path (required)")
     p.add_argument("--workers", type=int, default=_UNSET, help="accepted for compatibility (the GPU batches)")
     p.add_argument("--gpu-batch", type=int, default=_UNSET, dest="gpu_batch", help="utterances per launch")
-    p.add_argument("--device", type=int, default=_UNSET)
+    p.add_argument("--device", default=_UNSET, help="CUDA device: N, cuda or cuda:N")
 
     p = sub.add_parser("align", help="force-align transcripts to emissions")
     p.add_argument("--config", default=_UNSET, help="JSON config file")
@@ -605,7 +618,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--attribute-blanks", action=argparse.BooleanOptionalAction, default=_UNSET,
                    dest="attribute_blanks", help="widen spans so blanks attach to the preceding token")
     p.add_argument("--gpu-batch", type=int, default=_UNSET, dest="gpu_batch", help="utterances per launch")
-    p.add_argument("--device", type=int, default=_UNSET)
+    p.add_argument("--device", default=_UNSET, help="CUDA device: N, cuda or cuda:N")
     return parser
 
 

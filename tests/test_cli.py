@@ -89,6 +89,12 @@ def test_config_errors_exit_2(tmp_path, capsys):
     assert cli.main(base + ["--out", out, "--config", str(cfg)]) == 2 and "unknown key" in capsys.readouterr().err
 
 
+def test_device_argument():
+    assert cli._device_index("cuda") == 0 and cli._device_index("cuda:3") == 3 and cli._device_index(2) == 2
+    with pytest.raises(cli.ConfigError, match="--device"):
+        cli._device_index("cpu")
+
+
 def test_config_precedence(tmp_path):
     # CLI > --config file > defaults (cli.py:130-148)
     cfg = tmp_path / "c.json"
