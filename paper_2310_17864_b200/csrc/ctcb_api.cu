@@ -461,6 +461,10 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     P.lm_next = h->lm.next;
     P.lm_fin = h->lm.fin;
     P.lm_wmax = h->lm.wmax;
+    P.lm_wx = h->lm.wx;
+    P.lm_A = h->lm.A;
+    P.lm_wu = h->lm.wu;
+    P.lm_xbits = h->lm.xbits;
     P.lm_start = h->lm.start;
     P.lm_weight = h->lm_weight;
   }

@@ -61,6 +61,10 @@ struct Params {
   const int32_t* lm_next;   // [S, V] successor context
   const double* lm_fin;     // [S] score of "</s>"
   const double* lm_wmax;    // [S] max_c weight * lm_score[s, c] (pruning bound)
+  const double* lm_wx;      // [S] the same maximum over the explicit tokens of s
+  const double* lm_A;       // [S] accumulated backoff: other tokens score A_s + lm_score[0, c]
+  const double* lm_wu;      // [V] weight * lm_score[0, c] (-inf: blank / silence)
+  const uint32_t* lm_xbits; // [S, ceil(V/32)] explicit-token bitmap
   int lm_start;             // start context
   double lm_weight;
   int sil;                  // silence token (-1: none)
@@ -89,6 +93,10 @@ struct LmTables {
   int32_t* next;
   double* fin;
   double* wmax;
+  double* wx;
+  double* A;
+  double* wu;
+  uint32_t* xbits;
   int64_t n_states;
   int start;
 };

@@ -153,6 +153,65 @@ __global__ void ctcb_lm_bound_kernel(const double* __restrict__ score, const int
   }
 }
 
+// per context: the accumulated backoff A_s of a token with no explicit n-gram
+// above the unigram (the _backoff_score walk with no early hit, lm.py:247-262).
+// Such a token scores exactly A_s + U[c] (U = the empty context's row).
+__global__ void ctcb_lm_backoff_kernel(NgView m, long long S, double* __restrict__ A) {
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < S; s += (long long)gridDim.x * blockDim.x) {
+    int32_t ctx[kMaxOrder];
+    int n = 0;
+    const int e0 = m.state_entry[s];
+    if (e0 >= 0) {
+      n = m.lengths[e0];
+      for (int j = 0; j < n; j++) ctx[j] = m.words[(size_t)e0 * m.order + j];
+    }
+    double acc = 0.0;
+    for (int off = 0; off < n; off++) {
+      const int ce = ng_find(m, ctx + off, n - off);
+      if (ce >= 0) acc += m.backoff[ce];
+    }
+    A[s] = acc;
+  }
+}
+
+// explicit-token bitmap (bit c of context s: a word token whose score is not
+// A_s + U[c]), the maximum of weight * score over those tokens, and
+// weight * U[c] (-inf for blank / silence)
+__global__ void ctcb_lm_explicit_kernel(const double* __restrict__ score, const int32_t* __restrict__ token_word,
+                                        const double* __restrict__ A, int V, double w, uint32_t* __restrict__ xbits,
+                                        double* __restrict__ wx) {
+  const long long s = blockIdx.x;
+  const int W = (V + 31) / 32;
+  const double as = A[s];
+  double mx = -INFINITY;
+  for (int wi = threadIdx.x >> 5; wi < W; wi += blockDim.x >> 5) {
+    const int c = wi * 32 + (threadIdx.x & 31);
+    bool x = false;
+    if (c < V && token_word[c] != -2) {
+      const double l = score[s * V + c];
+      x = l != as + score[c];
+      if (x) mx = fmax(mx, w * l);
+    }
+    const unsigned bits = __ballot_sync(FULL, x);
+    if ((threadIdx.x & 31) == 0) xbits[s * W + wi] = bits;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    if (threadIdx.x == 0) wx[s] = mx;
+  }
+}
+
+__global__ void ctcb_lm_wu_kernel(const double* __restrict__ score, const int32_t* __restrict__ token_word, int V,
+                                  double w, double* __restrict__ wu) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < V; c += gridDim.x * blockDim.x)
+    wu[c] = token_word[c] == -2 ? -INFINITY : w * score[c];
+}
+
 NgView view_of(const LmModel* m) {
   NgView v;
   v.order = m->order;
@@ -256,7 +315,7 @@ void lm_model_destroy(LmModel* m) {
 int lm_tables_build(const LmModel* m, const int32_t* token_word, int V, double weight, LmTables* t, const char** err) {
   memset(t, 0, sizeof(*t));
   const long long S = m->n_states;
-  const size_t need = (size_t)S * V * 12 + (size_t)S * 16 + (size_t)V * 4;
+  const size_t need = (size_t)S * V * 12 + (size_t)S * ((V + 31) / 32) * 4 + (size_t)S * 32 + (size_t)V * 12;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { *err = "cudaMemGetInfo failed"; return CTCB_ERR_CUDA; }
   if (need > free_b / 2) { *err = "LM tables (contexts x tokens) do not fit in half the free device memory"; return CTCB_ERR_UNSUPPORTED; }
@@ -265,6 +324,10 @@ int lm_tables_build(const LmModel* m, const int32_t* token_word, int V, double w
   if (e == cudaSuccess) e = cudaMalloc(&t->next, (size_t)S * V * 4);
   if (e == cudaSuccess) e = cudaMalloc(&t->fin, (size_t)S * 8);
   if (e == cudaSuccess) e = cudaMalloc(&t->wmax, (size_t)S * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&t->wx, (size_t)S * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&t->A, (size_t)S * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&t->wu, (size_t)V * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&t->xbits, (size_t)S * ((V + 31) / 32) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&dtw, (size_t)V * 4);
   if (e == cudaSuccess) e = cudaMemcpy(dtw, token_word, (size_t)V * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
@@ -280,6 +343,19 @@ int lm_tables_build(const LmModel* m, const int32_t* token_word, int V, double w
     }
     if (e == cudaSuccess) {
       ctcb_lm_bound_kernel<<<(unsigned)S, 256>>>(t->score, dtw, V, weight, t->wmax);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      long long fb = (S + 255) / 256;
+      ctcb_lm_backoff_kernel<<<(int)(fb > 65536 ? 65536 : fb), 256>>>(v, S, t->A);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      ctcb_lm_explicit_kernel<<<(unsigned)S, 256>>>(t->score, dtw, t->A, V, weight, t->xbits, t->wx);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      ctcb_lm_wu_kernel<<<(V + 255) / 256, 256>>>(t->score, dtw, V, weight, t->wu);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -300,6 +376,10 @@ void lm_tables_free(LmTables* t) {
   cudaFree(t->next);
   cudaFree(t->fin);
   cudaFree(t->wmax);
+  cudaFree(t->wx);
+  cudaFree(t->A);
+  cudaFree(t->wu);
+  cudaFree(t->xbits);
   memset(t, 0, sizeof(*t));
 }
 
@@ -308,7 +388,7 @@ namespace {
 
 struct FusedLayout {
   size_t rows, mbar, cs, clm, ch, cph, cn, cl, cf, cst, ns, nlm, nh, nph, nn, nl, nf, nst, ntrel;
-  size_t first, dpi, e1, e2, f1, pd, lA, vmin, exd, exc;
+  size_t first, dpi, e1, e2, f1, pd, lA, vmin, vo1, vo2, exd, exc;
   size_t sp_sc, sp_lm, sp_base, sp_x, sp_flag, sp_src, sp_tok, sp_st;
   size_t lk, li, c_key, c_ord, c_id, c_sc, c_lm, c_src, c_st, excl, plist, seed, hist, misc;
   size_t total;
@@ -333,7 +413,7 @@ __host__ __device__ inline FusedLayout make_fused_layout(int beam, int V, int ri
   L.mbar = take((size_t)ring * 8, 8);
   L.cs = take(8 * B, 8); L.clm = take(8 * B, 8); L.ch = take(8 * B, 8); L.cph = take(8 * B, 8);
   L.ns = take(8 * B, 8); L.nlm = take(8 * B, 8); L.nh = take(8 * B, 8); L.nph = take(8 * B, 8);
-  L.lA = take(8 * B, 8); L.vmin = take(8 * B, 8);
+  L.lA = take(8 * B, 8); L.vmin = take(8 * B, 8); L.vo1 = take(8 * B, 8); L.vo2 = take(8 * B, 8);
   L.sp_sc = take(8 * (size_t)L.sp_cap, 8); L.sp_lm = take(8 * (size_t)L.sp_cap, 8);
   L.lk = take(8 * 32 * B, 8);
   L.c_key = take(8 * (size_t)L.cc_pad, 8);
@@ -369,7 +449,7 @@ struct FW {
   int lane, u, steps_done, V;
   uint8_t* rows;
   uint64_t* mbar;
-  double *cs, *clm, *ns, *nlm, *lA, *vmin, *sp_sc, *sp_lm, *c_sc, *c_lm;
+  double *cs, *clm, *ns, *nlm, *lA, *vmin, *vo1, *vo2, *sp_sc, *sp_lm, *c_sc, *c_lm;
   uint64_t *ch, *cph, *nh, *nph, *lk, *c_key;
   int *cn, *cl, *cf, *cst, *nn, *nl, *nf, *nst, *first, *dpi, *e1, *e2, *f1, *pd, *exd, *exc;
   int *sp_base, *sp_x, *sp_flag, *sp_src, *sp_tok, *sp_st, *c_ord, *c_src, *c_st, *misc, *seed, *plist;
@@ -397,6 +477,7 @@ __device__ void fcarve(FW& w, uint8_t* base, const Params& P) {
   w.ns = (double*)(base + L.ns); w.nlm = (double*)(base + L.nlm);
   w.nh = (uint64_t*)(base + L.nh); w.nph = (uint64_t*)(base + L.nph);
   w.lA = (double*)(base + L.lA); w.vmin = (double*)(base + L.vmin);
+  w.vo1 = (double*)(base + L.vo1); w.vo2 = (double*)(base + L.vo2);
   w.sp_sc = (double*)(base + L.sp_sc); w.sp_lm = (double*)(base + L.sp_lm);
   w.lk = (uint64_t*)(base + L.lk);
   w.c_key = (uint64_t*)(base + L.c_key);
@@ -748,27 +829,56 @@ __device__ int fused_step(FW& w, const float* row, int H) {
       if (valid_pair(d, bc)) offer(d, bc, approx(d, bc, bv));
   __syncwarp();
   theta = bound();
+  // upper-bound offsets of prefix d's append (d, c) minus v_c: coarse (any
+  // token: lA + max_c w L), explicit n-gram tokens (lA + wx_s) and backoff
+  // tokens (lA + w A_s, plus w U[c]; exact, read without the LM row)
+  const int W = (V + 31) / 32;
   for (int d = lane; d < nD; d += 32) {
-    const double wb = use_lm ? P.lm_wmax[w.cst[w.e1[d]]] : 0.0;
-    w.vmin[d] = w.lA[d] + wb;  // upper-bound offset of prefix d's appends (silence: lA)
+    const int sd = w.cst[w.e1[d]];
+    w.vmin[d] = w.lA[d] + (use_lm ? P.lm_wmax[sd] : 0.0);
+    w.vo1[d] = use_lm ? w.lA[d] + P.lm_wx[sd] : w.lA[d];
+    w.vo2[d] = use_lm ? w.lA[d] + P.lm_weight * P.lm_A[sd] : -INFINITY;
   }
   __syncwarp();
   auto fcut = [&](double th, double off) -> float {  // v < fcut  =>  off + v < th - tolF
     if (!(th > -INFINITY)) return -INFINITY;
     return __double2float_rd(th - 2.0 * tolF - off);  // rounded down: the cut stays conservative
   };
-  // (2) tokens whose emission can reach the cut for the most promising prefix
-  double amax = -INFINITY;
-  for (int d = lane; d < nD; d += 32) amax = fmax(amax, w.vmin[d]);
-  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(FULL, amax, o));
+  // (2) tokens whose emission can reach the cut for some prefix: a coarse
+  //     float cut, then (LM) the token's own bound: explicit in some prefix's
+  //     context (OR of the prefixes' bitmap words) or the backoff bound
+  double amax = -INFINITY, p1 = -INFINITY, p2 = -INFINITY;
+  for (int d = lane; d < nD; d += 32) {
+    amax = fmax(amax, w.vmin[d]);
+    p1 = fmax(p1, w.vo1[d]);
+    p2 = fmax(p2, w.vo2[d]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(FULL, amax, o));
+    p1 = fmax(p1, __shfl_xor_sync(FULL, p1, o));
+    p2 = fmax(p2, __shfl_xor_sync(FULL, p2, o));
+  }
   const float gcut = fcut(theta, amax);
+  const double gth = theta - 2.0 * tolF;
+  const int myst = (use_lm && lane < nD) ? w.cst[w.e1[lane]] : -1;  // nD <= beam <= 32 for the OR
   int nP = 0;
   for (int c0 = 0; c0 < V; c0 += 32) {
     const int c = c0 + lane;
+    uint32_t xor_any = 0u;
+    if (use_lm) {
+      uint32_t wbits = 0u;
+      if (myst >= 0) wbits = P.lm_xbits[(size_t)myst * W + (c0 >> 5)];
+      for (int d = lane + 32; d < nD; d += 32) wbits |= P.lm_xbits[(size_t)w.cst[w.e1[d]] * W + (c0 >> 5)];
+      xor_any = __reduce_or_sync(FULL, wbits);
+    }
     bool pass = false;
     if (c < V) {
       const float vf = row[c];
       pass = (!(vf < gcut) || c == P.sil) && c != P.blank && c != w.seed[lane] && selected(c);
+      if (pass && use_lm && c != P.sil) {
+        const double v = (double)vf;
+        pass = (((xor_any >> lane) & 1u) && !(v + p1 < gth)) || !(v + (p2 + P.lm_wu[c]) < gth);
+      }
     }
     const unsigned bal = __ballot_sync(FULL, pass);
     if (pass) w.plist[nP + __popc(bal & lanemask_lt())] = c;
@@ -778,7 +888,9 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   // (3) prefix-major over the listed tokens, each pair against its prefix's cut
   for (int d = 0; d < nD; d++) {
     const int lastc = w.cl[w.e1[d]];
-    const double off = w.vmin[d];
+    const double off = w.vmin[d], o1 = w.vo1[d], o2 = w.vo2[d];
+    const int sd = w.cst[w.e1[d]];
+    const double Ad = use_lm ? P.lm_A[sd] : 0.0;
     double mth = cnt == beam ? fmax(theta, unord64(minkey)) : theta;
     float cut = fcut(mth, off);
     const int rot = d & 31;
@@ -795,8 +907,20 @@ __device__ int fused_step(FW& w, const float* row, int H) {
         bool ok = c != ex0 && c != ex1;
         if (nex > 2)
           for (int k = 0; k < nEx; k++) ok &= !(w.exd[k] == d && w.exc[k] == c);
+        double x = -INFINITY;
         if (ok) {
-          const double x = approx(d, c, vf);
+          if (!use_lm || c == P.sil) {
+            x = approx(d, c, vf);
+          } else {
+            const double v = (double)vf, th2 = mth - 2.0 * tolF;
+            if ((P.lm_xbits[(size_t)sd * W + (c >> 5)] >> (c & 31)) & 1u) {
+              if (!(v + o1 < th2)) x = approx(d, c, vf);  // explicit n-gram: read the LM row
+            } else if (!(v + (o2 + P.lm_wu[c]) < th2)) {
+              // backoff token: score[s, c] == A_s + U[c] bit for bit
+              x = (w.lA[d] + v) + P.lm_weight * (Ad + P.lm_score[c]);
+              if (c == P.sil) x = x + P.sil_score;
+            }
+          }
           if (x > -INFINITY) {
             const uint64_t key = ord64(x);
             if (cnt < beam || key > minkey) {
