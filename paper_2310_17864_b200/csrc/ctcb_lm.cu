@@ -824,8 +824,11 @@ __device__ int fused_step(FW& w, const float* row, int H) {
     bc = (mk && (c1 & 31) == lane) ? c1 : -1;
   }
   w.seed[lane] = bc;
+  // seeds go to the best prefixes only (entries are in rank order); the
+  // remaining (prefix, seed token) pairs are scanned with the others below
+  const int nSeedD = (!use_lm || nD < 2) ? nD : 2;  // without an LM: the best token for every prefix
   if (bc >= 0)
-    for (int d = 0; d < nD; d++)
+    for (int d = 0; d < nSeedD; d++)
       if (valid_pair(d, bc)) offer(d, bc, approx(d, bc, bv));
   __syncwarp();
   theta = bound();
@@ -874,7 +877,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
     bool pass = false;
     if (c < V) {
       const float vf = row[c];
-      pass = (!(vf < gcut) || c == P.sil) && c != P.blank && c != w.seed[lane] && selected(c);
+      pass = (!(vf < gcut) || c == P.sil) && c != P.blank && (c != w.seed[lane] || nD > nSeedD) && selected(c);
       if (pass && use_lm && c != P.sil) {
         const double v = (double)vf;
         pass = (((xor_any >> lane) & 1u) && !(v + p1 < gth)) || !(v + (p2 + P.lm_wu[c]) < gth);
@@ -903,7 +906,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
       if (j >= nP) continue;
       const int c = w.plist[j];
       const float vf = row[c];
-      if ((!(vf < cut) || c == P.sil) && c != lastc) {
+      if ((!(vf < cut) || c == P.sil) && c != lastc && (d >= nSeedD || c != w.seed[c & 31])) {
         bool ok = c != ex0 && c != ex1;
         if (nex > 2)
           for (int k = 0; k < nEx; k++) ok &= !(w.exd[k] == d && w.exc[k] == c);

@@ -11,7 +11,7 @@ lens_all = synth.lengths(cfg); T = int(lens_all.max())
 host = np.zeros((cfg.batch, T, cfg.vocab), np.float32)
 _, lens = synth.batch(cfg, out=host, t_pad=T)
 dec = CUCTCDecoder(toks, beam_size=10, nbest=1, blank_skip_threshold=0.95)
-if sys.argv[1:] == ["sil"]:
+if sys.argv[1:2] == ["sil"]:
     dec.set_silence(cfg.vocab - 1, 0.5)
 else:
     dec.set_lm(synthetic_lm(tempfile.mktemp(), toks[1:], 2, 20), 2.0)
