@@ -258,3 +258,28 @@ def test_fused_host_buffer_path_matches_device_path(tmp_path):
     dev = dec(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
     host = dec(torch.from_numpy(lp).pin_memory(), torch.from_numpy(lens))
     assert dev == host and len(dev) == B
+
+
+def test_flatten_and_token_words(tmp_path):
+    """Device export: n-grams in ascending order with -1 padding, the start
+    context, the end word, and the token -> word map (identity for blank and
+    silence, <unk> for unknown strings, -1 without <unk>)."""
+    p = tmp_path / "f.arpa"
+    p.write_text("\\data\\\nngram 1=4\nngram 2=2\n\n\\1-grams:\n-1.0\t<s>\t-0.2\n-0.5\t</s>\n-0.7\ta\t-0.1\n"
+                 "-0.9\tb\n\n\\2-grams:\n-0.3\t<s> a\n-0.4\ta b\n\n\\end\\\n")
+    lm = glm.parse_arpa(p)
+    f = glm.flatten(lm)
+    assert f.order == 2 and f.words.shape == (6, 2) and f.lengths.tolist() == [1, 1, 1, 1, 2, 2]
+    assert (f.words[:4, 1] == -1).all()
+    assert f.start_len == 1 and f.start[0] == lm.vocab["<s>"] and f.eos == lm.vocab["</s>"] and f.unk == -1
+    assert f.logprob[4] == -0.3 * glm.LN10 and f.backoff[2] == -0.1 * glm.LN10
+    tw = glm.token_words(lm, ["-", "a", "b", "zz", "|"], 0, sil=4)
+    assert tw.tolist() == [-2, lm.vocab["a"], lm.vocab["b"], -1, -2]
+    p.write_text(p.read_text().replace("ngram 1=4", "ngram 1=5").replace("-0.9\tb\n", "-0.9\tb\n-2.0\t<unk>\n"))
+    lm2 = glm.parse_arpa(p)
+    assert glm.token_words(lm2, ["-", "zz"], 0).tolist() == [-2, lm2.vocab["<unk>"]]
+    assert glm.flatten(lm2).unk == lm2.vocab["<unk>"]
+    # a unigram model has the empty start context
+    q = tmp_path / "u.arpa"
+    q.write_text("\\data\\\nngram 1=2\n\n\\1-grams:\n-1.0\t<s>\n-0.5\ta\n\n\\end\\\n")
+    assert glm.flatten(glm.parse_arpa(q)).start_len == 0
