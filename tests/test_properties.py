@@ -3,7 +3,8 @@ own behavioural tests (ctcforge tests/test_decoder.py: greedy equivalence at
 beam 1 with max merge, the exhaustive CTC path-sum at unbounded beam, n-best
 ordering, max-merge beam monotonicity, batch-of-one and permutation
 invariance) with independent checkers written here (greedy collapse and an
-exhaustive enumeration of all frame paths), not the oracle."""
+exhaustive enumeration of all frame paths).  The last test covers the edge
+sizes (V = 2, T = 4000) against the oracle."""
 
 import itertools
 
@@ -133,3 +134,22 @@ def test_batch_of_one_equals_batch_member():
         single = decode(lp[b, : lens[b]], 6, nbest=3, thr=0.95)
         assert [t for t, _, _ in single] == [tok[b, j, : ln[b, j]].tolist() for j in range(cnt[b])]
         assert [s for _, s, _ in single] == [float(sc[b, j]) for j in range(cnt[b])]
+
+
+def test_two_token_vocabulary_and_long_utterances():
+    """V = 2 (blank + one token; top-k of 1) on both kernels, and T = 4000
+    frames (long trellis walks) against the oracle."""
+    import oracle
+    rng = np.random.default_rng(41)
+    for beam in (1, 2, 4, 20):
+        lp = logsoftmax32(rng.normal(size=(30, 2)) * 2)
+        got = decode(lp, beam, nbest=min(beam, 2), thr=0.95)
+        ref = oracle.decode(lp, beam_size=beam, n_best=min(beam, 2), blank_skip_threshold=0.95)
+        assert [t for t, _, _ in got] == ref.tokens and np.allclose([s for _, s, _ in got], ref.scores, atol=1e-9)
+    lp = logsoftmax32(rng.normal(size=(4000, 24)) * 3)
+    for beam in (10, 24):
+        got = decode(lp, beam, nbest=3, thr=0.95)
+        ref = oracle.decode(lp, beam_size=beam, n_best=3, blank_skip_threshold=0.95)
+        assert [t for t, _, _ in got] == ref.tokens
+        assert np.allclose([s for _, s, _ in got], ref.scores, rtol=0, atol=1e-6)
+        assert [ts for _, _, ts in got] == ref.timesteps
