@@ -283,3 +283,30 @@ def test_flatten_and_token_words(tmp_path):
     q = tmp_path / "u.arpa"
     q.write_text("\\data\\\nngram 1=2\n\n\\1-grams:\n-1.0\t<s>\n-0.5\ta\n\n\\end\\\n")
     assert glm.flatten(glm.parse_arpa(q)).start_len == 0
+
+
+@pytest.mark.gpu
+def test_fused_kernel_four_gram_model(tmp_path):
+    """Order 4 (contexts of three words, deeper backoff chains) against the oracle."""
+    import torch
+    from paper_2310_17864_b200 import CUCTCDecoder
+    rng = np.random.default_rng(404)
+    V, T, B = 9, 40, 10
+    toks = ["-"] + [f"w{i}" for i in range(1, V)]
+    lm = random_arpa(tmp_path / "q.arpa", rng, toks[1:], 4, 0.35)
+    assert lm.order == 4
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    x = rng.normal(size=(B, T, V)) * 2.0
+    x = x - x.max(2, keepdims=True)
+    lp = (x - np.log(np.exp(x).sum(2, keepdims=True))).astype(np.float32)
+    dec = CUCTCDecoder(toks, beam_size=12, nbest=3, blank_skip_threshold=1.0)
+    dec.set_lm(lm, 1.4)
+    out = dec.decode(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+    tokens, _, lengths, scores, counts = dec.to_host(out)
+    lms = out.lm.cpu().numpy()
+    tabs = oracle.lm_tables(glm.flatten(lm), glm.token_words(lm, toks, 0))
+    for b in range(B):
+        ref = oracle.decode(lp[b, : lens[b]], beam_size=12, n_best=3, lm=tabs, lm_weight=1.4)
+        assert [tokens[b, j, : lengths[b, j]].tolist() for j in range(counts[b])] == ref.tokens, b
+        for j in range(counts[b]):
+            assert _close(scores[b, j], ref.scores[j]) and _close(lms[b, j], ref.lm_scores[j])
