@@ -501,7 +501,10 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
     CTCB_CUDA(cudaGetLastError());
     ctcb::Params Q = P;
-    Q.smem_per_warp = (int)ctcb::align_up((size_t)ctcb::kTopkRing * P.row_bytes + 64 + 64 * 8 + 256 * 4 + 64 * 4 + 64 * 2, 128);
+    // V > 512 with 16-B rows: the top-k kernel reads rows from global memory
+    // (no staging ring, row_bytes = 0), so far more warps fit per SM
+    if (P.V > ctcb::kSmallV && P.bulk_ok && P.V % 4 == 0 && getenv("CTCB_TOPK_STAGED") == nullptr) Q.row_bytes = 0;
+    Q.smem_per_warp = (int)ctcb::align_up((size_t)ctcb::kTopkRing * Q.row_bytes + 64 + 64 * 8 + 256 * 4 + 64 * 4 + 64 * 2, 128);
     int twpb = h->max_smem_optin / Q.smem_per_warp;
     twpb = twpb < 1 ? 1 : (twpb > 8 ? 8 : twpb);
     const size_t tsmem = (size_t)Q.smem_per_warp * twpb;

@@ -215,14 +215,15 @@ __device__ bool fast_precedes(const Params& P, const FastSmem& S, int u, int sd,
 // Exact top-k fallback (rows with > 64 candidates above the lane-max
 // threshold, e.g. many exactly tied values): 8-bit radix select on the order
 // keys, ordered compaction, register sort.  Returns this lane's S key.
-__device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k, int lane) {
+template <class KeyOf>
+__device__ uint64_t topk_radix_f(const FastSmem& S, KeyOf key_of, int V, int k, int lane) {
   uint32_t prefix = 0, pmask = 0;
   int need = k;
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = lane; b < 256; b += 32) S.hist[b] = 0;
     __syncwarp();
     for (int c = lane; c < V; c += 32) {
-      uint32_t key = okey(row[c]);
+      uint32_t key = key_of(c);
       if (key && (key & pmask) == prefix) atomicAdd(&S.hist[(key >> shift) & 255u], 1u);
     }
     __syncwarp();
@@ -257,7 +258,7 @@ __device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k
   const unsigned lt = lanemask_lt();
   for (int c0 = 0; c0 < V; c0 += 32) {
     int c = c0 + lane;
-    uint32_t key = c < V ? okey(row[c]) : 0u;
+    uint32_t key = c < V ? key_of(c) : 0u;
     bool gt = key > kth, eq = key != 0u && key == kth;
     unsigned beq = __ballot_sync(FULL, eq);
     bool acc = gt || (eq && eq_taken + __popc(beq & lt) < need);
@@ -270,6 +271,9 @@ __device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k
   uint64_t x = lane < n ? S.cand[lane] : 0ull;
   __syncwarp();
   return sort_desc64(x, lane);
+}
+__device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k, int lane) {
+  return topk_radix_f(S, [&](int c) { return okey(row[c]); }, V, k, lane);
 }
 
 }  // namespace
@@ -358,6 +362,62 @@ __device__ __forceinline__ uint64_t topk_key(const FastSmem& S, const float* row
     skey = topk_radix(S, row, V, k, lane);
   }
   return skey;
+}
+// Top-k of one row read straight from global memory (large V, frame-parallel
+// kernel): the passes of topk_key with the blank column masked on the fly, so
+// nothing is staged in shared memory and many more warps fit per SM (the
+// passes after the first hit L1/L2).  Requires V % 4 == 0 and a 16-B aligned row.
+__device__ __forceinline__ uint64_t topk_key_g(const FastSmem& S, const float* __restrict__ grow, int V, int blank,
+                                               int k, int lane, unsigned long long* dbg) {
+  const float4* g4 = (const float4*)grow;
+  const int nch4 = V >> 2;
+  const float sent = __uint_as_float(kSentinel);
+  auto ld = [&](int c) -> float4 {
+    float4 q = __ldg(g4 + c);
+    const int b = blank - 4 * c;
+    if (b == 0) q.x = sent;
+    if (b == 1) q.y = sent;
+    if (b == 2) q.z = sent;
+    if (b == 3) q.w = sent;
+    return q;
+  };
+  float lmax = sent;
+  for (int c = lane; c < nch4; c += 32) {
+    const float4 q = ld(c);
+    lmax = fmaxf(lmax, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+  }
+  const uint32_t t0 = __shfl_sync(FULL, sort_desc32(isnan(lmax) ? 0u : okey(lmax), lane), k - 1);
+  const float tf = t0 == 0u ? -INFINITY : unord32(t0);
+  int cl = 0;
+  for (int c = lane; c < nch4; c += 32) {
+    const float4 q = ld(c);
+    cl += (q.x >= tf) + (q.y >= tf) + (q.z >= tf) + (q.w >= tf);
+  }
+  const int cnt = __reduce_add_sync(FULL, cl);
+  if (cnt > 64) {
+    if (lane == 0 && dbg) atomicAdd(&dbg[kDbgRadix], 1ull);
+    return topk_radix_f(S, [&](int c) { return c == blank ? 0u : okey(__ldg(grow + c)); }, V, k, lane);
+  }
+  int off = warp_incl_scan(cl, lane) - cl;
+  for (int c = lane; c < nch4; c += 32) {
+    const float4 q = ld(c);
+    const float vv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int z = 0; z < 4; z++)
+      if (vv[z] >= tf) S.cand[off++] = ((uint64_t)okey(vv[z]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)(4 * c + z));
+  }
+  __syncwarp();
+  uint64_t a = lane < cnt ? S.cand[lane] : 0ull;
+  uint64_t bq = lane + 32 < cnt ? S.cand[lane + 32] : 0ull;
+  __syncwarp();
+  a = sort_desc64(a, lane);
+  if (cnt > 32) {
+    bq = sort_desc64(bq, lane);
+    const uint64_t br = shfl64(bq, 31 - lane);
+    a = a > br ? a : br;
+    a = merge_desc64(a, lane);
+  }
+  return a;
 }
 __device__ __forceinline__ int skey_tok(uint64_t skey) { return (int)(0xffffffffu - (uint32_t)(skey & 0xffffffffu)); }
 
@@ -1272,6 +1332,29 @@ __global__ void __launch_bounds__(256, CTCB_TOPK_MIN_BLOCKS) ctcb_topk_kernel(co
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
   const long long g0 = total * w / nw, g1 = total * (w + 1) / nw;
   if (g0 >= g1) return;
+  if (P.row_bytes == 0) {
+    // large vocabulary: rows read straight from global memory (topk_key_g)
+    int lo = 0, hi = P.B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.rowoff[mid] <= g0) lo = mid; else hi = mid - 1;
+    }
+    int cu = lo, ci = (int)(g0 - P.rowoff[lo]);
+    while (cu < P.B && ci >= P.kept[cu]) { cu++; ci = 0; }
+    for (long long g = g0; g < g1; g++) {
+      const float* src = P.lp + (size_t)cu * P.stride_b + (size_t)P.frame_map[(size_t)cu * P.T_max + ci] * P.stride_t;
+      const int st = skey_tok(topk_key_g(S, src, V, P.blank, k, lane, nullptr));
+      if (lane < k) {
+        const size_t o = ((size_t)cu * P.T_max + ci) * k + lane;
+        P.topk_tok[o] = st;
+        P.topk_val[o] = __ldg(src + st);
+      }
+      __syncwarp();
+      ci++;
+      while (cu < P.B && ci >= P.kept[cu]) { cu++; ci = 0; }
+    }
+    return;
+  }
   // utterance of the first row: last u with rowoff[u] <= g0
   int lo = 0, hi = P.B - 1;
   while (lo < hi) {
