@@ -300,11 +300,27 @@ def test_fused_and_precomputed_topk_modes_agree(monkeypatch):
         cfg = synth.CONFIGS[cfg_id]
         lp, lens = synth.batch(cfg, indices=idx)
         cases.append((lp, lens, cfg.beam, cfg.nbest, cfg.threshold))
+    # V > 512: rows read from global memory (V % 4 == 0) or staged (odd V);
+    # a column of exact ties exercises the radix fallback
+    rng = np.random.default_rng(52)
+    for V in (1000, 1001):
+        x = rng.normal(size=(3, 60, V)) * 2.0
+        x[:, 7, :] = 0.0
+        x = x - x.max(2, keepdims=True)
+        lp = (x - np.log(np.exp(x).sum(2, keepdims=True))).astype(np.float32)
+        cases.append((lp, np.array([60, 41, 9], dtype=np.int32), 10, 3, 0.95))
     monkeypatch.setenv("CTCB_TOPK_MODE", "precomp")
     pre = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
+    monkeypatch.setenv("CTCB_TOPK_STAGED", "1")
+    staged = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
+    monkeypatch.delenv("CTCB_TOPK_STAGED")
     monkeypatch.setenv("CTCB_TOPK_MODE", "fused")
     fus = [run(lp, lens, beam, nb, thr, timesteps=True) for lp, lens, beam, nb, thr in cases]
-    assert pre == fus
+    assert pre == fus and staged == fus
+    for (lp, lens, beam, nb, thr), got in zip(cases[-2:], pre[-2:]):
+        for b in range(lp.shape[0]):
+            ref = oracle.decode(lp[b, : lens[b]], beam_size=beam, n_best=nb, blank_skip_threshold=thr)
+            assert [g for g in got[b]["tokens"]] == ref.tokens
 
 
 def test_host_buffer_path_matches_device_path():
