@@ -742,7 +742,6 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   uint32_t* myli = w.li + (size_t)lane * beam;
   int cnt = 0;
   uint64_t minkey = 0ull, dropmax = 0ull;  // dropmax: best key this lane evicted or rejected
-  uint64_t lmax = 0ull;                    // best key in this lane's list
   // lane list kept sorted descending: inserts near the cut shift few entries
   auto insert = [&](uint64_t key, uint32_t id) {
     int j;
@@ -758,7 +757,6 @@ __device__ int fused_step(FW& w, const float* row, int H) {
     while (j > 0 && mylk[j - 1] < key) { mylk[j] = mylk[j - 1]; myli[j] = myli[j - 1]; j--; }
     mylk[j] = key; myli[j] = id;
     if (cnt == beam) minkey = mylk[beam - 1];
-    lmax = key > lmax ? key : lmax;
   };
   for (int s = lane; s < nS; s += 32)
     if (w.sp_sc[s] > -INFINITY) insert(ord64(w.sp_sc[s]), kSpecialBit | (uint32_t)s);
@@ -767,11 +765,14 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   // candidates in distinct lanes reach it), or any full lane list's minimum.
   // Prefix d scans token c in lane (c + d) mod 32, so the same strong token of
   // different prefixes lands in different lanes.
+  // With m = ceil(beam / 32) and each lane's m-th best key, the j-th largest
+  // of those (j = ceil(beam / m)) has j * m >= beam candidates at or above it.
+  const int bm = (beam + 31) >> 5, bj = (beam + bm - 1) / bm;
   auto bound = [&]() -> double {
     const uint64_t m = cnt == beam ? minkey : 0ull;
     uint64_t g = warp_max64(m);
-    if (beam <= 32) {
-      uint64_t x = lmax;
+    {
+      uint64_t x = cnt >= bm ? mylk[bm - 1] : 0ull;
 #pragma unroll
       for (int k = 2; k <= 32; k <<= 1)
 #pragma unroll
@@ -781,8 +782,8 @@ __device__ int fused_step(FW& w, const float* row, int H) {
           const bool take_max = ((lane & j) == 0) == ((lane & k) == 0);
           x = take_max ? (x > y ? x : y) : (x < y ? x : y);
         }
-      const uint64_t kth = ((uint64_t)__shfl_sync(FULL, (uint32_t)(x >> 32), beam - 1) << 32) |
-                           __shfl_sync(FULL, (uint32_t)x, beam - 1);
+      const uint64_t kth = ((uint64_t)__shfl_sync(FULL, (uint32_t)(x >> 32), bj - 1) << 32) |
+                           __shfl_sync(FULL, (uint32_t)x, bj - 1);
       g = kth > g ? kth : g;
     }
     return g ? unord64(g) : -INFINITY;
@@ -1195,7 +1196,7 @@ __device__ void fused_finalize(FW& w, int H, int kept) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(128) ctcb_decode_fused_kernel(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(128, 4) ctcb_decode_fused_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   FW w;
