@@ -214,10 +214,10 @@ int ctcb_lm_destroy(ctcb_lm_t* lm);
  * entries): the LM word id of token c (its string, or "<unk>"), -1 when the
  * string is out of vocabulary and the model has no "<unk>" (fixed penalty
  * -20, context reset: lm.py:236-238), -2 for blank and the silence token
- * (identity: no LM score, context kept).  weight: lm_weight.  beam <= 64. */
+ * (identity: no LM score, context kept).  weight: lm_weight.  beam <= 128. */
 int ctcb_set_lm(ctcb_t* h, const ctcb_lm_t* lm, const int32_t* token_word, double weight);
 /* Silence token (-1: none) and its per-emission bonus sil_score
- * (decoder.py:485-486); a non-zero bonus selects the fused search (beam <= 64). */
+ * (decoder.py:485-486); a non-zero bonus selects the fused search (beam <= 128). */
 int ctcb_set_silence(ctcb_t* h, int silence_index, double sil_score);
 /* ctcb_decode plus out_lm: float64 [batch, nbest] LM total of each hypothesis
  * (Hypothesis.lm_score, finish score included; decoder.py:770-777), or NULL.

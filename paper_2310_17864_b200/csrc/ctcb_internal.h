@@ -73,7 +73,7 @@ struct Params {
 };
 
 // Fused search limits.
-constexpr int kFusedMaxBeam = 64;
+constexpr int kFusedMaxBeam = 128;
 constexpr int kUttOverflow = 4;  // fused search: too many near-tied candidates at the beam cut
 
 // Device copy of a flattened backoff n-gram model (ctcb_lm_t).

@@ -228,8 +228,8 @@ def test_fused_errors(tmp_path):
     rng = np.random.default_rng(3)
     toks = ["-", "a", "b", "c"]
     lm = random_arpa(tmp_path / "e.arpa", rng, toks[1:], 2, 0.5)
-    dec = CUCTCDecoder(toks, beam_size=100)
-    with pytest.raises(ValueError, match="beam_size <= 64"):
+    dec = CUCTCDecoder(toks, beam_size=200)
+    with pytest.raises(ValueError, match="beam_size <= 128"):
         dec.set_lm(lm, 1.0)
     dec = CUCTCDecoder(toks, beam_size=4)
     with pytest.raises(ValueError, match="silence_index must differ"):

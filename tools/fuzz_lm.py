@@ -1,6 +1,6 @@
 """Randomised parity sweep of the fused search (GPU): random token-level LMs
 (orders 1-3, <unk> / OOV tokens, random backoffs) and random options (beam
-1-64, V 3-600, lm_weight incl. 0 and negative, silence bonus, skip threshold,
+1-128, V 3-600, lm_weight incl. 0 and negative, silence bonus, skip threshold,
 beam threshold, merge mode, beam_size_token, peaky / flat / tied rows) decoded
 by the fused CUDA kernel and by the oracle; reports every mismatch beyond the
 north-star tolerances (tokens exact unless an adjacent final gap <= 1e-3,
@@ -53,7 +53,7 @@ def main():
     for it in range(n_batches):
         V = int(rng.choice([3, 5, 8, 16, 40, 100, 257, 600]))
         order = int(rng.choice([1, 2, 2, 3]))
-        beam = int(rng.integers(1, 20)) if rng.random() < 0.8 else int(rng.integers(20, 65))
+        beam = int(rng.integers(1, 20)) if rng.random() < 0.8 else int(rng.integers(20, 129))
         nb = int(rng.integers(1, beam + 1))
         thr = float(rng.choice([1.0, 0.95, 0.8]))
         bthr = float(rng.choice([50.0, 8.0, 2.0, np.inf]))
