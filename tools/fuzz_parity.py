@@ -14,6 +14,7 @@ from paper_2310_17864_b200 import CUCTCDecoder
 
 n_batches = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+only = int(sys.argv[3]) if len(sys.argv) > 3 else None  # replay one iteration (inputs saved to gpurun_out/)
 bad = checked = ties = 0
 for it in range(n_batches):
     V = int(rng.choice([3, 5, 8, 16, 32, 61, 100, 257, 500, 700]))
@@ -37,6 +38,12 @@ for it in range(n_batches):
             x = np.round(x * 2) / 2
         x = x - x.max(1, keepdims=True)
         lp[b] = (x - np.log(np.exp(x).sum(1, keepdims=True))).astype(np.float32)
+    if only is not None:
+        if it != only:
+            continue
+        os.makedirs("gpurun_out", exist_ok=True)
+        np.save(f"gpurun_out/fuzz_case_{it}.npy", lp)
+        print(dict(V=V, beam=beam, nb=nb, thr=thr, bthr=bthr, merge=merge, K=K, lens=lens.tolist()))
     for force in ("0", "1"):
         os.environ["CTCB_FORCE_GENERIC"] = force  # read when the handle is created
         dec = CUCTCDecoder(["-"] + [f"t{i}" for i in range(1, V)], beam_size=beam, nbest=nb,
