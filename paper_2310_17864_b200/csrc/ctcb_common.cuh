@@ -80,20 +80,102 @@ __device__ __forceinline__ double log1pexp_neg(double d) {
   return big ? res + kLn2Hi + kLn2Lo : res;
 }
 
+// log1p(exp(-d)) as libm computes it for numpy: exp(-d) rounded to double,
+// then log1p of that double rounded to double.  Each step is evaluated in
+// double-double (~1e-29 relative) and rounded once, so the result equals
+// libm's whenever libm rounds both steps correctly (its documented error is
+// below one ulp).  ~10x the instructions of log1pexp_neg, so it only runs
+// behind the guard in add_log1pexp_exact, and only the generic kernel (large
+// beams, where quantized inputs make exact score ties common) uses it; the fast
+// and fused kernels keep the polynomial.
+struct ddv { double hi, lo; };
+__device__ __forceinline__ ddv dd_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b), bb = __dsub_rn(s, a);
+  return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ ddv dd_quick(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ ddv dd_add(ddv a, ddv b) {
+  ddv s = dd_two_sum(a.hi, b.hi);
+  const ddv t = dd_two_sum(a.lo, b.lo);
+  s = dd_quick(s.hi, __dadd_rn(s.lo, t.hi));
+  return dd_quick(s.hi, __dadd_rn(s.lo, t.lo));
+}
+__device__ __forceinline__ ddv dd_mul(ddv a, ddv b) {
+  const double p = __dmul_rn(a.hi, b.hi);
+  const double e = fma(a.hi, b.hi, -p);
+  return dd_quick(p, fma(a.hi, b.lo, fma(a.lo, b.hi, e)));
+}
+// exp(y) for y in [-745, 0] in double-double: y = n ln2 + r (three-part ln2),
+// Taylor to degree 9 on r / 2^10, ten squarings, scale by 2^n
+__device__ __forceinline__ ddv dd_exp(ddv y) {
+  const double kH = 0.6931471805599453, kM = 2.3190468138462996e-17, kL = 5.707708438416212e-34;
+  const double n = rint(y.hi * 1.4426950408889634);
+  const double p = __dmul_rn(n, kH), pe = fma(n, kH, -p);
+  ddv r = dd_add(y, {-p, -pe});
+  const double q = __dmul_rn(n, kM), qe = fma(n, kM, -q);
+  r = dd_add(r, {-q, -qe});
+  r = dd_add(r, {-n * kL, 0.0});
+  r.hi = ldexp(r.hi, -10);
+  r.lo = ldexp(r.lo, -10);
+  ddv s = {1.0 / 362880.0, 0.0};
+  s = dd_add(dd_mul(s, r), {1.0 / 40320.0, 0.0});
+  s = dd_add(dd_mul(s, r), {1.0 / 5040.0, 0.0});
+  s = dd_add(dd_mul(s, r), {0.001388888888888889, -5.300543954373577e-20});   // 1/720
+  s = dd_add(dd_mul(s, r), {0.008333333333333333, 1.1564823173178714e-19});   // 1/120
+  s = dd_add(dd_mul(s, r), {0.041666666666666664, 2.3129646346357427e-18});   // 1/24
+  s = dd_add(dd_mul(s, r), {0.16666666666666666, 9.25185853854297e-18});      // 1/6
+  s = dd_add(dd_mul(s, r), {0.5, 0.0});
+  s = dd_add(dd_mul(s, r), {1.0, 0.0});
+  s = dd_add(dd_mul(s, r), {1.0, 0.0});
+#pragma unroll
+  for (int i = 0; i < 10; i++) s = dd_mul(s, s);
+  const int ni = (int)n;
+  return {ldexp(s.hi, ni), ldexp(s.lo, ni)};
+}
+__device__ __forceinline__ double log1pexp_cr(double d) {
+  if (!(d < 745.0)) return 0.0;            // exp(-d) underflows to 0
+  const double e = dd_exp({-d, 0.0}).hi;  // exp(-d), rounded
+  const ddv z = dd_two_sum(1.0, e);        // 1 + e, exact
+  const double y0 = log(z.hi);
+  const ddv w = dd_mul(z, dd_exp({-y0, 0.0}));
+  return dd_add({y0, 0.0}, dd_add(w, {-1.0, 0.0})).hi;  // one Newton step for log(1 + e)
+}
+
+// big + log1p(exp(-d)) with libm's rounding: the polynomial first; when the
+// sum is within the polynomial's error (+ half an ulp of the term) of a
+// rounding boundary of `big + term`, recompute the term with log1pexp_cr.
+__device__ __forceinline__ double add_log1pexp_exact(double big, double d) {
+  const double a = log1pexp_neg(d);
+  const double s = big + a;
+  const double bb = s - big;
+  const double err = (big - (s - bb)) + (a - bb);  // exact residual of the sum
+  const double half_ulp = s == 0.0 ? 0.0 : ldexp(1.0, ilogb(s) - 53);
+  if (fabs(err) + 4e-16 < half_ulp) return s;
+  return big + log1pexp_cr(d);
+}
+
 // numpy's npy_logaddexp: the fold np.logaddexp.reduceat performs when the
 // reference merges candidates (decoder.py:611) and flag variants (:791).
+// EXACT reproduces libm's rounding of the log1p(exp) term (see above).
+template <bool EXACT = false>
 __device__ __forceinline__ double np_logaddexp(double x, double y) {
   if (x == y) return x + CTCB_LN2;
   double tmp = x - y;
-  if (tmp > 0) return x + log1pexp_neg(tmp);
-  if (tmp <= 0) return y + log1pexp_neg(-tmp);
+  if (tmp > 0) return EXACT ? add_log1pexp_exact(x, tmp) : x + log1pexp_neg(tmp);
+  if (tmp <= 0) return EXACT ? add_log1pexp_exact(y, -tmp) : y + log1pexp_neg(-tmp);
   return tmp;
 }
 
 // Candidate merge of the reference (decoder.py:610-613, :789-791): logadd
 // (numpy's left fold) or max (merge_mode="max").
 __device__ __forceinline__ double merge2(double x, double y, bool mx) {
-  return mx ? (x > y ? x : y) : np_logaddexp(x, y);
+  return mx ? (x > y ? x : y) : np_logaddexp<false>(x, y);
+}
+__device__ __forceinline__ double merge2_exact(double x, double y, bool mx) {
+  return mx ? (x > y ? x : y) : np_logaddexp<true>(x, y);
 }
 
 // ---------------------------------------------------------------- prefixes

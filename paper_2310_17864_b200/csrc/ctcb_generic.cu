@@ -353,7 +353,7 @@ __device__ __forceinline__ double gen_score(const Warp& w, int d, int j) {
   double v = (double)w.sval[j];
   int a = w.e1[d], b = w.e2[d];
   double s = w.cs[a] + v;
-  if (b >= 0) s = merge2(s, w.cs[b] + v, w.P->merge_max != 0);
+  if (b >= 0) s = merge2_exact(s, w.cs[b] + v, w.P->merge_max != 0);
   return s;
 }
 
@@ -457,7 +457,7 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
     int a = w.e1[d], b = w.e2[d];
     if (has_blank) {
       double sc = w.cs[a] + eb;
-      if (b >= 0) sc = merge2(sc, w.cs[b] + eb, w.P->merge_max != 0);
+      if (b >= 0) sc = merge2_exact(sc, w.cs[b] + eb, w.P->merge_max != 0);
       int s = atomicAdd(&w.misc[0], 1);
       w.spsc[s] = sc; w.spbase[s] = a; w.spx[s] = -1; w.spflag[s] = 1; w.spsrc[s] = a; w.sptok[s] = -1;
     }
@@ -490,7 +490,7 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
         int h = srcs[q];
         if (h < 0 || (w.cf[h] == 0 && w.cl[h] == c)) continue;  // blocked repeat (decoder.py:495)
         double x = w.cs[h] + ec;
-        sc = merge2(sc, x, w.P->merge_max != 0);
+        sc = merge2_exact(sc, x, w.P->merge_max != 0);
         if (x > best) { best = x; src = h; tok = c; }
       }
     }
@@ -512,7 +512,7 @@ __device__ int beam_step(Warp& w, const float* row, int H) {
   //    scores are computed for key ties and, in parallel, for the winners.
   for (int d = lane; d < nD; d += 32) {
     const int a = w.e1[d], b = w.e2[d];
-    w.lA[d] = b >= 0 ? merge2(w.cs[a], w.cs[b], w.P->merge_max != 0) : w.cs[a];
+    w.lA[d] = b >= 0 ? merge2_exact(w.cs[a], w.cs[b], w.P->merge_max != 0) : w.cs[a];
     w.headj[d] = next_valid(w, d, -1);
   }
   __syncwarp();
@@ -663,7 +663,7 @@ __device__ void finalize(Warp& w, int H, int kept) {
     if (w.first[e] != e) continue;
     double sc = w.cs[e];  // entries are in rank order: the first is the payload (decoder.py:794-797)
     for (int q = e + 1; q < H; q++)
-      if (w.first[q] == e) sc = merge2(sc, w.cs[q], w.P->merge_max != 0);
+      if (w.first[q] == e) sc = merge2_exact(sc, w.cs[q], w.P->merge_max != 0);
     int s = atomicAdd(&w.misc[0], 1);
     w.spsc[s] = sc; w.spbase[s] = e; w.spx[s] = -1; w.spflag[s] = 0;
   }

@@ -451,3 +451,15 @@ def test_regression_short_append_lists(monkeypatch, force_generic):
             got = run(u[None, :T], [T], 8, 8, 0.8, timesteps=True, K=K)[0]
             ref = oracle.decode(u[:T], beam_size=8, n_best=8, blank_skip_threshold=0.8, beam_size_token=K)
             assert_same(got, ref.tokens, ref.scores, ref.timesteps, ctx=f"T {T} K {K}")
+
+
+def test_regression_threshold_tie_libm_rounding():
+    """Quantized logits put a candidate exactly at best - beam_threshold; the
+    generic kernel's logaddexp reproduces libm's rounding (guarded
+    double-double), so its keep / drop decision matches the reference."""
+    lp = np.load(os.path.join(os.path.dirname(__file__), "golden", "regress_threshold_688.npy"))
+    u = lp[1, :10]
+    got = run(u[None], [10], 62, 31, 0.8, 2.0, timesteps=True)[0]
+    ref = oracle.decode(u, beam_size=62, n_best=31, blank_skip_threshold=0.8, beam_threshold=2.0)
+    assert got["tokens"] == ref.tokens
+    assert got["scores"] == ref.scores

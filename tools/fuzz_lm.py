@@ -48,6 +48,7 @@ def random_model(path, rng, words, order, keep, unk):
 def main():
     n_batches = int(sys.argv[1]) if len(sys.argv) > 1 else 100
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+    only = int(sys.argv[3]) if len(sys.argv) > 3 else None  # replay one iteration
     tmp = tempfile.mkdtemp()
     bad = checked = ties = 0
     for it in range(n_batches):
@@ -81,6 +82,8 @@ def main():
                 x = np.round(x * 2) / 2
             x = x - x.max(1, keepdims=True)
             lp[b] = (x - np.log(np.exp(x).sum(1, keepdims=True))).astype(np.float32)
+        if only is not None and it != only:
+            continue
         dec = CUCTCDecoder(toks, beam_size=beam, nbest=nb, blank_skip_threshold=thr, beam_threshold=bthr)
         dec.set_merge_mode(merge)
         dec.set_beam_size_token(K)
