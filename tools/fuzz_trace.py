@@ -15,10 +15,12 @@ dec.set_beam_size_token(K)
 for T in range(1, u.shape[0] + 1):
     x = torch.from_numpy(np.ascontiguousarray(u[None, :T])).cuda()
     tok, _, ln, sc, cnt = dec.to_host(dec.decode(x, torch.tensor([T], dtype=torch.int32).cuda()))
-    got = [(tok[0, j, :ln[0, j]].tolist(), round(float(sc[0, j]), 9)) for j in range(cnt[0])]
+    digits = int(os.environ.get("TRACE_DIGITS", "9"))  # 0: compare scores bit for bit
+    rnd = (lambda v: float(v)) if digits == 0 else (lambda v: round(float(v), digits))
+    got = [(tok[0, j, :ln[0, j]].tolist(), rnd(sc[0, j])) for j in range(cnt[0])]
     ref = oracle.decode(u[:T], beam_size=beam, n_best=beam, blank_skip_threshold=thr, beam_size_token=K,
                         beam_threshold=bthr)
-    exp = [(t, round(s, 9)) for t, s in zip(ref.tokens, ref.scores)]
+    exp = [(t, rnd(s)) for t, s in zip(ref.tokens, ref.scores)]
     print(T, "OK" if got == exp else "DIFF", got if got != exp else "")
     if got != exp:
         print("   ref", exp)
