@@ -17,6 +17,7 @@ __global__ void ctcb_decode_fast_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_pre_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_small_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_pre_small_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_decode_pair_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_framemap_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_topk_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_rowoff_kernel(const __grid_constant__ Params P);
@@ -147,6 +148,17 @@ bool use_precomp(const ctcb_handle* h, int B) {
   if (m && strcmp(m, "fused") == 0) return false;
   if (m && strcmp(m, "precomp") == 0) return true;
   return B <= 2 * h->num_sms;
+}
+
+// Two utterances per warp (ctcb_pair.cu): the headline kernel for beam <= 16,
+// V <= 512, blank 0, full vocabulary, 16-B aligned rows, large batches.
+// CTCB_PAIR=0 disables it, CTCB_PAIR=1 forces it for any batch size.
+bool use_pair(const ctcb_handle* h, const ctcb::Params& P, int B) {
+  if (!use_fast(h) || h->tok_k != 0 || h->blank != 0 || h->V > ctcb::kSmallV || !P.bulk_ok) return false;
+  const char* m = getenv("CTCB_PAIR");
+  if (m && strcmp(m, "0") == 0) return false;
+  if (m && strcmp(m, "1") == 0) return true;
+  return false;  // opt-in while it is slower than the one-utterance-per-warp kernel
 }
 
 struct WsLayout {
@@ -482,15 +494,22 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   ctcb::ctcb_order_kernel<<<1, 1024, order_smem, s>>>(lens, B, P.order, P.counter);
   CTCB_CUDA(cudaGetLastError());
+  const bool pair = use_pair(h, P, B);
+  const bool pre = fast && !pair && use_precomp(h, B);
+  if (pair) {  // 4 warps = 8 utterances per block, two halves' shared memory per warp
+    P.smem_per_warp = (int)(2 * ctcb::make_pair_layout().total);
+    P.warps_per_block = 4;
+  }
   size_t smem = (size_t)P.smem_per_warp * P.warps_per_block;
-  const bool pre = fast && use_precomp(h, B);
-  const void* kfn = fused ? ctcb::fused_kernel_fn()
+  const void* kfn = pair ? (const void*)ctcb::ctcb_decode_pair_kernel
+                    : fused ? ctcb::fused_kernel_fn()
                     : fast ? fast_kernel_fn(P, pre) : (const void*)ctcb::ctcb_decode_generic_kernel;
   CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
   CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, 32 * P.warps_per_block, smem));
   if (blocks_per_sm < 1) blocks_per_sm = 1;
-  int need = (B + P.warps_per_block - 1) / P.warps_per_block;
+  const int per_block = pair ? 2 * P.warps_per_block : P.warps_per_block;
+  int need = (B + per_block - 1) / per_block;
   int grid = h->num_sms * blocks_per_sm;
   if (grid > need) grid = need;
   if (pre) {
@@ -516,7 +535,12 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   }
   const bool timed = h->timing && h->n_timed < 64;
   if (timed) CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed], s));
-  if (fused) {
+  if (pair) {
+    void* args[] = {(void*)&P};
+    CTCB_CUDA(cudaLaunchKernel((const void*)ctcb::ctcb_decode_pair_kernel, dim3(grid), dim3(32 * P.warps_per_block),
+                               args, smem, s));
+    h->last_kernel = "ctcb_decode_pair_kernel";
+  } else if (fused) {
     void* args[] = {(void*)&P};
     CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
     h->last_kernel = "ctcb_decode_fused_kernel";

@@ -172,6 +172,43 @@ __host__ __device__ constexpr inline FastLayout make_fast_layout(int V, int ring
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Two-utterances-per-warp kernel (ctcb_pair.cu): per-half shared memory.
+constexpr int kPairRing = 2;
+struct PairLayout {
+  size_t rows, mbar, sval, stok, wp, cidx, posmap, excl, rec, hs, hl, hsc, hp2, tie_sc, tie_i, tc_h, tc_r, tring, total;
+};
+__host__ __device__ constexpr inline PairLayout make_pair_layout() {
+  PairLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes, size_t align) {
+    o = (o + align - 1) / align * align;
+    size_t r = o;
+    o += bytes;
+    return r;
+  };
+  L.rows = take((size_t)kPairRing * kSmallRowBytes, 128);
+  L.mbar = take((size_t)kPairRing * 8, 8);
+  L.wp = take(32 * 8, 8);
+  L.hs = take(16 * 8, 8);
+  L.hsc = take(16 * 8, 8);
+  L.tie_sc = take(64 * 8, 8);      // also the 64-bit keys of the top-k exactness fix
+  L.tc_h = take(2 * kTieCache * 8, 8);
+  L.sval = take(32 * 4, 4);
+  L.stok = take(32 * 4, 4);
+  L.excl = take(16 * 4, 4);
+  L.rec = take(32 * 4, 4);
+  L.hl = take(16 * 4, 4);
+  L.hp2 = take(16 * 4, 4);
+  L.tie_i = take(32 * 4 * 4, 4);
+  L.tc_r = take((kTieCache + 1) * 4, 4);
+  L.cidx = take(64 * 2, 2);
+  L.tring = take((size_t)kChunk * 16 * 2, 2);
+  L.posmap = take((size_t)kSmallV, 1);
+  L.total = (o + 127) / 128 * 128;
+  return L;
+}
+
+
 // Byte offsets of the per-warp shared-memory arrays of the generic decode kernel.
 struct WarpLayout {
   size_t rows, mbar;
