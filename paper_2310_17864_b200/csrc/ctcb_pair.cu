@@ -45,15 +45,14 @@
 #else
 #define PCHK(c) do { } while (0)
 #endif
-#ifdef CTCB_PAIR_CHECK
-#define PDIV(tag)                                                                                  \
-  do {                                                                                             \
-    const unsigned am_ = __activemask();                                                           \
-    if (am_ != FULL && (__ffs(am_) - 1) == (int)(threadIdx.x & 31))                                \
-      printf("diverged at %s: block %d warp %d am %08x\n", tag, blockIdx.x, (int)(threadIdx.x >> 5), am_); \
+#ifdef CTCB_PAIR_DIVCHK
+#define PDIV(id)                                                                   \
+  do {                                                                             \
+    const unsigned am_ = __activemask();                                           \
+    if (am_ != FULL && (__ffs(am_) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&P.dbg[id], 1ull); \
   } while (0)
 #else
-#define PDIV(tag) do { } while (0)
+#define PDIV(id) do { } while (0)
 #endif
 
 namespace ctcb {
@@ -343,7 +342,6 @@ __device__ __forceinline__ void pair_topk(const PairSmem& S, const float* row, b
     else c1 |= (uint32_t)__popc(nib) << (8 * (j - 4));
   }
   const int hf = (threadIdx.x >> 4) & 1;
-  PDIV("topk threshold");
   const int cnt = (int)seg_sum((unsigned)__popc(pm), hf);
   const bool big = __any_sync(FULL, cnt > 32);  // warp-uniform sort width
   if (__any_sync(FULL, cnt > 64)) {
@@ -401,7 +399,6 @@ __device__ __forceinline__ void pair_topk(const PairSmem& S, const float* row, b
       }
     }
     __syncwarp();
-    PDIV("topk after compaction");
     // key = (order key with the low 6 bits cleared) | (63 - slot): value desc,
     // then index asc (slots are in index order); the lane holding rank p
     // writes stok[p]
@@ -745,9 +742,9 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
       if (__any_sync(FULL, !exhausted && !have_row)) continue;
       break;
     }
-    PDIV("after bookkeeping");
     if (__all_sync(FULL, exhausted)) break;
     const bool act = !exhausted;
+    PDIV(0);
     float* row = S.rows + (n_cons & 1) * kSmallV;
     if (act) {
       n_cons++;
@@ -756,9 +753,8 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
 
     // ---------------- frame step, both halves (warp-uniform control flow)
     const double eb = act ? (double)row[0] : 0.0;
-    PDIV("before topk");
     pair_topk(S, row, act, V, k, kScale, hl, seg, P.dbg);
-    PDIV("after topk");
+    PDIV(1);
 
     // merge structure: call A = utterance of half 0 (h on lanes 0-15, parent
     // hashes on 16-31), call B = half 1 (parents on 0-15, h on 16-31)
@@ -795,6 +791,7 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
     __syncwarp();
     const uint32_t childx = S.excl[hl];
 
+    PDIV(2);
     // ---------------- special groups
     const unsigned pr2 = parents & (parents - 1);
     const int pb = (ent && pr2) ? __ffs(pr2) - 1 : -1;
@@ -867,8 +864,7 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
     };
     const long long gG = gv ? pf2ll_floor((A - kbase) * kScale) : 0ll;
     const uint32_t gLow = (gv && A > -INFINITY) ? 1u : 0u;
-
-    PDIV("before merge");
+    PDIV(3);
     // ---------------- k-way merge (decoder.py:651-681)
     // Each lane pops from two queues: its <= 3 special groups (exact fp64,
     // locally sorted) and, as a prefix owner, its append list (head position
@@ -879,9 +875,95 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
       const long long tt = gG + S.wp[p];
       return tt < 1ll ? gLow : (tt > 0xffffffffll ? 0xffffffffu : (uint32_t)tt);
     };
+    // ---- one-shot selection: each lane's local top-4 of (specials, list),
+    // one 64-key register sort per half.  Keys carry (lane, item) in their low
+    // 7 bits; adjacent keys within one truncated unit, keys near the floor, or
+    // a lane whose next local candidate may still reach the beam fall back to
+    // the exact k-way merge below.
+    uint32_t lkk[5];
+    int lpk = 0;  // first four valid list positions, 5 bits each
+    {
+      uint32_t g2 = gv;
+#pragma unroll
+      for (int j = 0; j < 5; j++) {
+        const int p = g2 ? __ffs(g2) - 1 : 0;
+        lkk[j] = g2 ? lkey(p) : 0u;
+        if (j < 4) lpk |= p << (5 * j);
+        g2 &= g2 - 1u;
+      }
+    }
+    auto tagk = [&](uint32_t key, int item) -> uint32_t {
+      return key ? (((key < 128u ? 128u : key) & ~127u) | (uint32_t)(hl << 3) | (uint32_t)item) : 0u;
+    };
+    uint32_t xs[4];
+    {
+      const uint32_t a0 = tagk(sp0, 0), a1 = tagk(sp1, 1), a2 = tagk(sp2, 2);
+      xs[0] = max(a0, tagk(lkk[3], 6));
+      xs[1] = max(a1, tagk(lkk[2], 5));
+      xs[2] = max(a2, tagk(lkk[1], 4));
+      xs[3] = tagk(lkk[0], 3);  // (a3 = 0)
+      // bitonic sequence -> descending
+      uint32_t t0 = max(xs[0], xs[2]), t2 = min(xs[0], xs[2]), t1 = max(xs[1], xs[3]), t3 = min(xs[1], xs[3]);
+      xs[0] = max(t0, t1); xs[1] = min(t0, t1); xs[2] = max(t2, t3); xs[3] = min(t2, t3);
+    }
+    // largest local candidate left out: next special / next list key
+    uint32_t U;
+    {
+      int cA = 0;
+#pragma unroll
+      for (int r = 0; r < 4; r++) cA += (xs[r] != 0u && (xs[r] & 7u) <= 2u) ? 1 : 0;
+      int nz = 0;
+#pragma unroll
+      for (int r = 0; r < 4; r++) nz += xs[r] != 0u ? 1 : 0;
+      const int cB = nz - cA;
+      const uint32_t nA = cA == 0 ? sp0 : (cA == 1 ? sp1 : (cA == 2 ? sp2 : 0u));
+      const uint32_t nB = cB == 0 ? lkk[0] : (cB == 1 ? lkk[1] : (cB == 2 ? lkk[2] : (cB == 3 ? lkk[3] : lkk[4])));
+      U = max(nA, nB);
+    }
+    sort4_desc(xs, hl);
+    int Hn = 0;
+    bool fb;
+    {
+      // rank rho = 4 * hl + r; the beam is ranks < beam
+      const uint32_t nx0 = __shfl_down_sync(FULL, xs[0], 1, 16);
+      const uint32_t nxt = hl < 15 ? nx0 : 0u;
+      const int cl = (beam - 1) >> 2, cr = (beam - 1) & 3;
+      const uint32_t kc0 = hshu(xs[0], cl), kc1 = hshu(xs[1], cl), kc2 = hshu(xs[2], cl), kc3 = hshu(xs[3], cl);
+      const uint32_t kcut = cr == 0 ? kc0 : (cr == 1 ? kc1 : (cr == 2 ? kc2 : kc3));
+      bool bad = U != 0u && (kcut == 0u || (U >> 7) + 1u >= (kcut >> 7));
+      int cnt = 0;
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int rho = 4 * hl + r;
+        const uint32_t a = xs[r], b = r < 3 ? xs[r + 1] : nxt;
+        if (rho < beam) {
+          cnt += a != 0u ? 1 : 0;
+          bad |= a != 0u && (a >> 7) <= 1u;                              // near the floor
+          bad |= a != 0u && b != 0u && (a >> 7) - (b >> 7) <= 1u;         // not separated
+        }
+      }
+      const bool anybad = seg_any(bad, seg);
+      const int hcnt = (int)seg_sum((unsigned)cnt, hf);
+      fb = live && anybad;
+      Hn = live ? hcnt : 0;
+      if (live && !fb) {
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const int rho = 4 * hl + r;
+          const uint32_t a = xs[r];
+          if (rho < beam && a != 0u) {
+            const int id = (int)(a & 7u), wl = (int)((a >> 3) & 15u);
+            S.rec[rho] = wl | ((id <= 2 ? id : (0x40 | (id - 3))) << 8);
+          }
+        }
+      }
+    }
+    PDIV(4);
+    if (fb) Hn = 0;
+    live = fb;  // the exact k-way merge runs only for halves whose one-shot failed
+    if (__any_sync(FULL, fb) && hl == 0 && fb) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
     int lp0 = gv ? __ffs(gv) - 1 : 0;
     uint32_t lk0 = gv ? lkey(lp0) : 0u;
-    int Hn = 0;
     for (int r = 0; r < beam; r++) {
       if (!__any_sync(FULL, live)) break;
       const uint32_t hd = live ? max(sp0, lk0) : 0u;
@@ -963,13 +1045,12 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
     __syncwarp();
     if (act && !died && Hn == 0) { died = true; died_at = i; }
     const bool step = act && !died;
-
-    PDIV("after merge");
+    PDIV(5);
     // ---------------- commit (decoder.py:683-744): lane r builds new entry r
     const bool nent = step && hl < Hn;
     const int rec = S.rec[nent ? hl : 0];
     const int wl = nent ? (rec & 0xff) : hl, item = rec >> 8;
-    PCHK(!nent || (wl < 16 && ((item & 0x80) ? (item & 0x1f) < k : item < 3)));
+    PCHK(!nent || (wl < 16 && ((item & 0xc0) ? true : item < 3)));
     const int wk = hsh(kpack, wl);
     const double w_q0 = hshd(q0, wl), w_q1 = hshd(q1, wl), w_q2 = hshd(q2, wl);
     const int w_src = hsh(rep_src | (single_src << 8), wl);
@@ -978,10 +1059,11 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
     const int blast = hsh(last, wl), blen = hsh(len, wl);
     const double b_s1 = hshd(s, wl), b_s2 = hshd(s_p2, wl);
     const int b_p2 = hsh(p2, wl);
+    const int w_lpk = hsh(lpk, wl);
     double nsc;
     int x, src, tok, nfl;
-    if (item & 0x80) {  // append group (R+c,0): exact fold of R's entries in rank order
-      const int pos = item & 0x1f;
+    if (item & 0xc0) {  // append group (R+c,0): exact fold of R's entries in rank order
+      const int pos = (item & 0x80) ? (item & 0x1f) : ((w_lpk >> (5 * (item & 3))) & 0x1f);
       const int c = S.stok[pos];
       const double v = (double)S.sval[pos];
       nsc = b_s1 + v;
@@ -1011,6 +1093,7 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
       tr16[((size_t)u * P.T_max + i) * beam + hl] = tr;
       S.tring[(i % kChunk) * 16 + hl] = tr;
     }
+    PDIV(6);
     if (step) {
       H = Hn;
       if (hl == 0) P.frame_map[(size_t)u * P.T_max + i] = t;
@@ -1027,7 +1110,7 @@ __global__ void __launch_bounds__(128, CTCB_PAIR_MIN_BLOCKS) ctcb_decode_pair_ke
       }
     }
     __syncwarp();
-    PDIV("end of step");
+    PDIV(7);
     if (act) {
       if (step) i++;
       if (!died && t + 2 < len_u) issue(t + 2);
