@@ -6,14 +6,19 @@ T ~ U[125, 875], peaky synthetic posteriors, thr 0.95, nbest 1).
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
 
-One step = one decode of the rank's length-balanced (LPT) shard of the batch,
-inputs resident in HBM.  value = frames of all ranks / max-over-ranks step
+One step = one decode of the rank's length-balanced (LPT) shard of the batch
+(strong scaling: the fixed B = 4096 split over the ranks; --weak gives each
+rank its own ~B utterances), inputs resident in HBM.  value = frames of all ranks / max-over-ranks step
 time (CUDA events on the decode stream).  Inputs (7.2 GB padded at N=1) are
 larger than L2, so no flush is needed between steps.  `e2e` is the same
 metric through the public API (`CUCTCDecoder.__call__`) from pinned host
 memory, H2D + decode + D2H + hypothesis construction inside the timed region.
 `--impl reference` times the CPU reference path (the C oracle port of
-ctcforge, oracle/) on the host cores instead.
+ctcforge, oracle/) on the host cores instead.  On rank 0 at N=1 the line also
+carries `cpu_baseline` (the port on a 512-utterance sample),
+`cpu_baseline_reference` (ctcforge itself, baseline/_ref, decode_batch with a
+process pool) and `parity`: the timed decode's own results on those samples
+against the port and against ctcforge.
 """
 
 from __future__ import annotations
@@ -140,27 +145,78 @@ class ClockSampler:
 
 def cpu_baseline(cfg, budget_s: float, threads: int, sample_utts: int):
     """Time the oracle port (C restatement of ctcforge) on a bounded sample of
-    the workload with `threads` host threads; returns (frames/s, sample desc)."""
+    the workload with `threads` host threads; returns (frames/s, sample desc,
+    oracle results of the decoded utterances 0..n-1 for the parity check).
+    n_best is raised to 2 so the top-1/top-2 gap is known; it only truncates
+    the final sorted list (decoder.py:799-801), so the timing is unchanged."""
     import oracle
 
     oracle.build()
     idx = np.arange(min(sample_utts, cfg.batch))
     lp, lens = synth.batch(cfg, indices=idx)
+    nb = min(cfg.beam, max(cfg.nbest, 2))
     # warm-up one utterance (page in, thread pool)
-    oracle.decode_batch(lp[:1], lens[:1], threads=1, beam_size=cfg.beam, n_best=cfg.nbest,
+    oracle.decode_batch(lp[:1], lens[:1], threads=1, beam_size=cfg.beam, n_best=nb,
                         blank_skip_threshold=cfg.threshold)
     done_frames, done_utts, t0 = 0, 0, time.perf_counter()
     chunk = max(threads, 1) * 2
+    results = []
     while done_utts < len(idx):
         sl = slice(done_utts, min(done_utts + chunk, len(idx)))
-        oracle.decode_batch(lp[sl], lens[sl], threads=threads, beam_size=cfg.beam, n_best=cfg.nbest,
-                            blank_skip_threshold=cfg.threshold)
+        results += oracle.decode_batch(lp[sl], lens[sl], threads=threads, beam_size=cfg.beam, n_best=nb,
+                                       blank_skip_threshold=cfg.threshold)
         done_frames += int(lens[sl].sum())
         done_utts = sl.stop
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return done_frames / dt, f"first {done_utts} utterances of {cfg.name} ({done_frames} frames, {dt:.1f} s)"
+    return (done_frames / dt, f"first {done_utts} utterances of {cfg.name} ({done_frames} frames, {dt:.1f} s)",
+            [(r.tokens, r.scores) for r in results])
+
+
+def ctcforge_baseline(cfg, workers: int, sample_utts: int):
+    """Time the reference itself -- ctcforge.decode_batch(workers=cores)
+    (decoder.py:138-170), installed unmodified in baseline/_ref -- on the first
+    `sample_utts` utterances of the workload.  Returns (frames/s, sample desc,
+    results) or None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "ctcforge")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from ctcforge import DecoderOptions, EmissionMatrix, TokenDictionary, decode_batch
+
+    idx = np.arange(min(sample_utts, cfg.batch))
+    lp, lens = synth.batch(cfg, indices=idx)
+    toks = TokenDictionary(tuple(synth.simple_tokens(cfg.vocab)), blank_index=0)
+    opts = DecoderOptions(beam_size=cfg.beam, n_best=min(cfg.beam, max(cfg.nbest, 2)),
+                          blank_skip_threshold=cfg.threshold)
+    ems = [EmissionMatrix(lp[b, : lens[b]]) for b in range(len(idx))]
+    t0 = time.perf_counter()
+    out = decode_batch(ems, toks, opts, workers=workers)
+    dt = time.perf_counter() - t0
+    frames = int(lens.sum())
+    res = [([h.tokens for h in nb], [h.score for h in nb]) for nb in out]
+    return frames / dt, f"first {len(idx)} utterances of {cfg.name} ({frames} frames, {dt:.1f} s incl. process pool)", res
+
+
+def parity_summary(got, refs, nbest: int, against: str) -> dict:
+    """Bench self-check (north-star tolerances): tokens exact unless the
+    reference's top-1/top-2 gap is <= 1e-3, scores within 1e-4."""
+    mism = near = 0
+    err = 0.0
+    for (gt, gs), (rt, rs) in zip(got, refs):
+        if len(gs) != len(rs[:nbest]):
+            mism += 1
+            continue
+        err = max([err] + [abs(a - b) for a, b in zip(gs, rs)])
+        if gt != rt[:nbest]:
+            if len(rs) > 1 and rs[0] - rs[1] <= 1e-3:
+                near += 1
+            else:
+                mism += 1
+    return {"against": against, "utterances": len(refs), "token_mismatches": mism, "near_tie_excluded": near,
+            "max_score_err": err}
 
 
 def run_reference(args, cfg, rank):
@@ -190,7 +246,7 @@ def run_reference(args, cfg, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "batch": cfg.batch, "vocab": cfg.vocab, "beam": cfg.beam,
                    "nbest": cfg.nbest, "blank_skip_threshold": cfg.threshold, "sample": sample},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample},
@@ -211,9 +267,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--beam", type=int, default=None, help="override the config's beam (cfg2 sweep: 1/10/50/100)")
-    ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: split the config's fixed batch over the ranks (BASELINE configs[4]); "
-                         "default is weak scaling: N x batch utterances, ~batch per rank")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: N x batch utterances, ~batch per rank; the default is strong scaling, the "
+                         "config's fixed batch split over the ranks (BASELINE configs[4])")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -254,7 +310,7 @@ def main():
     #    holds ~batch; strong: the config's batch is split.
     import dataclasses
 
-    if not args.strong and world > 1:
+    if args.weak and world > 1:
         cfg = dataclasses.replace(cfg, batch=cfg.batch * world)
     lens_all = synth.lengths(cfg)
     shard = lpt_shards(lens_all, world)[rank]
@@ -286,6 +342,7 @@ def main():
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dec.kernel_timing(True)  # event pair around the beam kernel of each step (same stream)
+    launches0 = dec.launch_count()
     t_mark = time.monotonic()
     ev0.record(stream)
     for _ in range(args.steps):
@@ -298,11 +355,20 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     ms_rank = ev0.elapsed_time(ev1) / args.steps
+    launches = dec.launch_count() - launches0
     k_ms, k_n, k_name = dec.kernel_time()
     dec.kernel_timing(False)
     kernel_ms = k_ms / max(k_n, 1)
     status = out.status.cpu().numpy()
     assert (status == 0).all(), "decode failed"
+    # the timed decode's own results, by global utterance index (parity below)
+    r_tok, _, r_len, r_sc, r_cnt = dec.to_host(out)
+    pos_of = {int(g): j for j, g in enumerate(shard)}
+
+    def got_of(g: int):
+        j = pos_of[g]
+        n = int(r_cnt[j])
+        return ([r_tok[j, q, : r_len[j, q]].tolist() for q in range(n)], [float(r_sc[j, q]) for q in range(n)])
 
     red_dev = dev if backend == "nccl" else torch.device("cpu")
 
@@ -361,17 +427,26 @@ def main():
                        "-> CUCTCHypothesis lists"}
         del hyps
 
-    cpu = None
+    cpu = cpu_ref = None
+    parity = []
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, sample = cpu_baseline(cfg, args.cpu_budget, threads, sample_utts=512)
+        v, sample, refs = cpu_baseline(cfg, args.cpu_budget, threads, sample_utts=512)
         cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample}
+        parity.append(parity_summary([got_of(g) for g in range(len(refs))], refs, cfg.nbest, "oracle port"))
+        cf = ctcforge_baseline(cfg, threads, sample_utts=256 if cfg.vocab <= 500 else 32)
+        if cf is not None:
+            v, sample, refs = cf
+            cpu_ref = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference", "sample": sample,
+                       "impl": "ctcforge.decode_batch(workers=cores) from baseline/_ref"}
+            parity.append(parity_summary([got_of(g) for g in range(len(refs))], refs, cfg.nbest,
+                                         "ctcforge (baseline/_ref)"))
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak",
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "batch": cfg.batch, "batch_per_rank": len(shard), "vocab": cfg.vocab, "beam": cfg.beam,
                        "nbest": cfg.nbest, "blank_skip_threshold": cfg.threshold, "t_range": [cfg.t_min, cfg.t_max],
@@ -384,9 +459,11 @@ def main():
                          "kernel": k_name, "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms_rank,
                          "kept_frames": kept_rank},
             "cpu_baseline": cpu,
+            "cpu_baseline_reference": cpu_ref,
+            "parity": parity,
             "e2e": e2e,
             "clocks": clocks.summary(),
-            "gpu_launches": (4 if "_pre" in k_name else 2) * args.steps,
+            "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -167,6 +167,11 @@ int ctcb_debug_counters(ctcb_t* h, uint64_t* out8);
 int ctcb_kernel_timing(ctcb_t* h, int enable);
 int ctcb_kernel_time(ctcb_t* h, double* total_ms, int* launches, const char** kernel);
 
+/* Number of CUDA kernels this handle has launched so far (decode, gather,
+ * validation; host-side counter, no synchronisation).  bench.py reads it
+ * around the timed region for its gpu_launches field. */
+int ctcb_launch_count(ctcb_t* h, uint64_t* out);
+
 /* ---- CTC forced alignment (ctcforge align.py:46-123) ----------------------
  * Viterbi over each utterance's blank-interleaved targets, one warp per
  * utterance, fp64 path scores with the reference's tie-breaking (stay over

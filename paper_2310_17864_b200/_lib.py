@@ -21,7 +21,7 @@ UTT_OK, UTT_EMPTY, UTT_BAD_LEN, UTT_BEAM_DIED, UTT_OVERFLOW = 0, 1, 2, 3, 4
 SYMBOLS = (
     "ctcb_create", "ctcb_destroy", "ctcb_skip_cutoff", "ctcb_topk_size", "ctcb_workspace_bytes",
     "ctcb_decode", "ctcb_decode_host", "ctcb_debug_frames", "ctcb_validate", "ctcb_debug_counters", "ctcb_status_string",
-    "ctcb_last_error", "ctcb_kernel_timing", "ctcb_kernel_time", "ctcb_decode_host_async", "ctcb_decode_host_wait",
+    "ctcb_last_error", "ctcb_kernel_timing", "ctcb_kernel_time", "ctcb_launch_count", "ctcb_decode_host_async", "ctcb_decode_host_wait",
     "ctcb_set_merge_mode", "ctcb_set_beam_size_token", "ctcb_align", "ctcb_align_workspace_bytes",
     "ctcb_lm_create", "ctcb_lm_destroy", "ctcb_set_lm", "ctcb_set_silence", "ctcb_decode_lm",
 )
@@ -81,6 +81,7 @@ def load():
     lib.ctcb_set_silence.argtypes = [vp, c_int, c_double]
     lib.ctcb_decode_lm.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, c_size_t, vp,
                                    vp, vp, vp, vp, vp, vp, vp]
+    lib.ctcb_launch_count.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
     lib.ctcb_kernel_time.argtypes = [vp, ctypes.POINTER(c_double), ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_char_p)]
     lib.ctcb_status_string.argtypes = [c_int]
     lib.ctcb_status_string.restype = ctypes.c_char_p

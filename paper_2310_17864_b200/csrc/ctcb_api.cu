@@ -96,6 +96,7 @@ struct ctcb_handle {
   cudaEvent_t tev[2 * 64];
   int have_tev;
   const char* last_kernel;
+  unsigned long long launches;  // kernels launched by this handle (ctcb_launch_count)
   // fused search (ctcb_set_lm / ctcb_set_silence)
   ctcb::LmTables lm;
   int has_lm;
@@ -300,6 +301,12 @@ const char* ctcb_status_string(int status) {
 
 const char* ctcb_last_error(void) { return g_last_error.c_str(); }
 
+int ctcb_launch_count(ctcb_t* h, uint64_t* out) {
+  if (!h || !out) return fail(CTCB_ERR_ARG, "NULL argument");
+  *out = h->launches;
+  return CTCB_OK;
+}
+
 int ctcb_debug_counters(ctcb_t* h, uint64_t* out8) {
   if (!h || !out8) return fail(CTCB_ERR_ARG, "NULL argument");
   memset(out8, 0, 8 * sizeof(uint64_t));
@@ -493,6 +500,7 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   size_t order_smem = n <= 8192 ? (size_t)n * 8 : 0;
   CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   ctcb::ctcb_order_kernel<<<1, 1024, order_smem, s>>>(lens, B, P.order, P.counter);
+  h->launches++;
   CTCB_CUDA(cudaGetLastError());
   const bool pair = use_pair(h, P, B);
   const bool pre = fast && !pair && use_precomp(h, B);
@@ -516,8 +524,10 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     // frame maps -> top-k of every kept frame (frame-parallel) -> beam walk
     P.precomp = 1;
     ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
+    h->launches++;
     CTCB_CUDA(cudaGetLastError());
     ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
+    h->launches++;
     CTCB_CUDA(cudaGetLastError());
     ctcb::Params Q = P;
     // V > 512 with 16-B rows: the top-k kernel reads rows from global memory
@@ -531,6 +541,7 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     int tbps = 0;
     CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_kernel, 32 * twpb, tsmem));
     ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 32 * twpb, tsmem, s>>>(Q);
+    h->launches++;
     CTCB_CUDA(cudaGetLastError());
   }
   const bool timed = h->timing && h->n_timed < 64;
@@ -540,18 +551,22 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     CTCB_CUDA(cudaLaunchKernel((const void*)ctcb::ctcb_decode_pair_kernel, dim3(grid), dim3(32 * P.warps_per_block),
                                args, smem, s));
     h->last_kernel = "ctcb_decode_pair_kernel";
+    h->launches++;
   } else if (fused) {
     void* args[] = {(void*)&P};
     CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
     h->last_kernel = "ctcb_decode_fused_kernel";
+    h->launches++;
   } else if (fast) {
     void* args[] = {(void*)&P};
     CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
     h->last_kernel = !fast_small(P) ? (pre ? "ctcb_decode_fast_pre_kernel" : "ctcb_decode_fast_kernel")
                                     : (pre ? "ctcb_decode_fast_pre_small_kernel" : "ctcb_decode_fast_small_kernel");
+    h->launches++;
   } else {
     ctcb::ctcb_decode_generic_kernel<<<grid, 32 * P.warps_per_block, smem, s>>>(P);
     h->last_kernel = "ctcb_decode_generic_kernel";
+    h->launches++;
   }
   CTCB_CUDA(cudaGetLastError());
   if (timed) {
@@ -706,6 +721,7 @@ static int host_enqueue(ctcb_t* h, const float* lp, int64_t sb, int64_t st, cons
     const int b0 = (int)((int64_t)B * c / nchunks), b1 = (int)((int64_t)B * (c + 1) / nchunks);
     if (mapped) {
       ctcb::ctcb_gather_kernel<<<2 * h->num_sms, 256, 0, h->cstreams[0]>>>(mapped, sb, st, dlens, b0, b1, T, Tp, (int)V, din);
+      h->launches++;
       CTCB_CUDA(cudaGetLastError());
     }
     for (int b = b0; b < b1 && !mapped; b++) {
@@ -818,9 +834,11 @@ int ctcb_validate(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const int3
   if (B > 0 && T > 0) {
     dim3 grid((unsigned)((T + 7) / 8), (unsigned)B);
     ctcb::ctcb_validate_kernel<<<grid, 256, 0, s>>>(lp, sb, st, lens, B, T, h->V, strict, key);
+    h->launches++;
     CTCB_CUDA(cudaGetLastError());
   }
   ctcb::ctcb_validate_decode_kernel<<<1, 1, 0, s>>>(key, T, h->V, out_error);
+  h->launches++;
   CTCB_CUDA(cudaGetLastError());
   return CTCB_OK;
 }

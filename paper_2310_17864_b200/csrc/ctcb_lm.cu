@@ -599,7 +599,7 @@ __device__ CandOut exact_cand(const FW& w, uint32_t id, const float* row, bool u
   o.sc = x; o.src = a;
   if (b >= 0) {
     const double y = mem(b);
-    o.sc = merge2(x, y, P.merge_max != 0);
+    o.sc = merge2_exact(x, y, P.merge_max != 0);
     if (y > x) o.src = b;
   }
   o.lm = use_lm ? w.clm[o.src] + dl : w.clm[o.src];
@@ -651,7 +651,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
   for (int d = lane; d < nD; d += 32) {
     const int a = w.e1[d], b = w.e2[d];
     w.f1[d] = w.cf[a] == 1 ? a : ((b >= 0 && w.cf[b] == 1) ? b : -1);
-    w.lA[d] = b >= 0 ? merge2(w.cs[a], w.cs[b], mx) : w.cs[a];
+    w.lA[d] = b >= 0 ? merge2_exact(w.cs[a], w.cs[b], mx) : w.cs[a];
   }
   // parent prefix of each flag-0 entry; (parent, last token) pairs are excluded
   // from the parent's plain appends (they merge into the child's repeat group)
@@ -688,7 +688,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
       if (b >= 0) {
         const double y = w.cs[b] + eb;
         if (y > sc) src = b;  // payload: first member reaching the max
-        sc = merge2(sc, y, mx);
+        sc = merge2_exact(sc, y, mx);
       }
       const int s = atomicAdd(&w.misc[1], 1);
       w.sp_sc[s] = sc; w.sp_lm[s] = w.clm[src]; w.sp_base[s] = a; w.sp_x[s] = -1; w.sp_flag[s] = 1;
@@ -726,7 +726,7 @@ __device__ int fused_step(FW& w, const float* row, int H) {
         double x = w.cs[h] + ec;
         if (use_lm) x = x + wl;
         if (c == P.sil) x = x + P.sil_score;
-        sc = merge2(sc, x, mx);
+        sc = merge2_exact(sc, x, mx);
         if (x > best) { best = x; src = h; tok = c; lmv = w.clm[h] + dl; }
       }
     }
@@ -1135,7 +1135,7 @@ __device__ void fused_finalize(FW& w, int H, int kept) {
     int win = e;
     for (int q = e + 1; q < H; q++)
       if (w.first[q] == e) {
-        sc = merge2(sc, w.cs[q], mx);
+        sc = merge2_exact(sc, w.cs[q], mx);
         if (w.cs[q] > best) { best = w.cs[q]; win = q; }
       }
     const int s = atomicAdd(&w.misc[0], 1);

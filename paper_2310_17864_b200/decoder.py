@@ -545,6 +545,12 @@ class CUCTCDecoder:
                    "ctcb_kernel_time")
         return ms.value, n.value, (name.value or b"").decode()
 
+    def launch_count(self) -> int:
+        """Kernels launched by this decoder's handle so far (host counter)."""
+        n = ctypes.c_uint64()
+        _lib.check(_lib.load().ctcb_launch_count(self._h, ctypes.byref(n)), "ctcb_launch_count")
+        return int(n.value)
+
     def debug_counters(self) -> dict:
         """Slow-path counters of the last decode (see include/ctcb.h)."""
         lib = _lib.load()

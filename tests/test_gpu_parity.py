@@ -7,6 +7,7 @@ typically agrees to ~1e-12); blank-skip frame maps bit-exact.
 """
 
 import dataclasses
+import math
 import json
 import os
 import hashlib
@@ -463,3 +464,142 @@ def test_regression_threshold_tie_libm_rounding():
     ref = oracle.decode(u, beam_size=62, n_best=31, blank_skip_threshold=0.8, beam_threshold=2.0)
     assert got["tokens"] == ref.tokens
     assert got["scores"] == ref.scores
+
+
+# ---------------------------------------------------------------- headline path
+# The bench decodes B = 4096 > 2 x SMs utterances, which selects the fused
+# one-warp-per-utterance kernel (top-k inside the beam walk); the small-batch
+# tests above run the precomputed-top-k kernels.  These decode full batches
+# through the exact kernel and mode the headline number comes from and compare
+# every utterance with the oracle (decoder.py:102-170 restated).
+
+def _full_vs_oracle(lp, lens, beam, nbest, thr, expect_kernel=None):
+    dec = CUCTCDecoder(vocab(lp.shape[2]), beam_size=beam, nbest=nbest, blank_skip_threshold=thr)
+    dec.kernel_timing(True)
+    out = dec.decode(torch.from_numpy(np.ascontiguousarray(lp)).cuda(), torch.from_numpy(lens).cuda())
+    tokens, _, lengths, scores, counts = dec.to_host(out)
+    _, _, kname = dec.kernel_time()
+    if expect_kernel is not None:
+        assert kname == expect_kernel, kname
+    ref = oracle.decode_batch(lp, lens, beam_size=beam, n_best=min(beam, max(nbest, 2)), blank_skip_threshold=thr)
+    near = 0
+    for b, r in enumerate(ref):
+        n = int(counts[b])
+        exp_t, exp_s = r.tokens[:nbest], r.scores[:nbest]
+        assert n == len(exp_s), f"utt {b}: {n} hypotheses vs {len(exp_s)}"
+        for j in range(n):
+            assert abs(float(scores[b, j]) - exp_s[j]) <= SCORE_TOL, f"utt {b} rank {j}"
+        got_t = [tokens[b, j, : lengths[b, j]].tolist() for j in range(n)]
+        if got_t != exp_t:
+            gap = r.scores[0] - r.scores[1] if len(r.scores) > 1 else None
+            assert gap is not None and gap <= NEAR_TIE, f"utt {b}: tokens differ (top-1/top-2 gap {gap})"
+            near += 1
+    return near
+
+
+def test_cfg4_headline_kernel_512():
+    """512 cfg4 utterances (every 8th of the 4096, all lengths) in one call:
+    B > 2 x SMs selects ctcb_decode_fast_small_kernel, the benchmarked kernel."""
+    cfg = synth.CONFIGS[4]
+    lp, lens = synth.batch(cfg, indices=range(0, 4096, 8))
+    near = _full_vs_oracle(lp, lens, cfg.beam, cfg.nbest, cfg.threshold, "ctcb_decode_fast_small_kernel")
+    assert near <= 5
+
+
+@pytest.mark.parametrize("beam", [1, 10])
+def test_cfg2_full_batch(beam):
+    cfg = synth.CONFIGS[2]
+    lp, lens = synth.batch(cfg)
+    _full_vs_oracle(lp, lens, beam, min(beam, 10), cfg.threshold)
+
+
+def test_cfg3_full_batch():
+    cfg = synth.CONFIGS[3]
+    lp, lens = synth.batch(cfg)
+    _full_vs_oracle(lp, lens, cfg.beam, cfg.nbest, cfg.threshold)
+
+
+# ---------------------------------------------------------------- known ulp-level cases
+# Both cases need exactly tied scores in quantized inputs.  The kernels'
+# logaddexp rounds log1p(exp(-d)) with a polynomial (ctcb_common.cuh), glibc
+# (numpy, the reference) with its own rounding, so an exact fp64 tie can land
+# one ulp apart and reorder hypotheses INSIDE the tie.  Within the north-star
+# tolerances (tokens exact only where adjacent gaps exceed 1e-3, scores 1e-4)
+# both decodes agree; the bitwise ranking checks are expected failures.
+
+def _rank_ok(got, ref, nb):
+    """north-star comparison: scores 1e-4, tokens exact where both adjacent
+    final gaps of the reference exceed 1e-3"""
+    if len(got["scores"]) != len(ref.scores[:nb]):
+        return False
+    for a, e in zip(got["scores"], ref.scores[:nb]):
+        if abs(a - e) > SCORE_TOL:
+            return False
+    allsc = ref.scores
+    for j in range(len(got["tokens"])):
+        lo = allsc[j - 1] - allsc[j] if j > 0 else 1.0
+        hi = allsc[j] - allsc[j + 1] if j + 1 < len(allsc) else 1.0
+        if lo > NEAR_TIE and hi > NEAR_TIE and got["tokens"][j] != ref.tokens[j]:
+            return False
+    return True
+
+
+def _beam39_case():
+    u = np.load(os.path.join(os.path.dirname(__file__), "golden", "regress_ties_beam39.npy"))
+    got = run(u[None], [u.shape[0]], 39, 39, 1.0, 5.0)[0]
+    ref = oracle.decode(u, beam_size=39, n_best=39, blank_skip_threshold=1.0, beam_threshold=5.0)
+    return got, ref
+
+
+def test_regression_ties_beam39_tolerant():
+    got, ref = _beam39_case()
+    assert _rank_ok(got, ref, 39)
+
+
+@pytest.mark.xfail(reason="3-way exact fp64 tie at ranks 27-29: device logaddexp lands one ulp from glibc's",
+                   strict=False)
+def test_regression_ties_beam39_bitwise():
+    got, ref = _beam39_case()
+    assert got["tokens"] == ref.tokens and got["scores"] == ref.scores
+
+
+def _lm602_case():
+    import json
+    from paper_2310_17864_b200 import lm as glm
+    base = os.path.join(os.path.dirname(__file__), "golden", "regress_lm_s62_602")
+    meta = json.load(open(base + ".json"))
+    lp = np.load(base + ".npy")
+    lens = np.array(meta["lens"], np.int32)
+    toks = ["-"] + [f"t{i}" for i in range(1, meta["V"])]
+    lm = glm.parse_arpa(base + ".arpa")
+    bthr = math.inf if meta["bthr"] == "inf" else meta["bthr"]
+    dec = CUCTCDecoder(toks, beam_size=meta["beam"], nbest=meta["nb"], blank_skip_threshold=meta["thr"],
+                       beam_threshold=bthr)
+    dec.set_lm(lm, meta["w"])
+    out = dec.decode(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+    tok, _, ln, sc, cnt = dec.to_host(out)
+    tabs = oracle.lm_tables(glm.flatten(lm), glm.token_words(lm, toks, 0, None))
+    res = []
+    for b in range(len(lens)):
+        ref = oracle.decode(lp[b, : lens[b]], beam_size=meta["beam"], n_best=meta["nb"],
+                            blank_skip_threshold=meta["thr"], beam_threshold=bthr, lm=tabs, lm_weight=meta["w"])
+        got = {"tokens": [tok[b, j, : ln[b, j]].tolist() for j in range(cnt[b])],
+               "scores": [float(sc[b, j]) for j in range(cnt[b])]}
+        res.append((got, ref))
+    return res, meta["nb"]
+
+
+def test_regression_lm_fuzz_s62_602_tolerant():
+    """tools/fuzz_lm.py seed 62 iteration 602 (V=3, beam 25, quantized rows,
+    bigram-free unigram model with weight 0.3), replayed with FUZZ_DUMP."""
+    res, nb = _lm602_case()
+    bad = [b for b, (g, r) in enumerate(res) if not _rank_ok(g, r, nb)]
+    assert not bad, bad
+
+
+@pytest.mark.xfail(reason="exact score ties in quantized rows: one-ulp logaddexp differences reorder tied ranks",
+                   strict=False)
+def test_regression_lm_fuzz_s62_602_bitwise():
+    res, nb = _lm602_case()
+    for g, r in res:
+        assert g["tokens"] == r.tokens[:nb] and g["scores"] == r.scores[:nb]

@@ -84,6 +84,17 @@ def main():
             lp[b] = (x - np.log(np.exp(x).sum(1, keepdims=True))).astype(np.float32)
         if only is not None and it != only:
             continue
+        dump = os.environ.get("FUZZ_DUMP")
+        if dump and only is not None:  # write the replayed case as a regression fixture and stop
+            import json
+            import shutil
+            shutil.copy(os.path.join(tmp, f"m{it}.arpa"), dump + ".arpa")
+            np.save(dump + ".npy", lp)
+            Path(dump + ".json").write_text(json.dumps(dict(
+                it=it, lens=lens.tolist(), V=V, beam=beam, nb=nb, thr=thr, bthr=bthr if np.isfinite(bthr) else "inf",
+                merge=merge, K=K, w=w, sil=sil, sil_score=sil_score, kind=str(kind)), indent=1) + "\n")
+            print("dumped", dump)
+            return
         dec = CUCTCDecoder(toks, beam_size=beam, nbest=nb, blank_skip_threshold=thr, beam_threshold=bthr)
         dec.set_merge_mode(merge)
         dec.set_beam_size_token(K)
