@@ -14,8 +14,10 @@
  * Conventions: plain pointers and sizes; every function returns a ctcb status
  * (0 = OK).  Device pointers are CUDA device memory on the handle's device.
  * ctcb_decode only enqueues work on `stream`; outputs are valid once the
- * stream has been synchronised.  A handle is not thread-safe: use one handle
- * per host thread / stream.
+ * stream has been synchronised.  A handle is not thread-safe and is
+ * single-stream: its scratch (cached workspace, host staging, debug counters)
+ * is shared by all its calls, so two decodes on one handle must be ordered on
+ * one stream.  Use one handle per host thread / stream.
  */
 #ifndef CTCB_H
 #define CTCB_H

@@ -30,7 +30,7 @@ ids, decoder options).  Exit codes: 0 success, 1 when any utterance failed
 What differs from the CPU command: the decoder is the lexicon-free CUDA search
 (token-level ``--lm`` fusion and the ``--sil-score`` bonus included), so
 ``--lexicon`` is a configuration error (exit 2), as is ``--lm`` with a beam
-above 64; TSV values are rounded to
+above 128; TSV values are rounded to
 float32, the decoder's input dtype (CTCE files are float32 already, so their
 decode is bit-identical to the CPU command's); per-utterance times in the meta
 file are the utterance's share of its batch (load + decode).

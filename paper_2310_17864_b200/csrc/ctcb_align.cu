@@ -11,6 +11,7 @@
 #include <cmath>
 
 #include "../../include/ctcb.h"
+#include "ctcb_internal.h"
 #include "ctcb_common.cuh"
 
 namespace ctcb {
@@ -120,7 +121,8 @@ size_t align_smem_per_warp(int S_max) { return ((size_t)S_max * (8 + 8 + 4 + 1) 
 extern "C" {
 
 int ctcb_align_workspace_bytes(int batch, int t_max, int s_max, size_t* bytes) {
-  if (!bytes || batch < 0 || t_max < 0 || s_max < 1) return CTCB_ERR_ARG;
+  if (!bytes || batch < 0 || t_max < 0 || s_max < 1)
+    return ctcb::set_error(CTCB_ERR_ARG, "ctcb_align_workspace_bytes: bytes must not be NULL, batch/t_max >= 0, s_max >= 1");
   *bytes = (size_t)batch * (size_t)t_max * (size_t)s_max;
   return CTCB_OK;
 }
@@ -131,24 +133,29 @@ int ctcb_align(const float* log_probs, int64_t stride_b, int64_t stride_t, const
                float* out_scores, int32_t* out_status) {
   if (batch == 0) return CTCB_OK;
   if (!log_probs || !lens || !targets || !target_offsets || !workspace || !out_labels || !out_scores || !out_status)
-    return CTCB_ERR_ARG;
-  if (batch < 0 || t_max < 1 || vocab < 1 || blank < 0 || blank >= vocab || s_max < 1) return CTCB_ERR_ARG;
-  if (stride_t < vocab || stride_b < stride_t * t_max) return CTCB_ERR_ARG;
-  if (workspace_bytes < (size_t)batch * t_max * s_max) return CTCB_ERR_WORKSPACE;
+    return ctcb::set_error(CTCB_ERR_ARG, "ctcb_align: pointer arguments must not be NULL");
+  if (batch < 0 || t_max < 1 || vocab < 1 || blank < 0 || blank >= vocab || s_max < 1)
+    return ctcb::set_error(CTCB_ERR_ARG, "ctcb_align: need batch >= 0, t_max >= 1, 0 <= blank < vocab, s_max >= 1");
+  if (stride_t < vocab || stride_b < stride_t * t_max)
+    return ctcb::set_error(CTCB_ERR_ARG, "ctcb_align: strides must describe a [batch, t_max, vocab] layout");
+  if (workspace_bytes < (size_t)batch * t_max * s_max)
+    return ctcb::set_error(CTCB_ERR_WORKSPACE, "ctcb_align: workspace too small");
   const int wpb = 4;
   const size_t smem = align_smem_per_warp(s_max) * wpb;
   int dev = 0, optin = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return CTCB_ERR_CUDA;
+  if (cudaGetDevice(&dev) != cudaSuccess) return ctcb::set_error(CTCB_ERR_CUDA, "ctcb_align: cudaGetDevice failed");
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
-    return CTCB_ERR_CUDA;
-  if (smem > (size_t)optin) return CTCB_ERR_UNSUPPORTED;
+    return ctcb::set_error(CTCB_ERR_CUDA, "ctcb_align: cudaDeviceGetAttribute failed");
+  if (smem > (size_t)optin)
+    return ctcb::set_error(CTCB_ERR_UNSUPPORTED, "ctcb_align: target sequence too long for one warp's shared memory");
   if (cudaFuncSetAttribute(ctcb::ctcb_align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
-    return CTCB_ERR_CUDA;
+    return ctcb::set_error(CTCB_ERR_CUDA, "ctcb_align: cudaFuncSetAttribute failed");
   ctcb::ctcb_align_kernel<<<(batch + wpb - 1) / wpb, 32 * wpb, smem, (cudaStream_t)stream>>>(
       log_probs, stride_b, stride_t, lens, targets, target_offsets, batch, t_max, vocab, blank, s_max,
       (int8_t*)workspace, out_labels, out_scores, out_status);
-  return cudaGetLastError() == cudaSuccess ? CTCB_OK : CTCB_ERR_CUDA;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CTCB_OK : ctcb::set_error(CTCB_ERR_CUDA, cudaGetErrorString(e));
 }
 
 }  // extern "C"

@@ -130,6 +130,13 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+}  // namespace
+namespace ctcb {
+// Shared with the other translation units (ctcb_align.cu): record the message
+// ctcb_last_error returns and pass the status through.
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace ctcb
+namespace {
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(CTCB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
@@ -613,27 +620,37 @@ int ctcb_lm_destroy(ctcb_lm_t* lm) {
   return CTCB_OK;
 }
 
+// Transactional: arguments are validated and the new tables built before the
+// attached ones are released, so a failure leaves the previous LM in place.
 int ctcb_set_lm(ctcb_t* h, const ctcb_lm_t* lm, const int32_t* token_word, double weight) {
   if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
   CTCB_CUDA(cudaSetDevice(h->device));
+  ctcb::LmTables fresh{};
+  if (lm) {
+    if (!token_word) return fail(CTCB_ERR_ARG, "token_word must not be NULL");
+    if (!std::isfinite(weight)) return fail(CTCB_ERR_ARG, "lm_weight must be finite");
+    if (h->beam > ctcb::kFusedMaxBeam)
+      return fail(CTCB_ERR_UNSUPPORTED, "LM fusion supports beam_size <= " + std::to_string(ctcb::kFusedMaxBeam));
+    if (lm->m->device != h->device) return fail(CTCB_ERR_ARG, "LM and decoder are on different devices");
+    for (int c = 0; c < h->V; c++)
+      if (token_word[c] < -2) return fail(CTCB_ERR_ARG, "token_word entries must be >= -2");
+    const char* err = "";
+    const int rc = ctcb::lm_tables_build(lm->m, token_word, h->V, weight, &fresh, &err);
+    if (rc) {
+      ctcb::lm_tables_free(&fresh);
+      return fail(rc, std::string("ctcb_set_lm: ") + err);
+    }
+  }
   if (h->has_lm) {
-    CTCB_CUDA(cudaDeviceSynchronize());
+    CTCB_CUDA(cudaDeviceSynchronize());  // decodes still reading the old tables
     ctcb::lm_tables_free(&h->lm);
     h->has_lm = 0;
   }
-  if (!lm) return CTCB_OK;
-  if (!token_word) return fail(CTCB_ERR_ARG, "token_word must not be NULL");
-  if (!std::isfinite(weight)) return fail(CTCB_ERR_ARG, "lm_weight must be finite");
-  if (h->beam > ctcb::kFusedMaxBeam)
-    return fail(CTCB_ERR_UNSUPPORTED, "LM fusion supports beam_size <= " + std::to_string(ctcb::kFusedMaxBeam));
-  if (lm->m->device != h->device) return fail(CTCB_ERR_ARG, "LM and decoder are on different devices");
-  for (int c = 0; c < h->V; c++)
-    if (token_word[c] < -2) return fail(CTCB_ERR_ARG, "token_word entries must be >= -2");
-  const char* err = "";
-  int rc = ctcb::lm_tables_build(lm->m, token_word, h->V, weight, &h->lm, &err);
-  if (rc) return fail(rc, std::string("ctcb_set_lm: ") + err);
-  h->has_lm = 1;
-  h->lm_weight = weight;
+  if (lm) {
+    h->lm = fresh;
+    h->has_lm = 1;
+    h->lm_weight = weight;
+  }
   return CTCB_OK;
 }
 

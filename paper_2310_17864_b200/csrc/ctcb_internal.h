@@ -109,6 +109,9 @@ void lm_tables_free(LmTables* t);
 size_t fused_smem_per_warp(int beam, int V, int ring, int row_bytes);
 const void* fused_kernel_fn();
 
+// Record the error message of a failing C-ABI call (ctcb_last_error).
+int set_error(int code, const char* msg);
+
 enum DbgCounter {
   kDbgTies = 0, kDbgExactTies = 1, kDbgMaterialize = 2, kDbgMatSteps = 3, kDbgRadix = 4, kDbgFrames = 5, kDbgTopkFix = 6, kDbgOneshotFallback = 7
 };

@@ -110,7 +110,12 @@ def skip_cutoff(threshold: float) -> float:
 
 
 class CUCTCDecoder:
-    """CUDA CTC prefix beam-search decoder (build with :func:`cuda_ctc_decoder`)."""
+    """CUDA CTC prefix beam-search decoder (build with :func:`cuda_ctc_decoder`).
+
+    One decoder = one C handle = one stream: its scratch buffers are reused
+    by every call, so calls are enqueued on ``cuda_stream`` (or the current
+    stream at construction) and must not be issued concurrently from several
+    threads or streams; use one decoder per stream (see MultiDeviceDecoder)."""
 
     def __init__(
         self,

@@ -84,23 +84,21 @@ class MultiDeviceDecoder:
             out.extend(dec._hypotheses(tokens, lengths, scores, counts))
         return out
 
-    def _run_device(self, dec: CUCTCDecoder, lp: torch.Tensor, lens: torch.Tensor, b0: int):
+    def _run_device(self, dec: CUCTCDecoder, lp: torch.Tensor, lens: torch.Tensor, b0: int,
+                    ready: "torch.cuda.Event"):
+        """`ready` was recorded on the CALLER's current stream of the input's
+        device (streams are thread-local: this may run on a worker thread,
+        whose current stream is the default one), so the decode -- or the
+        peer copy -- is ordered after the producer of `lp`, whatever stream
+        produced it."""
         with torch.cuda.device(dec.device):
+            dec.cuda_stream.wait_event(ready)
             if lp.device != dec.device:
-                # peer copy on the target device's stream, ordered after the source's pending work
-                src_ev = torch.cuda.Event()
-                src_ev.record(torch.cuda.current_stream(lp.device))
-                dec.cuda_stream.wait_event(src_ev)
+                # peer copy on the target device's stream
                 with torch.cuda.stream(dec.cuda_stream):
                     lp = lp.to(dec.device, non_blocking=True)
                     lens = lens.to(dec.device, non_blocking=True)
-                out = dec.decode(lp, lens, offset=b0)
-            else:
-                # same device as the input: order the decode after the producer's stream
-                ev = torch.cuda.Event()
-                ev.record(torch.cuda.current_stream(lp.device))
-                dec.cuda_stream.wait_event(ev)
-                out = dec.decode(lp, lens, offset=b0)
+            out = dec.decode(lp, lens, offset=b0)
             tokens, _, lengths, scores, counts = dec.to_host(out, offset=b0)
             return dec._hypotheses(tokens, lengths, scores, counts)
 
@@ -115,6 +113,12 @@ class MultiDeviceDecoder:
         ranges = balanced_ranges(lens_cpu.numpy(), len(self.decoders))
         self.last_ranges = ranges
         on_host = not log_prob.is_cuda
+        ready = None
+        if not on_host:  # recorded here, on the calling thread's current stream
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(log_prob.device))
+            if lens_t.is_cuda and lens_t.device != log_prob.device:
+                raise ValueError("log_prob and encoder_out_lens must be on the same device")
         results: list = [None] * len(ranges)
         errors: list = [None] * len(ranges)
 
@@ -128,7 +132,7 @@ class MultiDeviceDecoder:
                 if on_host:
                     results[i] = self._run_host(dec, log_prob[b0:b1], lens_cpu[b0:b1], b0)
                 else:
-                    results[i] = self._run_device(dec, log_prob[b0:b1], lens_t[b0:b1], b0)
+                    results[i] = self._run_device(dec, log_prob[b0:b1], lens_t[b0:b1], b0, ready)
             except BaseException as exc:  # re-raised on the calling thread
                 errors[i] = exc
 

@@ -389,6 +389,30 @@ def test_multi_device_decoder_matches_single():
         single(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
 
 
+def test_multi_device_decoder_side_stream_producer():
+    """Input produced on a side stream (delayed by a device-side sleep) and
+    decoded from that stream: every range's decoder -- including those run
+    on worker threads, whose current stream is the default one -- must wait
+    for the producer (thread-local current streams)."""
+    from paper_2310_17864_b200 import MultiDeviceDecoder
+    cfg = dataclasses.replace(synth.CONFIGS[0], batch=300)
+    lp, lens = synth.batch(cfg)
+    src = torch.from_numpy(lp).cuda()
+    lens_d = torch.from_numpy(lens).cuda()
+    single = cuda_ctc_decoder(vocab(cfg.vocab), nbest=2, beam_size=10, blank_skip_threshold=cfg.threshold)
+    ref = single(src, lens_d)
+    multi = MultiDeviceDecoder(vocab(cfg.vocab), devices=[0, 0, 0], nbest=2, beam_size=10,
+                               blank_skip_threshold=cfg.threshold)
+    side = torch.cuda.Stream()
+    for _ in range(3):
+        with torch.cuda.stream(side):
+            dst = torch.zeros_like(src)
+            torch.cuda._sleep(20_000_000)
+            dst.copy_(src)
+            got = multi(dst, lens_d)
+        assert got == ref
+
+
 @pytest.mark.parametrize("force_generic", ["0", "1"])
 def test_merge_mode_max_matches_oracle(monkeypatch, force_generic):
     """merge_mode="max" (decoder.py:610-613, :789-791) on both kernels against the
