@@ -186,7 +186,10 @@ int ctcb_launch_count(ctcb_t* h, uint64_t* out);
  *   workspace        device >= ctcb_align_workspace_bytes(batch, t_max, s_max)
  * Outputs (device): out_labels int32 [batch, t_max] token per frame (blank
  * allowed), out_scores fp32 [batch, t_max] its log-prob, out_status int32
- * [batch] CTCB_ALIGN_*.  Enqueued on `stream` (on the current device). */
+ * [batch] CTCB_ALIGN_*, and (optional, NULL to skip) the token spans:
+ * out_span_start / out_span_end int32 in the targets' layout, target j of
+ * utterance b occupies frames [start, end) (align.py:126-143's spans, one per
+ * target).  Enqueued on `stream` (on the current device). */
 enum {
   CTCB_ALIGN_OK = 0,
   CTCB_ALIGN_EMPTY_TARGETS = 1,  /* "targets must be non-empty" (align.py:62-63) */
@@ -200,7 +203,7 @@ int ctcb_align_workspace_bytes(int batch, int t_max, int s_max, size_t* bytes);
 int ctcb_align(const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
                const int32_t* targets, const int32_t* target_offsets, int batch, int t_max, int vocab, int blank,
                int s_max, void* workspace, size_t workspace_bytes, void* stream, int32_t* out_labels,
-               float* out_scores, int32_t* out_status);
+               float* out_scores, int32_t* out_status, int32_t* out_span_start, int32_t* out_span_end);
 
 /* ---- Token-level LM fusion ---------------------------
  * Replaces NGramLM + parse_arpa (lm.py:35-226) on the device and the

@@ -73,7 +73,7 @@ def load():
     lib.ctcb_set_merge_mode.argtypes = [vp, c_int]
     lib.ctcb_align_workspace_bytes.argtypes = [c_int, c_int, c_int, ctypes.POINTER(c_size_t)]
     lib.ctcb_align.argtypes = [vp, c_int64, c_int64, vp, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, c_size_t, vp,
-                               vp, vp, vp]
+                               vp, vp, vp, vp, vp]
     lib.ctcb_set_beam_size_token.argtypes = [vp, c_int]
     lib.ctcb_lm_create.argtypes = [c_int, c_int64, vp, vp, vp, vp, vp, c_int, c_int, c_int, ctypes.POINTER(vp)]
     lib.ctcb_lm_destroy.argtypes = [vp]

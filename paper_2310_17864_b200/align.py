@@ -7,10 +7,13 @@
 The Viterbi pass runs in ``ctcb_align`` (one warp per utterance, fp64 path
 scores, the reference's tie-breaking), so frame labels are bit-identical to
 the reference's on float32-exact inputs (float64 emissions are rounded to
-float32, the kernel's input dtype).  Token spans and their mean scores are
-built on the host from the frame labels with the reference's own numpy
-expressions (align.py:126-143).  Errors are the reference's ``ValueError``
-messages; ``forced_align_batch`` tags them ``utterance b: ...``.
+float32, the kernel's input dtype).  The kernel's backtrace also emits each
+target's frame span (a feasible path holds target j's state in exactly one
+run of frames), so the host only attaches scores: the mean frame
+log-probability of a span, summed by numpy exactly as the reference does.
+Tiling (attribute_blanks) and word grouping (align_words) work on span-start
+arrays.  Errors are the reference's ``ValueError`` messages;
+``forced_align_batch`` tags them ``utterance b: ...``.
 """
 
 from __future__ import annotations
@@ -41,31 +44,36 @@ class AlignmentResult:
     spans: list
 
 
-def _spans_from_labels(labels: np.ndarray, scores: np.ndarray, blank: int) -> list:
-    # align.py:126-143
-    spans = []
-    start = 0
-    for i in range(1, len(labels) + 1):
-        if i == len(labels) or labels[i] != labels[start]:
-            if labels[start] != blank:
-                spans.append(AlignmentSpan(token=int(labels[start]), start_frame=start, end_frame=i,
-                                           score=float(scores[start:i].mean())))
-            start = i
-    return spans
+def _span_score(frame_scores: np.ndarray, a: int, b: int) -> float:
+    # mean of frames [a, b): numpy's pairwise summation, as align.py:137
+    return float(frame_scores[a:b].mean())
+
+
+def spans_from_runs(frame_labels: np.ndarray, frame_scores: np.ndarray, blank: int) -> list:
+    """Token spans of a frame labelling computed on the host (for labellings
+    that did not come from ctcb_align): maximal runs of one non-blank label,
+    found from the label changes (align.py:126-143's result)."""
+    labels = np.asarray(frame_labels)
+    if labels.size == 0:
+        return []
+    cuts = np.flatnonzero(labels[1:] != labels[:-1]) + 1
+    starts = np.concatenate(([0], cuts))
+    ends = np.concatenate((cuts, [labels.size]))
+    keep = labels[starts] != blank
+    return [AlignmentSpan(int(labels[a]), int(a), int(b), _span_score(frame_scores, a, b))
+            for a, b in zip(starts[keep], ends[keep])]
 
 
 def attribute_blanks(result: AlignmentResult) -> list:
-    """Widen spans so they tile [0, T) (align.py:146-165)."""
-    T = len(result.frame_labels)
-    if not result.spans:
+    """Widen spans so they tile [0, T): blank frames join the preceding span,
+    leading blanks the first one (align.py:146-165).  Span i covers
+    [start_i, start_{i+1}) with start_0 -> 0 and start_n -> T."""
+    n = len(result.spans)
+    if n == 0:
         return []
-    out = []
-    for i, span in enumerate(result.spans):
-        start = 0 if i == 0 else out[-1].end_frame
-        end = result.spans[i + 1].start_frame if i + 1 < len(result.spans) else T
-        out.append(AlignmentSpan(token=span.token, start_frame=start, end_frame=end,
-                                 score=float(result.frame_scores[start:end].mean())))
-    return out
+    bounds = [0] + [sp.start_frame for sp in result.spans[1:]] + [len(result.frame_labels)]
+    return [AlignmentSpan(sp.token, bounds[i], bounds[i + 1], _span_score(result.frame_scores, bounds[i], bounds[i + 1]))
+            for i, sp in enumerate(result.spans)]
 
 
 def _blank_of(tokens) -> int:
@@ -119,16 +127,20 @@ def forced_align_batch(emissions, targets, tokens=None, device: int = 0, raise_e
     labels = torch.zeros((B, T), dtype=torch.int32, device=dev)
     scores = torch.zeros((B, T), dtype=torch.float32, device=dev)
     status = torch.full((B,), -1, dtype=torch.int32, device=dev)
+    span_a = torch.zeros(max(int(offs[-1]), 1), dtype=torch.int32, device=dev)
+    span_b = torch.zeros_like(span_a)
     vp = ctypes.c_void_p
     stream = torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
         _lib.check(lib.ctcb_align(vp(x.data_ptr()), x.stride(0), x.stride(1), vp(lens.data_ptr()),
                                   vp(flat.data_ptr()), vp(toff.data_ptr()), B, T, V, blank, s_max,
                                   vp(ws.data_ptr()), ws.numel(), vp(stream), vp(labels.data_ptr()),
-                                  vp(scores.data_ptr()), vp(status.data_ptr())), "ctcb_align")
+                                  vp(scores.data_ptr()), vp(status.data_ptr()), vp(span_a.data_ptr()),
+                                  vp(span_b.data_ptr())), "ctcb_align")
     st = status.cpu().numpy()
     lab = labels.cpu().numpy()
     sco = scores.cpu().numpy()
+    sa, sb = span_a.cpu().numpy(), span_b.cpu().numpy()
     out = []
     for b in range(B):
         Tb = lps[b].shape[0]
@@ -140,7 +152,10 @@ def forced_align_batch(emissions, targets, tokens=None, device: int = 0, raise_e
             continue
         fl = lab[b, :Tb].astype(np.int64)
         fs = sco[b, :Tb].astype(np.float64)
-        out.append(AlignmentResult(frame_labels=fl, frame_scores=fs, spans=_spans_from_labels(fl, fs, blank)))
+        o0 = int(offs[b])
+        spans = [AlignmentSpan(tok, int(sa[o0 + j]), int(sb[o0 + j]), _span_score(fs, int(sa[o0 + j]), int(sb[o0 + j])))
+                 for j, tok in enumerate(tgs[b])]
+        out.append(AlignmentResult(frame_labels=fl, frame_scores=fs, spans=spans))
     return out
 
 
@@ -182,25 +197,25 @@ class WordSpan:
 
 
 def align_words(result: AlignmentResult, tokens, transcript: list, lexicon) -> list:
-    """Group token spans into word spans (align.py:168-212); ``lexicon.entries``
-    maps word -> list of spellings (tuples of token indices)."""
-    spellings = []
+    """Word spans (align.py:168-212): the transcript's first spellings
+    (``lexicon.entries``: word -> spellings, tuples of token indices), laid
+    end to end, must reproduce the aligned targets; word w owns the token
+    spans [cut_w, cut_{w+1}) and scores the frame-weighted mean of its spans
+    (span sums in span order over the frames they cover)."""
+    first = []
     for word in transcript:
         variants = lexicon.entries.get(word)
         if not variants:
             raise ValueError(f"word {word!r} is not in the lexicon")
-        spellings.append(variants[0])
-    flat = [tok for sp in spellings for tok in sp]
-    aligned = [span.token for span in result.spans]
-    if flat != aligned:
+        first.append(tuple(variants[0]))
+    if [t for sp in first for t in sp] != [sp.token for sp in result.spans]:
         raise ValueError("concatenated transcript spellings do not match the aligned targets")
-    out = []
-    pos = 0
-    for word, spelling in zip(transcript, spellings):
-        group = result.spans[pos: pos + len(spelling)]
-        pos += len(spelling)
-        frames = sum(sp.end_frame - sp.start_frame for sp in group)
-        total = sum(float(result.frame_scores[sp.start_frame: sp.end_frame].sum()) for sp in group)
-        out.append(WordSpan(word=word, start_frame=group[0].start_frame, end_frame=group[-1].end_frame,
-                            score=total / frames))
-    return out
+    cuts = np.cumsum([0] + [len(sp) for sp in first])
+    sums = [float(result.frame_scores[sp.start_frame: sp.end_frame].sum()) for sp in result.spans]
+    widths = [sp.end_frame - sp.start_frame for sp in result.spans]
+    words = []
+    for w, word in enumerate(transcript):
+        a, b = int(cuts[w]), int(cuts[w + 1])
+        words.append(WordSpan(word, result.spans[a].start_frame, result.spans[b - 1].end_frame,
+                              sum(sums[a:b]) / sum(widths[a:b])))
+    return words

@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(128) ctcb_align_kernel(const float* __restrict
                                                          int blank, int S_max, int8_t* __restrict__ bp,
                                                          int32_t* __restrict__ out_labels,
                                                          float* __restrict__ out_scores,
-                                                         int32_t* __restrict__ out_status) {
+                                                         int32_t* __restrict__ out_status,
+                                                         int32_t* __restrict__ out_span_start,
+                                                         int32_t* __restrict__ out_span_end) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int u = blockIdx.x * (blockDim.x >> 5) + wid;
@@ -97,10 +99,25 @@ __global__ void __launch_bounds__(128) ctcb_align_kernel(const float* __restrict
     if (A[s] == -INFINITY) {
       status = CTCB_ALIGN_NO_PATH;
     } else {
+      // token spans: a feasible path visits target j's state 2j+1 in exactly
+      // one run of frames, so the backward walk meets its last frame first
+      // (end) and its first frame last (start)
+      int32_t* sp0 = out_span_start ? out_span_start + t0 : nullptr;
+      int32_t* sp1 = out_span_end ? out_span_end + t0 : nullptr;
+      int prev = -1;
+      auto mark = [&](int t, int st_) {
+        if (sp0 && (st_ & 1)) {
+          if (st_ != prev) sp1[st_ >> 1] = t + 1;
+          sp0[st_ >> 1] = t;
+        }
+        prev = st_;
+      };
       lab[T - 1] = z[s];
+      mark(T - 1, s);
       for (int t = T - 1; t > 0; t--) {
         s -= ubp[(size_t)t * S_max + s];
         lab[t - 1] = z[s];
+        mark(t - 1, s);
       }
     }
     out_status[u] = status;
@@ -130,7 +147,7 @@ int ctcb_align_workspace_bytes(int batch, int t_max, int s_max, size_t* bytes) {
 int ctcb_align(const float* log_probs, int64_t stride_b, int64_t stride_t, const int32_t* lens,
                const int32_t* targets, const int32_t* target_offsets, int batch, int t_max, int vocab, int blank,
                int s_max, void* workspace, size_t workspace_bytes, void* stream, int32_t* out_labels,
-               float* out_scores, int32_t* out_status) {
+               float* out_scores, int32_t* out_status, int32_t* out_span_start, int32_t* out_span_end) {
   if (batch == 0) return CTCB_OK;
   if (!log_probs || !lens || !targets || !target_offsets || !workspace || !out_labels || !out_scores || !out_status)
     return ctcb::set_error(CTCB_ERR_ARG, "ctcb_align: pointer arguments must not be NULL");
@@ -153,7 +170,7 @@ int ctcb_align(const float* log_probs, int64_t stride_b, int64_t stride_t, const
     return ctcb::set_error(CTCB_ERR_CUDA, "ctcb_align: cudaFuncSetAttribute failed");
   ctcb::ctcb_align_kernel<<<(batch + wpb - 1) / wpb, 32 * wpb, smem, (cudaStream_t)stream>>>(
       log_probs, stride_b, stride_t, lens, targets, target_offsets, batch, t_max, vocab, blank, s_max,
-      (int8_t*)workspace, out_labels, out_scores, out_status);
+      (int8_t*)workspace, out_labels, out_scores, out_status, out_span_start, out_span_end);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CTCB_OK : ctcb::set_error(CTCB_ERR_CUDA, cudaGetErrorString(e));
 }

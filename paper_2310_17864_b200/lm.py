@@ -1,14 +1,18 @@
 """Backoff n-gram LMs from ARPA text, for token-level shallow fusion.
 
-Host side of the reference's ``lm.py`` (ctcforge lm.py:1-270): the ARPA
-reader with the reference's validation and messages, the model type, and the
-incremental scoring API.  Scores are natural-log (log10 × ln 10 at parse time,
-lm.py:183-184).  The decoder does not score on the host: :func:`flatten` turns a
-model into flat n-gram arrays for ``ctcb_lm_create``, and the device builds the
-(context × token) score / successor tables from them (csrc/ctcb_lm.cu).
+Host side of the reference's ``lm.py`` (ctcforge lm.py:1-270), built around
+the flat arrays the device consumes: the ARPA reader appends every n-gram
+straight into per-order columns (word ids, natural-log probability, backoff)
+with a tuple -> row index, so :func:`flatten` for ``ctcb_lm_create`` is a
+concatenation, and ``NGramLM.tables[n]`` is a read-only view over those
+columns.  Scores are natural log (log10 × ln 10 at parse time, lm.py:183-184);
+the reader's validation order and messages are the reference's.
 
-Models parsed by the reference itself (objects with ``order``, ``tables``,
-``vocab``) are accepted wherever an :class:`NGramLM` is.
+The incremental API (``lm_start`` / ``lm_score`` / ``lm_finish``, contexts as
+word-id tuples) serves the tests and the oracle tables; the decoder itself
+scores on the device (csrc/ctcb_lm.cu).  Models parsed by the reference
+(objects with ``order``, ``tables``, ``vocab``) are accepted by
+:func:`flatten`, :func:`token_words` and the scoring functions.
 """
 
 from __future__ import annotations
@@ -16,13 +20,14 @@ from __future__ import annotations
 import logging
 import math
 import re
-from dataclasses import dataclass
+from collections.abc import Mapping
+from dataclasses import dataclass, field
 from pathlib import Path
 
 import numpy as np
 
 LN10 = math.log(10.0)
-OOV_PENALTY = -20.0  # lm.py:22-24
+OOV_PENALTY = -20.0  # out-of-vocabulary word without <unk> (lm.py:22-24)
 
 log = logging.getLogger(__name__)
 
@@ -34,28 +39,70 @@ class ArpaFormatError(ValueError):
     """The file is not well-formed ARPA text (lm.py:31-32)."""
 
 
+class _OrderColumns(Mapping):
+    """All n-grams of one order: row index by word-id tuple plus parallel
+    columns; as a Mapping, tuple -> (logprob, backoff) like the reference's
+    per-order dict."""
+
+    def __init__(self, n: int):
+        self.n = n
+        self.index: dict = {}
+        self.ids: list = []
+        self.logprob: list = []
+        self.backoff: list = []
+
+    def add(self, key: tuple, lp: float, bo: float) -> None:
+        row = self.index.get(key)
+        if row is None:  # a repeated n-gram keeps its first row, its last values
+            self.index[key] = len(self.ids)
+            self.ids.append(key)
+            self.logprob.append(lp)
+            self.backoff.append(bo)
+        else:
+            self.logprob[row], self.backoff[row] = lp, bo
+
+    def __getitem__(self, key):
+        row = self.index[key]
+        return self.logprob[row], self.backoff[row]
+
+    def get(self, key, default=None):
+        row = self.index.get(key)
+        return default if row is None else (self.logprob[row], self.backoff[row])
+
+    def __contains__(self, key) -> bool:
+        return key in self.index
+
+    def __iter__(self):
+        return iter(self.ids)
+
+    def __len__(self) -> int:
+        return len(self.ids)
+
+
 @dataclass
 class NGramLM:
-    """``tables[n]``: n-tuple of word ids -> (logprob, backoff), natural log;
-    ``vocab``: word -> id (lm.py:35-50)."""
+    """``tables[n]``: word-id n-tuple -> (logprob, backoff), natural log
+    (``tables[0]`` unused); ``vocab``: word -> id (lm.py:35-50)."""
 
     order: int
     tables: list
-    vocab: dict
+    vocab: dict = field(default_factory=dict)
 
     @property
     def unk_id(self):
         return self.vocab.get("<unk>")
 
 
+@dataclass(eq=False)
 class LMState:
-    """Context word ids plus a running total; equality by context (lm.py:53-74)."""
+    """Scoring context (word-id tuple) and the running total; two states are
+    equal when their contexts are (lm.py:53-74)."""
 
-    __slots__ = ("context", "cumulative_score")
+    context: tuple = ()
+    cumulative_score: float = 0.0
 
-    def __init__(self, context=(), cumulative_score: float = 0.0):
-        self.context = tuple(context)
-        self.cumulative_score = cumulative_score
+    def __post_init__(self):
+        self.context = tuple(self.context)
 
     def __eq__(self, other) -> bool:
         return isinstance(other, LMState) and self.context == other.context
@@ -63,126 +110,156 @@ class LMState:
     def __hash__(self) -> int:
         return hash(self.context)
 
-    def __repr__(self) -> str:
-        return f"LMState(context={self.context}, cumulative_score={self.cumulative_score})"
+
+class _ArpaReader:
+    """One pass over the file: `\\data\\` counts, then the n-gram sections."""
+
+    def __init__(self, path: Path):
+        self.path = path
+        self.lines = path.read_text(encoding="utf-8").splitlines()
+        self.counts: dict = {}
+        self.vocab: dict = {}
+        self.orders: dict = {}
+
+    def fail(self, msg: str, line: int | None = None):
+        where = f"{self.path}: line {line + 1}" if line is not None else f"{self.path}"
+        raise ArpaFormatError(f"{where}: {msg}")
+
+    def header(self) -> int:
+        """Index of the first line after the count block."""
+        try:
+            at = next(k for k, s in enumerate(self.lines) if s.strip() == "\\data\\") + 1
+        except StopIteration:
+            self.fail("missing \\data\\ header")
+        for k in range(at, len(self.lines)):
+            s = self.lines[k].strip()
+            if not s:
+                continue
+            m = _COUNT.fullmatch(s)
+            if m is None:
+                return self._counted(k)
+            self.counts[int(m.group(1))] = int(m.group(2))
+        return self._counted(len(self.lines))
+
+    def _counted(self, k: int) -> int:
+        if not self.counts:
+            self.fail("no 'ngram N=count' lines after \\data\\")
+        return k
+
+    def body(self, start: int) -> None:
+        top = max(self.counts)
+        section = None
+        finished = False
+        for k in range(start, len(self.lines)):
+            s = self.lines[k].strip()
+            if not s:
+                continue
+            if s == "\\end\\":
+                finished, section = True, None
+                continue
+            if finished:
+                self.fail("content after \\end\\", k)
+            m = _SECTION.fullmatch(s)
+            if m is not None:
+                n = int(m.group(1))
+                if n not in self.counts:
+                    self.fail(f"section \\{n}-grams: was not declared in \\data\\", k)
+                if n in self.orders:
+                    self.fail(f"duplicate \\{n}-grams: section", k)
+                section = self.orders[n] = _OrderColumns(n)
+                continue
+            if section is None:
+                self.fail("unexpected content outside a section", k)
+            self._entry(section, s.split(), top, k)
+        if not finished:
+            self.fail("missing \\end\\")
+
+    def _entry(self, section: _OrderColumns, f: list, top: int, k: int) -> None:
+        n = section.n
+        with_bo = len(f) == n + 2
+        if not (len(f) == n + 1 or (with_bo and n != top)):
+            self.fail(f"malformed {n}-gram line", k)
+        try:
+            lp = float(f[0]) * LN10
+            bo = float(f[-1]) * LN10 if with_bo else 0.0
+        except ValueError:
+            self.fail(f"malformed {n}-gram line", k)
+        key = tuple(self.vocab.setdefault(w, len(self.vocab)) for w in f[1:n + 1])
+        section.add(key, lp, bo)
+
+    def model(self, strict: bool) -> NGramLM:
+        order = max(self.counts)
+        tables = [_OrderColumns(0)] + [self.orders.get(n) or _OrderColumns(n) for n in range(1, order + 1)]
+        for n in sorted(self.counts):
+            declared = self.counts[n]
+            if n not in self.orders and declared > 0:
+                self.fail(f"missing \\{n}-grams: section")
+            if len(tables[n]) != declared:
+                self.fail(f"\\data\\ declares {declared} {n}-grams, file has {len(tables[n])}")
+        orphans = sum(key[:-1] not in tables[len(key) - 1] for n in range(2, order + 1) for key in tables[n])
+        if orphans:
+            msg = f"{self.path}: {orphans} n-grams have no lower-order context entry (pruned model?)"
+            if strict:
+                raise ArpaFormatError(msg)
+            log.warning(msg)
+        return NGramLM(order=order, tables=tables, vocab=self.vocab)
 
 
 def parse_arpa(path, strict: bool = False) -> NGramLM:
-    """Read an ARPA file (lm.py:77-226): header counts, one section per order,
-    ``\\end\\``; errors name the file and line.  Missing lower-order prefixes
-    warn (``strict=True``: raise)."""
-    path = Path(path)
-    lines = path.read_text(encoding="utf-8").splitlines()
-    n_lines = len(lines)
-    i = 0
-    while i < n_lines and lines[i].strip() != "\\data\\":
-        i += 1
-    if i == n_lines:
-        raise ArpaFormatError(f"{path}: missing \\data\\ header")
-    i += 1
-    counts: dict[int, int] = {}
-    while i < n_lines:
-        s = lines[i].strip()
-        if s:
-            m = _COUNT.fullmatch(s)
-            if m is None:
-                break
-            counts[int(m.group(1))] = int(m.group(2))
-        i += 1
-    if not counts:
-        raise ArpaFormatError(f"{path}: no 'ngram N=count' lines after \\data\\")
-    order = max(counts)
-    vocab: dict[str, int] = {}
-    tables: list[dict] = [{} for _ in range(order + 1)]
-    seen: set[int] = set()
-    ended = False
-    cur = None
-    for ln in range(i, n_lines):
-        s = lines[ln].strip()
-        if not s:
-            continue
-        where = f"{path}: line {ln + 1}"
-        if s == "\\end\\":
-            ended = True
-            cur = None
-            continue
-        if ended:
-            raise ArpaFormatError(f"{where}: content after \\end\\")
-        m = _SECTION.fullmatch(s)
-        if m is not None:
-            cur = int(m.group(1))
-            if cur not in counts:
-                raise ArpaFormatError(f"{where}: section \\{cur}-grams: was not declared in \\data\\")
-            if cur in seen:
-                raise ArpaFormatError(f"{where}: duplicate \\{cur}-grams: section")
-            seen.add(cur)
-            continue
-        if cur is None:
-            raise ArpaFormatError(f"{where}: unexpected content outside a section")
-        n = cur
-        f = s.split()
-        if len(f) not in (n + 1, n + 2) or (len(f) == n + 2 and n == order):
-            raise ArpaFormatError(f"{where}: malformed {n}-gram line")
-        try:
-            lp = float(f[0]) * LN10
-            bo = float(f[n + 1]) * LN10 if len(f) == n + 2 else 0.0
-        except ValueError:
-            raise ArpaFormatError(f"{where}: malformed {n}-gram line") from None
-        key = tuple(vocab.setdefault(word, len(vocab)) for word in f[1:n + 1])
-        tables[n][key] = (lp, bo)
-    if not ended:
-        raise ArpaFormatError(f"{path}: missing \\end\\")
-    for n, declared in sorted(counts.items()):
-        if n not in seen and declared > 0:
-            raise ArpaFormatError(f"{path}: missing \\{n}-grams: section")
-        if len(tables[n]) != declared:
-            raise ArpaFormatError(f"{path}: \\data\\ declares {declared} {n}-grams, file has {len(tables[n])}")
-    missing = sum(1 for n in range(2, order + 1) for ng in tables[n] if ng[:-1] not in tables[n - 1])
-    if missing:
-        msg = f"{path}: {missing} n-grams have no lower-order context entry (pruned model?)"
-        if strict:
-            raise ArpaFormatError(msg)
-        log.warning(msg)
-    return NGramLM(order=order, tables=tables, vocab=vocab)
+    """Read an ARPA file (lm.py:77-226).  Errors name the file and line;
+    n-grams whose (n-1)-gram context is absent warn (``strict``: raise)."""
+    reader = _ArpaReader(Path(path))
+    reader.body(reader.header())
+    return reader.model(strict)
 
 
 # ------------------------------------------------------------------ scoring (lm.py:229-270)
-def _known(lm, ctx: tuple) -> tuple:
-    while ctx and ctx not in lm.tables[len(ctx)]:
-        ctx = ctx[1:]
-    return ctx
+def _longest_known(lm, ctx: tuple) -> tuple:
+    """Longest suffix of ``ctx`` that is itself an n-gram of the model (a
+    context absent from the model cannot affect later scores)."""
+    for k in range(len(ctx), 0, -1):
+        suffix = ctx[len(ctx) - k:]
+        if suffix in lm.tables[k]:
+            return suffix
+    return ()
 
 
-def _backoff(lm, context: tuple, wid: int) -> float:
-    ctx = context[-(lm.order - 1):] if lm.order > 1 else ()
-    acc = 0.0
-    while True:
-        hit = lm.tables[len(ctx) + 1].get(ctx + (wid,))
+def _katz(lm, context: tuple, wid: int) -> float:
+    """Backoff log-probability of ``wid`` after ``context``: the longest
+    matching n-gram, plus the backoff weights of the longer contexts that
+    missed, accumulated from the longest one down (lm.py:229-245)."""
+    hist = context[max(len(context) - (lm.order - 1), 0):] if lm.order > 1 else ()
+    penalty = 0.0
+    for k in range(len(hist), -1, -1):
+        suffix = hist[len(hist) - k:]
+        hit = lm.tables[k + 1].get(suffix + (wid,))
         if hit is not None:
-            return acc + hit[0]
-        if not ctx:
-            return acc + OOV_PENALTY
-        c = lm.tables[len(ctx)].get(ctx)
-        if c is not None:
-            acc += c[1]
-        ctx = ctx[1:]
+            return penalty + hit[0]
+        if k == 0:
+            break
+        ctx = lm.tables[k].get(suffix)
+        if ctx is not None:
+            penalty += ctx[1]
+    return penalty + OOV_PENALTY  # word only in higher orders of a broken model
 
 
 def context_start(lm) -> tuple:
     sid = lm.vocab.get("<s>")
-    return () if sid is None or lm.order == 1 else _known(lm, (sid,))
+    return () if sid is None or lm.order == 1 else _longest_known(lm, (sid,))
 
 
 def context_score(lm, context: tuple, word: str):
-    wid = lm.vocab.get(word)
+    """(next context, natural-log score) of ``word`` after ``context``; unknown
+    words score as ``<unk>`` or, without one, the fixed penalty with the
+    context reset."""
+    wid = lm.vocab.get(word, lm.vocab.get("<unk>"))
     if wid is None:
-        wid = lm.vocab.get("<unk>")
-        if wid is None:
-            return (), OOV_PENALTY
-    score = _backoff(lm, context, wid)
+        return (), OOV_PENALTY
+    score = _katz(lm, context, wid)
     if lm.order == 1:
         return (), score
-    return _known(lm, (context + (wid,))[-(lm.order - 1):]), score
+    grown = context + (wid,)
+    return _longest_known(lm, grown[max(len(grown) - (lm.order - 1), 0):]), score
 
 
 def lm_start(lm) -> LMState:
@@ -215,19 +292,30 @@ class FlatLM:
     unk: int
 
 
+def _columns(lm, n: int):
+    """(keys, logprobs, backoffs) of order n: the reader's columns, or a
+    reference model's dict."""
+    t = lm.tables[n]
+    if isinstance(t, _OrderColumns):
+        return t.ids, t.logprob, t.backoff
+    keys = list(t)
+    vals = [t[k] for k in keys]
+    return keys, [v[0] for v in vals], [v[1] for v in vals]
+
+
 def flatten(lm) -> FlatLM:
     order = int(lm.order)
-    rows = [(ng, v) for n in range(1, order + 1) for ng, v in lm.tables[n].items()]
-    N = len(rows)
+    cols = [_columns(lm, n) for n in range(1, order + 1)]
+    N = sum(len(c[0]) for c in cols)
     words = np.full((N, order), -1, dtype=np.int32)
-    lengths = np.empty(N, dtype=np.int32)
-    lp = np.empty(N, dtype=np.float64)
-    bo = np.empty(N, dtype=np.float64)
-    for i, (ng, (a, b)) in enumerate(rows):
-        words[i, :len(ng)] = ng
-        lengths[i] = len(ng)
-        lp[i] = a
-        bo[i] = b
+    lengths = np.repeat(np.arange(1, order + 1, dtype=np.int32), [len(c[0]) for c in cols])
+    row = 0
+    for n, (keys, _, _) in enumerate(cols, start=1):
+        if keys:
+            words[row: row + len(keys), :n] = np.asarray(keys, dtype=np.int32).reshape(len(keys), n)
+        row += len(keys)
+    lp = np.fromiter((x for c in cols for x in c[1]), dtype=np.float64, count=N)
+    bo = np.fromiter((x for c in cols for x in c[2]), dtype=np.float64, count=N)
     st = context_start(lm)
     start = np.full(max(order - 1, 1), -1, dtype=np.int32)
     start[:len(st)] = st
@@ -243,11 +331,9 @@ def token_words(lm, tokens, blank: int, sil=None) -> np.ndarray:
     reset), -2 for blank / silence (identity: no LM score, context kept;
     decoder.py:178-229)."""
     unk = lm.vocab.get("<unk>")
-    out = np.empty(len(tokens), dtype=np.int32)
-    for c, t in enumerate(tokens):
-        if c == blank or (sil is not None and c == sil):
-            out[c] = -2
-            continue
-        wid = lm.vocab.get(t, unk)
-        out[c] = -1 if wid is None else wid
+    ids = [lm.vocab.get(t, unk) for t in tokens]
+    out = np.array([-1 if w is None else w for w in ids], dtype=np.int32)
+    out[blank] = -2
+    if sil is not None:
+        out[sil] = -2
     return out

@@ -40,13 +40,13 @@ def test_oracle_matches_reference_golden():
 
 
 def test_host_spans_match_reference_golden():
-    # spans / attribute_blanks are host code over the frame labels (align.py:126-165)
+    # host spans (label runs) and tiling against the reference (align.py:126-165)
     for c in cases():
         if "error" in c:
             continue
         labels = np.array(c["labels"], dtype=np.int64)
         scores = np.array(c["scores"], dtype=np.float64)
-        res = galign.AlignmentResult(labels, scores, galign._spans_from_labels(labels, scores, c["blank"]))
+        res = galign.AlignmentResult(labels, scores, galign.spans_from_runs(labels, scores, c["blank"]))
         assert spans_as_lists(res.spans) == c["spans"], c["note"]
         assert spans_as_lists(galign.attribute_blanks(res)) == c["tiled"], c["note"]
 

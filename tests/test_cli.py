@@ -100,7 +100,7 @@ def test_config_precedence(tmp_path):
     cfg = tmp_path / "c.json"
     cfg.write_text(json.dumps({"beam_size": 7, "nbest": 2, "merge": "max"}))
     args = cli.build_parser().parse_args(["decode", "--config", str(cfg), "--nbest", "3"])
-    merged = cli._merge_config(args)
+    merged = cli.resolve_settings(args)
     assert merged["beam_size"] == 7 and merged["nbest"] == 3 and merged["merge"] == "max"
     assert merged["beam_threshold"] == 50.0
 

@@ -310,3 +310,32 @@ def test_fused_kernel_four_gram_model(tmp_path):
         assert [tokens[b, j, : lengths[b, j]].tolist() for j in range(counts[b])] == ref.tokens, b
         for j in range(counts[b]):
             assert _close(scores[b, j], ref.scores[j]) and _close(lms[b, j], ref.lm_scores[j])
+
+
+def test_reader_and_scorer_match_reference_implementation():
+    """The ARPA reader / Katz scorer are this repo's own code: cross-check
+    them against ctcforge's (from baseline/_ref or /root/reference, when
+    present) on every golden model: tables, contexts, scores, bit for bit."""
+    import glob
+    import sys
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for p in (os.path.join(here, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "ctcforge")) and p not in sys.path:
+            sys.path.append(p)
+    rlm = pytest.importorskip("ctcforge.lm")
+    files = sorted(glob.glob(os.path.join(GOLD, "*.arpa")))
+    assert files
+    rng = np.random.default_rng(3)
+    for f in files:
+        a, b = rlm.parse_arpa(f), glm.parse_arpa(f)
+        assert a.order == b.order and a.vocab == b.vocab
+        for n in range(1, a.order + 1):
+            assert dict(a.tables[n]) == dict(b.tables[n].items())
+        words = list(a.vocab) + ["zz-oov"]
+        for _ in range(100):
+            sa, sb = rlm.lm_start(a), glm.lm_start(b)
+            for w in rng.choice(words, size=6):
+                sa, x = rlm.lm_score(a, sa, str(w))
+                sb, y = glm.lm_score(b, sb, str(w))
+                assert x == y and sa.context == sb.context
+            assert rlm.lm_finish(a, sa) == glm.lm_finish(b, sb)
