@@ -37,6 +37,7 @@ __device__ __forceinline__ double log1pexp_neg(double d) {
   // exp(-d) = 2^n * exp(g), n = rint(-d*log2e), |g| <= ln2/2 (Cody-Waite)
   const double n = rint(-d * kLog2e);
   const double g = fma(-n, kLn2Lo, fma(-n, kLn2Hi, -d));
+#ifdef CTCB_LAE_HORNER
   double p = 1.0 / 6227020800.0;  // 1/13!
   p = fma(p, g, 1.0 / 479001600.0);
   p = fma(p, g, 1.0 / 39916800.0);
@@ -51,6 +52,18 @@ __device__ __forceinline__ double log1pexp_neg(double d) {
   p = fma(p, g, 0.5);
   p = fma(p, g, 1.0);
   p = fma(p, g, 1.0);
+#else
+  // Estrin evaluation of sum_{i<=13} g^i / i!: the frame step is bound by
+  // dependent-latency chains, so a 5-deep tree beats the 13-deep Horner chain
+  const double g2 = g * g, g4 = g2 * g2, g8 = g4 * g4;
+  const double c01 = fma(g, 1.0, 1.0), c23 = fma(g, 1.0 / 6.0, 0.5);
+  const double c45 = fma(g, 1.0 / 120.0, 1.0 / 24.0), c67 = fma(g, 1.0 / 5040.0, 1.0 / 720.0);
+  const double c89 = fma(g, 1.0 / 362880.0, 1.0 / 40320.0), cab = fma(g, 1.0 / 39916800.0, 1.0 / 3628800.0);
+  const double ccd = fma(g, 1.0 / 6227020800.0, 1.0 / 479001600.0);
+  const double d03 = fma(g2, c23, c01), d47 = fma(g2, c67, c45), d8b = fma(g2, cab, c89);
+  const double e07 = fma(g4, d47, d03), e8f = fma(g4, ccd, d8b);
+  const double p = fma(g8, e8f, e07);
+#endif
   const int ni = d < 700.0 ? (int)n : -1100;
   const double e = ni > -1022 ? p * __longlong_as_double((long long)(ni + 1023) << 52) : 0.0;
   // log1p(e) = log(z), z = 1 + e in (1, 2]: split at sqrt(2), atanh series
@@ -65,6 +78,7 @@ __device__ __forceinline__ double log1pexp_neg(double d) {
   double u = num * r;
   u = fma(r, fma(-den, u, num), u);
   const double u2 = u * u;
+#ifdef CTCB_LAE_HORNER
   double s = 1.0 / 23.0;
   s = fma(s, u2, 1.0 / 21.0);
   s = fma(s, u2, 1.0 / 19.0);
@@ -76,6 +90,15 @@ __device__ __forceinline__ double log1pexp_neg(double d) {
   s = fma(s, u2, 1.0 / 7.0);
   s = fma(s, u2, 1.0 / 5.0);
   s = fma(s, u2, 1.0 / 3.0);
+#else
+  // sum_{i=0..10} u2^i / (2i+3), Estrin
+  const double w2 = u2 * u2, w4 = w2 * w2, w8 = w4 * w4;
+  const double a01 = fma(u2, 1.0 / 5.0, 1.0 / 3.0), a23 = fma(u2, 1.0 / 9.0, 1.0 / 7.0);
+  const double a45 = fma(u2, 1.0 / 13.0, 1.0 / 11.0), a67 = fma(u2, 1.0 / 17.0, 1.0 / 15.0);
+  const double a89 = fma(u2, 1.0 / 21.0, 1.0 / 19.0);
+  const double b03 = fma(w2, a23, a01), b47 = fma(w2, a67, a45), b8a = fma(w2, 1.0 / 23.0, a89);
+  const double s = fma(w8, b8a, fma(w4, b47, b03));
+#endif
   double res = fma(2.0 * u, u2 * s, 2.0 * u) + corr * (double)__frcp_rn((float)zz);
   return big ? res + kLn2Hi + kLn2Lo : res;
 }

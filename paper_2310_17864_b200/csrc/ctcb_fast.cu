@@ -707,50 +707,77 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         __syncwarp();
       }
 
-      // ================= top-k (k <= 32) =================
-      int st;
-      float sv;
-      if (PRE) {
-        st = pre_st;
-        sv = pre_sv;
-        if (i + 1 < kept && lane < k) {
-          pre_st = P.topk_tok[tk_base + (size_t)(i + 1) * k + lane];
-          pre_sv = P.topk_val[tk_base + (size_t)(i + 1) * k + lane];
+      // ---- blank-frame shortcut (full vocabulary).  Every append group
+      // (R+c, 0), including the last-token append from (R,1), scores at most
+      // A_R + max_c v_c <= U = max_R A_R + vmax.  When at least `beam` blank /
+      // repeat groups score above U, the new beam is made of those groups
+      // alone and the frame needs no top-k, append lists or list selection
+      // (~60 % of cfg4 frames).  vmax comes from a lane-max pass over the
+      // staged row (blank holds the sentinel).
+      const bool sc_on = !tokK && (PRE || tiny_v);
+      double vmax = -INFINITY;
+      if (sc_on && !PRE) {
+        const float4* r4 = (const float4*)row;
+        float lm = __uint_as_float(kSentinel);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const float4 q = r4[lane + 32 * j];
+          lm = fmaxf(lm, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
         }
-      } else {
-        if (tiny_v) st = topk_small(S, row, V, k, lane, nch4, P.dbg);
-        else st = skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, P.dbg));
-        st = lane < k ? st : 0;
-        sv = lane < k ? row[st] : 0.0f;
+        const uint32_t mk = __reduce_max_sync(FULL, isnan(lm) ? 0u : okey(lm));
+        vmax = mk ? (double)unord32(mk) : -INFINITY;
       }
-      // per-position key term: floor(v_p * 2^32 / R) (64-bit)
-      if (lane < k) {
-        S.sval[lane] = sv;
-        S.stok[lane] = st;
-        S.posmap[st] = (uint8_t)lane;
-        S.wp[lane] = f2ll_floor((double)sv * kScale);
-      }
-      __syncwarp();
-      // beam_size_token = K < V (decoder.py:440-458): the selected non-blank
-      // tokens are a prefix (mS) of S when K <= k; otherwise all of S plus
-      // tokens beyond it, tested against the K-th key (kth_token)
+      int st = 0;
+      float sv = 0.0f;
       uint32_t selk = fullk;
       bool has_blank = true, wide = false;
       int mS = k;
       uint32_t tv = 0u;
       int ti = 0;
-      if (tokK) {
-        const uint32_t kb = ord32((float)eb);
-        if (tokK <= k) {
-          const bool above = lane < k && (ord32(sv) > kb || (ord32(sv) == kb && st < P.blank));
-          has_blank = __popc(__ballot_sync(FULL, above)) < tokK;
-          mS = has_blank ? tokK - 1 : tokK;
-          selk = mS >= 32 ? 0xffffffffu : ((1u << mS) - 1u);
+      // ================= top-k (k <= 32) =================
+      auto full_topk = [&]() {
+        if (PRE) {
+          st = pre_st;
+          sv = pre_sv;
+          if (i + 1 < kept && lane < k) {
+            pre_st = P.topk_tok[tk_base + (size_t)(i + 1) * k + lane];
+            pre_sv = P.topk_val[tk_base + (size_t)(i + 1) * k + lane];
+          }
         } else {
-          kth_token(row, V, P.blank, (float)eb, tokK, S.hist, lane, tv, ti);
-          has_blank = token_selected(kb, P.blank, tv, ti);
-          wide = true;
+          if (tiny_v) st = topk_small(S, row, V, k, lane, nch4, P.dbg);
+          else st = skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, P.dbg));
+          st = lane < k ? st : 0;
+          sv = lane < k ? row[st] : 0.0f;
         }
+        // per-position key term: floor(v_p * 2^32 / R) (64-bit)
+        if (lane < k) {
+          S.sval[lane] = sv;
+          S.stok[lane] = st;
+          S.posmap[st] = (uint8_t)lane;
+          S.wp[lane] = f2ll_floor((double)sv * kScale);
+        }
+        __syncwarp();
+        // beam_size_token = K < V (decoder.py:440-458): the selected non-blank
+        // tokens are a prefix (mS) of S when K <= k; otherwise all of S plus
+        // tokens beyond it, tested against the K-th key (kth_token)
+        if (tokK) {
+          const uint32_t kb = ord32((float)eb);
+          if (tokK <= k) {
+            const bool above = lane < k && (ord32(sv) > kb || (ord32(sv) == kb && st < P.blank));
+            has_blank = __popc(__ballot_sync(FULL, above)) < tokK;
+            mS = has_blank ? tokK - 1 : tokK;
+            selk = mS >= 32 ? 0xffffffffu : ((1u << mS) - 1u);
+          } else {
+            kth_token(row, V, P.blank, (float)eb, tokK, S.hist, lane, tv, ti);
+            has_blank = token_selected(kb, P.blank, tv, ti);
+            wide = true;
+          }
+        }
+      };
+      if (!sc_on || PRE) full_topk();
+      if (sc_on && PRE) {  // precomputed lists: vmax is the top entry
+        const float v0 = __shfl_sync(FULL, sv, 0);
+        vmax = k > 0 ? (double)v0 : -INFINITY;
       }
 
       // ================= merge structure =================
@@ -770,22 +797,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       const int p2 = (ent && pmask) ? __ffs(pmask) - 1 : -1;
       const double s_p2 = __shfl_sync(FULL, s, p2 >= 0 ? p2 : lane);
       const int fl_p2 = __shfl_sync(FULL, fl, p2 >= 0 ? p2 : lane);
-
-      // S positions of last tokens; flag-0 children exclude their token from
-      // the parent's append list (they become repeat groups)
-      const int mypos = (ent && last >= 0) ? (int)S.posmap[last] : 0xff;
-      const uint32_t mybit = mypos < 32 ? (1u << mypos) : 0u;
-      if (lane < 16) S.excl[lane] = 0u;
-      __syncwarp();
       const int pa = (ent && parents) ? __ffs(parents) - 1 : -1;
-      if (ent && fl == 0 && pa >= 0 && mybit) atomicOr(&S.excl[pa], mybit);
-      __syncwarp();
-      const uint32_t childx = lane < 16 ? S.excl[lane] : 0u;
-      // last(R) selected this frame (repeat groups and the last-token append need it)
-      const bool mem_last = !tokK || (ent && last >= 0 &&
-                                        (wide ? token_selected(ord32(row[last]), last, tv, ti) : mypos < mS));
-
-      // ================= special groups (lanes < 16) =================
       const unsigned pr2 = parents & (parents - 1);
       const int pb = (ent && pr2) ? __ffs(pr2) - 1 : -1;
       const double s_pa = __shfl_sync(FULL, s, pa >= 0 ? pa : lane);
@@ -794,59 +806,139 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       const double s_pb = __shfl_sync(FULL, s, pb >= 0 ? pb : lane);
       const int fl_pb = __shfl_sync(FULL, fl, pb >= 0 ? pb : lane);
       const int last_pb = __shfl_sync(FULL, last, pb >= 0 ? pb : lane);
+      // A = logaddexp of the prefix's entries (append-list base)
+      const double A = isfirst ? (p2 >= 0 ? merge2(s, s_p2, MX) : s) : 0.0;
+
+      // blank / repeat groups need only the staged row (decoder.py:513-530);
+      // with beam_size_token they are computed after the top-k (selection)
       double c_blank = -INFINITY, c_rep = -INFINITY, c_single = -INFINITY;
       int rep_src = lane, rep_tok = -1, single_src = lane;
-      if (isfirst && has_blank) {  // blank group (R,1): entries of R in rank order (decoder.py:513-521)
-        c_blank = s + eb;
-        if (p2 >= 0) c_blank = merge2(c_blank, s_p2 + eb, MX);
-      }
-      if (ent && fl == 0 && mem_last) {  // repeat group (R',0): repeat first, then parent appends (:522-543)
-        const double ec = (double)row[last];
-        double sc = s + ec, bst = sc;
-        if (pa >= 0 && !(fl_pa == 0 && last_pa == last)) {
-          double x = s_pa + ec;
-          sc = merge2(sc, x, MX);
-          if (x > bst) { bst = x; rep_src = pa; rep_tok = last; }
+      auto blank_repeat = [&](bool mem_last) {
+        if (isfirst && has_blank) {  // blank group (R,1): entries of R in rank order (decoder.py:513-521)
+          c_blank = s + eb;
+          if (p2 >= 0) c_blank = merge2(c_blank, s_p2 + eb, MX);
         }
-        if (pb >= 0 && !(fl_pb == 0 && last_pb == last)) {
-          double x = s_pb + ec;
-          sc = merge2(sc, x, MX);
-          if (x > bst) { bst = x; rep_src = pb; rep_tok = last; }
+        if (ent && fl == 0 && mem_last) {  // repeat group (R',0): repeat first, then parent appends (:522-543)
+          const double ec = (double)row[last];
+          double sc = s + ec, bst = sc;
+          if (pa >= 0 && !(fl_pa == 0 && last_pa == last)) {
+            double x = s_pa + ec;
+            sc = merge2(sc, x, MX);
+            if (x > bst) { bst = x; rep_src = pa; rep_tok = last; }
+          }
+          if (pb >= 0 && !(fl_pb == 0 && last_pb == last)) {
+            double x = s_pb + ec;
+            sc = merge2(sc, x, MX);
+            if (x > bst) { bst = x; rep_src = pb; rep_tok = last; }
+          }
+          c_rep = sc;
         }
-        c_rep = sc;
-      }
-      if (isfirst && mybit && mem_last && !(childx & mybit)) {  // (R+last(R),0) from (R,1) only (blocked repeat)
-        const int f1 = fl == 1 ? lane : ((p2 >= 0 && fl_p2 == 1) ? p2 : -1);
-        if (f1 >= 0) {
-          c_single = (f1 == lane ? s : s_p2) + (double)S.sval[mypos];
-          single_src = f1;
-        }
-      }
-      // local order: score desc; ties repeat (R,0) < blank (R,1) < single (R+c,0)
-      double q0 = c_rep, q1 = c_blank, q2 = c_single;
-      int k0 = 1, k1 = 0, k2 = 2;
-      if (q1 > q0) { double t = q0; q0 = q1; q1 = t; int x = k0; k0 = k1; k1 = x; }
-      if (q2 > q1) {
-        double t = q1; q1 = q2; q2 = t; int x = k1; k1 = k2; k2 = x;
-        if (q1 > q0) { t = q0; q0 = q1; q1 = t; x = k0; k0 = k1; k1 = x; }
-      }
-      const int kpack = k0 | (k1 << 2) | (k2 << 4);
+      };
+      if (!tokK) blank_repeat(true);
 
-      // ================= append lists (lanes 16..16+nD) =================
-      // first lanes publish (lane, A, valid positions) at their distinct index
-      const double A = isfirst ? (p2 >= 0 ? merge2(s, s_p2, MX) : s) : 0.0;
-      if (isfirst) {
-        const int d = __popc(firstmask & lanemask_lt());
-        S.dlane[d] = lane;
-        S.dA[d] = A;
-        S.dgv[d] = selk & ~(childx | mybit);
+      bool shortcut = false;
+      int Hn = 0;
+      if (sc_on) {
+        // U: bound of every append score this frame
+        const uint64_t ak = (isfirst && A > -INFINITY) ? ord64(A) : 0ull;
+        const uint32_t ahi = __reduce_max_sync(FULL, (uint32_t)(ak >> 32));
+        const uint32_t alo = __reduce_max_sync(FULL, (uint32_t)(ak >> 32) == ahi ? (uint32_t)ak : 0u);
+        const uint64_t ab = ((uint64_t)ahi << 32) | alo;
+        const double U = (ab == 0ull || !(vmax > -INFINITY)) ? -INFINITY : unord64(ab) + vmax;
+        const double Um = U + 1e-9 * (1.0 + fabs(U));  // appends are scored ~A + v: fp64 rounding margin
+        const bool above_b = lane < 16 && c_blank > Um, above_r = lane < 16 && c_rep > Um;
+        shortcut = __popc(__ballot_sync(FULL, above_b)) + __popc(__ballot_sync(FULL, above_r)) >= beam;
+        if (shortcut) {
+          // candidates: repeat group of entry e on lane e, blank group of
+          // entry e on lane 16 + e (both exact fp64); frame best among them
+          const double cb = __shfl_sync(FULL, c_blank, me), cr = c_rep;
+          const double mine = lane < 16 ? cr : cb;
+          const uint64_t o64 = (mine > -INFINITY && (lane < 16 ? lane < H : me < H)) ? ord64(mine) : 0ull;
+          const uint32_t bhi = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32));
+          const uint32_t blo = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32) == bhi ? (uint32_t)o64 : 0u);
+          const double sbest = unord64(((uint64_t)bhi << 32) | blo);
+          const double sbase = sbest - kR;
+          // merge record of each candidate: (entry lane | item << 8), item =
+          // the group's index in the entry's local order (repeat before
+          // blank on equal scores; no last-token append in this frame)
+          const int rf = __shfl_sync(FULL, (c_rep >= c_blank) ? 1 : 0, me);
+          S.slot_rec[lane] = lane < 16 ? (lane | ((rf ? 0 : 1) << 8)) : (me | ((rf ? 1 : 0) << 8));
+          uint32_t key = 0u;
+          if (o64) {
+            const uint32_t t = f2u_sat((mine - sbase) * kScale);
+            key = ((t > 1u ? t : 1u) & ~63u) | (uint32_t)(63 - lane);
+          }
+          key = sort_desc32(key, lane);
+          const uint32_t nxt = __shfl_down_sync(FULL, key, 1);
+          // not separated by a truncated unit, or near the threshold floor:
+          // the full path decides this frame
+          const bool bad = lane < beam && key != 0u &&
+                           ((nxt != 0u && (key >> 6) - (nxt >> 6) <= 1u) || key < 256u);
+          __syncwarp();
+          if (__any_sync(FULL, bad)) {
+            shortcut = false;
+            if (lane == 0) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
+          } else {
+            Hn = __popc(__ballot_sync(FULL, lane < beam && key != 0u));
+            if (lane < Hn) S.rec_i[lane] = S.slot_rec[63 - (int)(key & 63u)];
+          }
+          __syncwarp();
+        }
       }
-      __syncwarp();
-      const bool gen = lane >= 16 && me < nD;
-      const int gsrc = gen ? S.dlane[me] : lane;
-      const double gA = gen ? S.dA[me] : 0.0;
-      uint32_t gv = gen ? S.dgv[me] : 0u;
-      const int gf = gv ? __ffs(gv) - 1 : 0;  // first valid position of the list
+      // local order of an entry's groups: score desc; ties repeat (R,0) <
+      // blank (R,1) < single (R+c,0)
+      double q0, q1, q2;
+      int kpack;
+      auto local_order = [&]() {
+        q0 = c_rep; q1 = c_blank; q2 = c_single;
+        int k0 = 1, k1 = 0, k2 = 2;
+        if (q1 > q0) { double t = q0; q0 = q1; q1 = t; int x = k0; k0 = k1; k1 = x; }
+        if (q2 > q1) {
+          double t = q1; q1 = q2; q2 = t; int x = k1; k1 = k2; k2 = x;
+          if (q1 > q0) { t = q0; q0 = q1; q1 = t; x = k0; k0 = k1; k1 = x; }
+        }
+        kpack = k0 | (k1 << 2) | (k2 << 4);
+      };
+      int gsrc = lane;
+      if (shortcut) local_order();
+      if (!shortcut) {
+        if (sc_on && !PRE) full_topk();
+        // S positions of last tokens; flag-0 children exclude their token from
+        // the parent's append list (they become repeat groups)
+        const int mypos = (ent && last >= 0) ? (int)S.posmap[last] : 0xff;
+        const uint32_t mybit = mypos < 32 ? (1u << mypos) : 0u;
+        if (lane < 16) S.excl[lane] = 0u;
+        __syncwarp();
+        if (ent && fl == 0 && pa >= 0 && mybit) atomicOr(&S.excl[pa], mybit);
+        __syncwarp();
+        const uint32_t childx = lane < 16 ? S.excl[lane] : 0u;
+        // last(R) selected this frame (repeat groups and the last-token append need it)
+        const bool mem_last = !tokK || (ent && last >= 0 &&
+                                          (wide ? token_selected(ord32(row[last]), last, tv, ti) : mypos < mS));
+        if (tokK) blank_repeat(mem_last);
+        if (isfirst && mybit && mem_last && !(childx & mybit)) {  // (R+last(R),0) from (R,1) only (blocked repeat)
+          const int f1 = fl == 1 ? lane : ((p2 >= 0 && fl_p2 == 1) ? p2 : -1);
+          if (f1 >= 0) {
+            c_single = (f1 == lane ? s : s_p2) + (double)S.sval[mypos];
+            single_src = f1;
+          }
+        }
+        local_order();
+
+        // ================= append lists (lanes 16..16+nD) =================
+        // first lanes publish (lane, A, valid positions) at their distinct index
+        if (isfirst) {
+          const int d = __popc(firstmask & lanemask_lt());
+          S.dlane[d] = lane;
+          S.dA[d] = A;
+          S.dgv[d] = selk & ~(childx | mybit);
+        }
+        __syncwarp();
+        const bool gen = lane >= 16 && me < nD;
+        gsrc = gen ? S.dlane[me] : lane;
+        const double gA = gen ? S.dA[me] : 0.0;
+        uint32_t gv = gen ? S.dgv[me] : 0u;
+        const int gf = gv ? __ffs(gv) - 1 : 0;  // first valid position of the list
 
       // frame best (approximate append scores A + v; exact on key ties)
       const double hsc0 = lane < 16 ? q0 : (gv ? gA + (double)S.sval[gf] : -INFINITY);
@@ -868,7 +960,6 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // [1, 2^32 - 1] for a live list (A > -inf), 0 otherwise
       const long long gG = gv ? f2ll_floor((gA - kbase) * kScale) : 0ll;
       const uint32_t gLow = (gv && gA > -INFINITY) ? 1u : 0u;
-      int Hn = 0;
       // ---- one-shot selection (beam <= 10): when the distinct prefixes are
       // ordered by A with a margin, append (d, j) (j-th valid S position of
       // the d-th prefix) is beaten by the (d+1)(j+1)-1 appends (d' <= d,
@@ -1059,6 +1150,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         Hn = r + 1;
       }
       }  // !oneshot
+      }  // !shortcut
       __syncwarp();
       if (Hn == 0) { died = true; died_at = i; break; }
 
