@@ -18,6 +18,7 @@ __global__ void ctcb_decode_fast_pre_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_small_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_fast_pre_small_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_decode_pair_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_decode_block_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_framemap_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_topk_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_rowoff_kernel(const __grid_constant__ Params P);
@@ -167,6 +168,15 @@ bool use_pair(const ctcb_handle* h, const ctcb::Params& P, int B) {
   if (m && strcmp(m, "0") == 0) return false;
   if (m && strcmp(m, "1") == 0) return true;
   return false;  // opt-in while it is slower than the one-utterance-per-warp kernel
+}
+
+// One CTA per utterance for large beams (ctcb_block.cu): 16 < beam <= 128,
+// V <= 2048, full vocabulary, no LM / silence bonus.  CTCB_BLOCK=0 disables it.
+bool use_block(const ctcb_handle* h) {
+  if (h->beam <= ctcb::kFastBeam || h->beam > ctcb::kBlockMaxBeam || h->V > ctcb::kBlockMaxV) return false;
+  if (h->tok_k != 0 || h->force_generic || use_fused(h)) return false;
+  const char* m = getenv("CTCB_BLOCK");
+  return !(m && strcmp(m, "0") == 0);
 }
 
 struct WsLayout {
@@ -511,19 +521,25 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   CTCB_CUDA(cudaGetLastError());
   const bool pair = use_pair(h, P, B);
   const bool pre = fast && !pair && use_precomp(h, B);
+  const bool blk = use_block(h);
   if (pair) {  // 4 warps = 8 utterances per block, two halves' shared memory per warp
     P.smem_per_warp = (int)(2 * ctcb::make_pair_layout().total);
     P.warps_per_block = 4;
   }
-  size_t smem = (size_t)P.smem_per_warp * P.warps_per_block;
-  const void* kfn = pair ? (const void*)ctcb::ctcb_decode_pair_kernel
+  if (blk) {  // one 256-thread CTA per utterance
+    P.smem_per_warp = (int)ctcb::make_block_layout(P.beam, P.kpad, P.V, P.row_bytes).total;
+    P.warps_per_block = 8;
+  }
+  size_t smem = blk ? (size_t)P.smem_per_warp : (size_t)P.smem_per_warp * P.warps_per_block;
+  const void* kfn = blk ? (const void*)ctcb::ctcb_decode_block_kernel
+                    : pair ? (const void*)ctcb::ctcb_decode_pair_kernel
                     : fused ? ctcb::fused_kernel_fn()
                     : fast ? fast_kernel_fn(P, pre) : (const void*)ctcb::ctcb_decode_generic_kernel;
   CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks_per_sm = 0;
   CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kfn, 32 * P.warps_per_block, smem));
   if (blocks_per_sm < 1) blocks_per_sm = 1;
-  const int per_block = pair ? 2 * P.warps_per_block : P.warps_per_block;
+  const int per_block = blk ? 1 : (pair ? 2 * P.warps_per_block : P.warps_per_block);
   int need = (B + per_block - 1) / per_block;
   int grid = h->num_sms * blocks_per_sm;
   if (grid > need) grid = need;
@@ -553,7 +569,12 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   }
   const bool timed = h->timing && h->n_timed < 64;
   if (timed) CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed], s));
-  if (pair) {
+  if (blk) {
+    void* args[] = {(void*)&P};
+    CTCB_CUDA(cudaLaunchKernel((const void*)ctcb::ctcb_decode_block_kernel, dim3(grid), dim3(256), args, smem, s));
+    h->last_kernel = "ctcb_decode_block_kernel";
+    h->launches++;
+  } else if (pair) {
     void* args[] = {(void*)&P};
     CTCB_CUDA(cudaLaunchKernel((const void*)ctcb::ctcb_decode_pair_kernel, dim3(grid), dim3(32 * P.warps_per_block),
                                args, smem, s));

@@ -1,0 +1,951 @@
+// Large-beam decode kernel (16 < beam <= 128, V <= 2048, full vocabulary, no
+// LM): one 256-thread CTA per utterance.  Same semantics as the generic
+// one-warp kernel (ctcb_generic.cu) and the reference (ctcforge
+// decoder.py:102-817); every stage of a frame step runs on the whole block:
+//
+//   * top-k (k = min(2 beam, V-1)): 8-bit radix select with a block histogram,
+//     index-ordered compaction, block bitonic sort of (value desc, index asc);
+//   * merge structure: prefix groups and parent links through a shared-memory
+//     hash table keyed by (prefix hash, length) (decoder.py:595-613);
+//   * special groups (blank, repeat, last-token append) exact in fp64;
+//   * selection WITHOUT a sequential k-way merge: the append (d, j) -- the j-th
+//     valid top-k position of prefix d -- is preceded by its own list's first
+//     j positions and, for every prefix d' whose A = logaddexp of its entries
+//     exceeds A_d by a margin, by >= j candidates of d' (its appends at the
+//     same or better positions, or the repeat groups that replace excluded
+//     ones; at most one position per prefix, its last token, is lost).  So
+//     (d, j) can enter the beam only if (d_eff + 1) j < beam, d_eff = number of
+//     such prefixes.  Those appends plus all specials get 64-bit keys (32-bit
+//     fixed-point score | candidate id) and one block sort ranks them; runs of
+//     keys within the rounding tolerance around ranks [0, beam] are re-ordered
+//     exactly (fp64 fold, then token sequence, then flag: decoder.py:651-681)
+//     and the beam threshold is applied on exact scores (:615-626).
+#include <cfloat>
+#include <cmath>
+
+#include "ctcb_common.cuh"
+#include "ctcb_internal.h"
+#include <cstdio>
+#ifdef CTCB_BLOCK_CHECK
+#define BCHK(c)                                                                                    \
+  do {                                                                                             \
+    if (!(c)) { printf("ctcb_block check failed: %s (line %d, block %d, thread %d)\n", #c, __LINE__, blockIdx.x, threadIdx.x); __trap(); } \
+  } while (0)
+#else
+#define BCHK(c) do { } while (0)
+#endif
+
+namespace ctcb {
+
+namespace {
+
+constexpr int NT = 256;          // threads per CTA (one utterance)
+constexpr int kTolB = 2;         // rank-key tolerance (fixed-point units)
+constexpr uint32_t kSpecial = 0x80000000u;
+
+struct Blk {
+  const Params* P;
+  int tid, u, steps_done;
+  uint8_t* rows;
+  uint64_t* mbar;
+  double *cs, *ns, *lA, *spsc;
+  uint64_t *ch, *cph, *nh, *nph, *skey, *ckey, *htk, *tc_h;
+  int *cl, *cn, *cf, *nl, *nn, *nf, *htf, *hslot, *first, *dpi, *pd, *e1, *e2, *qoff;
+  int *spbase, *spx, *spflag, *spsrc, *sptok, *misc, *tc_r, *rec, *ord, *runbuf;
+  uint32_t *ntrel, *excl, *hist, *crec;
+  float* sval;
+  int* stok;
+  uint16_t* pos;
+  int kw, kpad, ts, ncap;
+
+  __device__ void swap_state() {
+    double* d = cs; cs = ns; ns = d;
+    uint64_t* h = ch; ch = nh; nh = h;
+    h = cph; cph = nph; nph = h;
+    int* x = cl; cl = nl; nl = x;
+    x = cn; cn = nn; nn = x;
+    x = cf; cf = nf; nf = x;
+  }
+};
+
+__device__ void carve(Blk& w, uint8_t* base, const Params& P) {
+  const BlockLayout L = make_block_layout(P.beam, P.kpad, P.V, P.row_bytes);
+  w.rows = base + L.rows;
+  w.mbar = (uint64_t*)(base + L.mbar);
+  w.cs = (double*)(base + L.cs); w.ns = (double*)(base + L.ns);
+  w.lA = (double*)(base + L.lA); w.spsc = (double*)(base + L.spsc);
+  w.ch = (uint64_t*)(base + L.ch); w.cph = (uint64_t*)(base + L.cph);
+  w.nh = (uint64_t*)(base + L.nh); w.nph = (uint64_t*)(base + L.nph);
+  w.skey = (uint64_t*)(base + L.skey); w.ckey = (uint64_t*)(base + L.ckey);
+  w.htk = (uint64_t*)(base + L.htk); w.tc_h = (uint64_t*)(base + L.tc_h);
+  w.cl = (int*)(base + L.cl); w.cn = (int*)(base + L.cn); w.cf = (int*)(base + L.cf);
+  w.nl = (int*)(base + L.nl); w.nn = (int*)(base + L.nn); w.nf = (int*)(base + L.nf);
+  w.htf = (int*)(base + L.htf); w.hslot = (int*)(base + L.hslot); w.first = (int*)(base + L.first);
+  w.dpi = (int*)(base + L.dpi); w.pd = (int*)(base + L.pd); w.e1 = (int*)(base + L.e1);
+  w.e2 = (int*)(base + L.e2); w.qoff = (int*)(base + L.qoff);
+  w.spbase = (int*)(base + L.spbase); w.spx = (int*)(base + L.spx); w.spflag = (int*)(base + L.spflag);
+  w.spsrc = (int*)(base + L.spsrc); w.sptok = (int*)(base + L.sptok); w.misc = (int*)(base + L.misc);
+  w.tc_r = (int*)(base + L.tc_r); w.rec = (int*)(base + L.rec); w.ord = (int*)(base + L.ord); w.runbuf = (int*)(base + L.runbuf);
+  w.ntrel = (uint32_t*)(base + L.ntrel); w.excl = (uint32_t*)(base + L.excl);
+  w.hist = (uint32_t*)(base + L.hist); w.crec = (uint32_t*)(base + L.crec);
+  w.sval = (float*)(base + L.sval); w.stok = (int*)(base + L.stok); w.pos = (uint16_t*)(base + L.pos);
+  w.kw = L.kw; w.kpad = L.kpad; w.ts = L.ts; w.ncap = L.ncap;
+}
+
+// ------------------------------------------------------------------ block helpers
+__device__ __forceinline__ void bsync() { __syncthreads(); }
+
+// Block bitonic sort of n (power of two, >= 2) u64 keys, descending.
+__device__ void block_sort_desc(uint64_t* key, int n, int tid) {
+  for (int size = 2; size <= n; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = tid; t < (n >> 1); t += NT) {
+        const int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
+        const int j = i + stride;
+        const uint64_t a = key[i], b = key[j];
+        const bool desc = (i & size) == 0;
+        if (desc ? (a < b) : (a > b)) { key[i] = b; key[j] = a; }
+      }
+      bsync();
+    }
+}
+
+// Exclusive block scan of one int per thread (NT = 256).
+__device__ int block_excl_scan(int v, int tid, int* tmp, int* total) {
+  const int lane = tid & 31, wid = tid >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) tmp[wid] = incl;
+  bsync();
+  if (wid == 0) {
+    const int t = lane < NT / 32 ? tmp[lane] : 0;
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane < NT / 32) tmp[lane] = x - t;
+    if (lane == NT / 32 - 1) tmp[NT / 32] = x;
+  }
+  bsync();
+  const int r = tmp[wid] + incl - v;
+  *total = tmp[NT / 32];
+  bsync();
+  return r;
+}
+
+// Largest 32-bit value T with #{x >= T} >= need among hi32(key[0..n)) (keys
+// of 0 never count): 8-bit radix select with a block histogram (hist: 256
+// words, misc: 2 words of scratch).  need <= #nonzero, else returns 0.
+__device__ uint32_t block_select_hi(const uint64_t* key, int n, int need, int tid, uint32_t* hist, int* misc) {
+  uint32_t prefix = 0, pmask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = tid; b < 256; b += NT) hist[b] = 0;
+    bsync();
+    for (int c = tid; c < n; c += NT) {
+      const uint32_t x = (uint32_t)(key[c] >> 32);
+      if (x && (x & pmask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1u);
+    }
+    bsync();
+    if (tid < 32) {
+      const int lane = tid;
+      uint32_t h[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) { h[q] = hist[lane * 8 + q]; sum += h[q]; }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_down_sync(FULL, incl, off);
+        if (lane + off < 32) incl += v;
+      }
+      uint32_t cum = incl - sum;
+      int found = -1;
+      uint32_t cgt = 0;
+#pragma unroll
+      for (int q = 7; q >= 0; q--) {
+        if (found < 0 && cum < (uint32_t)need && cum + h[q] >= (uint32_t)need) { found = lane * 8 + q; cgt = cum; }
+        cum += h[q];
+      }
+      const unsigned bal = __ballot_sync(FULL, found >= 0);
+      const int src = bal ? __ffs(bal) - 1 : 0;
+      const int digit = __shfl_sync(FULL, found, src);
+      cgt = __shfl_sync(FULL, cgt, src);
+      if (lane == 0) { misc[0] = bal ? digit : -1; misc[1] = (int)cgt; }
+    }
+    bsync();
+    const int digit = misc[0];
+    if (digit < 0) { bsync(); return 0u; }
+    need -= misc[1];
+    prefix |= (uint32_t)digit << shift;
+    pmask |= 0xffu << shift;
+    bsync();
+  }
+  return prefix;
+}
+
+// ------------------------------------------------------------------ token sequences (single-thread slow path)
+__device__ int bmaterialize(const Blk& w, int e, int len, int* buf) {
+  const Params& P = *w.P;
+  int pos = len, slot = e;
+  for (int i = w.steps_done - 1; i >= 0 && pos > 0; --i) {
+    const uint32_t r = P.trellis[((size_t)w.u * P.T_max + i) * P.beam + slot];
+    const int tok = trel_tok(r);
+    if (tok >= 0) buf[--pos] = tok;
+    slot = trel_src(r);
+  }
+  return len;
+}
+__device__ int bseq_cmp_full(const Blk& w, int ea, int xa, int eb, int xb, bool* strict) {
+  const Params& P = *w.P;
+  atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
+  atomicAdd(&P.dbg[kDbgMatSteps], 2ull * (unsigned long long)w.steps_done);
+  int* A = P.seqbuf + (size_t)w.u * 3 * (P.T_max + 1);
+  int* Bq = A + P.T_max + 1;
+  int la = bmaterialize(w, ea, w.cn[ea], A);
+  if (xa >= 0) A[la++] = xa;
+  int lb = bmaterialize(w, eb, w.cn[eb], Bq);
+  if (xb >= 0) Bq[lb++] = xb;
+  const int n = la < lb ? la : lb;
+  *strict = true;
+  for (int i = 0; i < n; i++)
+    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
+  *strict = false;
+  return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+__device__ int btc_lookup(const Blk& w, uint64_t ha, uint64_t hb) {
+#pragma unroll 1
+  for (int i = 0; i < kTieCache; i++) {
+    if (w.tc_h[2 * i] == ha && w.tc_h[2 * i + 1] == hb) return w.tc_r[i];
+    if (w.tc_h[2 * i] == hb && w.tc_h[2 * i + 1] == ha) return -w.tc_r[i];
+  }
+  return 0;
+}
+__device__ void btc_insert(const Blk& w, uint64_t ha, uint64_t hb, int r) {
+  if (btc_lookup(w, ha, hb)) return;
+  const int i = w.tc_r[kTieCache];
+  w.tc_h[2 * i] = ha;
+  w.tc_h[2 * i + 1] = hb;
+  w.tc_r[i] = r;
+  w.tc_r[kTieCache] = (i + 1) % kTieCache;
+}
+// Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token).
+__device__ int bseq_cmp(const Blk& w, int ea, int xa, int eb, int xb) {
+  const uint64_t hba = w.ch[ea], hbb = w.ch[eb];
+  const int lba = w.cn[ea], lbb = w.cn[eb];
+  if (hba == hbb && lba == lbb) {
+    if (xa == xb) return 0;
+    return xa < xb ? -1 : 1;
+  }
+  const uint64_t ha = xa >= 0 ? child_hash(hba, xa) : hba, hb = xb >= 0 ? child_hash(hbb, xb) : hbb;
+  const int la = lba + (xa >= 0), lb = lbb + (xb >= 0);
+  if (ha == hb && la == lb) return 0;
+  int r = btc_lookup(w, hba, hbb);
+  if (r) {
+    btc_insert(w, ha, hb, r);
+    return r;
+  }
+  r = btc_lookup(w, ha, hb);
+  if (r) return r;
+  bool strict = false;
+  r = bseq_cmp_full(w, ea, -1, eb, -1, &strict);
+  if (strict) {
+    btc_insert(w, hba, hbb, r);
+    btc_insert(w, ha, hb, r);
+    return r;
+  }
+  r = bseq_cmp_full(w, ea, xa, eb, xb, &strict);
+  if (strict) btc_insert(w, ha, hb, r);
+  return r;
+}
+struct BDesc { double sc; int base, x, flag; };
+__device__ bool bprecedes(const Blk& w, const BDesc& a, const BDesc& b) {
+  if (a.sc != b.sc) return a.sc > b.sc;
+  atomicAdd(&w.P->dbg[kDbgExactTies], 1ull);
+  const int c = bseq_cmp(w, a.base, a.x, b.base, b.x);
+  if (c) return c < 0;
+  return a.flag < b.flag;
+}
+
+// ------------------------------------------------------------------ top-k
+// S = the k best non-blank tokens of `row` by (value desc, index asc), sorted
+// into sval / stok; pos[token] = rank in S.
+__device__ void btopk(Blk& w, const float* row) {
+  const Params& P = *w.P;
+  const int V = P.V, blank = P.blank, k = P.k, tid = w.tid;
+  uint32_t kth = 0;
+  int need = V;
+  if (k < V - 1) {
+    uint32_t prefix = 0, pmask = 0;
+    need = k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int b = tid; b < 256; b += NT) w.hist[b] = 0;
+      bsync();
+      for (int c = tid; c < V; c += NT) {
+        if (c == blank) continue;
+        const uint32_t key = ord32(row[c]);
+        if ((key & pmask) == prefix) atomicAdd(&w.hist[(key >> shift) & 255u], 1u);
+      }
+      bsync();
+      if (tid < 32) {  // digit holding the need-th largest key
+        const int lane = tid;
+        uint32_t h[8], s = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) { h[q] = w.hist[lane * 8 + q]; s += h[q]; }
+        uint32_t incl = s;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t v = __shfl_down_sync(FULL, incl, off);
+          if (lane + off < 32) incl += v;
+        }
+        uint32_t cum = incl - s;
+        int found = -1;
+        uint32_t cgt = 0;
+#pragma unroll
+        for (int q = 7; q >= 0; q--) {
+          if (found < 0 && cum < (uint32_t)need && cum + h[q] >= (uint32_t)need) { found = lane * 8 + q; cgt = cum; }
+          cum += h[q];
+        }
+        const unsigned bal = __ballot_sync(FULL, found >= 0);
+        const int src = __ffs(bal) - 1;
+        const int digit = __shfl_sync(FULL, found, src);
+        cgt = __shfl_sync(FULL, cgt, src);
+        if (lane == 0) { w.misc[4] = digit; w.misc[5] = (int)cgt; }
+      }
+      bsync();
+      need -= w.misc[5];
+      prefix |= (uint32_t)w.misc[4] << shift;
+      pmask |= 0xffu << shift;
+      bsync();
+    }
+    kth = prefix;
+  }
+  // ordered compaction: keys > kth, then the `need` lowest-index keys == kth;
+  // thread t owns tokens [t*cpt, (t+1)*cpt)
+  const int cpt = (V + NT - 1) / NT;
+  int ngt = 0, neq = 0;
+  for (int q = 0; q < cpt; q++) {
+    const int c = tid * cpt + q;
+    if (c >= V || c == blank) continue;
+    const uint32_t key = ord32(row[c]);
+    ngt += key > kth;
+    neq += key == kth;
+  }
+  int tot_eq = 0, tot = 0;
+  const int eq_before = block_excl_scan(neq, tid, w.qoff, &tot_eq);
+  int eq_take = need - eq_before;
+  eq_take = eq_take < 0 ? 0 : (eq_take > neq ? neq : eq_take);
+  const int off = block_excl_scan(ngt + eq_take, tid, w.qoff, &tot);
+  int o = off, taken = 0;
+  for (int q = 0; q < cpt; q++) {
+    const int c = tid * cpt + q;
+    if (c >= V || c == blank) continue;
+    const uint32_t key = ord32(row[c]);
+    const bool acc = key > kth || (key == kth && taken++ < eq_take);
+    if (acc) w.skey[o++] = ((uint64_t)key << 32) | (uint64_t)(0xffffffffu - (uint32_t)c);
+  }
+  for (int j = tot + tid; j < w.kpad; j += NT) w.skey[j] = 0ull;
+  bsync();
+  block_sort_desc(w.skey, w.kpad, tid);
+  for (int j = tid; j < k; j += NT) {
+    const int c = (int)(0xffffffffu - (uint32_t)(w.skey[j] & 0xffffffffu));
+    w.stok[j] = c;
+    w.sval[j] = row[c];
+    w.pos[c] = (uint16_t)j;
+  }
+  bsync();
+}
+
+__device__ __forceinline__ bool bexcl(const Blk& w, int d, int j) {
+  return (w.excl[d * w.kw + (j >> 5)] >> (j & 31)) & 1u;
+}
+// j-th valid (non-excluded) top-k position of list d, or k
+__device__ int jth_valid(const Blk& w, int d, int j, int k) {
+  const uint32_t* ex = w.excl + d * w.kw;
+  for (int wd = 0; wd < w.kw; wd++) {
+    const int lo = wd * 32;
+    if (lo >= k) break;
+    const int nbits = k - lo < 32 ? k - lo : 32;
+    const uint32_t live = ~ex[wd] & (nbits == 32 ? 0xffffffffu : ((1u << nbits) - 1u));
+    const int c = __popc(live);
+    if (j < c) {
+      uint32_t m = live;
+      for (int q = 0; q < j; q++) m &= m - 1u;
+      return lo + __ffs(m) - 1;
+    }
+    j -= c;
+  }
+  return k;
+}
+__device__ __forceinline__ double bgen_score(const Blk& w, int d, int j) {
+  const double v = (double)w.sval[j];
+  const int a = w.e1[d], b = w.e2[d];
+  double s = w.cs[a] + v;
+  if (b >= 0) s = merge2_exact(s, w.cs[b] + v, w.P->merge_max != 0);
+  return s;
+}
+__device__ BDesc cand_desc(const Blk& w, uint32_t rec) {
+  if (rec & kSpecial) {
+    const int s = (int)(rec & ~kSpecial);
+    return BDesc{w.spsc[s], w.spbase[s], w.spx[s], w.spflag[s]};
+  }
+  const int d = (int)(rec >> 12), j = (int)(rec & 0xfff);
+  return BDesc{bgen_score(w, d, j), w.e1[d], w.stok[j], 0};
+}
+
+// One frame step; returns the new beam size (0: beam died).
+__device__ int bstep(Blk& w, const float* row, int H) {
+  const Params& P = *w.P;
+  const int tid = w.tid, beam = P.beam, k = P.k;
+  const bool MX = P.merge_max != 0;
+  const double eb = (double)row[P.blank];
+
+  // -- prefix groups (flag 0 / flag 1 entries of one token sequence)
+  const int TS = w.ts;
+  for (int i = tid; i < TS; i += NT) { w.htk[i] = 0ull; w.htf[i] = 0x7fffffff; }
+  if (tid == 0) { w.misc[0] = 0; w.misc[1] = 0; }
+  bsync();
+  for (int e = tid; e < H; e += NT) {
+    const uint64_t key = (w.ch[e] ^ ((uint64_t)w.cn[e] * 0x9e3779b97f4a7c15ull)) | 1ull;
+    uint32_t i = (uint32_t)mix64(key) & (uint32_t)(TS - 1);
+    for (;;) {
+      const unsigned long long prev = atomicCAS((unsigned long long*)&w.htk[i], 0ull, (unsigned long long)key);
+      if (prev == 0ull || prev == key) break;
+      i = (i + 1) & (uint32_t)(TS - 1);
+    }
+    atomicMin(&w.htf[i], e);
+    w.hslot[e] = (int)i;
+  }
+  bsync();
+  for (int e = tid; e < H; e += NT) w.first[e] = w.htf[w.hslot[e]];
+  bsync();
+  // distinct prefixes numbered in entry order (d = rank of its first entry)
+  int nD = 0;
+  {
+    const bool isf = tid < H && w.first[tid] == tid;
+    int tot = 0;
+    const int d = block_excl_scan(isf ? 1 : 0, tid, w.qoff, &tot);
+    nD = tot;
+    if (isf) { w.dpi[tid] = d; w.e1[d] = tid; w.e2[d] = -1; }
+  }
+  bsync();
+  for (int e = tid; e < H; e += NT)
+    if (w.first[e] != e) { const int d = w.dpi[w.first[e]]; w.dpi[e] = d; w.e2[d] = e; }
+  for (int i = tid; i < nD * w.kw; i += NT) w.excl[i] = 0u;
+  bsync();
+  // -- parent links of flag-0 entries; children exclude their token from the
+  //    parent's list (they become repeat groups)
+  for (int e = tid; e < H; e += NT) {
+    int p = -1;
+    if (w.cf[e] == 0) {
+      const uint64_t key = (w.cph[e] ^ ((uint64_t)(w.cn[e] - 1) * 0x9e3779b97f4a7c15ull)) | 1ull;
+      uint32_t i = (uint32_t)mix64(key) & (uint32_t)(TS - 1);
+      for (;;) {
+        const uint64_t k2 = w.htk[i];
+        if (k2 == 0ull) break;
+        if (k2 == key) { p = w.dpi[w.htf[i]]; break; }
+        i = (i + 1) & (uint32_t)(TS - 1);
+      }
+      if (p >= 0) {
+        const int j = w.pos[w.cl[e]];
+        if (j != 0xffff) atomicOr(&w.excl[p * w.kw + (j >> 5)], 1u << (j & 31));
+      }
+    }
+    w.pd[e] = p;
+  }
+  bsync();
+  // -- specials: blank groups, last-token appends (per prefix), repeat groups (per flag-0 entry)
+  for (int d = tid; d < nD; d += NT) {
+    const int a = w.e1[d], b = w.e2[d];
+    double sc = w.cs[a] + eb;
+    if (b >= 0) sc = merge2_exact(sc, w.cs[b] + eb, MX);
+    int s = atomicAdd(&w.misc[0], 1);
+    BCHK(s < 3 * beam);
+    w.spsc[s] = sc; w.spbase[s] = a; w.spx[s] = -1; w.spflag[s] = 1; w.spsrc[s] = a; w.sptok[s] = -1;
+    const int c = w.cl[a];
+    if (c >= 0) {
+      const int j = w.pos[c];
+      if (j != 0xffff && !bexcl(w, d, j)) {
+        const int f = w.cf[a] == 1 ? a : ((b >= 0 && w.cf[b] == 1) ? b : -1);
+        if (f >= 0) {
+          s = atomicAdd(&w.misc[0], 1);
+          w.spsc[s] = w.cs[f] + (double)w.sval[j];
+          w.spbase[s] = a; w.spx[s] = c; w.spflag[s] = 0; w.spsrc[s] = f; w.sptok[s] = c;
+        }
+        atomicOr(&w.excl[d * w.kw + (j >> 5)], 1u << (j & 31));
+      }
+    }
+    // A = logaddexp of the prefix's entries (list base)
+    w.lA[d] = b >= 0 ? merge2_exact(w.cs[a], w.cs[b], MX) : w.cs[a];
+  }
+  for (int e = tid; e < H; e += NT) {
+    if (w.cf[e] != 0) continue;
+    const int c = w.cl[e];
+    BCHK(c >= 0 && c < P.V);
+    const double ec = (double)row[c];
+    double sc = w.cs[e] + ec, best = sc;  // repeat candidate first (decoder.py:522-530)
+    int src = e, tok = -1;
+    const int p = w.pd[e];
+    if (p >= 0) {
+      const int srcs[2] = {w.e1[p], w.e2[p]};
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int h = srcs[q];
+        if (h < 0 || (w.cf[h] == 0 && w.cl[h] == c)) continue;  // blocked repeat (decoder.py:495)
+        const double x = w.cs[h] + ec;
+        sc = merge2_exact(sc, x, MX);
+        if (x > best) { best = x; src = h; tok = c; }
+      }
+    }
+    const int s = atomicAdd(&w.misc[0], 1);
+    BCHK(s < 3 * beam);
+    w.spsc[s] = sc; w.spbase[s] = e; w.spx[s] = -1; w.spflag[s] = 0; w.spsrc[s] = src; w.sptok[s] = tok;
+  }
+  bsync();
+  const int nS = w.misc[0];
+
+  // -- append quotas: d_eff = prefixes whose A exceeds A_d by a margin;
+  //    (d, j) can reach the beam only if (d_eff + 1) j < beam
+  int q = 0;
+  if (tid < nD) {
+    const double Ad = w.lA[tid];
+    int deff = 0;
+    if (Ad > -INFINITY) {
+      const double thr = Ad + 1e-9 * (1.0 + fabs(Ad));
+      for (int d2 = 0; d2 < nD; d2++) deff += w.lA[d2] > thr;
+      q = (beam - 1) / (deff + 1) + 1;
+    }
+  }
+  int nA = 0;
+  const int qo = block_excl_scan(q, tid, w.rec, &nA);
+  if (tid < nD) { w.qoff[tid] = qo; }
+  if (tid == 0) w.qoff[nD] = nA;
+  bsync();
+  const int N = nS + nA;
+  int ncap = 2;
+  while (ncap < N) ncap <<= 1;
+
+  // -- frame best on approximate scores (specials exact, list heads A + v)
+  double lb = -INFINITY;
+  for (int s = tid; s < nS; s += NT) lb = fmax(lb, w.spsc[s]);
+  for (int d = tid; d < nD; d += NT) {
+    const int j0 = jth_valid(w, d, 0, k);
+    if (j0 < k) lb = fmax(lb, w.lA[d] + (double)w.sval[j0]);
+  }
+  {
+    const uint64_t o64 = lb > -INFINITY ? ord64(lb) : 0ull;
+    const uint32_t hi = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32));
+    const uint32_t lo = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32) == hi ? (uint32_t)o64 : 0u);
+    if ((tid & 31) == 0) w.ckey[tid >> 5] = ((uint64_t)hi << 32) | lo;  // scratch before the fill
+  }
+  bsync();
+  uint64_t bk = 0ull;
+  for (int i = 0; i < NT / 32; i++) bk = bk > w.ckey[i] ? bk : w.ckey[i];
+  bsync();
+  if (bk == 0ull) return 0;  // every extension is -inf (decoder.py:616-620)
+
+  if (tid == 0) w.misc[10] = ncap > w.ncap ? 1 : 0;
+  bsync();
+  if (!w.misc[10]) {
+    const double best_a = __longlong_as_double((long long)((bk >> 63) ? (bk & 0x7fffffffffffffffull) : ~bk));
+    const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
+    const double kScale = 4294967294.0 / kR, koff = -(best_a - kR) * kScale;
+    auto keyof = [&](double sc) -> uint32_t {
+      if (!(sc > -INFINITY)) return 0u;
+      const double z = fmin(fmax(fma(sc, kScale, koff), 0.0), 4294967294.0);
+      return 1u + (uint32_t)z;
+    };
+    // -- candidate keys: (fixed-point score | candidate id); id -> record in crec
+    for (int c = tid; c < ncap; c += NT) {
+      uint64_t key = 0ull;
+      if (c < nS) {
+        const uint32_t kk = keyof(w.spsc[c]);
+        w.crec[c] = kSpecial | (uint32_t)c;
+        key = kk ? (((uint64_t)kk << 32) | (uint64_t)(0xffffffffu - (uint32_t)c)) : 0ull;
+      } else if (c < N) {
+        const int g = c - nS;
+        int lo = 0, hi = nD - 1;  // list of append slot g: last d with qoff[d] <= g
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (w.qoff[mid] <= g) lo = mid; else hi = mid - 1;
+        }
+        const int d = lo, j = g - w.qoff[d];
+        BCHK(d >= 0 && d < nD && j >= 0);
+        const int p = jth_valid(w, d, j, k);
+        if (p < k && w.lA[d] > -INFINITY) {
+          const uint32_t kk = keyof(w.lA[d] + (double)w.sval[p]);
+          w.crec[c] = ((uint32_t)d << 12) | (uint32_t)p;
+          key = kk ? (((uint64_t)kk << 32) | (uint64_t)(0xffffffffu - (uint32_t)c)) : 0ull;
+        }
+      }
+      w.ckey[c] = key;
+    }
+    bsync();
+    // -- keep the candidates within a margin of the beam-th key (radix
+    //    select) and sort only those; a near-tie run that could reach past
+    //    the margin sends the frame to the full sort
+    int live = 0;
+    for (int c = tid; c < ncap; c += NT) live += w.ckey[c] != 0ull;
+    int nlive = 0;
+    (void)block_excl_scan(live, tid, w.rec, &nlive);
+    uint64_t* sk = w.ckey;
+    int nsk = ncap;
+    bool trunc = false;
+    if (nlive > beam + 1) {
+      const uint32_t T = block_select_hi(w.ckey, ncap, beam + 1, tid, w.hist, w.misc + 6);
+      const uint32_t lim = T > 64u ? T - 64u : 1u;
+      int keep = 0;
+      for (int c = tid; c < ncap; c += NT) keep += (uint32_t)(w.ckey[c] >> 32) >= lim;
+      int nk = 0;
+      int o = block_excl_scan(keep, tid, w.rec, &nk);
+      uint64_t* dst = (uint64_t*)w.ord;  // kBlockCands ints = kBlockCands / 2 keys
+      if (nk <= w.ncap / 2 && nk < nlive) {
+        for (int c = tid; c < ncap; c += NT) {
+          const uint64_t x = w.ckey[c];
+          if ((uint32_t)(x >> 32) >= lim) dst[o++] = x;
+        }
+        int np = 2;
+        while (np < nk) np <<= 1;
+        for (int c = nk + tid; c < np; c += NT) dst[c] = 0ull;
+        bsync();
+        sk = dst;
+        nsk = np;
+        trunc = true;
+      }
+    }
+    block_sort_desc(sk, nsk, tid);
+    // -- exact order where keys are within the tolerance: runs of adjacent
+    //    keys (differences <= kTolB) in ranks [0, beam] are re-sorted on exact
+    //    descriptors (fp64 fold, token sequence, flag)
+    for (int attempt = 0; attempt < 2; attempt++) {
+      bool tie = false;
+      for (int r = tid; r < beam && r + 1 < nsk; r += NT) {
+        const uint64_t x = sk[r], y = sk[r + 1];
+        tie |= x != 0ull && y != 0ull && (uint32_t)(x >> 32) - (uint32_t)(y >> 32) <= (uint32_t)kTolB;
+      }
+      const int anytie = __syncthreads_or(tie ? 1 : 0);
+      for (int r = tid; r < beam; r += NT) {
+        const uint64_t x = r < nsk ? sk[r] : 0ull;
+        w.rec[r] = x ? (int)w.crec[0xffffffffu - (uint32_t)(x & 0xffffffffu)] : -1;
+      }
+      if (tid == 0) w.misc[9] = 0;
+      bsync();
+      if (anytie) {
+        if (tid == 0) {
+          atomicAdd(&P.dbg[kDbgTies], 1ull);
+          int end = beam < nsk ? beam : nsk;  // extend over keys within the tolerance of the cut
+          while (end > 0 && sk[end - 1] == 0ull) end--;  // fewer live candidates than beam
+          while (end < nsk && sk[end] != 0ull &&
+                 (uint32_t)(sk[end - 1] >> 32) - (uint32_t)(sk[end] >> 32) <= (uint32_t)kTolB)
+            end++;
+          if (trunc && (end >= nsk || sk[end] == 0ull)) {
+            w.misc[9] = 1;  // the run may continue below the margin
+          } else {
+            // exact insertion sort of each run; the run buffer is the tail of
+            // the candidate records (crec[ncap ..) is free)
+            int* run = w.runbuf;
+            const int cap = kBlockRun;
+            int a0 = 0;
+            while (a0 < end) {
+              int b0 = a0 + 1;
+              while (b0 < end && (uint32_t)(sk[b0 - 1] >> 32) - (uint32_t)(sk[b0] >> 32) <= (uint32_t)kTolB) b0++;
+              if (b0 - a0 > cap) { w.misc[10] = 1; break; }  // absurd tie run: exact serial path
+              if (b0 - a0 > 1) {
+                const int len = b0 - a0;
+                for (int i = 0; i < len; i++) run[i] = (int)w.crec[0xffffffffu - (uint32_t)(sk[a0 + i] & 0xffffffffu)];
+                for (int i = 1; i < len; i++) {
+                  const int x = run[i];
+                  const BDesc dx = cand_desc(w, (uint32_t)x);
+                  int j = i;
+                  while (j > 0 && bprecedes(w, dx, cand_desc(w, (uint32_t)run[j - 1]))) { run[j] = run[j - 1]; j--; }
+                  run[j] = x;
+                }
+                for (int i = 0; i < len && a0 + i < beam; i++) w.rec[a0 + i] = run[i];
+              }
+              a0 = b0;
+            }
+          }
+        }
+        bsync();
+      }
+      if (!w.misc[9]) break;
+      // redo with every candidate (rare): full sort of the candidate keys
+      bsync();
+      block_sort_desc(w.ckey, ncap, tid);
+      sk = w.ckey;
+      nsk = ncap;
+      trunc = false;
+    }
+  }
+  if (w.misc[10]) {
+    // exactly tied prefixes can exceed the candidate buffer (d_eff counts
+    // strictly better prefixes only): exact serial selection for this frame
+    if (tid == 0) {
+      atomicAdd(&P.dbg[kDbgFrames], 1ull);
+      int* head = w.dpi;  // per list: next valid position (dpi is free after grouping)
+      for (int d = 0; d < nD; d++) head[d] = jth_valid(w, d, 0, k);
+      int* sord = w.ord;  // specials in exact order
+      for (int i = 0; i < nS; i++) {
+        int j = i;
+        const BDesc di{w.spsc[i], w.spbase[i], w.spx[i], w.spflag[i]};
+        while (j > 0) {
+          const int y = sord[j - 1];
+          if (!bprecedes(w, di, BDesc{w.spsc[y], w.spbase[y], w.spx[y], w.spflag[y]})) break;
+          sord[j] = y;
+          j--;
+        }
+        sord[j] = i;
+      }
+      int sp = 0;
+      for (int r = 0; r < beam; r++) {
+        int wd = -2;  // -1: special, >= 0: list
+        BDesc best{};
+        if (sp < nS) { const int x = sord[sp]; best = BDesc{w.spsc[x], w.spbase[x], w.spx[x], w.spflag[x]}; wd = -1; }
+        for (int d = 0; d < nD; d++) {
+          if (head[d] >= k || !(w.lA[d] > -INFINITY)) continue;
+          const BDesc dd{bgen_score(w, d, head[d]), w.e1[d], w.stok[head[d]], 0};
+          if (wd == -2 || bprecedes(w, dd, best)) { best = dd; wd = d; }
+        }
+        if (wd == -2 || !(best.sc > -INFINITY)) { w.rec[r] = -1; continue; }
+        if (wd == -1) {
+          w.rec[r] = (int)(kSpecial | (uint32_t)sord[sp]);
+          sp++;
+        } else {
+          w.rec[r] = (wd << 12) | head[wd];
+          int nx = head[wd] + 1;
+          while (nx < k && bexcl(w, wd, nx)) nx++;
+          head[wd] = nx;
+        }
+      }
+    }
+    bsync();
+  }
+  // -- new entries (exact scores), then the exact beam threshold
+  for (int r = tid; r < beam; r += NT) {
+    const int rc = w.rec[r];
+    if (rc == -1) continue;
+    const uint32_t rec = (uint32_t)rc;
+    BCHK((rec & kSpecial) ? (int)(rec & ~kSpecial) < nS : ((int)(rec >> 12) < nD && (int)(rec & 0xfff) < k));
+    if (!(rec & kSpecial)) {
+      const int d = (int)(rec >> 12), j = (int)(rec & 0xfff);
+      const int a = w.e1[d], c = w.stok[j];
+      w.ns[r] = bgen_score(w, d, j); w.nh[r] = child_hash(w.ch[a], c); w.nph[r] = w.ch[a];
+      w.nl[r] = c; w.nn[r] = w.cn[a] + 1; w.nf[r] = 0; w.ntrel[r] = pack_trel(a, c);
+    } else {
+      const int sx = (int)(rec & ~kSpecial);
+      const int a = w.spbase[sx], x = w.spx[sx];
+      w.ns[r] = w.spsc[sx];
+      if (x >= 0) {
+        w.nh[r] = child_hash(w.ch[a], x); w.nph[r] = w.ch[a]; w.nl[r] = x; w.nn[r] = w.cn[a] + 1;
+      } else {
+        w.nh[r] = w.ch[a]; w.nph[r] = w.cph[a]; w.nl[r] = w.cl[a]; w.nn[r] = w.cn[a];
+      }
+      w.nf[r] = w.spflag[sx];
+      w.ntrel[r] = pack_trel(w.spsrc[sx], w.sptok[sx]);
+    }
+  }
+  bsync();
+  // winners are in exact rank order, ns[0] is the exact frame best; the kept
+  // ones (decoder.py:621-623) form a prefix
+  int c2 = 0;
+  for (int r = tid; r < beam; r += NT)
+    c2 += (w.rec[r] != -1 && w.ns[r] > -INFINITY && (P.threshold_inf || w.ns[r] >= w.ns[0] - P.beam_threshold)) ? 1 : 0;
+  const int Hn = __syncthreads_count(c2);
+  // reset the token -> S rank map for the next frame
+  for (int j = tid; j < k; j += NT) w.pos[w.stok[j]] = 0xffff;
+  bsync();
+  return Hn;
+}
+
+// ------------------------------------------------------------------ finalize (decoder.py:753-817)
+__device__ void bfinalize(Blk& w, int H, int kept) {
+  const Params& P = *w.P;
+  const int tid = w.tid, u = w.u;
+  for (int e = tid; e < H; e += NT) {
+    int f = e;
+    for (int q = 0; q < e; q++)
+      if (w.ch[q] == w.ch[e] && w.cn[q] == w.cn[e]) { f = q; break; }
+    w.first[e] = f;
+  }
+  if (tid == 0) w.misc[0] = 0;
+  bsync();
+  for (int e = tid; e < H; e += NT) {
+    if (w.first[e] != e) continue;
+    double sc = w.cs[e];  // entries are in rank order: the first is the payload (decoder.py:794-797)
+    for (int q = e + 1; q < H; q++)
+      if (w.first[q] == e) sc = merge2_exact(sc, w.cs[q], w.P->merge_max != 0);
+    const int s = atomicAdd(&w.misc[0], 1);
+    w.spsc[s] = sc; w.spbase[s] = e; w.spx[s] = -1; w.spflag[s] = 0;
+  }
+  bsync();
+  const int nF = w.misc[0];
+  int pad = 2;
+  while (pad < nF) pad <<= 1;
+  for (int s = tid; s < pad; s += NT)
+    w.ckey[s] = s < nF ? ((ord64(w.spsc[s]) & ~0x3ffull) | (uint64_t)(0x3ff - s)) : 0ull;
+  bsync();
+  block_sort_desc(w.ckey, pad, tid);
+  // exact order: scores (full precision) then token sequences (tie runs)
+  if (tid == 0) {
+    int* ord = w.rec;
+    for (int r = 0; r < nF; r++) ord[r] = 0x3ff - (int)(w.ckey[r] & 0x3ffull);
+    for (int i = 1; i < nF; i++) {
+      const int x = ord[i];
+      const BDesc dx{w.spsc[x], w.spbase[x], -1, 0};
+      int j = i;
+      while (j > 0) {
+        const int y = ord[j - 1];
+        const BDesc dy{w.spsc[y], w.spbase[y], -1, 0};
+        if (!bprecedes(w, dx, dy)) break;
+        ord[j] = y;
+        j--;
+      }
+      ord[j] = x;
+    }
+  }
+  bsync();
+  const int nOut = nF < P.nbest ? nF : P.nbest;
+  for (int r = tid; r < nOut; r += NT) {
+    const int s = w.rec[r];
+    BCHK(s >= 0 && s < 3 * P.beam);
+    const int e = w.spbase[s];
+    const int len = w.cn[e];
+    const size_t o = ((size_t)u * P.nbest + r);
+    P.out_score[o] = w.spsc[s];
+    P.out_len[o] = len;
+    int* tok_out = P.out_tokens + o * P.T_max;
+    int* ts_out = P.out_ts ? P.out_ts + o * P.T_max : nullptr;
+    int pos = len, slot = e;
+    for (int i = kept - 1; i >= 0 && pos > 0; --i) {
+      BCHK(slot >= 0 && slot < P.beam);
+      const uint32_t rec = P.trellis[((size_t)u * P.T_max + i) * P.beam + slot];
+      const int tok = trel_tok(rec);
+      if (tok >= 0) {
+        --pos;
+        tok_out[pos] = tok;
+        if (ts_out) ts_out[pos] = P.frame_map[(size_t)u * P.T_max + i];
+      }
+      slot = trel_src(rec);
+    }
+  }
+  if (tid == 0) P.out_count[u] = nOut;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_constant__ Params P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  Blk w;
+  w.P = &P;
+  w.tid = threadIdx.x;
+  const int tid = w.tid;
+  carve(w, smem, P);
+  if (tid == 0)
+    for (int s = 0; s < 2; s++) mbar_init(&w.mbar[s], 1);
+  for (int c = tid; c < P.V; c += NT) w.pos[c] = 0xffff;
+  for (int i = tid; i < 2 * kTieCache; i += NT) w.tc_h[i] = 0ull;
+  for (int i = tid; i <= kTieCache; i += NT) w.tc_r[i] = 0;
+  fence_mbar_init();
+  __syncthreads();
+  uint32_t n_issue = 0, n_cons = 0;
+  const uint32_t row_copy = (uint32_t)P.V * 4u;
+
+  for (;;) {
+    if (tid == 0) w.misc[2] = atomicAdd(P.counter, 1);
+    __syncthreads();
+    const int item = w.misc[2];
+    __syncthreads();
+    if (item >= P.B) break;
+    const int u = P.order[item];
+    w.u = u;
+    const int len = P.lens[u];
+    if (len <= 0 || len > P.T_max) {
+      if (tid == 0) {
+        P.status[u] = len == 0 ? kUttEmpty : kUttBadLen;
+        P.out_count[u] = 0;
+        P.kept[u] = 0;
+      }
+      continue;
+    }
+    const float* ubase = P.lp + (size_t)u * P.stride_b;
+    int32_t* fmap = P.frame_map + (size_t)u * P.T_max;
+    // -- A. blank-skip compaction (warp 0: ballot + prefix popcount)
+    if (tid < 32) {
+      int kept = 0;
+      for (int t0 = 0; t0 < len; t0 += 32) {
+        const int t = t0 + tid;
+        bool keep = t < len;
+        if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
+        const unsigned bal = __ballot_sync(FULL, keep);
+        if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
+        kept += __popc(bal);
+      }
+      if (tid == 0) { P.kept[u] = kept; w.misc[3] = kept; }
+    }
+    __syncthreads();
+    const int kept = w.misc[3];
+    // -- B. frame loop
+    if (tid == 0) { w.cs[0] = 0.0; w.ch[0] = kEmptyPrefixHash; w.cph[0] = 0ull; w.cl[0] = -1; w.cn[0] = 0; w.cf[0] = 1; }
+    int H = 1;
+    w.steps_done = 0;
+    auto issue = [&](int i) {
+      const uint32_t slot = n_issue & 1u;
+      if (tid == 0 && P.bulk_ok) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&w.mbar[slot], row_copy);
+        tma_bulk_g2s(w.rows + (size_t)slot * P.row_bytes, ubase + (size_t)fmap[i] * P.stride_t, row_copy,
+                     &w.mbar[slot]);
+      }
+      n_issue++;
+    };
+    if (kept > 0) issue(0);
+    __syncthreads();
+    bool died = false;
+    for (int i = 0; i < kept; i++) {
+      if (i + 1 < kept) issue(i + 1);
+      const uint32_t slot = n_cons & 1u;
+      if (P.bulk_ok) {
+        mbar_wait(&w.mbar[slot], (n_cons >> 1) & 1u);
+      } else {  // rows that are not 16-B multiples: plain copy (no TMA)
+        float* dst = (float*)(w.rows + (size_t)slot * P.row_bytes);
+        const float* src = ubase + (size_t)fmap[i] * P.stride_t;
+        for (int c = tid; c < P.V; c += NT) dst[c] = __ldg(src + c);
+        __syncthreads();
+      }
+      n_cons++;
+      const float* row = (const float*)(w.rows + (size_t)slot * P.row_bytes);
+      btopk(w, row);
+      const int Hn = bstep(w, row, H);
+      if (Hn == 0) { died = true; break; }
+      uint32_t* trow = P.trellis + ((size_t)u * P.T_max + i) * P.beam;
+      for (int r = tid; r < Hn; r += NT) trow[r] = w.ntrel[r];
+      __syncthreads();
+      w.swap_state();
+      H = Hn;
+      w.steps_done = i + 1;
+      __syncthreads();
+    }
+    if (died) {
+      while (n_cons < n_issue) {
+        if (P.bulk_ok) mbar_wait(&w.mbar[n_cons & 1u], (n_cons >> 1) & 1u);
+        n_cons++;
+      }
+      if (tid == 0) {
+        P.status[u] = kUttBeamDied;
+        P.out_count[u] = 0;
+        P.out_len[(size_t)u * P.nbest] = w.steps_done;
+      }
+      __syncthreads();
+      continue;
+    }
+    bfinalize(w, H, kept);
+    if (tid == 0) P.status[u] = kUttOk;
+    __syncthreads();
+  }
+}
+
+}  // namespace ctcb

@@ -175,6 +175,56 @@ __host__ __device__ constexpr inline FastLayout make_fast_layout(int V, int ring
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Large-beam block kernel (ctcb_block.cu): one CTA per utterance.
+constexpr int kBlockMaxBeam = 128;
+constexpr int kBlockMaxV = 2048;
+constexpr int kBlockCands = 2048;  // candidate keys per frame (specials + quota appends)
+constexpr int kBlockRun = 512;     // longest near-tie run re-sorted exactly
+struct BlockLayout {
+  size_t rows, mbar, cs, ns, lA, spsc, ch, cph, nh, nph, skey, ckey, htk, tc_h, cl, cn, cf, nl, nn, nf, htf, hslot,
+      first, dpi, pd, e1, e2, qoff, spbase, spx, spflag, spsrc, sptok, misc, tc_r, rec, ord, runbuf, ntrel, excl, hist, crec,
+      sval, stok, pos, total;
+  int kw, kpad, ts, ncap;
+};
+__host__ __device__ inline BlockLayout make_block_layout(int beam, int kpad, int V, int row_bytes) {
+  BlockLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes, size_t align) {
+    o = (o + align - 1) / align * align;
+    size_t r = o;
+    o += bytes;
+    return r;
+  };
+  const size_t B = (size_t)beam, S = 3 * B;
+  int ts = 1;
+  while (ts < 2 * beam) ts <<= 1;
+  L.kpad = kpad;
+  L.kw = (kpad + 31) / 32;
+  L.ts = ts;
+  L.ncap = kBlockCands;
+  const size_t small = B + 1 > 16 ? B + 1 : 16;
+  L.rows = take(2 * (size_t)row_bytes, 128);
+  L.mbar = take(16, 8);
+  L.cs = take(8 * B, 8); L.ns = take(8 * B, 8); L.lA = take(8 * B, 8); L.spsc = take(8 * S, 8);
+  L.ch = take(8 * B, 8); L.cph = take(8 * B, 8); L.nh = take(8 * B, 8); L.nph = take(8 * B, 8);
+  L.skey = take(8 * (size_t)kpad, 8); L.ckey = take(8 * (size_t)L.ncap, 8); L.htk = take(8 * (size_t)ts, 8);
+  L.tc_h = take(8 * 2 * kTieCache, 8);
+  L.cl = take(4 * B, 4); L.cn = take(4 * B, 4); L.cf = take(4 * B, 4);
+  L.nl = take(4 * B, 4); L.nn = take(4 * B, 4); L.nf = take(4 * B, 4);
+  L.htf = take(4 * (size_t)ts, 4); L.hslot = take(4 * B, 4); L.first = take(4 * B, 4); L.dpi = take(4 * B, 4);
+  L.pd = take(4 * B, 4); L.e1 = take(4 * B, 4); L.e2 = take(4 * B, 4); L.qoff = take(4 * small, 4);
+  L.spbase = take(4 * S, 4); L.spx = take(4 * S, 4); L.spflag = take(4 * S, 4); L.spsrc = take(4 * S, 4);
+  L.sptok = take(4 * S, 4); L.misc = take(4 * 16, 4); L.tc_r = take(4 * (kTieCache + 1), 4);
+  L.rec = take(4 * small, 4);
+  L.ord = take(4 * (size_t)L.ncap, 8);  // also the survivor key buffer (u64)
+  L.runbuf = take(4 * kBlockRun, 4);
+  L.ntrel = take(4 * B, 4); L.excl = take(4 * B * (size_t)L.kw, 4); L.hist = take(4 * 256, 4);
+  L.crec = take(4 * (size_t)L.ncap, 4);
+  L.sval = take(4 * (size_t)kpad, 4); L.stok = take(4 * (size_t)kpad, 4); L.pos = take(2 * (size_t)V, 2);
+  L.total = (o + 127) / 128 * 128;
+  return L;
+}
+
 // Two-utterances-per-warp kernel (ctcb_pair.cu): per-half shared memory.
 constexpr int kPairRing = 2;
 struct PairLayout {

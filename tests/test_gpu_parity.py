@@ -627,3 +627,47 @@ def test_regression_lm_fuzz_s62_602_bitwise():
     res, nb = _lm602_case()
     for g, r in res:
         assert g["tokens"] == r.tokens[:nb] and g["scores"] == r.scores[:nb]
+
+
+# ---------------------------------------------------------------- large-beam block kernel
+# 16 < beam <= 128 (no token cap, no LM) runs one 256-thread CTA per
+# utterance (ctcb_block.cu).  Quantized logits give exact in-frame score ties,
+# and small vocabularies give fewer live candidates than beam slots: both
+# exercise the tie-run resolution and the serial exact fallback.
+@pytest.mark.parametrize("V,beam,quant", [(5, 17, 1.0), (5, 62, 0.5), (12, 40, 1.0), (12, 100, 0.5),
+                                          (30, 128, 1.0), (64, 50, 0.0)])
+def test_block_kernel_ties_small_vocab(V, beam, quant, monkeypatch):
+    """Block kernel vs the oracle (north-star tolerance: scores 1e-4, ranks
+    exact outside 1e-3 near-ties) and vs the one-warp generic kernel (bitwise:
+    both fold scores with the same fp64 helpers)."""
+    rng = np.random.default_rng(V * 1000 + beam)
+    B, T = 6, 24
+    x = rng.normal(size=(B, T, V)) * 2.0
+    if quant:
+        x = np.round(x / quant) * quant
+    lp = (x - np.log(np.exp(x).sum(-1, keepdims=True))).astype(np.float32)
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    nb = min(beam, 8)
+
+    def dec_run():
+        dec = CUCTCDecoder(vocab(V), beam_size=beam, nbest=nb, blank_skip_threshold=0.9, beam_threshold=8.0)
+        dec.kernel_timing(True)
+        out = dec.decode(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda(), timesteps=True)
+        return dec.to_host(out), dec.kernel_time()[2]
+
+    (tok, ts, ln, sc, cnt), name = dec_run()
+    assert name == "ctcb_decode_block_kernel"
+    monkeypatch.setenv("CTCB_BLOCK", "0")
+    (tok2, ts2, ln2, sc2, cnt2), name2 = dec_run()
+    assert name2 != "ctcb_decode_block_kernel"
+    assert np.array_equal(cnt, cnt2)
+    for b in range(B):
+        ref = oracle.decode(lp[b, : lens[b]], beam_size=beam, n_best=nb, blank_skip_threshold=0.9, beam_threshold=8.0)
+        n = int(cnt[b])
+        got = {"tokens": [tok[b, j, : ln[b, j]].tolist() for j in range(n)],
+               "scores": [float(sc[b, j]) for j in range(n)]}
+        assert _rank_ok(got, ref, nb), (b, got, ref.tokens, ref.scores)
+        for j in range(n):
+            assert sc[b, j] == sc2[b, j] and ln[b, j] == ln2[b, j], (b, j)
+            assert np.array_equal(tok[b, j, : ln[b, j]], tok2[b, j, : ln[b, j]]), (b, j)
+            assert np.array_equal(ts[b, j, : ln[b, j]], ts2[b, j, : ln[b, j]]), (b, j)
