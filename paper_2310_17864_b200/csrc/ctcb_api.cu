@@ -527,7 +527,7 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     P.warps_per_block = 4;
   }
   if (blk) {  // one 256-thread CTA per utterance
-    P.smem_per_warp = (int)ctcb::make_block_layout(P.beam, P.kpad, P.V, P.row_bytes).total;
+    P.smem_per_warp = (int)ctcb::make_block_layout(ctcb::kBlockMaxBeam, 256, ctcb::kBlockMaxV, ctcb::kBlockMaxV * 4).total;
     P.warps_per_block = 8;
   }
   size_t smem = blk ? (size_t)P.smem_per_warp : (size_t)P.smem_per_warp * P.warps_per_block;

@@ -43,60 +43,73 @@ constexpr int NT = 256;          // threads per CTA (one utterance)
 constexpr int kTolB = 2;         // rank-key tolerance (fixed-point units)
 constexpr uint32_t kSpecial = 0x80000000u;
 
+// Dynamic shared memory of the block kernel: one fixed layout for the largest
+// supported beam / vocabulary, so every array base below is a link-time
+// constant (an immediate offset in the shared-memory instructions) instead of
+// a pointer held in registers or spilled to the stack.
+extern __shared__ __align__(128) uint8_t blk_smem[];
+
 struct Blk {
+  static constexpr BlockLayout L = make_block_layout(kBlockMaxBeam, 256, kBlockMaxV, kBlockMaxV * 4);
+  static constexpr int kw = L.kw, kpad = L.kpad, ts = L.ts, ncap = L.ncap;
+  static constexpr size_t row_bytes = kBlockMaxV * 4;
   const Params* P;
   int tid, u, steps_done;
-  uint8_t* rows;
-  uint64_t* mbar;
-  double *cs, *ns, *lA, *spsc;
-  uint64_t *ch, *cph, *nh, *nph, *skey, *ckey, *htk, *tc_h;
-  int *cl, *cn, *cf, *nl, *nn, *nf, *htf, *hslot, *first, *dpi, *pd, *e1, *e2, *qoff;
-  int *spbase, *spx, *spflag, *spsrc, *sptok, *misc, *tc_r, *rec, *ord, *runbuf;
-  uint32_t *ntrel, *excl, *hist, *crec;
-  float* sval;
-  int* stok;
-  uint16_t* pos;
-  int kw, kpad, ts, ncap;
+  int par;  // which half of the double-buffered entry state is current
+  __device__ uint8_t* rows() const { return (uint8_t*)(blk_smem + L.rows); }
+  __device__ uint64_t* mbar() const { return (uint64_t*)(blk_smem + L.mbar); }
+  __device__ double* lA() const { return (double*)(blk_smem + L.lA); }
+  __device__ double* spsc() const { return (double*)(blk_smem + L.spsc); }
+  __device__ uint64_t* skey() const { return (uint64_t*)(blk_smem + L.skey); }
+  __device__ uint64_t* ckey() const { return (uint64_t*)(blk_smem + L.ckey); }
+  __device__ uint64_t* htk() const { return (uint64_t*)(blk_smem + L.htk); }
+  __device__ uint64_t* tc_h() const { return (uint64_t*)(blk_smem + L.tc_h); }
+  __device__ int* htf() const { return (int*)(blk_smem + L.htf); }
+  __device__ int* hslot() const { return (int*)(blk_smem + L.hslot); }
+  __device__ int* first() const { return (int*)(blk_smem + L.first); }
+  __device__ int* dpi() const { return (int*)(blk_smem + L.dpi); }
+  __device__ int* pd() const { return (int*)(blk_smem + L.pd); }
+  __device__ int* e1() const { return (int*)(blk_smem + L.e1); }
+  __device__ int* e2() const { return (int*)(blk_smem + L.e2); }
+  __device__ int* qoff() const { return (int*)(blk_smem + L.qoff); }
+  __device__ int* spbase() const { return (int*)(blk_smem + L.spbase); }
+  __device__ int* spx() const { return (int*)(blk_smem + L.spx); }
+  __device__ int* spflag() const { return (int*)(blk_smem + L.spflag); }
+  __device__ int* spsrc() const { return (int*)(blk_smem + L.spsrc); }
+  __device__ int* sptok() const { return (int*)(blk_smem + L.sptok); }
+  __device__ int* misc() const { return (int*)(blk_smem + L.misc); }
+  __device__ int* tc_r() const { return (int*)(blk_smem + L.tc_r); }
+  __device__ int* rec() const { return (int*)(blk_smem + L.rec); }
+  __device__ int* ord() const { return (int*)(blk_smem + L.ord); }
+  __device__ int* runbuf() const { return (int*)(blk_smem + L.runbuf); }
+  __device__ uint32_t* ntrel() const { return (uint32_t*)(blk_smem + L.ntrel); }
+  __device__ uint32_t* excl() const { return (uint32_t*)(blk_smem + L.excl); }
+  __device__ uint32_t* hist() const { return (uint32_t*)(blk_smem + L.hist); }
+  __device__ uint32_t* crec() const { return (uint32_t*)(blk_smem + L.crec); }
+  __device__ float* sval() const { return (float*)(blk_smem + L.sval); }
+  __device__ int* stok() const { return (int*)(blk_smem + L.stok); }
+  __device__ uint16_t* pos() const { return (uint16_t*)(blk_smem + L.pos); }
+  __device__ double* cs() const { return (double*)(blk_smem + (par ? L.ns : L.cs)); }
+  __device__ double* ns() const { return (double*)(blk_smem + (par ? L.cs : L.ns)); }
+  __device__ uint64_t* ch() const { return (uint64_t*)(blk_smem + (par ? L.nh : L.ch)); }
+  __device__ uint64_t* nh() const { return (uint64_t*)(blk_smem + (par ? L.ch : L.nh)); }
+  __device__ uint64_t* cph() const { return (uint64_t*)(blk_smem + (par ? L.nph : L.cph)); }
+  __device__ uint64_t* nph() const { return (uint64_t*)(blk_smem + (par ? L.cph : L.nph)); }
+  __device__ int* cl() const { return (int*)(blk_smem + (par ? L.nl : L.cl)); }
+  __device__ int* nl() const { return (int*)(blk_smem + (par ? L.cl : L.nl)); }
+  __device__ int* cn() const { return (int*)(blk_smem + (par ? L.nn : L.cn)); }
+  __device__ int* nn() const { return (int*)(blk_smem + (par ? L.cn : L.nn)); }
+  __device__ int* cf() const { return (int*)(blk_smem + (par ? L.nf : L.cf)); }
+  __device__ int* nf() const { return (int*)(blk_smem + (par ? L.cf : L.nf)); }
 
-  __device__ void swap_state() {
-    double* d = cs; cs = ns; ns = d;
-    uint64_t* h = ch; ch = nh; nh = h;
-    h = cph; cph = nph; nph = h;
-    int* x = cl; cl = nl; nl = x;
-    x = cn; cn = nn; nn = x;
-    x = cf; cf = nf; nf = x;
-  }
+  __device__ void swap_state() { par ^= 1; }
 };
-
-__device__ void carve(Blk& w, uint8_t* base, const Params& P) {
-  const BlockLayout L = make_block_layout(P.beam, P.kpad, P.V, P.row_bytes);
-  w.rows = base + L.rows;
-  w.mbar = (uint64_t*)(base + L.mbar);
-  w.cs = (double*)(base + L.cs); w.ns = (double*)(base + L.ns);
-  w.lA = (double*)(base + L.lA); w.spsc = (double*)(base + L.spsc);
-  w.ch = (uint64_t*)(base + L.ch); w.cph = (uint64_t*)(base + L.cph);
-  w.nh = (uint64_t*)(base + L.nh); w.nph = (uint64_t*)(base + L.nph);
-  w.skey = (uint64_t*)(base + L.skey); w.ckey = (uint64_t*)(base + L.ckey);
-  w.htk = (uint64_t*)(base + L.htk); w.tc_h = (uint64_t*)(base + L.tc_h);
-  w.cl = (int*)(base + L.cl); w.cn = (int*)(base + L.cn); w.cf = (int*)(base + L.cf);
-  w.nl = (int*)(base + L.nl); w.nn = (int*)(base + L.nn); w.nf = (int*)(base + L.nf);
-  w.htf = (int*)(base + L.htf); w.hslot = (int*)(base + L.hslot); w.first = (int*)(base + L.first);
-  w.dpi = (int*)(base + L.dpi); w.pd = (int*)(base + L.pd); w.e1 = (int*)(base + L.e1);
-  w.e2 = (int*)(base + L.e2); w.qoff = (int*)(base + L.qoff);
-  w.spbase = (int*)(base + L.spbase); w.spx = (int*)(base + L.spx); w.spflag = (int*)(base + L.spflag);
-  w.spsrc = (int*)(base + L.spsrc); w.sptok = (int*)(base + L.sptok); w.misc = (int*)(base + L.misc);
-  w.tc_r = (int*)(base + L.tc_r); w.rec = (int*)(base + L.rec); w.ord = (int*)(base + L.ord); w.runbuf = (int*)(base + L.runbuf);
-  w.ntrel = (uint32_t*)(base + L.ntrel); w.excl = (uint32_t*)(base + L.excl);
-  w.hist = (uint32_t*)(base + L.hist); w.crec = (uint32_t*)(base + L.crec);
-  w.sval = (float*)(base + L.sval); w.stok = (int*)(base + L.stok); w.pos = (uint16_t*)(base + L.pos);
-  w.kw = L.kw; w.kpad = L.kpad; w.ts = L.ts; w.ncap = L.ncap;
-}
 
 // ------------------------------------------------------------------ block helpers
 __device__ __forceinline__ void bsync() { __syncthreads(); }
 
 // Block bitonic sort of n (power of two, >= 2) u64 keys, descending.
-__device__ void block_sort_desc(uint64_t* key, int n, int tid) {
+__device__ __forceinline__ void block_sort_desc(uint64_t* key, int n, int tid) {
   for (int size = 2; size <= n; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int t = tid; t < (n >> 1); t += NT) {
@@ -110,8 +123,88 @@ __device__ void block_sort_desc(uint64_t* key, int n, int tid) {
     }
 }
 
+// One-warp bitonic sort of 32 R u64 keys held in registers, descending; key
+// i = lane R + r.  Strides >= R exchange across lanes (two shuffles per key),
+// smaller ones inside a lane: no barriers, unlike block_sort_desc.
+__device__ __forceinline__ uint64_t shfl_xor64(uint64_t x, int m) {
+  const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)x, m), hi = __shfl_xor_sync(FULL, (uint32_t)(x >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+template <int R>
+__device__ __forceinline__ void warp_sort_desc(uint64_t (&k)[R], int lane) {
+  constexpr int N = 32 * R;
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= R) {
+        const int lm = stride / R;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const uint64_t o = shfl_xor64(k[r], lm);
+          const bool desc = ((lane * R + r) & size) == 0;
+          k[r] = (lower == desc) ? (k[r] > o ? k[r] : o) : (k[r] < o ? k[r] : o);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const int p = r ^ stride;
+          if (p > r) {
+            const bool desc = ((lane * R + r) & size) == 0;
+            const uint64_t a = k[r], b = k[p];
+            if (desc ? a < b : a > b) { k[r] = b; k[p] = a; }
+          }
+        }
+      }
+    }
+  }
+}
+// Block sort of n <= 512 keys (nonzero keys distinct; zeros are padding and
+// are dropped): each warp sorts a 64-key chunk in registers, then every key's
+// rank is its chunk position plus, per other chunk, the number of larger keys
+// (binary search).  dst[0 .. #nonzero) receives the nonzero keys descending.
+// Two barriers instead of the 45 of a block bitonic network.  tmp: 512 keys.
+__device__ __forceinline__ void block_sort512(const uint64_t* src, int n, uint64_t* tmp, uint64_t* dst, int tid) {
+  const int wid = tid >> 5, lane = tid & 31;
+  const int nch = (n + 63) >> 6;
+  uint64_t k[2] = {0ull, 0ull};
+  if (wid < nch) {
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      const int i = wid * 64 + r * 32 + lane;
+      k[r] = i < n ? src[i] : 0ull;
+    }
+    warp_sort_desc<2>(k, lane);
+#pragma unroll
+    for (int r = 0; r < 2; r++) tmp[wid * 64 + lane * 2 + r] = k[r];
+  }
+  __syncthreads();
+  if (wid < nch) {
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      const uint64_t key = k[r];
+      if (key == 0ull) continue;
+      int rank = lane * 2 + r;
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        if (c == wid || c >= nch) continue;
+        const uint64_t* ch = tmp + c * 64;
+        int lo = 0;  // number of keys > key in the descending chunk
+#pragma unroll
+        for (int step = 32; step > 0; step >>= 1)
+          if (ch[lo + step - 1] > key) lo += step;
+        lo += ch[lo] > key ? 1 : 0;  // lo <= 63 here; all 64 larger
+        rank += lo;
+      }
+      dst[rank] = key;
+    }
+  }
+  __syncthreads();
+}
+
 // Exclusive block scan of one int per thread (NT = 256).
-__device__ int block_excl_scan(int v, int tid, int* tmp, int* total) {
+__device__ __forceinline__ int block_excl_scan(int v, int tid, int* tmp, int* total) {
   const int lane = tid & 31, wid = tid >> 5;
   int incl = v;
 #pragma unroll
@@ -142,7 +235,7 @@ __device__ int block_excl_scan(int v, int tid, int* tmp, int* total) {
 // Largest 32-bit value T with #{x >= T} >= need among hi32(key[0..n)) (keys
 // of 0 never count): 8-bit radix select with a block histogram (hist: 256
 // words, misc: 2 words of scratch).  need <= #nonzero, else returns 0.
-__device__ uint32_t block_select_hi(const uint64_t* key, int n, int need, int tid, uint32_t* hist, int* misc) {
+__device__ __forceinline__ uint32_t block_select_hi(const uint64_t* key, int n, int need, int tid, uint32_t* hist, int* misc) {
   uint32_t prefix = 0, pmask = 0;
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int b = tid; b < 256; b += NT) hist[b] = 0;
@@ -189,7 +282,7 @@ __device__ uint32_t block_select_hi(const uint64_t* key, int n, int need, int ti
 }
 
 // ------------------------------------------------------------------ token sequences (single-thread slow path)
-__device__ int bmaterialize(const Blk& w, int e, int len, int* buf) {
+__device__ __forceinline__ int bmaterialize(const Blk& w, int e, int len, int* buf) {
   const Params& P = *w.P;
   int pos = len, slot = e;
   for (int i = w.steps_done - 1; i >= 0 && pos > 0; --i) {
@@ -200,15 +293,15 @@ __device__ int bmaterialize(const Blk& w, int e, int len, int* buf) {
   }
   return len;
 }
-__device__ int bseq_cmp_full(const Blk& w, int ea, int xa, int eb, int xb, bool* strict) {
+__device__ __forceinline__ int bseq_cmp_full(const Blk& w, int ea, int xa, int eb, int xb, bool* strict) {
   const Params& P = *w.P;
   atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
   atomicAdd(&P.dbg[kDbgMatSteps], 2ull * (unsigned long long)w.steps_done);
   int* A = P.seqbuf + (size_t)w.u * 3 * (P.T_max + 1);
   int* Bq = A + P.T_max + 1;
-  int la = bmaterialize(w, ea, w.cn[ea], A);
+  int la = bmaterialize(w, ea, w.cn()[ea], A);
   if (xa >= 0) A[la++] = xa;
-  int lb = bmaterialize(w, eb, w.cn[eb], Bq);
+  int lb = bmaterialize(w, eb, w.cn()[eb], Bq);
   if (xb >= 0) Bq[lb++] = xb;
   const int n = la < lb ? la : lb;
   *strict = true;
@@ -217,26 +310,26 @@ __device__ int bseq_cmp_full(const Blk& w, int ea, int xa, int eb, int xb, bool*
   *strict = false;
   return la < lb ? -1 : (la > lb ? 1 : 0);
 }
-__device__ int btc_lookup(const Blk& w, uint64_t ha, uint64_t hb) {
+__device__ __forceinline__ int btc_lookup(const Blk& w, uint64_t ha, uint64_t hb) {
 #pragma unroll 1
   for (int i = 0; i < kTieCache; i++) {
-    if (w.tc_h[2 * i] == ha && w.tc_h[2 * i + 1] == hb) return w.tc_r[i];
-    if (w.tc_h[2 * i] == hb && w.tc_h[2 * i + 1] == ha) return -w.tc_r[i];
+    if (w.tc_h()[2 * i] == ha && w.tc_h()[2 * i + 1] == hb) return w.tc_r()[i];
+    if (w.tc_h()[2 * i] == hb && w.tc_h()[2 * i + 1] == ha) return -w.tc_r()[i];
   }
   return 0;
 }
-__device__ void btc_insert(const Blk& w, uint64_t ha, uint64_t hb, int r) {
+__device__ __forceinline__ void btc_insert(const Blk& w, uint64_t ha, uint64_t hb, int r) {
   if (btc_lookup(w, ha, hb)) return;
-  const int i = w.tc_r[kTieCache];
-  w.tc_h[2 * i] = ha;
-  w.tc_h[2 * i + 1] = hb;
-  w.tc_r[i] = r;
-  w.tc_r[kTieCache] = (i + 1) % kTieCache;
+  const int i = w.tc_r()[kTieCache];
+  w.tc_h()[2 * i] = ha;
+  w.tc_h()[2 * i + 1] = hb;
+  w.tc_r()[i] = r;
+  w.tc_r()[kTieCache] = (i + 1) % kTieCache;
 }
 // Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token).
-__device__ int bseq_cmp(const Blk& w, int ea, int xa, int eb, int xb) {
-  const uint64_t hba = w.ch[ea], hbb = w.ch[eb];
-  const int lba = w.cn[ea], lbb = w.cn[eb];
+__device__ __forceinline__ int bseq_cmp(const Blk& w, int ea, int xa, int eb, int xb) {
+  const uint64_t hba = w.ch()[ea], hbb = w.ch()[eb];
+  const int lba = w.cn()[ea], lbb = w.cn()[eb];
   if (hba == hbb && lba == lbb) {
     if (xa == xb) return 0;
     return xa < xb ? -1 : 1;
@@ -263,7 +356,9 @@ __device__ int bseq_cmp(const Blk& w, int ea, int xa, int eb, int xb) {
   return r;
 }
 struct BDesc { double sc; int base, x, flag; };
-__device__ bool bprecedes(const Blk& w, const BDesc& a, const BDesc& b) {
+// out of line: the exact tie path is rare and would otherwise be inlined at
+// every call site
+__device__ __noinline__ bool bprecedes(const Blk w, const BDesc a, const BDesc b) {
   if (a.sc != b.sc) return a.sc > b.sc;
   atomicAdd(&w.P->dbg[kDbgExactTies], 1ull);
   const int c = bseq_cmp(w, a.base, a.x, b.base, b.x);
@@ -274,28 +369,44 @@ __device__ bool bprecedes(const Blk& w, const BDesc& a, const BDesc& b) {
 // ------------------------------------------------------------------ top-k
 // S = the k best non-blank tokens of `row` by (value desc, index asc), sorted
 // into sval / stok; pos[token] = rank in S.
-__device__ void btopk(Blk& w, const float* row) {
+__device__ __forceinline__ void btopk(Blk& w, const float* row) {
   const Params& P = *w.P;
   const int V = P.V, blank = P.blank, k = P.k, tid = w.tid;
+  if (V <= 512) {
+    // whole row: block sort by (value desc, index asc); the first k are S
+    // (same order as select + compaction + sort below)
+    for (int c = tid; c < V; c += NT)
+      w.skey()[c] = c != blank ? (((uint64_t)ord32(row[c]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)c)) : 0ull;
+    bsync();
+    block_sort512(w.skey(), V, w.ckey(), w.ckey() + 512, tid);
+    for (int j = tid; j < k; j += NT) {
+      const int c = (int)(0xffffffffu - (uint32_t)(w.ckey()[512 + j] & 0xffffffffu));
+      w.stok()[j] = c;
+      w.sval()[j] = row[c];
+      w.pos()[c] = (uint16_t)j;
+    }
+    bsync();
+    return;
+  }
   uint32_t kth = 0;
   int need = V;
   if (k < V - 1) {
     uint32_t prefix = 0, pmask = 0;
     need = k;
     for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int b = tid; b < 256; b += NT) w.hist[b] = 0;
+      for (int b = tid; b < 256; b += NT) w.hist()[b] = 0;
       bsync();
       for (int c = tid; c < V; c += NT) {
         if (c == blank) continue;
         const uint32_t key = ord32(row[c]);
-        if ((key & pmask) == prefix) atomicAdd(&w.hist[(key >> shift) & 255u], 1u);
+        if ((key & pmask) == prefix) atomicAdd(&w.hist()[(key >> shift) & 255u], 1u);
       }
       bsync();
       if (tid < 32) {  // digit holding the need-th largest key
         const int lane = tid;
         uint32_t h[8], s = 0;
 #pragma unroll
-        for (int q = 0; q < 8; q++) { h[q] = w.hist[lane * 8 + q]; s += h[q]; }
+        for (int q = 0; q < 8; q++) { h[q] = w.hist()[lane * 8 + q]; s += h[q]; }
         uint32_t incl = s;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -314,11 +425,11 @@ __device__ void btopk(Blk& w, const float* row) {
         const int src = __ffs(bal) - 1;
         const int digit = __shfl_sync(FULL, found, src);
         cgt = __shfl_sync(FULL, cgt, src);
-        if (lane == 0) { w.misc[4] = digit; w.misc[5] = (int)cgt; }
+        if (lane == 0) { w.misc()[4] = digit; w.misc()[5] = (int)cgt; }
       }
       bsync();
-      need -= w.misc[5];
-      prefix |= (uint32_t)w.misc[4] << shift;
+      need -= w.misc()[5];
+      prefix |= (uint32_t)w.misc()[4] << shift;
       pmask |= 0xffu << shift;
       bsync();
     }
@@ -336,36 +447,35 @@ __device__ void btopk(Blk& w, const float* row) {
     neq += key == kth;
   }
   int tot_eq = 0, tot = 0;
-  const int eq_before = block_excl_scan(neq, tid, w.qoff, &tot_eq);
+  const int eq_before = block_excl_scan(neq, tid, w.qoff(), &tot_eq);
   int eq_take = need - eq_before;
   eq_take = eq_take < 0 ? 0 : (eq_take > neq ? neq : eq_take);
-  const int off = block_excl_scan(ngt + eq_take, tid, w.qoff, &tot);
+  const int off = block_excl_scan(ngt + eq_take, tid, w.qoff(), &tot);
   int o = off, taken = 0;
   for (int q = 0; q < cpt; q++) {
     const int c = tid * cpt + q;
     if (c >= V || c == blank) continue;
     const uint32_t key = ord32(row[c]);
     const bool acc = key > kth || (key == kth && taken++ < eq_take);
-    if (acc) w.skey[o++] = ((uint64_t)key << 32) | (uint64_t)(0xffffffffu - (uint32_t)c);
+    if (acc) w.skey()[o++] = ((uint64_t)key << 32) | (uint64_t)(0xffffffffu - (uint32_t)c);
   }
-  for (int j = tot + tid; j < w.kpad; j += NT) w.skey[j] = 0ull;
   bsync();
-  block_sort_desc(w.skey, w.kpad, tid);
+  block_sort512(w.skey(), tot, w.ckey(), w.ckey() + 512, tid);  // tot = k <= 256
   for (int j = tid; j < k; j += NT) {
-    const int c = (int)(0xffffffffu - (uint32_t)(w.skey[j] & 0xffffffffu));
-    w.stok[j] = c;
-    w.sval[j] = row[c];
-    w.pos[c] = (uint16_t)j;
+    const int c = (int)(0xffffffffu - (uint32_t)(w.ckey()[512 + j] & 0xffffffffu));
+    w.stok()[j] = c;
+    w.sval()[j] = row[c];
+    w.pos()[c] = (uint16_t)j;
   }
   bsync();
 }
 
 __device__ __forceinline__ bool bexcl(const Blk& w, int d, int j) {
-  return (w.excl[d * w.kw + (j >> 5)] >> (j & 31)) & 1u;
+  return (w.excl()[d * w.kw + (j >> 5)] >> (j & 31)) & 1u;
 }
 // j-th valid (non-excluded) top-k position of list d, or k
-__device__ int jth_valid(const Blk& w, int d, int j, int k) {
-  const uint32_t* ex = w.excl + d * w.kw;
+__device__ __forceinline__ int jth_valid(const Blk& w, int d, int j, int k) {
+  const uint32_t* ex = w.excl() + d * w.kw;
   for (int wd = 0; wd < w.kw; wd++) {
     const int lo = wd * 32;
     if (lo >= k) break;
@@ -373,32 +483,37 @@ __device__ int jth_valid(const Blk& w, int d, int j, int k) {
     const uint32_t live = ~ex[wd] & (nbits == 32 ? 0xffffffffu : ((1u << nbits) - 1u));
     const int c = __popc(live);
     if (j < c) {
-      uint32_t m = live;
-      for (int q = 0; q < j; q++) m &= m - 1u;
-      return lo + __ffs(m) - 1;
+      uint32_t m = live;  // position of its (j+1)-th set bit: binary search on popcounts
+      int p = 0;
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) {
+        const int h = __popc(m & ((1u << s) - 1u));
+        if (j >= h) { j -= h; m >>= s; p += s; }
+      }
+      return lo + p;
     }
     j -= c;
   }
   return k;
 }
 __device__ __forceinline__ double bgen_score(const Blk& w, int d, int j) {
-  const double v = (double)w.sval[j];
-  const int a = w.e1[d], b = w.e2[d];
-  double s = w.cs[a] + v;
-  if (b >= 0) s = merge2_exact(s, w.cs[b] + v, w.P->merge_max != 0);
+  const double v = (double)w.sval()[j];
+  const int a = w.e1()[d], b = w.e2()[d];
+  double s = w.cs()[a] + v;
+  if (b >= 0) s = merge2_exact(s, w.cs()[b] + v, w.P->merge_max != 0);
   return s;
 }
-__device__ BDesc cand_desc(const Blk& w, uint32_t rec) {
+__device__ __forceinline__ BDesc cand_desc(const Blk& w, uint32_t rec) {
   if (rec & kSpecial) {
     const int s = (int)(rec & ~kSpecial);
-    return BDesc{w.spsc[s], w.spbase[s], w.spx[s], w.spflag[s]};
+    return BDesc{w.spsc()[s], w.spbase()[s], w.spx()[s], w.spflag()[s]};
   }
   const int d = (int)(rec >> 12), j = (int)(rec & 0xfff);
-  return BDesc{bgen_score(w, d, j), w.e1[d], w.stok[j], 0};
+  return BDesc{bgen_score(w, d, j), w.e1()[d], w.stok()[j], 0};
 }
 
 // One frame step; returns the new beam size (0: beam died).
-__device__ int bstep(Blk& w, const float* row, int H) {
+__device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
   const Params& P = *w.P;
   const int tid = w.tid, beam = P.beam, k = P.k;
   const bool MX = P.merge_max != 0;
@@ -406,124 +521,124 @@ __device__ int bstep(Blk& w, const float* row, int H) {
 
   // -- prefix groups (flag 0 / flag 1 entries of one token sequence)
   const int TS = w.ts;
-  for (int i = tid; i < TS; i += NT) { w.htk[i] = 0ull; w.htf[i] = 0x7fffffff; }
-  if (tid == 0) { w.misc[0] = 0; w.misc[1] = 0; }
+  for (int i = tid; i < TS; i += NT) { w.htk()[i] = 0ull; w.htf()[i] = 0x7fffffff; }
+  if (tid == 0) { w.misc()[0] = 0; w.misc()[1] = 0; }
   bsync();
   for (int e = tid; e < H; e += NT) {
-    const uint64_t key = (w.ch[e] ^ ((uint64_t)w.cn[e] * 0x9e3779b97f4a7c15ull)) | 1ull;
+    const uint64_t key = (w.ch()[e] ^ ((uint64_t)w.cn()[e] * 0x9e3779b97f4a7c15ull)) | 1ull;
     uint32_t i = (uint32_t)mix64(key) & (uint32_t)(TS - 1);
     for (;;) {
-      const unsigned long long prev = atomicCAS((unsigned long long*)&w.htk[i], 0ull, (unsigned long long)key);
+      const unsigned long long prev = atomicCAS((unsigned long long*)&w.htk()[i], 0ull, (unsigned long long)key);
       if (prev == 0ull || prev == key) break;
       i = (i + 1) & (uint32_t)(TS - 1);
     }
-    atomicMin(&w.htf[i], e);
-    w.hslot[e] = (int)i;
+    atomicMin(&w.htf()[i], e);
+    w.hslot()[e] = (int)i;
   }
   bsync();
-  for (int e = tid; e < H; e += NT) w.first[e] = w.htf[w.hslot[e]];
+  for (int e = tid; e < H; e += NT) w.first()[e] = w.htf()[w.hslot()[e]];
   bsync();
   // distinct prefixes numbered in entry order (d = rank of its first entry)
   int nD = 0;
   {
-    const bool isf = tid < H && w.first[tid] == tid;
+    const bool isf = tid < H && w.first()[tid] == tid;
     int tot = 0;
-    const int d = block_excl_scan(isf ? 1 : 0, tid, w.qoff, &tot);
+    const int d = block_excl_scan(isf ? 1 : 0, tid, w.qoff(), &tot);
     nD = tot;
-    if (isf) { w.dpi[tid] = d; w.e1[d] = tid; w.e2[d] = -1; }
+    if (isf) { w.dpi()[tid] = d; w.e1()[d] = tid; w.e2()[d] = -1; }
   }
   bsync();
   for (int e = tid; e < H; e += NT)
-    if (w.first[e] != e) { const int d = w.dpi[w.first[e]]; w.dpi[e] = d; w.e2[d] = e; }
-  for (int i = tid; i < nD * w.kw; i += NT) w.excl[i] = 0u;
+    if (w.first()[e] != e) { const int d = w.dpi()[w.first()[e]]; w.dpi()[e] = d; w.e2()[d] = e; }
+  for (int i = tid; i < nD * w.kw; i += NT) w.excl()[i] = 0u;
   bsync();
   // -- parent links of flag-0 entries; children exclude their token from the
   //    parent's list (they become repeat groups)
   for (int e = tid; e < H; e += NT) {
     int p = -1;
-    if (w.cf[e] == 0) {
-      const uint64_t key = (w.cph[e] ^ ((uint64_t)(w.cn[e] - 1) * 0x9e3779b97f4a7c15ull)) | 1ull;
+    if (w.cf()[e] == 0) {
+      const uint64_t key = (w.cph()[e] ^ ((uint64_t)(w.cn()[e] - 1) * 0x9e3779b97f4a7c15ull)) | 1ull;
       uint32_t i = (uint32_t)mix64(key) & (uint32_t)(TS - 1);
       for (;;) {
-        const uint64_t k2 = w.htk[i];
+        const uint64_t k2 = w.htk()[i];
         if (k2 == 0ull) break;
-        if (k2 == key) { p = w.dpi[w.htf[i]]; break; }
+        if (k2 == key) { p = w.dpi()[w.htf()[i]]; break; }
         i = (i + 1) & (uint32_t)(TS - 1);
       }
       if (p >= 0) {
-        const int j = w.pos[w.cl[e]];
-        if (j != 0xffff) atomicOr(&w.excl[p * w.kw + (j >> 5)], 1u << (j & 31));
+        const int j = w.pos()[w.cl()[e]];
+        if (j != 0xffff) atomicOr(&w.excl()[p * w.kw + (j >> 5)], 1u << (j & 31));
       }
     }
-    w.pd[e] = p;
+    w.pd()[e] = p;
   }
   bsync();
   // -- specials: blank groups, last-token appends (per prefix), repeat groups (per flag-0 entry)
   for (int d = tid; d < nD; d += NT) {
-    const int a = w.e1[d], b = w.e2[d];
-    double sc = w.cs[a] + eb;
-    if (b >= 0) sc = merge2_exact(sc, w.cs[b] + eb, MX);
-    int s = atomicAdd(&w.misc[0], 1);
+    const int a = w.e1()[d], b = w.e2()[d];
+    double sc = w.cs()[a] + eb;
+    if (b >= 0) sc = merge2_exact(sc, w.cs()[b] + eb, MX);
+    int s = atomicAdd(&w.misc()[0], 1);
     BCHK(s < 3 * beam);
-    w.spsc[s] = sc; w.spbase[s] = a; w.spx[s] = -1; w.spflag[s] = 1; w.spsrc[s] = a; w.sptok[s] = -1;
-    const int c = w.cl[a];
+    w.spsc()[s] = sc; w.spbase()[s] = a; w.spx()[s] = -1; w.spflag()[s] = 1; w.spsrc()[s] = a; w.sptok()[s] = -1;
+    const int c = w.cl()[a];
     if (c >= 0) {
-      const int j = w.pos[c];
+      const int j = w.pos()[c];
       if (j != 0xffff && !bexcl(w, d, j)) {
-        const int f = w.cf[a] == 1 ? a : ((b >= 0 && w.cf[b] == 1) ? b : -1);
+        const int f = w.cf()[a] == 1 ? a : ((b >= 0 && w.cf()[b] == 1) ? b : -1);
         if (f >= 0) {
-          s = atomicAdd(&w.misc[0], 1);
-          w.spsc[s] = w.cs[f] + (double)w.sval[j];
-          w.spbase[s] = a; w.spx[s] = c; w.spflag[s] = 0; w.spsrc[s] = f; w.sptok[s] = c;
+          s = atomicAdd(&w.misc()[0], 1);
+          w.spsc()[s] = w.cs()[f] + (double)w.sval()[j];
+          w.spbase()[s] = a; w.spx()[s] = c; w.spflag()[s] = 0; w.spsrc()[s] = f; w.sptok()[s] = c;
         }
-        atomicOr(&w.excl[d * w.kw + (j >> 5)], 1u << (j & 31));
+        atomicOr(&w.excl()[d * w.kw + (j >> 5)], 1u << (j & 31));
       }
     }
     // A = logaddexp of the prefix's entries (list base)
-    w.lA[d] = b >= 0 ? merge2_exact(w.cs[a], w.cs[b], MX) : w.cs[a];
+    w.lA()[d] = b >= 0 ? merge2_exact(w.cs()[a], w.cs()[b], MX) : w.cs()[a];
   }
   for (int e = tid; e < H; e += NT) {
-    if (w.cf[e] != 0) continue;
-    const int c = w.cl[e];
+    if (w.cf()[e] != 0) continue;
+    const int c = w.cl()[e];
     BCHK(c >= 0 && c < P.V);
     const double ec = (double)row[c];
-    double sc = w.cs[e] + ec, best = sc;  // repeat candidate first (decoder.py:522-530)
+    double sc = w.cs()[e] + ec, best = sc;  // repeat candidate first (decoder.py:522-530)
     int src = e, tok = -1;
-    const int p = w.pd[e];
+    const int p = w.pd()[e];
     if (p >= 0) {
-      const int srcs[2] = {w.e1[p], w.e2[p]};
+      const int srcs[2] = {w.e1()[p], w.e2()[p]};
 #pragma unroll
       for (int q = 0; q < 2; q++) {
         const int h = srcs[q];
-        if (h < 0 || (w.cf[h] == 0 && w.cl[h] == c)) continue;  // blocked repeat (decoder.py:495)
-        const double x = w.cs[h] + ec;
+        if (h < 0 || (w.cf()[h] == 0 && w.cl()[h] == c)) continue;  // blocked repeat (decoder.py:495)
+        const double x = w.cs()[h] + ec;
         sc = merge2_exact(sc, x, MX);
         if (x > best) { best = x; src = h; tok = c; }
       }
     }
-    const int s = atomicAdd(&w.misc[0], 1);
+    const int s = atomicAdd(&w.misc()[0], 1);
     BCHK(s < 3 * beam);
-    w.spsc[s] = sc; w.spbase[s] = e; w.spx[s] = -1; w.spflag[s] = 0; w.spsrc[s] = src; w.sptok[s] = tok;
+    w.spsc()[s] = sc; w.spbase()[s] = e; w.spx()[s] = -1; w.spflag()[s] = 0; w.spsrc()[s] = src; w.sptok()[s] = tok;
   }
   bsync();
-  const int nS = w.misc[0];
+  const int nS = w.misc()[0];
 
   // -- append quotas: d_eff = prefixes whose A exceeds A_d by a margin;
   //    (d, j) can reach the beam only if (d_eff + 1) j < beam
   int q = 0;
   if (tid < nD) {
-    const double Ad = w.lA[tid];
+    const double Ad = w.lA()[tid];
     int deff = 0;
     if (Ad > -INFINITY) {
       const double thr = Ad + 1e-9 * (1.0 + fabs(Ad));
-      for (int d2 = 0; d2 < nD; d2++) deff += w.lA[d2] > thr;
+      for (int d2 = 0; d2 < nD; d2++) deff += w.lA()[d2] > thr;
       q = (beam - 1) / (deff + 1) + 1;
     }
   }
   int nA = 0;
-  const int qo = block_excl_scan(q, tid, w.rec, &nA);
-  if (tid < nD) { w.qoff[tid] = qo; }
-  if (tid == 0) w.qoff[nD] = nA;
+  const int qo = block_excl_scan(q, tid, w.rec(), &nA);
+  if (tid < nD) { w.qoff()[tid] = qo; }
+  if (tid == 0) w.qoff()[nD] = nA;
   bsync();
   const int N = nS + nA;
   int ncap = 2;
@@ -531,26 +646,26 @@ __device__ int bstep(Blk& w, const float* row, int H) {
 
   // -- frame best on approximate scores (specials exact, list heads A + v)
   double lb = -INFINITY;
-  for (int s = tid; s < nS; s += NT) lb = fmax(lb, w.spsc[s]);
+  for (int s = tid; s < nS; s += NT) lb = fmax(lb, w.spsc()[s]);
   for (int d = tid; d < nD; d += NT) {
     const int j0 = jth_valid(w, d, 0, k);
-    if (j0 < k) lb = fmax(lb, w.lA[d] + (double)w.sval[j0]);
+    if (j0 < k) lb = fmax(lb, w.lA()[d] + (double)w.sval()[j0]);
   }
   {
     const uint64_t o64 = lb > -INFINITY ? ord64(lb) : 0ull;
     const uint32_t hi = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32));
     const uint32_t lo = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32) == hi ? (uint32_t)o64 : 0u);
-    if ((tid & 31) == 0) w.ckey[tid >> 5] = ((uint64_t)hi << 32) | lo;  // scratch before the fill
+    if ((tid & 31) == 0) w.ckey()[tid >> 5] = ((uint64_t)hi << 32) | lo;  // scratch before the fill
   }
   bsync();
   uint64_t bk = 0ull;
-  for (int i = 0; i < NT / 32; i++) bk = bk > w.ckey[i] ? bk : w.ckey[i];
+  for (int i = 0; i < NT / 32; i++) bk = bk > w.ckey()[i] ? bk : w.ckey()[i];
   bsync();
   if (bk == 0ull) return 0;  // every extension is -inf (decoder.py:616-620)
 
-  if (tid == 0) w.misc[10] = ncap > w.ncap ? 1 : 0;
+  if (tid == 0) w.misc()[10] = ncap > w.ncap ? 1 : 0;
   bsync();
-  if (!w.misc[10]) {
+  if (!w.misc()[10]) {
     const double best_a = __longlong_as_double((long long)((bk >> 63) ? (bk & 0x7fffffffffffffffull) : ~bk));
     const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
     const double kScale = 4294967294.0 / kR, koff = -(best_a - kR) * kScale;
@@ -560,64 +675,81 @@ __device__ int bstep(Blk& w, const float* row, int H) {
       return 1u + (uint32_t)z;
     };
     // -- candidate keys: (fixed-point score | candidate id); id -> record in crec
+    int live = 0;
     for (int c = tid; c < ncap; c += NT) {
       uint64_t key = 0ull;
       if (c < nS) {
-        const uint32_t kk = keyof(w.spsc[c]);
-        w.crec[c] = kSpecial | (uint32_t)c;
+        const uint32_t kk = keyof(w.spsc()[c]);
+        w.crec()[c] = kSpecial | (uint32_t)c;
         key = kk ? (((uint64_t)kk << 32) | (uint64_t)(0xffffffffu - (uint32_t)c)) : 0ull;
       } else if (c < N) {
         const int g = c - nS;
         int lo = 0, hi = nD - 1;  // list of append slot g: last d with qoff[d] <= g
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (w.qoff[mid] <= g) lo = mid; else hi = mid - 1;
+          if (w.qoff()[mid] <= g) lo = mid; else hi = mid - 1;
         }
-        const int d = lo, j = g - w.qoff[d];
+        const int d = lo, j = g - w.qoff()[d];
         BCHK(d >= 0 && d < nD && j >= 0);
         const int p = jth_valid(w, d, j, k);
-        if (p < k && w.lA[d] > -INFINITY) {
-          const uint32_t kk = keyof(w.lA[d] + (double)w.sval[p]);
-          w.crec[c] = ((uint32_t)d << 12) | (uint32_t)p;
+        if (p < k && w.lA()[d] > -INFINITY) {
+          const uint32_t kk = keyof(w.lA()[d] + (double)w.sval()[p]);
+          w.crec()[c] = ((uint32_t)d << 12) | (uint32_t)p;
           key = kk ? (((uint64_t)kk << 32) | (uint64_t)(0xffffffffu - (uint32_t)c)) : 0ull;
         }
       }
-      w.ckey[c] = key;
+      w.ckey()[c] = key;
+      live += key != 0ull;
     }
     bsync();
     // -- keep the candidates within a margin of the beam-th key (radix
     //    select) and sort only those; a near-tie run that could reach past
     //    the margin sends the frame to the full sort
-    int live = 0;
-    for (int c = tid; c < ncap; c += NT) live += w.ckey[c] != 0ull;
     int nlive = 0;
-    (void)block_excl_scan(live, tid, w.rec, &nlive);
-    uint64_t* sk = w.ckey;
+    (void)block_excl_scan(live, tid, w.rec(), &nlive);
+    uint64_t* sk = w.ckey();
     int nsk = ncap;
     bool trunc = false;
+    uint32_t lim = 1u;
     if (nlive > beam + 1) {
-      const uint32_t T = block_select_hi(w.ckey, ncap, beam + 1, tid, w.hist, w.misc + 6);
-      const uint32_t lim = T > 64u ? T - 64u : 1u;
-      int keep = 0;
-      for (int c = tid; c < ncap; c += NT) keep += (uint32_t)(w.ckey[c] >> 32) >= lim;
-      int nk = 0;
-      int o = block_excl_scan(keep, tid, w.rec, &nk);
-      uint64_t* dst = (uint64_t*)w.ord;  // kBlockCands ints = kBlockCands / 2 keys
-      if (nk <= w.ncap / 2 && nk < nlive) {
-        for (int c = tid; c < ncap; c += NT) {
-          const uint64_t x = w.ckey[c];
-          if ((uint32_t)(x >> 32) >= lim) dst[o++] = x;
-        }
-        int np = 2;
-        while (np < nk) np <<= 1;
-        for (int c = nk + tid; c < np; c += NT) dst[c] = 0ull;
-        bsync();
-        sk = dst;
-        nsk = np;
-        trunc = true;
-      }
+      const uint32_t T = block_select_hi(w.ckey(), ncap, beam + 1, tid, w.hist(), w.misc() + 6);
+      lim = T > 64u ? T - 64u : 1u;
     }
-    block_sort_desc(sk, nsk, tid);
+    int keep = live;
+    if (lim > 1u) {
+      keep = 0;
+      for (int c = tid; c < ncap; c += NT) keep += (uint32_t)(w.ckey()[c] >> 32) >= lim;
+    }
+    int nk = 0;
+    int o = block_excl_scan(keep, tid, w.rec(), &nk);
+    uint64_t* dst = (uint64_t*)w.ord();  // kBlockCands ints = kBlockCands / 2 keys
+    if (nk <= 512) {
+      // survivors: compact to dst[512..), sorted into dst[0, nk)
+      for (int c = tid; c < ncap; c += NT) {
+        const uint64_t x = w.ckey()[c];
+        if ((uint32_t)(x >> 32) >= lim) dst[512 + o++] = x;
+      }
+      bsync();
+      block_sort512(dst + 512, nk, w.skey(), dst, tid);  // skey is free after the top-k
+      sk = dst;
+      nsk = nk;
+      trunc = lim > 1u;
+    } else if (lim > 1u && nk <= w.ncap / 2 && nk < nlive) {
+      for (int c = tid; c < ncap; c += NT) {
+        const uint64_t x = w.ckey()[c];
+        if ((uint32_t)(x >> 32) >= lim) dst[o++] = x;
+      }
+      int np = 2;
+      while (np < nk) np <<= 1;
+      for (int c = nk + tid; c < np; c += NT) dst[c] = 0ull;
+      bsync();
+      sk = dst;
+      nsk = np;
+      trunc = true;
+      block_sort_desc(sk, nsk, tid);
+    } else {
+      block_sort_desc(sk, nsk, tid);
+    }
     // -- exact order where keys are within the tolerance: runs of adjacent
     //    keys (differences <= kTolB) in ranks [0, beam] are re-sorted on exact
     //    descriptors (fp64 fold, token sequence, flag)
@@ -630,9 +762,9 @@ __device__ int bstep(Blk& w, const float* row, int H) {
       const int anytie = __syncthreads_or(tie ? 1 : 0);
       for (int r = tid; r < beam; r += NT) {
         const uint64_t x = r < nsk ? sk[r] : 0ull;
-        w.rec[r] = x ? (int)w.crec[0xffffffffu - (uint32_t)(x & 0xffffffffu)] : -1;
+        w.rec()[r] = x ? (int)w.crec()[0xffffffffu - (uint32_t)(x & 0xffffffffu)] : -1;
       }
-      if (tid == 0) w.misc[9] = 0;
+      if (tid == 0) w.misc()[9] = 0;
       bsync();
       if (anytie) {
         if (tid == 0) {
@@ -643,20 +775,20 @@ __device__ int bstep(Blk& w, const float* row, int H) {
                  (uint32_t)(sk[end - 1] >> 32) - (uint32_t)(sk[end] >> 32) <= (uint32_t)kTolB)
             end++;
           if (trunc && (end >= nsk || sk[end] == 0ull)) {
-            w.misc[9] = 1;  // the run may continue below the margin
+            w.misc()[9] = 1;  // the run may continue below the margin
           } else {
             // exact insertion sort of each run; the run buffer is the tail of
             // the candidate records (crec[ncap ..) is free)
-            int* run = w.runbuf;
+            int* run = w.runbuf();
             const int cap = kBlockRun;
             int a0 = 0;
             while (a0 < end) {
               int b0 = a0 + 1;
               while (b0 < end && (uint32_t)(sk[b0 - 1] >> 32) - (uint32_t)(sk[b0] >> 32) <= (uint32_t)kTolB) b0++;
-              if (b0 - a0 > cap) { w.misc[10] = 1; break; }  // absurd tie run: exact serial path
+              if (b0 - a0 > cap) { w.misc()[10] = 1; break; }  // absurd tie run: exact serial path
               if (b0 - a0 > 1) {
                 const int len = b0 - a0;
-                for (int i = 0; i < len; i++) run[i] = (int)w.crec[0xffffffffu - (uint32_t)(sk[a0 + i] & 0xffffffffu)];
+                for (int i = 0; i < len; i++) run[i] = (int)w.crec()[0xffffffffu - (uint32_t)(sk[a0 + i] & 0xffffffffu)];
                 for (int i = 1; i < len; i++) {
                   const int x = run[i];
                   const BDesc dx = cand_desc(w, (uint32_t)x);
@@ -664,7 +796,7 @@ __device__ int bstep(Blk& w, const float* row, int H) {
                   while (j > 0 && bprecedes(w, dx, cand_desc(w, (uint32_t)run[j - 1]))) { run[j] = run[j - 1]; j--; }
                   run[j] = x;
                 }
-                for (int i = 0; i < len && a0 + i < beam; i++) w.rec[a0 + i] = run[i];
+                for (int i = 0; i < len && a0 + i < beam; i++) w.rec()[a0 + i] = run[i];
               }
               a0 = b0;
             }
@@ -672,29 +804,29 @@ __device__ int bstep(Blk& w, const float* row, int H) {
         }
         bsync();
       }
-      if (!w.misc[9]) break;
+      if (!w.misc()[9]) break;
       // redo with every candidate (rare): full sort of the candidate keys
       bsync();
-      block_sort_desc(w.ckey, ncap, tid);
-      sk = w.ckey;
+      block_sort_desc(w.ckey(), ncap, tid);
+      sk = w.ckey();
       nsk = ncap;
       trunc = false;
     }
   }
-  if (w.misc[10]) {
+  if (w.misc()[10]) {
     // exactly tied prefixes can exceed the candidate buffer (d_eff counts
     // strictly better prefixes only): exact serial selection for this frame
     if (tid == 0) {
       atomicAdd(&P.dbg[kDbgFrames], 1ull);
-      int* head = w.dpi;  // per list: next valid position (dpi is free after grouping)
+      int* head = w.dpi();  // per list: next valid position (dpi is free after grouping)
       for (int d = 0; d < nD; d++) head[d] = jth_valid(w, d, 0, k);
-      int* sord = w.ord;  // specials in exact order
+      int* sord = w.ord();  // specials in exact order
       for (int i = 0; i < nS; i++) {
         int j = i;
-        const BDesc di{w.spsc[i], w.spbase[i], w.spx[i], w.spflag[i]};
+        const BDesc di{w.spsc()[i], w.spbase()[i], w.spx()[i], w.spflag()[i]};
         while (j > 0) {
           const int y = sord[j - 1];
-          if (!bprecedes(w, di, BDesc{w.spsc[y], w.spbase[y], w.spx[y], w.spflag[y]})) break;
+          if (!bprecedes(w, di, BDesc{w.spsc()[y], w.spbase()[y], w.spx()[y], w.spflag()[y]})) break;
           sord[j] = y;
           j--;
         }
@@ -704,18 +836,18 @@ __device__ int bstep(Blk& w, const float* row, int H) {
       for (int r = 0; r < beam; r++) {
         int wd = -2;  // -1: special, >= 0: list
         BDesc best{};
-        if (sp < nS) { const int x = sord[sp]; best = BDesc{w.spsc[x], w.spbase[x], w.spx[x], w.spflag[x]}; wd = -1; }
+        if (sp < nS) { const int x = sord[sp]; best = BDesc{w.spsc()[x], w.spbase()[x], w.spx()[x], w.spflag()[x]}; wd = -1; }
         for (int d = 0; d < nD; d++) {
-          if (head[d] >= k || !(w.lA[d] > -INFINITY)) continue;
-          const BDesc dd{bgen_score(w, d, head[d]), w.e1[d], w.stok[head[d]], 0};
+          if (head[d] >= k || !(w.lA()[d] > -INFINITY)) continue;
+          const BDesc dd{bgen_score(w, d, head[d]), w.e1()[d], w.stok()[head[d]], 0};
           if (wd == -2 || bprecedes(w, dd, best)) { best = dd; wd = d; }
         }
-        if (wd == -2 || !(best.sc > -INFINITY)) { w.rec[r] = -1; continue; }
+        if (wd == -2 || !(best.sc > -INFINITY)) { w.rec()[r] = -1; continue; }
         if (wd == -1) {
-          w.rec[r] = (int)(kSpecial | (uint32_t)sord[sp]);
+          w.rec()[r] = (int)(kSpecial | (uint32_t)sord[sp]);
           sp++;
         } else {
-          w.rec[r] = (wd << 12) | head[wd];
+          w.rec()[r] = (wd << 12) | head[wd];
           int nx = head[wd] + 1;
           while (nx < k && bexcl(w, wd, nx)) nx++;
           head[wd] = nx;
@@ -726,26 +858,26 @@ __device__ int bstep(Blk& w, const float* row, int H) {
   }
   // -- new entries (exact scores), then the exact beam threshold
   for (int r = tid; r < beam; r += NT) {
-    const int rc = w.rec[r];
+    const int rc = w.rec()[r];
     if (rc == -1) continue;
     const uint32_t rec = (uint32_t)rc;
     BCHK((rec & kSpecial) ? (int)(rec & ~kSpecial) < nS : ((int)(rec >> 12) < nD && (int)(rec & 0xfff) < k));
     if (!(rec & kSpecial)) {
       const int d = (int)(rec >> 12), j = (int)(rec & 0xfff);
-      const int a = w.e1[d], c = w.stok[j];
-      w.ns[r] = bgen_score(w, d, j); w.nh[r] = child_hash(w.ch[a], c); w.nph[r] = w.ch[a];
-      w.nl[r] = c; w.nn[r] = w.cn[a] + 1; w.nf[r] = 0; w.ntrel[r] = pack_trel(a, c);
+      const int a = w.e1()[d], c = w.stok()[j];
+      w.ns()[r] = bgen_score(w, d, j); w.nh()[r] = child_hash(w.ch()[a], c); w.nph()[r] = w.ch()[a];
+      w.nl()[r] = c; w.nn()[r] = w.cn()[a] + 1; w.nf()[r] = 0; w.ntrel()[r] = pack_trel(a, c);
     } else {
       const int sx = (int)(rec & ~kSpecial);
-      const int a = w.spbase[sx], x = w.spx[sx];
-      w.ns[r] = w.spsc[sx];
+      const int a = w.spbase()[sx], x = w.spx()[sx];
+      w.ns()[r] = w.spsc()[sx];
       if (x >= 0) {
-        w.nh[r] = child_hash(w.ch[a], x); w.nph[r] = w.ch[a]; w.nl[r] = x; w.nn[r] = w.cn[a] + 1;
+        w.nh()[r] = child_hash(w.ch()[a], x); w.nph()[r] = w.ch()[a]; w.nl()[r] = x; w.nn()[r] = w.cn()[a] + 1;
       } else {
-        w.nh[r] = w.ch[a]; w.nph[r] = w.cph[a]; w.nl[r] = w.cl[a]; w.nn[r] = w.cn[a];
+        w.nh()[r] = w.ch()[a]; w.nph()[r] = w.cph()[a]; w.nl()[r] = w.cl()[a]; w.nn()[r] = w.cn()[a];
       }
-      w.nf[r] = w.spflag[sx];
-      w.ntrel[r] = pack_trel(w.spsrc[sx], w.sptok[sx]);
+      w.nf()[r] = w.spflag()[sx];
+      w.ntrel()[r] = pack_trel(w.spsrc()[sx], w.sptok()[sx]);
     }
   }
   bsync();
@@ -753,53 +885,53 @@ __device__ int bstep(Blk& w, const float* row, int H) {
   // ones (decoder.py:621-623) form a prefix
   int c2 = 0;
   for (int r = tid; r < beam; r += NT)
-    c2 += (w.rec[r] != -1 && w.ns[r] > -INFINITY && (P.threshold_inf || w.ns[r] >= w.ns[0] - P.beam_threshold)) ? 1 : 0;
+    c2 += (w.rec()[r] != -1 && w.ns()[r] > -INFINITY && (P.threshold_inf || w.ns()[r] >= w.ns()[0] - P.beam_threshold)) ? 1 : 0;
   const int Hn = __syncthreads_count(c2);
   // reset the token -> S rank map for the next frame
-  for (int j = tid; j < k; j += NT) w.pos[w.stok[j]] = 0xffff;
+  for (int j = tid; j < k; j += NT) w.pos()[w.stok()[j]] = 0xffff;
   bsync();
   return Hn;
 }
 
 // ------------------------------------------------------------------ finalize (decoder.py:753-817)
-__device__ void bfinalize(Blk& w, int H, int kept) {
+__device__ __forceinline__ void bfinalize(Blk& w, int H, int kept) {
   const Params& P = *w.P;
   const int tid = w.tid, u = w.u;
   for (int e = tid; e < H; e += NT) {
     int f = e;
     for (int q = 0; q < e; q++)
-      if (w.ch[q] == w.ch[e] && w.cn[q] == w.cn[e]) { f = q; break; }
-    w.first[e] = f;
+      if (w.ch()[q] == w.ch()[e] && w.cn()[q] == w.cn()[e]) { f = q; break; }
+    w.first()[e] = f;
   }
-  if (tid == 0) w.misc[0] = 0;
+  if (tid == 0) w.misc()[0] = 0;
   bsync();
   for (int e = tid; e < H; e += NT) {
-    if (w.first[e] != e) continue;
-    double sc = w.cs[e];  // entries are in rank order: the first is the payload (decoder.py:794-797)
+    if (w.first()[e] != e) continue;
+    double sc = w.cs()[e];  // entries are in rank order: the first is the payload (decoder.py:794-797)
     for (int q = e + 1; q < H; q++)
-      if (w.first[q] == e) sc = merge2_exact(sc, w.cs[q], w.P->merge_max != 0);
-    const int s = atomicAdd(&w.misc[0], 1);
-    w.spsc[s] = sc; w.spbase[s] = e; w.spx[s] = -1; w.spflag[s] = 0;
+      if (w.first()[q] == e) sc = merge2_exact(sc, w.cs()[q], w.P->merge_max != 0);
+    const int s = atomicAdd(&w.misc()[0], 1);
+    w.spsc()[s] = sc; w.spbase()[s] = e; w.spx()[s] = -1; w.spflag()[s] = 0;
   }
   bsync();
-  const int nF = w.misc[0];
+  const int nF = w.misc()[0];
   int pad = 2;
   while (pad < nF) pad <<= 1;
   for (int s = tid; s < pad; s += NT)
-    w.ckey[s] = s < nF ? ((ord64(w.spsc[s]) & ~0x3ffull) | (uint64_t)(0x3ff - s)) : 0ull;
+    w.ckey()[s] = s < nF ? ((ord64(w.spsc()[s]) & ~0x3ffull) | (uint64_t)(0x3ff - s)) : 0ull;
   bsync();
-  block_sort_desc(w.ckey, pad, tid);
+  block_sort_desc(w.ckey(), pad, tid);
   // exact order: scores (full precision) then token sequences (tie runs)
   if (tid == 0) {
-    int* ord = w.rec;
-    for (int r = 0; r < nF; r++) ord[r] = 0x3ff - (int)(w.ckey[r] & 0x3ffull);
+    int* ord = w.rec();
+    for (int r = 0; r < nF; r++) ord[r] = 0x3ff - (int)(w.ckey()[r] & 0x3ffull);
     for (int i = 1; i < nF; i++) {
       const int x = ord[i];
-      const BDesc dx{w.spsc[x], w.spbase[x], -1, 0};
+      const BDesc dx{w.spsc()[x], w.spbase()[x], -1, 0};
       int j = i;
       while (j > 0) {
         const int y = ord[j - 1];
-        const BDesc dy{w.spsc[y], w.spbase[y], -1, 0};
+        const BDesc dy{w.spsc()[y], w.spbase()[y], -1, 0};
         if (!bprecedes(w, dx, dy)) break;
         ord[j] = y;
         j--;
@@ -810,12 +942,12 @@ __device__ void bfinalize(Blk& w, int H, int kept) {
   bsync();
   const int nOut = nF < P.nbest ? nF : P.nbest;
   for (int r = tid; r < nOut; r += NT) {
-    const int s = w.rec[r];
+    const int s = w.rec()[r];
     BCHK(s >= 0 && s < 3 * P.beam);
-    const int e = w.spbase[s];
-    const int len = w.cn[e];
+    const int e = w.spbase()[s];
+    const int len = w.cn()[e];
     const size_t o = ((size_t)u * P.nbest + r);
-    P.out_score[o] = w.spsc[s];
+    P.out_score[o] = w.spsc()[s];
     P.out_len[o] = len;
     int* tok_out = P.out_tokens + o * P.T_max;
     int* ts_out = P.out_ts ? P.out_ts + o * P.T_max : nullptr;
@@ -838,26 +970,25 @@ __device__ void bfinalize(Blk& w, int H, int kept) {
 }  // namespace
 
 __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_constant__ Params P) {
-  extern __shared__ __align__(128) uint8_t smem[];
   Blk w;
   w.P = &P;
   w.tid = threadIdx.x;
   const int tid = w.tid;
-  carve(w, smem, P);
+  w.par = 0;
   if (tid == 0)
-    for (int s = 0; s < 2; s++) mbar_init(&w.mbar[s], 1);
-  for (int c = tid; c < P.V; c += NT) w.pos[c] = 0xffff;
-  for (int i = tid; i < 2 * kTieCache; i += NT) w.tc_h[i] = 0ull;
-  for (int i = tid; i <= kTieCache; i += NT) w.tc_r[i] = 0;
+    for (int s = 0; s < 2; s++) mbar_init(&w.mbar()[s], 1);
+  for (int c = tid; c < P.V; c += NT) w.pos()[c] = 0xffff;
+  for (int i = tid; i < 2 * kTieCache; i += NT) w.tc_h()[i] = 0ull;
+  for (int i = tid; i <= kTieCache; i += NT) w.tc_r()[i] = 0;
   fence_mbar_init();
   __syncthreads();
   uint32_t n_issue = 0, n_cons = 0;
   const uint32_t row_copy = (uint32_t)P.V * 4u;
 
   for (;;) {
-    if (tid == 0) w.misc[2] = atomicAdd(P.counter, 1);
+    if (tid == 0) w.misc()[2] = atomicAdd(P.counter, 1);
     __syncthreads();
-    const int item = w.misc[2];
+    const int item = w.misc()[2];
     __syncthreads();
     if (item >= P.B) break;
     const int u = P.order[item];
@@ -884,21 +1015,21 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
         if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
         kept += __popc(bal);
       }
-      if (tid == 0) { P.kept[u] = kept; w.misc[3] = kept; }
+      if (tid == 0) { P.kept[u] = kept; w.misc()[3] = kept; }
     }
     __syncthreads();
-    const int kept = w.misc[3];
+    const int kept = w.misc()[3];
     // -- B. frame loop
-    if (tid == 0) { w.cs[0] = 0.0; w.ch[0] = kEmptyPrefixHash; w.cph[0] = 0ull; w.cl[0] = -1; w.cn[0] = 0; w.cf[0] = 1; }
+    if (tid == 0) { w.cs()[0] = 0.0; w.ch()[0] = kEmptyPrefixHash; w.cph()[0] = 0ull; w.cl()[0] = -1; w.cn()[0] = 0; w.cf()[0] = 1; }
     int H = 1;
     w.steps_done = 0;
     auto issue = [&](int i) {
       const uint32_t slot = n_issue & 1u;
       if (tid == 0 && P.bulk_ok) {
         fence_proxy_async();
-        mbar_arrive_expect_tx(&w.mbar[slot], row_copy);
-        tma_bulk_g2s(w.rows + (size_t)slot * P.row_bytes, ubase + (size_t)fmap[i] * P.stride_t, row_copy,
-                     &w.mbar[slot]);
+        mbar_arrive_expect_tx(&w.mbar()[slot], row_copy);
+        tma_bulk_g2s(w.rows() + (size_t)slot * Blk::row_bytes, ubase + (size_t)fmap[i] * P.stride_t, row_copy,
+                     &w.mbar()[slot]);
       }
       n_issue++;
     };
@@ -909,20 +1040,20 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
       if (i + 1 < kept) issue(i + 1);
       const uint32_t slot = n_cons & 1u;
       if (P.bulk_ok) {
-        mbar_wait(&w.mbar[slot], (n_cons >> 1) & 1u);
+        mbar_wait(&w.mbar()[slot], (n_cons >> 1) & 1u);
       } else {  // rows that are not 16-B multiples: plain copy (no TMA)
-        float* dst = (float*)(w.rows + (size_t)slot * P.row_bytes);
+        float* dst = (float*)(w.rows() + (size_t)slot * Blk::row_bytes);
         const float* src = ubase + (size_t)fmap[i] * P.stride_t;
         for (int c = tid; c < P.V; c += NT) dst[c] = __ldg(src + c);
         __syncthreads();
       }
       n_cons++;
-      const float* row = (const float*)(w.rows + (size_t)slot * P.row_bytes);
+      const float* row = (const float*)(w.rows() + (size_t)slot * Blk::row_bytes);
       btopk(w, row);
       const int Hn = bstep(w, row, H);
       if (Hn == 0) { died = true; break; }
       uint32_t* trow = P.trellis + ((size_t)u * P.T_max + i) * P.beam;
-      for (int r = tid; r < Hn; r += NT) trow[r] = w.ntrel[r];
+      for (int r = tid; r < Hn; r += NT) trow[r] = w.ntrel()[r];
       __syncthreads();
       w.swap_state();
       H = Hn;
@@ -931,7 +1062,7 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
     }
     if (died) {
       while (n_cons < n_issue) {
-        if (P.bulk_ok) mbar_wait(&w.mbar[n_cons & 1u], (n_cons >> 1) & 1u);
+        if (P.bulk_ok) mbar_wait(&w.mbar()[n_cons & 1u], (n_cons >> 1) & 1u);
         n_cons++;
       }
       if (tid == 0) {

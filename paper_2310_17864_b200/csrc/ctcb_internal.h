@@ -186,7 +186,7 @@ struct BlockLayout {
       sval, stok, pos, total;
   int kw, kpad, ts, ncap;
 };
-__host__ __device__ inline BlockLayout make_block_layout(int beam, int kpad, int V, int row_bytes) {
+__host__ __device__ constexpr inline BlockLayout make_block_layout(int beam, int kpad, int V, int row_bytes) {
   BlockLayout L{};
   size_t o = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -207,7 +207,8 @@ __host__ __device__ inline BlockLayout make_block_layout(int beam, int kpad, int
   L.mbar = take(16, 8);
   L.cs = take(8 * B, 8); L.ns = take(8 * B, 8); L.lA = take(8 * B, 8); L.spsc = take(8 * S, 8);
   L.ch = take(8 * B, 8); L.cph = take(8 * B, 8); L.nh = take(8 * B, 8); L.nph = take(8 * B, 8);
-  L.skey = take(8 * (size_t)kpad, 8); L.ckey = take(8 * (size_t)L.ncap, 8); L.htk = take(8 * (size_t)ts, 8);
+  L.skey = take(8 * (size_t)(kpad > 512 ? kpad : 512), 8);  // also sort scratch
+  L.ckey = take(8 * (size_t)L.ncap, 8); L.htk = take(8 * (size_t)ts, 8);
   L.tc_h = take(8 * 2 * kTieCache, 8);
   L.cl = take(4 * B, 4); L.cn = take(4 * B, 4); L.cf = take(4 * B, 4);
   L.nl = take(4 * B, 4); L.nn = take(4 * B, 4); L.nf = take(4 * B, 4);

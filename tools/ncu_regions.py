@@ -5,7 +5,7 @@ kernel code region.
 
 The cuda+sass source view lists a SASS instruction once under every source
 line of its inline call stack; instructions are deduplicated by address and
-attributed to the deepest line of FILE.cu at or after the first region start
+attributed (executed instructions and warp-state samples) to the deepest line of FILE.cu at or after the first region start
 (the call site inside the kernel body), else to the region of the preceding
 address.  Counts are divided by UNITS (e.g. warp-frames).
 """
@@ -21,7 +21,7 @@ first = regions[0][0]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 cur_file, cur_line = "?", 0
-count, lines = {}, {}
+count, samp, lines = {}, {}, {}
 for r in csv.reader(io.StringIO(out)):
     if not r:
         continue
@@ -34,6 +34,10 @@ for r in csv.reader(io.StringIO(out)):
             count[a] = float(r[7])
         except ValueError:
             count.setdefault(a, 0.0)
+        try:
+            samp[a] = float(r[4])
+        except ValueError:
+            samp.setdefault(a, 0.0)
         if cur_file == fname and cur_line >= first:
             lines.setdefault(a, []).append(cur_line)
     else:
@@ -51,12 +55,15 @@ def region_of(line):
     return name
 
 
-agg, last = {}, "prologue"
+agg, sagg, last = {}, {}, "prologue"
 for a in sorted(count):
     if a in lines:
         last = region_of(max(lines[a]))
     agg[last] = agg.get(last, 0.0) + count[a]
+    sagg[last] = sagg.get(last, 0.0) + samp.get(a, 0.0)
 tot = sum(agg.values())
-for k, v in sorted(agg.items(), key=lambda x: -x[1]):
-    print(f"{k:24s} {v / units:8.1f}  {100 * v / tot:5.1f}%")
-print(f"{'total':24s} {tot / units:8.1f}")
+stot = sum(sagg.values()) or 1.0
+print(f"{'region':24s} {'inst/unit':>9s}  {'inst%':>5s}  {'stall-samples%':>14s}")
+for k, v in sorted(agg.items(), key=lambda x: -sagg[x[0]]):
+    print(f"{k:24s} {v / units:9.1f}  {100 * v / tot:5.1f}  {100 * sagg[k] / stot:14.1f}")
+print(f"{'total':24s} {tot / units:9.1f}")
