@@ -282,31 +282,35 @@ __device__ __forceinline__ uint32_t block_select_hi(const uint64_t* key, int n, 
 }
 
 // ------------------------------------------------------------------ token sequences (single-thread slow path)
-__device__ __forceinline__ int bmaterialize(const Blk& w, int e, int len, int* buf) {
-  const Params& P = *w.P;
-  int pos = len, slot = e;
-  for (int i = w.steps_done - 1; i >= 0 && pos > 0; --i) {
-    const uint32_t r = P.trellis[((size_t)w.u * P.T_max + i) * P.beam + slot];
-    const int tok = trel_tok(r);
-    if (tok >= 0) buf[--pos] = tok;
-    slot = trel_src(r);
-  }
-  return len;
-}
+// Token sequences of entries ea, eb (plus an extra token each when x >= 0)
+// in Python tuple order.  Both trellis paths are walked back in lockstep
+// until they reach the same entry: everything before it is a common prefix,
+// so only the two tails (collected last token first) are compared.
 __device__ __forceinline__ int bseq_cmp_full(const Blk& w, int ea, int xa, int eb, int xb, bool* strict) {
   const Params& P = *w.P;
-  atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
-  atomicAdd(&P.dbg[kDbgMatSteps], 2ull * (unsigned long long)w.steps_done);
   int* A = P.seqbuf + (size_t)w.u * 3 * (P.T_max + 1);
   int* Bq = A + P.T_max + 1;
-  int la = bmaterialize(w, ea, w.cn()[ea], A);
+  int la = 0, lb = 0;
   if (xa >= 0) A[la++] = xa;
-  int lb = bmaterialize(w, eb, w.cn()[eb], Bq);
   if (xb >= 0) Bq[lb++] = xb;
+  const uint32_t* tr = P.trellis + (size_t)w.u * P.T_max * P.beam;
+  int sa = ea, sb = eb, i = w.steps_done - 1;
+  for (; i >= 0 && sa != sb; --i) {
+    const uint32_t ra = tr[(size_t)i * P.beam + sa], rb = tr[(size_t)i * P.beam + sb];
+    const int ta = trel_tok(ra), tb = trel_tok(rb);
+    if (ta >= 0) A[la++] = ta;
+    if (tb >= 0) Bq[lb++] = tb;
+    sa = trel_src(ra);
+    sb = trel_src(rb);
+  }
+  atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
+  atomicAdd(&P.dbg[kDbgMatSteps], 2ull * (unsigned long long)(w.steps_done - 1 - i));
   const int n = la < lb ? la : lb;
   *strict = true;
-  for (int i = 0; i < n; i++)
-    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
+  for (int q = 1; q <= n; q++) {
+    const int x = A[la - q], y = Bq[lb - q];
+    if (x != y) return x < y ? -1 : 1;
+  }
   *strict = false;
   return la < lb ? -1 : (la > lb ? 1 : 0);
 }
