@@ -22,6 +22,7 @@ __global__ void ctcb_decode_block_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_framemap_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_topk_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_rowoff_kernel(const __grid_constant__ Params P);
+__global__ void ctcb_topk_wide_kernel(const __grid_constant__ Params P);
 __global__ void ctcb_order_kernel(const int32_t* lens, int B, int32_t* order, int32_t* counter);
 __global__ void ctcb_debug_kernel(const __grid_constant__ Params P, int32_t* out_topk_tok, float* out_topk_val,
                                   float* out_blank);
@@ -178,6 +179,14 @@ bool use_block(const ctcb_handle* h) {
   const char* m = getenv("CTCB_BLOCK");
   return !(m && strcmp(m, "0") == 0);
 }
+// Block kernel with the top-k lists precomputed frame-parallel
+// (ctcb_topk_wide_kernel): V <= 512.  CTCB_BLOCK_TOPK=inline keeps the
+// in-kernel top-k.
+bool use_block_pre(const ctcb_handle* h) {
+  if (!use_block(h) || h->V > ctcb::kSmallV) return false;
+  const char* m = getenv("CTCB_BLOCK_TOPK");
+  return !(m && strcmp(m, "inline") == 0);
+}
 
 struct WsLayout {
   size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, rowoff, total;
@@ -197,7 +206,7 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   w.counter = take(4);
   w.seqbuf = take((size_t)B * 3 * (T + 1) * 4);
   w.anc = take((size_t)B * ((T + ctcb::kChunk - 1) / ctcb::kChunk) * 16);
-  const size_t ntk = use_precomp(h, B) ? (size_t)B * T * h->k : 0;
+  const size_t ntk = use_precomp(h, B) || use_block_pre(h) ? (size_t)B * T * h->k : 0;
   w.topk_tok = take(ntk * 4);
   w.topk_val = take(ntk * 4);
   w.rowoff = take(ntk ? ((size_t)B + 1) * 4 : 0);
@@ -525,6 +534,21 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   if (pair) {  // 4 warps = 8 utterances per block, two halves' shared memory per warp
     P.smem_per_warp = (int)(2 * ctcb::make_pair_layout().total);
     P.warps_per_block = 4;
+  }
+  if (blk && use_block_pre(h)) {
+    // frame maps -> top-k of every kept frame (one warp per row) -> beam walk
+    P.precomp = 1;
+    ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
+    h->launches++;
+    CTCB_CUDA(cudaGetLastError());
+    ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
+    h->launches++;
+    CTCB_CUDA(cudaGetLastError());
+    int tbps = 0;
+    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_wide_kernel, 256, 0));
+    ctcb::ctcb_topk_wide_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 256, 0, s>>>(P);
+    h->launches++;
+    CTCB_CUDA(cudaGetLastError());
   }
   if (blk) {  // one 256-thread CTA per utterance
     P.smem_per_warp = (int)ctcb::make_block_layout(ctcb::kBlockMaxBeam, 256, ctcb::kBlockMaxV, ctcb::kBlockMaxV * 4).total;

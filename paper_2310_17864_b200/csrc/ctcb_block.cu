@@ -1008,8 +1008,11 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
     }
     const float* ubase = P.lp + (size_t)u * P.stride_b;
     int32_t* fmap = P.frame_map + (size_t)u * P.T_max;
-    // -- A. blank-skip compaction (warp 0: ballot + prefix popcount)
-    if (tid < 32) {
+    // -- A. blank-skip compaction (warp 0: ballot + prefix popcount); in
+    //    precomputed mode ctcb_framemap_kernel already did it
+    if (P.precomp) {
+      if (tid == 0) w.misc()[3] = P.kept[u];
+    } else if (tid < 32) {
       int kept = 0;
       for (int t0 = 0; t0 < len; t0 += 32) {
         const int t = t0 + tid;
@@ -1038,6 +1041,15 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
       n_issue++;
     };
     if (kept > 0) issue(0);
+    // precomputed top-k lists (ctcb_topk_wide_kernel), one frame ahead in registers
+    const int k = P.k;
+    const size_t tk_base = (size_t)u * P.T_max * k;
+    int pre_t = 0;
+    float pre_v = 0.0f;
+    if (P.precomp && kept > 0 && tid < k) {
+      pre_t = P.topk_tok[tk_base + tid];
+      pre_v = P.topk_val[tk_base + tid];
+    }
     __syncthreads();
     bool died = false;
     for (int i = 0; i < kept; i++) {
@@ -1053,16 +1065,28 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
       }
       n_cons++;
       const float* row = (const float*)(w.rows() + (size_t)slot * Blk::row_bytes);
-      btopk(w, row);
+      if (P.precomp) {
+        // S of this frame; bstep's first barrier publishes it
+        if (tid < k) {
+          w.stok()[tid] = pre_t;
+          w.sval()[tid] = pre_v;
+          w.pos()[pre_t] = (uint16_t)tid;
+          if (i + 1 < kept) {
+            pre_t = P.topk_tok[tk_base + (size_t)(i + 1) * k + tid];
+            pre_v = P.topk_val[tk_base + (size_t)(i + 1) * k + tid];
+          }
+        }
+      } else {
+        btopk(w, row);
+      }
       const int Hn = bstep(w, row, H);
       if (Hn == 0) { died = true; break; }
+      // ntrel / the row slot are rewritten only after later barriers
       uint32_t* trow = P.trellis + ((size_t)u * P.T_max + i) * P.beam;
       for (int r = tid; r < Hn; r += NT) trow[r] = w.ntrel()[r];
-      __syncthreads();
       w.swap_state();
       H = Hn;
       w.steps_done = i + 1;
-      __syncthreads();
     }
     if (died) {
       while (n_cons < n_issue) {
@@ -1080,6 +1104,44 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
     bfinalize(w, H, kept);
     if (tid == 0) P.status[u] = kUttOk;
     __syncthreads();
+  }
+}
+
+// Frame-parallel top-k for the block kernel (V <= 512, k <= 256): one warp
+// per kept row of the flattened (utterance, kept frame) space, the row's keys
+// (value desc, index asc) sorted in registers, 16 per lane; the first k go to
+// topk_tok / topk_val[u, i, :].  Same order as btopk.
+__global__ void __launch_bounds__(256) ctcb_topk_wide_kernel(const __grid_constant__ Params P) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long total = P.rowoff[P.B];
+  const int V = P.V, k = P.k, blank = P.blank;
+  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < total; g += nw) {
+    int lo = 0, hi = P.B - 1;  // utterance: last u with rowoff[u] <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.rowoff[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const int u = lo, i = (int)(g - P.rowoff[u]);
+    const float* src = P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
+    uint64_t kk[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int c = r * 32 + lane;
+      kk[r] = (c < V && c != blank) ? (((uint64_t)ord32(__ldg(src + c)) << 32) | (uint64_t)(0xffffffffu - (uint32_t)c))
+                                    : 0ull;
+    }
+    warp_sort_desc<16>(kk, lane);
+    const size_t o = ((size_t)u * P.T_max + i) * k;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int j = lane * 16 + r;
+      if (j < k) {
+        const int c = (int)(0xffffffffu - (uint32_t)(kk[r] & 0xffffffffu));
+        P.topk_tok[o + j] = c;
+        P.topk_val[o + j] = __ldg(src + c);  // the row's own bits (signed zeros)
+      }
+    }
   }
 }
 
