@@ -204,6 +204,8 @@ __device__ __forceinline__ void block_sort512(const uint64_t* src, int n, uint64
 }
 
 // Exclusive block scan of one int per thread (NT = 256).
+// kTail = false: the caller guarantees a barrier before tmp is written again.
+template <bool kTail = true>
 __device__ __forceinline__ int block_excl_scan(int v, int tid, int* tmp, int* total) {
   const int lane = tid & 31, wid = tid >> 5;
   int incl = v;
@@ -228,57 +230,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int tid, int* tmp, int* to
   bsync();
   const int r = tmp[wid] + incl - v;
   *total = tmp[NT / 32];
-  bsync();
+  if (kTail) bsync();  // tmp reusable at once
   return r;
-}
-
-// Largest 32-bit value T with #{x >= T} >= need among hi32(key[0..n)) (keys
-// of 0 never count): 8-bit radix select with a block histogram (hist: 256
-// words, misc: 2 words of scratch).  need <= #nonzero, else returns 0.
-__device__ __forceinline__ uint32_t block_select_hi(const uint64_t* key, int n, int need, int tid, uint32_t* hist, int* misc) {
-  uint32_t prefix = 0, pmask = 0;
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int b = tid; b < 256; b += NT) hist[b] = 0;
-    bsync();
-    for (int c = tid; c < n; c += NT) {
-      const uint32_t x = (uint32_t)(key[c] >> 32);
-      if (x && (x & pmask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1u);
-    }
-    bsync();
-    if (tid < 32) {
-      const int lane = tid;
-      uint32_t h[8], sum = 0;
-#pragma unroll
-      for (int q = 0; q < 8; q++) { h[q] = hist[lane * 8 + q]; sum += h[q]; }
-      uint32_t incl = sum;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_down_sync(FULL, incl, off);
-        if (lane + off < 32) incl += v;
-      }
-      uint32_t cum = incl - sum;
-      int found = -1;
-      uint32_t cgt = 0;
-#pragma unroll
-      for (int q = 7; q >= 0; q--) {
-        if (found < 0 && cum < (uint32_t)need && cum + h[q] >= (uint32_t)need) { found = lane * 8 + q; cgt = cum; }
-        cum += h[q];
-      }
-      const unsigned bal = __ballot_sync(FULL, found >= 0);
-      const int src = bal ? __ffs(bal) - 1 : 0;
-      const int digit = __shfl_sync(FULL, found, src);
-      cgt = __shfl_sync(FULL, cgt, src);
-      if (lane == 0) { misc[0] = bal ? digit : -1; misc[1] = (int)cgt; }
-    }
-    bsync();
-    const int digit = misc[0];
-    if (digit < 0) { bsync(); return 0u; }
-    need -= misc[1];
-    prefix |= (uint32_t)digit << shift;
-    pmask |= 0xffu << shift;
-    bsync();
-  }
-  return prefix;
 }
 
 // ------------------------------------------------------------------ token sequences (single-thread slow path)
@@ -454,7 +407,7 @@ __device__ __forceinline__ void btopk(Blk& w, const float* row) {
   const int eq_before = block_excl_scan(neq, tid, w.qoff(), &tot_eq);
   int eq_take = need - eq_before;
   eq_take = eq_take < 0 ? 0 : (eq_take > neq ? neq : eq_take);
-  const int off = block_excl_scan(ngt + eq_take, tid, w.qoff(), &tot);
+  const int off = block_excl_scan<false>(ngt + eq_take, tid, w.qoff(), &tot);
   int o = off, taken = 0;
   for (int q = 0; q < cpt; q++) {
     const int c = tid * cpt + q;
@@ -547,7 +500,7 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
   {
     const bool isf = tid < H && w.first()[tid] == tid;
     int tot = 0;
-    const int d = block_excl_scan(isf ? 1 : 0, tid, w.qoff(), &tot);
+    const int d = block_excl_scan<false>(isf ? 1 : 0, tid, w.qoff(), &tot);
     nD = tot;
     if (isf) { w.dpi()[tid] = d; w.e1()[d] = tid; w.e2()[d] = -1; }
   }
@@ -640,7 +593,7 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
     }
   }
   int nA = 0;
-  const int qo = block_excl_scan(q, tid, w.rec(), &nA);
+  const int qo = block_excl_scan<false>(q, tid, w.rec(), &nA);
   if (tid < nD) { w.qoff()[tid] = qo; }
   if (tid == 0) w.qoff()[nD] = nA;
   bsync();
@@ -659,17 +612,19 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
     const uint64_t o64 = lb > -INFINITY ? ord64(lb) : 0ull;
     const uint32_t hi = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32));
     const uint32_t lo = __reduce_max_sync(FULL, (uint32_t)(o64 >> 32) == hi ? (uint32_t)o64 : 0u);
-    if ((tid & 31) == 0) w.ckey()[tid >> 5] = ((uint64_t)hi << 32) | lo;  // scratch before the fill
+    if ((tid & 31) == 0) w.skey()[tid >> 5] = ((uint64_t)hi << 32) | lo;  // skey: free after the top-k
   }
   bsync();
   uint64_t bk = 0ull;
-  for (int i = 0; i < NT / 32; i++) bk = bk > w.ckey()[i] ? bk : w.ckey()[i];
-  bsync();
+  for (int i = 0; i < NT / 32; i++) bk = bk > w.skey()[i] ? bk : w.skey()[i];
   if (bk == 0ull) return 0;  // every extension is -inf (decoder.py:616-620)
 
-  if (tid == 0) w.misc()[10] = ncap > w.ncap ? 1 : 0;
-  bsync();
-  if (!w.misc()[10]) {
+  // more candidates than the key buffer holds (exactly tied prefixes defeat
+  // the quotas): exact serial selection below; misc[10] is also raised by an
+  // absurdly long tie run and read only after the barriers that follow
+  const bool big = ncap > w.ncap;
+  if (tid == 0) w.misc()[10] = big ? 1 : 0;
+  if (!big) {
     const double best_a = __longlong_as_double((long long)((bk >> 63) ? (bk & 0x7fffffffffffffffull) : ~bk));
     const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
     const double kScale = 4294967294.0 / kR, koff = -(best_a - kR) * kScale;
@@ -679,7 +634,6 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
       return 1u + (uint32_t)z;
     };
     // -- candidate keys: (fixed-point score | candidate id); id -> record in crec
-    int live = 0;
     for (int c = tid; c < ncap; c += NT) {
       uint64_t key = 0ull;
       if (c < nS) {
@@ -703,56 +657,108 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
         }
       }
       w.ckey()[c] = key;
-      live += key != 0ull;
     }
     bsync();
-    // -- keep the candidates within a margin of the beam-th key (radix
-    //    select) and sort only those; a near-tie run that could reach past
-    //    the margin sends the frame to the full sort
-    int nlive = 0;
-    (void)block_excl_scan(live, tid, w.rec(), &nlive);
-    uint64_t* sk = w.ckey();
-    int nsk = ncap;
-    bool trunc = false;
-    uint32_t lim = 1u;
-    if (nlive > beam + 1) {
-      const uint32_t T = block_select_hi(w.ckey(), ncap, beam + 1, tid, w.hist(), w.misc() + 6);
-      lim = T > 64u ? T - 64u : 1u;
+    // -- survivors: keys within a margin of the beam-th, exactly ranked.
+    //    Warps sort strided 64-key chunks of ckey in registers (chunk c =
+    //    slots c, c + nch, ...; at most 4 per warp).  Each chunk's q-th key,
+    //    q = ceil((beam + 1) / nch), bounds the (beam + 1)-th key from below;
+    //    keys under that bound minus the margin cannot reach the beam or its
+    //    tie runs.  The survivors (a prefix of every sorted chunk) are
+    //    compacted and ranked by counting: four barriers in all.
+    const int need = beam + 1;
+    const int nch = (ncap + 63) >> 6;
+    const int q = (need + nch - 1) / nch;
+    const int lane = tid & 31, wid = tid >> 5;
+    uint64_t kk[4][2];
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      const int c = wid + h * (NT / 32);
+      kk[h][0] = kk[h][1] = 0ull;
+      if (c < nch) {
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+          const int i = c + nch * (r * 32 + lane);
+          kk[h][r] = i < ncap ? w.ckey()[i] : 0ull;
+        }
+        const int nz = __popc(__ballot_sync(FULL, kk[h][0] != 0ull)) + __popc(__ballot_sync(FULL, kk[h][1] != 0ull));
+        warp_sort_desc<2>(kk[h], lane);
+#pragma unroll
+        for (int r = 0; r < 2; r++)
+          if (lane * 2 + r == q - 1) w.hist()[32 + c] = (uint32_t)(kk[h][r] >> 32);
+        if (lane == 0) w.hist()[c] = (uint32_t)nz;
+      }
     }
-    int keep = live;
-    if (lim > 1u) {
-      keep = 0;
-      for (int c = tid; c < ncap; c += NT) keep += (uint32_t)(w.ckey()[c] >> 32) >= lim;
+    bsync();
+    uint32_t tau = 0xffffffffu;
+    bool fb = false;
+    for (int c = 0; c < nch; c++) {
+      if ((int)w.hist()[c] < q) fb = true;
+      tau = min(tau, w.hist()[32 + c]);
     }
-    int nk = 0;
-    int o = block_excl_scan(keep, tid, w.rec(), &nk);
-    uint64_t* dst = (uint64_t*)w.ord();  // kBlockCands ints = kBlockCands / 2 keys
-    if (nk <= 512) {
-      // survivors: compact to dst[512..), sorted into dst[0, nk)
-      for (int c = tid; c < ncap; c += NT) {
-        const uint64_t x = w.ckey()[c];
-        if ((uint32_t)(x >> 32) >= lim) dst[512 + o++] = x;
+    const uint32_t lim = fb ? 1u : (tau > 64u ? tau - 64u : 1u);
+    auto surv = [&](uint64_t x) { return x != 0ull && (uint32_t)(x >> 32) >= lim; };
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      const int c = wid + h * (NT / 32);
+      if (c < nch) {
+        const int sc = __popc(__ballot_sync(FULL, surv(kk[h][0]))) + __popc(__ballot_sync(FULL, surv(kk[h][1])));
+        if (lane == 0) w.hist()[64 + c] = (uint32_t)sc;
+      }
+    }
+    bsync();
+    uint64_t* dst = (uint64_t*)w.ord();  // [0, 512): ranked survivors, [512, 1024): compacted
+    int nsurv = 0;
+    for (int c = 0; c < nch; c++) nsurv += (int)w.hist()[64 + c];
+    uint64_t* sk = dst;
+    int nsk = nsurv;
+    bool trunc = lim > 1u;
+    if (nsurv <= 512) {
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        const int c = wid + h * (NT / 32);
+        if (c < nch) {
+          int off = 0;
+          for (int c2 = 0; c2 < c; c2++) off += (int)w.hist()[64 + c2];
+#pragma unroll
+          for (int r = 0; r < 2; r++)
+            if (surv(kk[h][r])) dst[512 + off + lane * 2 + r] = kk[h][r];
+        }
       }
       bsync();
-      block_sort512(dst + 512, nk, w.skey(), dst, tid);  // skey is free after the top-k
-      sk = dst;
-      nsk = nk;
-      trunc = lim > 1u;
-    } else if (lim > 1u && nk <= w.ncap / 2 && nk < nlive) {
-      for (int c = tid; c < ncap; c += NT) {
-        const uint64_t x = w.ckey()[c];
-        if ((uint32_t)(x >> 32) >= lim) dst[o++] = x;
+      for (int t = tid; t < nsurv; t += NT) {
+        const uint64_t x = dst[512 + t];
+        int rank = 0;
+        int i = 0;
+        for (; i + 1 < nsurv; i += 2) {
+          const ulonglong2 y = *(const ulonglong2*)&dst[512 + i];  // 16-B aligned pair
+          rank += (y.x > x) + (y.y > x);
+        }
+        if (i < nsurv) rank += dst[512 + i] > x;
+        dst[rank] = x;
       }
-      int np = 2;
-      while (np < nk) np <<= 1;
-      for (int c = nk + tid; c < np; c += NT) dst[c] = 0ull;
       bsync();
-      sk = dst;
-      nsk = np;
-      trunc = true;
-      block_sort_desc(sk, nsk, tid);
-    } else {
-      block_sort_desc(sk, nsk, tid);
+    } else {  // (almost) every candidate survives: full sort
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        const int c = wid + h * (NT / 32);
+        if (c < nch)
+#pragma unroll
+          for (int r = 0; r < 2; r++) {
+            const int i = c + nch * (lane * 2 + r);
+            if (i < ncap) w.ckey()[i] = kk[h][r];
+          }
+      }
+      bsync();
+      block_sort_desc(w.ckey(), ncap, tid);
+      sk = w.ckey();
+      nsk = ncap;
+      trunc = false;
+    }
+    if (tid == 0) {  // selection statistics (debug counters)
+      atomicAdd(&P.dbg[kDbgRadix], (unsigned long long)N);
+      atomicAdd(&P.dbg[kDbgTopkFix], (unsigned long long)nsurv);
+      atomicAdd(&P.dbg[kDbgOneshotFallback], fb ? 1ull : 0ull);
     }
     // -- exact order where keys are within the tolerance: runs of adjacent
     //    keys (differences <= kTolB) in ranks [0, beam] are re-sorted on exact
@@ -817,7 +823,7 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
       trunc = false;
     }
   }
-  if (w.misc()[10]) {
+  if (big || w.misc()[10]) {
     // exactly tied prefixes can exceed the candidate buffer (d_eff counts
     // strictly better prefixes only): exact serial selection for this frame
     if (tid == 0) {

@@ -217,7 +217,7 @@ __host__ __device__ constexpr inline BlockLayout make_block_layout(int beam, int
   L.spbase = take(4 * S, 4); L.spx = take(4 * S, 4); L.spflag = take(4 * S, 4); L.spsrc = take(4 * S, 4);
   L.sptok = take(4 * S, 4); L.misc = take(4 * 16, 4); L.tc_r = take(4 * (kTieCache + 1), 4);
   L.rec = take(4 * small, 4);
-  L.ord = take(4 * (size_t)L.ncap, 8);  // also the survivor key buffer (u64)
+  L.ord = take(4 * (size_t)L.ncap, 16);  // also the survivor key buffer (u64, read in 16-B pairs)
   L.runbuf = take(4 * kBlockRun, 4);
   L.ntrel = take(4 * B, 4); L.excl = take(4 * B * (size_t)L.kw, 4); L.hist = take(4 * 256, 4);
   L.crec = take(4 * (size_t)L.ncap, 4);
