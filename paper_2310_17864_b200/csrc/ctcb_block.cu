@@ -78,10 +78,11 @@ struct Blk {
   __device__ int* spsrc() const { return (int*)(blk_smem + L.spsrc); }
   __device__ int* sptok() const { return (int*)(blk_smem + L.sptok); }
   __device__ int* misc() const { return (int*)(blk_smem + L.misc); }
-  __device__ int* tc_r() const { return (int*)(blk_smem + L.tc_r); }
+  __device__ int8_t* tc_r() const { return (int8_t*)(blk_smem + L.tc_r); }
   __device__ int* rec() const { return (int*)(blk_smem + L.rec); }
   __device__ int* ord() const { return (int*)(blk_smem + L.ord); }
   __device__ int* runbuf() const { return (int*)(blk_smem + L.runbuf); }
+  __device__ double* runsc() const { return (double*)(blk_smem + L.runsc); }
   __device__ uint32_t* ntrel() const { return (uint32_t*)(blk_smem + L.ntrel); }
   __device__ uint32_t* excl() const { return (uint32_t*)(blk_smem + L.excl); }
   __device__ uint32_t* hist() const { return (uint32_t*)(blk_smem + L.hist); }
@@ -267,21 +268,25 @@ __device__ __forceinline__ int bseq_cmp_full(const Blk& w, int ea, int xa, int e
   *strict = false;
   return la < lb ? -1 : (la > lb ? 1 : 0);
 }
+// Sequence-order cache: direct-mapped on the unordered pair of sequence
+// hashes, holding the order of the lower hash's sequence against the other.
+// Results hold across utterances (a hash names one token sequence).
+__device__ __forceinline__ int btc_slot(uint64_t lo, uint64_t hi) {
+  return (int)(mix64(lo * 0x9e3779b97f4a7c15ull ^ hi) & (uint64_t)(kBlockTieCache - 1));
+}
 __device__ __forceinline__ int btc_lookup(const Blk& w, uint64_t ha, uint64_t hb) {
-#pragma unroll 1
-  for (int i = 0; i < kTieCache; i++) {
-    if (w.tc_h()[2 * i] == ha && w.tc_h()[2 * i + 1] == hb) return w.tc_r()[i];
-    if (w.tc_h()[2 * i] == hb && w.tc_h()[2 * i + 1] == ha) return -w.tc_r()[i];
-  }
-  return 0;
+  const uint64_t lo = ha < hb ? ha : hb, hi = ha < hb ? hb : ha;
+  const int i = btc_slot(lo, hi);
+  if (w.tc_h()[2 * i] != lo || w.tc_h()[2 * i + 1] != hi) return 0;
+  const int r = w.tc_r()[i];
+  return ha < hb ? r : -r;
 }
 __device__ __forceinline__ void btc_insert(const Blk& w, uint64_t ha, uint64_t hb, int r) {
-  if (btc_lookup(w, ha, hb)) return;
-  const int i = w.tc_r()[kTieCache];
-  w.tc_h()[2 * i] = ha;
-  w.tc_h()[2 * i + 1] = hb;
-  w.tc_r()[i] = r;
-  w.tc_r()[kTieCache] = (i + 1) % kTieCache;
+  const uint64_t lo = ha < hb ? ha : hb, hi = ha < hb ? hb : ha;
+  const int i = btc_slot(lo, hi);
+  w.tc_h()[2 * i] = lo;
+  w.tc_h()[2 * i + 1] = hi;
+  w.tc_r()[i] = (int8_t)(ha < hb ? r : -r);
 }
 // Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token).
 __device__ __forceinline__ int bseq_cmp(const Blk& w, int ea, int xa, int eb, int xb) {
@@ -467,6 +472,15 @@ __device__ __forceinline__ BDesc cand_desc(const Blk& w, uint32_t rec) {
   }
   const int d = (int)(rec >> 12), j = (int)(rec & 0xfff);
   return BDesc{bgen_score(w, d, j), w.e1()[d], w.stok()[j], 0};
+}
+
+// Descriptor of candidate record `rec` with its exact score already known.
+__device__ __forceinline__ BDesc desc_sc(const Blk& w, uint32_t rec, double sc) {
+  if (rec & kSpecial) {
+    const int s = (int)(rec & ~kSpecial);
+    return BDesc{sc, w.spbase()[s], w.spx()[s], w.spflag()[s]};
+  }
+  return BDesc{sc, w.e1()[(int)(rec >> 12)], w.stok()[(int)(rec & 0xfff)], 0};
 }
 
 // One frame step; returns the new beam size (0: beam died).
@@ -784,35 +798,56 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
           while (end < nsk && sk[end] != 0ull &&
                  (uint32_t)(sk[end - 1] >> 32) - (uint32_t)(sk[end] >> 32) <= (uint32_t)kTolB)
             end++;
-          if (trunc && (end >= nsk || sk[end] == 0ull)) {
-            w.misc()[9] = 1;  // the run may continue below the margin
-          } else {
-            // exact insertion sort of each run; the run buffer is the tail of
-            // the candidate records (crec[ncap ..) is free)
-            int* run = w.runbuf();
-            const int cap = kBlockRun;
-            int a0 = 0;
-            while (a0 < end) {
-              int b0 = a0 + 1;
-              while (b0 < end && (uint32_t)(sk[b0 - 1] >> 32) - (uint32_t)(sk[b0] >> 32) <= (uint32_t)kTolB) b0++;
-              if (b0 - a0 > cap) { w.misc()[10] = 1; break; }  // absurd tie run: exact serial path
-              if (b0 - a0 > 1) {
-                const int len = b0 - a0;
-                for (int i = 0; i < len; i++) run[i] = (int)w.crec()[0xffffffffu - (uint32_t)(sk[a0 + i] & 0xffffffffu)];
-                for (int i = 1; i < len; i++) {
-                  const int x = run[i];
-                  const BDesc dx = cand_desc(w, (uint32_t)x);
-                  int j = i;
-                  while (j > 0 && bprecedes(w, dx, cand_desc(w, (uint32_t)run[j - 1]))) { run[j] = run[j - 1]; j--; }
-                  run[j] = x;
-                }
-                for (int i = 0; i < len && a0 + i < beam; i++) w.rec()[a0 + i] = run[i];
-              }
-              a0 = b0;
-            }
-          }
+          // the run may continue below the margin: redo on all candidates
+          w.misc()[9] = (trunc && (end >= nsk || sk[end] == 0ull)) ? 1 : 0;
+          w.misc()[12] = end;
         }
         bsync();
+        const int end = w.misc()[12];
+        if (!w.misc()[9]) {
+          // exact fp64 scores of ranks [0, end) in parallel, then thread 0
+          // insertion-sorts each run (token sequences only on exact ties)
+          if (end <= kBlockRun)
+            for (int r = tid; r < end; r += NT) {
+              const uint32_t id = w.crec()[0xffffffffu - (uint32_t)(sk[r] & 0xffffffffu)];
+              w.runbuf()[r] = (int)id;
+              w.runsc()[r] = cand_desc(w, id).sc;
+            }
+          bsync();
+          if (tid == 0) {
+            if (end > kBlockRun) {
+              w.misc()[10] = 1;  // absurd tie run: exact serial path
+            } else {
+              int* run = w.runbuf();
+              double* rsc = w.runsc();
+              int a0 = 0;
+              while (a0 < end) {
+                int b0 = a0 + 1;
+                while (b0 < end && (uint32_t)(sk[b0 - 1] >> 32) - (uint32_t)(sk[b0] >> 32) <= (uint32_t)kTolB) b0++;
+                for (int i = a0 + 1; i < b0; i++) {
+                  const int x = run[i];
+                  const double xs = rsc[i];
+                  int j = i;
+                  while (j > a0) {
+                    const double ys = rsc[j - 1];
+                    bool prec = xs > ys;
+                    if (xs == ys) prec = bprecedes(w, desc_sc(w, (uint32_t)x, xs), desc_sc(w, (uint32_t)run[j - 1], ys));
+                    if (!prec) break;
+                    run[j] = run[j - 1];
+                    rsc[j] = ys;
+                    j--;
+                  }
+                  run[j] = x;
+                  rsc[j] = xs;
+                }
+                if (b0 - a0 > 1)
+                  for (int i = a0; i < b0 && i < beam; i++) w.rec()[i] = run[i];
+                a0 = b0;
+              }
+            }
+          }
+          bsync();
+        }
       }
       if (!w.misc()[9]) break;
       // redo with every candidate (rare): full sort of the candidate keys
@@ -988,8 +1023,8 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
   if (tid == 0)
     for (int s = 0; s < 2; s++) mbar_init(&w.mbar()[s], 1);
   for (int c = tid; c < P.V; c += NT) w.pos()[c] = 0xffff;
-  for (int i = tid; i < 2 * kTieCache; i += NT) w.tc_h()[i] = 0ull;
-  for (int i = tid; i <= kTieCache; i += NT) w.tc_r()[i] = 0;
+  for (int i = tid; i < 2 * kBlockTieCache; i += NT) w.tc_h()[i] = 0ull;
+  for (int i = tid; i < kBlockTieCache; i += NT) w.tc_r()[i] = 0;
   fence_mbar_init();
   __syncthreads();
   uint32_t n_issue = 0, n_cons = 0;

@@ -180,9 +180,10 @@ constexpr int kBlockMaxBeam = 128;
 constexpr int kBlockMaxV = 2048;
 constexpr int kBlockCands = 2048;  // candidate keys per frame (specials + quota appends)
 constexpr int kBlockRun = 512;     // longest near-tie run re-sorted exactly
+constexpr int kBlockTieCache = 512;  // hashed sequence-order cache entries (power of 2)
 struct BlockLayout {
   size_t rows, mbar, cs, ns, lA, spsc, ch, cph, nh, nph, skey, ckey, htk, tc_h, cl, cn, cf, nl, nn, nf, htf, hslot,
-      first, dpi, pd, e1, e2, qoff, spbase, spx, spflag, spsrc, sptok, misc, tc_r, rec, ord, runbuf, ntrel, excl, hist, crec,
+      first, dpi, pd, e1, e2, qoff, spbase, spx, spflag, spsrc, sptok, misc, tc_r, rec, ord, runbuf, runsc, ntrel, excl, hist, crec,
       sval, stok, pos, total;
   int kw, kpad, ts, ncap;
 };
@@ -209,16 +210,16 @@ __host__ __device__ constexpr inline BlockLayout make_block_layout(int beam, int
   L.ch = take(8 * B, 8); L.cph = take(8 * B, 8); L.nh = take(8 * B, 8); L.nph = take(8 * B, 8);
   L.skey = take(8 * (size_t)(kpad > 512 ? kpad : 512), 8);  // also sort scratch
   L.ckey = take(8 * (size_t)L.ncap, 8); L.htk = take(8 * (size_t)ts, 8);
-  L.tc_h = take(8 * 2 * kTieCache, 8);
+  L.tc_h = take(8 * 2 * kBlockTieCache, 8);
   L.cl = take(4 * B, 4); L.cn = take(4 * B, 4); L.cf = take(4 * B, 4);
   L.nl = take(4 * B, 4); L.nn = take(4 * B, 4); L.nf = take(4 * B, 4);
   L.htf = take(4 * (size_t)ts, 4); L.hslot = take(4 * B, 4); L.first = take(4 * B, 4); L.dpi = take(4 * B, 4);
   L.pd = take(4 * B, 4); L.e1 = take(4 * B, 4); L.e2 = take(4 * B, 4); L.qoff = take(4 * small, 4);
   L.spbase = take(4 * S, 4); L.spx = take(4 * S, 4); L.spflag = take(4 * S, 4); L.spsrc = take(4 * S, 4);
-  L.sptok = take(4 * S, 4); L.misc = take(4 * 16, 4); L.tc_r = take(4 * (kTieCache + 1), 4);
+  L.sptok = take(4 * S, 4); L.misc = take(4 * 16, 4); L.tc_r = take(kBlockTieCache, 4);
   L.rec = take(4 * small, 4);
   L.ord = take(4 * (size_t)L.ncap, 16);  // also the survivor key buffer (u64, read in 16-B pairs)
-  L.runbuf = take(4 * kBlockRun, 4);
+  L.runbuf = take(4 * kBlockRun, 4); L.runsc = take(8 * kBlockRun, 8);
   L.ntrel = take(4 * B, 4); L.excl = take(4 * B * (size_t)L.kw, 4); L.hist = take(4 * 256, 4);
   L.crec = take(4 * (size_t)L.ncap, 4);
   L.sval = take(4 * (size_t)kpad, 4); L.stok = take(4 * (size_t)kpad, 4); L.pos = take(2 * (size_t)V, 2);
