@@ -772,7 +772,6 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
     if (tid == 0) {  // selection statistics (debug counters)
       atomicAdd(&P.dbg[kDbgRadix], (unsigned long long)N);
       atomicAdd(&P.dbg[kDbgTopkFix], (unsigned long long)nsurv);
-      atomicAdd(&P.dbg[kDbgOneshotFallback], fb ? 1ull : 0ull);
     }
     // -- exact order where keys are within the tolerance: runs of adjacent
     //    keys (differences <= kTolB) in ranks [0, beam] are re-sorted on exact
@@ -801,6 +800,7 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
           // the run may continue below the margin: redo on all candidates
           w.misc()[9] = (trunc && (end >= nsk || sk[end] == 0ull)) ? 1 : 0;
           w.misc()[12] = end;
+          w.misc()[13] = 0;
         }
         bsync();
         const int end = w.misc()[12];
@@ -814,16 +814,56 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
               w.runsc()[r] = cand_desc(w, id).sc;
             }
           bsync();
-          if (tid == 0) {
+          // each run's first rank sorts it by exact score; runs holding
+          // exactly equal scores (token-sequence order, shared scratch) are
+          // left to thread 0
+          auto near = [&](int r) {  // ranks r - 1 and r within the key tolerance
+            return (uint32_t)(sk[r - 1] >> 32) - (uint32_t)(sk[r] >> 32) <= (uint32_t)kTolB;
+          };
+          int* run = w.runbuf();
+          double* rsc = w.runsc();
+          if (end <= kBlockRun)
+            for (int r0 = tid; r0 + 1 < end; r0 += NT) {
+              if ((r0 > 0 && near(r0)) || !near(r0 + 1)) continue;  // not the start of a run of >= 2
+              int b0 = r0 + 2;
+              while (b0 < end && near(b0)) b0++;
+              bool eq = false;
+              for (int i = r0 + 1; i < b0; i++) {
+                const int x = run[i];
+                const double xs = rsc[i];
+                int j = i;
+                while (j > r0 && xs >= rsc[j - 1]) {
+                  if (xs == rsc[j - 1]) { eq = true; break; }
+                  run[j] = run[j - 1];
+                  rsc[j] = rsc[j - 1];
+                  j--;
+                }
+                run[j] = x;
+                rsc[j] = xs;
+              }
+              if (eq) {
+                const int f = atomicAdd(&w.misc()[13], 1);
+                if (f < 64) { w.hist()[128 + 2 * f] = (uint32_t)r0; w.hist()[129 + 2 * f] = (uint32_t)b0; }
+              } else {
+                for (int i = r0; i < b0 && i < beam; i++) w.rec()[i] = run[i];
+              }
+            }
+          bsync();
+          const int nflag = w.misc()[13];
+          if (tid == 0 && (nflag || end > kBlockRun)) {
             if (end > kBlockRun) {
               w.misc()[10] = 1;  // absurd tie run: exact serial path
             } else {
-              int* run = w.runbuf();
-              double* rsc = w.runsc();
-              int a0 = 0;
-              while (a0 < end) {
-                int b0 = a0 + 1;
-                while (b0 < end && (uint32_t)(sk[b0 - 1] >> 32) - (uint32_t)(sk[b0] >> 32) <= (uint32_t)kTolB) b0++;
+              for (int f = 0; f < nflag; f++) {
+                int a0, b0;
+                if (nflag <= 64) {
+                  a0 = (int)w.hist()[128 + 2 * f];
+                  b0 = (int)w.hist()[129 + 2 * f];
+                } else {  // too many to list: rescan every run
+                  if (f > 0) break;
+                  a0 = 0;
+                  b0 = end;
+                }
                 for (int i = a0 + 1; i < b0; i++) {
                   const int x = run[i];
                   const double xs = rsc[i];
@@ -840,9 +880,7 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
                   run[j] = x;
                   rsc[j] = xs;
                 }
-                if (b0 - a0 > 1)
-                  for (int i = a0; i < b0 && i < beam; i++) w.rec()[i] = run[i];
-                a0 = b0;
+                for (int i = a0; i < b0 && i < beam; i++) w.rec()[i] = run[i];
               }
             }
           }
@@ -850,6 +888,7 @@ __device__ __forceinline__ int bstep(Blk& w, const float* row, int H) {
         }
       }
       if (!w.misc()[9]) break;
+      if (tid == 0) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);  // redo count
       // redo with every candidate (rare): full sort of the candidate keys
       bsync();
       block_sort_desc(w.ckey(), ncap, tid);
