@@ -1188,15 +1188,39 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
 }
 
 // Frame-parallel top-k for the block kernel (V <= 512, k <= 256): one warp
-// per kept row of the flattened (utterance, kept frame) space, the row's keys
-// (value desc, index asc) sorted in registers, 16 per lane; the first k go to
-// topk_tok / topk_val[u, i, :].  Same order as btopk.
-__global__ void __launch_bounds__(256) ctcb_topk_wide_kernel(const __grid_constant__ Params P) {
-  const int lane = threadIdx.x & 31;
+// per kept row of the flattened (utterance, kept frame) space.  The k-th
+// largest value key is found by a bitwise radix select (one warp reduction
+// per bit), the keys above it plus the lowest-index ones equal to it are
+// ballot-compacted into shared memory and sorted in registers (value desc,
+// index asc); they go to topk_tok / topk_val[u, i, :].  Same S as btopk.
+template <int R>
+__device__ __forceinline__ void topk_sort_write(const uint64_t* buf, int k, const float* src, int32_t* tok,
+                                                float* val, int lane) {
+  uint64_t kk[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const int i = r * 32 + lane;
+    kk[r] = i < k ? buf[i] : 0ull;
+  }
+  warp_sort_desc<R>(kk, lane);
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const int j = lane * R + r;
+    if (j < k) {
+      const int c = (int)(0xffffffffu - (uint32_t)(kk[r] & 0xffffffffu));
+      tok[j] = c;
+      val[j] = __ldg(src + c);  // the row's own bits (signed zeros)
+    }
+  }
+}
+__global__ void __launch_bounds__(256, 3) ctcb_topk_wide_kernel(const __grid_constant__ Params P) {
+  __shared__ uint64_t sbuf[8][256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t* buf = sbuf[wid];
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   const long long total = P.rowoff[P.B];
   const int V = P.V, k = P.k, blank = P.blank;
-  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < total; g += nw) {
+  for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + wid; g < total; g += nw) {
     int lo = 0, hi = P.B - 1;  // utterance: last u with rowoff[u] <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -1204,24 +1228,45 @@ __global__ void __launch_bounds__(256) ctcb_topk_wide_kernel(const __grid_consta
     }
     const int u = lo, i = (int)(g - P.rowoff[u]);
     const float* src = P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
-    uint64_t kk[16];
+    uint32_t key[16];  // ord32 + 1 (0: absent), token r * 32 + lane
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const int c = r * 32 + lane;
-      kk[r] = (c < V && c != blank) ? (((uint64_t)ord32(__ldg(src + c)) << 32) | (uint64_t)(0xffffffffu - (uint32_t)c))
-                                    : 0ull;
+      key[r] = (c < V && c != blank) ? ord32(__ldg(src + c)) : 0u;
     }
-    warp_sort_desc<16>(kk, lane);
-    const size_t o = ((size_t)u * P.T_max + i) * k;
+    // largest T with #{key >= T} >= k
+    uint32_t T = 0u;
+    for (int bit = 31; bit >= 0; bit--) {
+      const uint32_t cand = T | (1u << bit);
+      int n = 0;
+#pragma unroll
+      for (int r = 0; r < 16; r++) n += key[r] >= cand;
+      if (__reduce_add_sync(FULL, n) >= k) T = cand;
+    }
+    // keys > T, then the lowest-index keys == T up to k, compacted in token order
+    int ngt = 0;
+#pragma unroll
+    for (int r = 0; r < 16; r++) ngt += key[r] > T;
+    int need_eq = k - (int)__reduce_add_sync(FULL, ngt);
+    int o = 0;
 #pragma unroll
     for (int r = 0; r < 16; r++) {
-      const int j = lane * 16 + r;
-      if (j < k) {
-        const int c = (int)(0xffffffffu - (uint32_t)(kk[r] & 0xffffffffu));
-        P.topk_tok[o + j] = c;
-        P.topk_val[o + j] = __ldg(src + c);  // the row's own bits (signed zeros)
-      }
+      const int c = r * 32 + lane;
+      const bool eq = key[r] == T && (c < V && c != blank);
+      const unsigned beq = __ballot_sync(FULL, eq);
+      const int rank_eq = __popc(beq & lanemask_lt());
+      const bool take = key[r] > T || (eq && rank_eq < need_eq);
+      need_eq -= __popc(beq) < need_eq ? __popc(beq) : need_eq;
+      const unsigned bt = __ballot_sync(FULL, take);
+      if (take) buf[o + __popc(bt & lanemask_lt())] = ((uint64_t)key[r] << 32) | (uint64_t)(0xffffffffu - (uint32_t)c);
+      o += __popc(bt);
     }
+    __syncwarp();
+    const size_t ob = ((size_t)u * P.T_max + i) * k;
+    if (k <= 64) topk_sort_write<2>(buf, k, src, P.topk_tok + ob, P.topk_val + ob, lane);
+    else if (k <= 128) topk_sort_write<4>(buf, k, src, P.topk_tok + ob, P.topk_val + ob, lane);
+    else topk_sort_write<8>(buf, k, src, P.topk_tok + ob, P.topk_val + ob, lane);
+    __syncwarp();
   }
 }
 
