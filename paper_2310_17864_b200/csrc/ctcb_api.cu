@@ -569,9 +569,10 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     // up to 2 utterances per SM: one CTA per SM walking the longest-first
     // queue beats two co-resident CTAs (the longest utterances set the time
     // and run ~25 % slower sharing an SM); CTCB_BLOCK_PER_SM overrides
+    const int occ = blocks_per_sm;
     if (B <= 2 * h->num_sms) blocks_per_sm = 1;
     const char* m = getenv("CTCB_BLOCK_PER_SM");
-    if (m && atoi(m) > 0 && atoi(m) <= blocks_per_sm) blocks_per_sm = atoi(m);
+    if (m && atoi(m) > 0) blocks_per_sm = atoi(m) < occ ? atoi(m) : occ;
   }
   int grid = h->num_sms * blocks_per_sm;
   if (grid > need) grid = need;
