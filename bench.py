@@ -265,6 +265,8 @@ def main():
     ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-validate", action="store_true",
+                    help="turn off the input validation fused into the decode (on by default, as in ctcforge)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--beam", type=int, default=None, help="override the config's beam (cfg2 sweep: 1/10/50/100)")
     ap.add_argument("--weak", action="store_true",
@@ -326,7 +328,7 @@ def main():
     torch.cuda.synchronize(dev)
 
     dec = cuda_ctc_decoder(synth.simple_tokens(cfg.vocab), nbest=cfg.nbest, beam_size=cfg.beam,
-                           blank_skip_threshold=cfg.threshold)
+                           blank_skip_threshold=cfg.threshold, validate=not args.no_validate)
     frames_rank = int(lens.sum())
     alg_bytes, kept_rank = algorithmic_bytes(host.numpy(), lens, dec.cutoff)
 
@@ -451,6 +453,7 @@ def main():
             "config": {"workload": cfg.name, "batch": cfg.batch, "batch_per_rank": len(shard), "vocab": cfg.vocab, "beam": cfg.beam,
                        "nbest": cfg.nbest, "blank_skip_threshold": cfg.threshold, "t_range": [cfg.t_min, cfg.t_max],
                        "frames": int(frames_all), "parallelism": f"lpt-shard x{world}",
+                       "validate": "off" if args.no_validate else "strict (fused)",
                        "l2": f"inputs larger than L2 ({host.numel() * 4 / 1e9:.1f} GB per rank), no flush"},
             "utterances_per_s": utts_all / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -49,6 +49,11 @@ enum {
                               kept-frame index where it died */
   CTCB_UTT_OVERFLOW = 4,   /* fused search (LM / silence bonus): more near-tied candidates at the
                               beam cut than the kernel's window holds; out_len[b][0] = frame */
+  /* input validation (ctcb_set_validate; EmissionMatrix.__post_init__, emissions.py:128-150):
+     out_len[b][0] = the first offending frame, out_count[b] = its token (-1 for NOT_NORMALIZED) */
+  CTCB_UTT_NONFINITE = 5,       /* a NaN or infinite log-probability */
+  CTCB_UTT_ABOVE_ZERO = 6,      /* a log-probability above MAX_LOG_PROB = 1e-4 */
+  CTCB_UTT_NOT_NORMALIZED = 7,  /* |fp64 logsumexp(row)| > ROW_NORM_TOL = 1e-3 (strict mode) */
 };
 
 /* Create a decoder.  Replaces DecoderOptions (decoder.py:34-66) + the
@@ -147,6 +152,16 @@ int ctcb_decode_host_wait(ctcb_t* h, int chunk, int* b0, int* b1);
 int ctcb_debug_frames(ctcb_t* h, const float* log_probs, int64_t stride_b, int64_t stride_t,
                       const int32_t* lens, int batch, int t_max, void* stream, int32_t* out_frame_map,
                       int32_t* out_kept, int32_t* out_topk_tok, float* out_topk_val, float* out_blank);
+
+/* Input validation fused into every decode (default mode 1), replacing
+ * EmissionMatrix(strict=True).__post_init__ (emissions.py:128-150) that
+ * ctcforge runs on each utterance before decoding: mode 0 off, 1 strict,
+ * 2 without the normalisation check (strict=False).  The decode kernels screen
+ * each row as they stage it; rows they do not stage (blank-skipped frames,
+ * frames after a dead beam) are checked by a follow-up kernel.  An invalid
+ * utterance's out_status is CTCB_UTT_NONFINITE / _ABOVE_ZERO / _NOT_NORMALIZED
+ * for its first offender in the reference's order, overriding the decode's. */
+int ctcb_set_validate(ctcb_t* h, int mode);
 
 /* Validation pass mirroring EmissionMatrix(strict=True) (emissions.py:128-150):
  * first offending (b, t, v) of: non-finite value (code 1), value > 1e-4

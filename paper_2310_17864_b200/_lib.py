@@ -16,11 +16,12 @@ LIB_PATH = os.environ.get("CTCB_LIB") or os.path.join(_HERE, "libctcb.so")
 
 CTCB_OK, CTCB_ERR_ARG, CTCB_ERR_CUDA, CTCB_ERR_WORKSPACE, CTCB_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 UTT_OK, UTT_EMPTY, UTT_BAD_LEN, UTT_BEAM_DIED, UTT_OVERFLOW = 0, 1, 2, 3, 4
+UTT_NONFINITE, UTT_ABOVE_ZERO, UTT_NOT_NORMALIZED = 5, 6, 7
 
 # every symbol include/ctcb.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
     "ctcb_create", "ctcb_destroy", "ctcb_skip_cutoff", "ctcb_topk_size", "ctcb_workspace_bytes",
-    "ctcb_decode", "ctcb_decode_host", "ctcb_debug_frames", "ctcb_validate", "ctcb_debug_counters", "ctcb_status_string",
+    "ctcb_decode", "ctcb_decode_host", "ctcb_debug_frames", "ctcb_validate", "ctcb_set_validate", "ctcb_debug_counters", "ctcb_status_string",
     "ctcb_last_error", "ctcb_kernel_timing", "ctcb_kernel_time", "ctcb_launch_count", "ctcb_decode_host_async", "ctcb_decode_host_wait",
     "ctcb_set_merge_mode", "ctcb_set_beam_size_token", "ctcb_align", "ctcb_align_workspace_bytes",
     "ctcb_lm_create", "ctcb_lm_destroy", "ctcb_set_lm", "ctcb_set_silence", "ctcb_decode_lm",
@@ -65,6 +66,7 @@ def load():
     lib.ctcb_decode_host.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp]
     lib.ctcb_debug_frames.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp]
     lib.ctcb_validate.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, c_int, vp, vp]
+    lib.ctcb_set_validate.argtypes = [vp, c_int]
     lib.ctcb_debug_counters.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
     lib.ctcb_decode_host_async.argtypes = [vp, vp, c_int64, c_int64, vp, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp,
                                            vp, ctypes.POINTER(c_int)]

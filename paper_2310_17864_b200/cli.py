@@ -404,8 +404,8 @@ def _token_dictionary(cfg: dict) -> TokenDictionary:
 
 class _DecodeJob:
     """One CUDA decoder for the whole corpus; per batch: map / parse the
-    files, copy their rows into one pinned [B, T, V] buffer, validate on the
-    device (ctcb_validate), decode, and build the records."""
+    files, copy their rows into one pinned [B, T, V] buffer, decode with the
+    input checks fused in (ctcb_set_validate), and build the records."""
 
     def __init__(self, cfg: dict, opts, tokens: TokenDictionary, lm):
         import torch
@@ -460,8 +460,6 @@ class _DecodeJob:
                 self.failed.append(utt)
 
     def _decode(self, files: list) -> dict:
-        import ctypes
-
         from . import _lib
 
         torch, dec = self.torch, self.dec
@@ -475,23 +473,10 @@ class _DecodeJob:
         x = host.to(dec.device, non_blocking=True)
         lens_dev = torch.from_numpy(lens).to(dec.device)
         errors = {}
-        # EmissionMatrix checks (emissions.py:128-150) on the device: the first
-        # offending (b, t, v) fails utterance b, which is masked out (length 0)
-        # before the batch is checked again
-        lib = _lib.load()
-        first = torch.empty(4, dtype=torch.int64, device=dec.device)
-        while True:
-            _lib.check(lib.ctcb_validate(dec._h, ctypes.c_void_p(x.data_ptr()), T * V, V,
-                                         ctypes.c_void_p(lens_dev.data_ptr()), B, T, int(self.strict),
-                                         dec._stream(), ctypes.c_void_p(first.data_ptr())), "ctcb_validate")
-            code, b, t, v = first.cpu().tolist()
-            if code == 0:
-                break
-            errors[files[b][0]] = _validation_message(code, staged[b].astype(np.float64), t, v)
-            lens[b] = 0
-            lens_dev[b] = 0
-        errors.update({files[b][0]: "empty emissions" for b in np.flatnonzero(lens == 0)  # decoder.py:117-118
-                       if files[b][0] not in errors})
+        # EmissionMatrix checks (emissions.py:128-150) run inside the decode
+        # (ctcb_set_validate): every invalid utterance comes back with its own
+        # status and first offender
+        dec.set_validate("strict" if self.strict else "nonstrict")
         out = dec.decode(x, lens_dev, timesteps=True)
         status = out.status.cpu().numpy()
         counts = out.counts.cpu().numpy()
@@ -502,7 +487,12 @@ class _DecodeJob:
         ts = out.timesteps[:, :, :width].cpu().numpy()
         lms = out.lm.cpu().numpy() if out.lm is not None else None
         for b, (utt, _) in enumerate(files):
-            if utt in errors:
+            if status[b] in (_lib.UTT_NONFINITE, _lib.UTT_ABOVE_ZERO, _lib.UTT_NOT_NORMALIZED):
+                errors[utt] = _validation_message(int(status[b]) - 4, staged[b].astype(np.float64),
+                                                  int(lengths[b, 0]), int(counts[b]))
+                continue
+            if status[b] == _lib.UTT_EMPTY:
+                errors[utt] = "empty emissions"  # decoder.py:117-118
                 continue
             if status[b] == _lib.UTT_BEAM_DIED:
                 limit = dec.beam_size_token or V
@@ -542,7 +532,7 @@ class _DecodeJob:
 
 
 def _validation_message(code: int, lp: np.ndarray, t: int, v: int) -> str:
-    """ctcb_validate's code -> EmissionMatrix's message (emissions.py:133-150)."""
+    """Validation check code -> EmissionMatrix's message (emissions.py:133-150)."""
     if code == 1:
         return f"non-finite log-probability at frame {t}, token {v}"
     if code == 2:

@@ -29,6 +29,7 @@ __global__ void ctcb_debug_kernel(const __grid_constant__ Params P, int32_t* out
 __global__ void ctcb_validate_kernel(const float* lp, long long sb, long long st, const int32_t* lens, int B,
                                      int T, int V, int strict, unsigned long long* out_key);
 __global__ void ctcb_validate_decode_kernel(const unsigned long long* key, int T, int V, int64_t* out);
+__global__ void ctcb_validate_post_kernel(const __grid_constant__ Params P);
 }  // namespace ctcb
 
 namespace ctcb {
@@ -78,6 +79,7 @@ struct ctcb_handle {
   int num_sms, max_smem_optin;
   int merge_max;      // ctcb_set_merge_mode
   int tok_k;          // ctcb_set_beam_size_token (0: full vocabulary)
+  int validate;       // ctcb_set_validate: 0 off, 1 strict (default), 2 without the norm check
   int force_generic;  // CTCB_FORCE_GENERIC=1: use the generic kernel for every beam (testing)
   unsigned long long* dbg;  // device [8] debug counters
   void* ws;
@@ -189,7 +191,7 @@ bool use_block_pre(const ctcb_handle* h) {
 }
 
 struct WsLayout {
-  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, rowoff, total;
+  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, rowoff, vkey, vdone, total;
 };
 WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   WsLayout w{};
@@ -210,6 +212,8 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   w.topk_tok = take(ntk * 4);
   w.topk_val = take(ntk * 4);
   w.rowoff = take(ntk ? ((size_t)B + 1) * 4 : 0);
+  w.vkey = take((size_t)B * 8);
+  w.vdone = take((size_t)B * 4);
   w.total = ctcb::align_up(o, 256);
   return w;
 }
@@ -267,6 +271,9 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.topk_tok = (int32_t*)(base + L.topk_tok);
   P.topk_val = (float*)(base + L.topk_val);
   P.rowoff = (int32_t*)(base + L.rowoff);
+  P.validate = h->validate;
+  P.vkey = (unsigned long long*)(base + L.vkey);
+  P.vdone = (int32_t*)(base + L.vdone);
   // rows of V <= 512 are padded to 512 floats: the fast top-k reads 4 float4
   // chunks per lane without bounds checks (padding holds the sentinel)
   P.row_bytes = (int)ctcb::align_up((size_t)(h->V <= 512 ? 512 : h->V) * 4, 16);
@@ -390,6 +397,7 @@ int ctcb_create(int V, int blank, int beam, int nbest, float skip_cutoff, double
   h->has_lm = 0;
   h->sil = -1;
   h->sil_score = 0.0;
+  h->validate = 1;
   {
     const char* fg = getenv("CTCB_FORCE_GENERIC");
     h->force_generic = (fg && fg[0] == '1') ? 1 : 0;
@@ -408,6 +416,13 @@ int ctcb_set_merge_mode(ctcb_t* h, int max_mode) {
   if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
   if (max_mode != 0 && max_mode != 1) return fail(CTCB_ERR_ARG, "merge mode must be 0 (logadd) or 1 (max)");
   h->merge_max = max_mode;
+  return CTCB_OK;
+}
+
+int ctcb_set_validate(ctcb_t* h, int mode) {
+  if (!h) return fail(CTCB_ERR_ARG, "NULL handle");
+  if (mode < 0 || mode > 2) return fail(CTCB_ERR_ARG, "validate mode must be 0 (off), 1 (strict) or 2 (no norm check)");
+  h->validate = mode;
   return CTCB_OK;
 }
 
@@ -521,6 +536,7 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   if (!h->dbg) CTCB_CUDA(cudaMalloc(&h->dbg, 8 * sizeof(unsigned long long)));
   CTCB_CUDA(cudaMemsetAsync(h->dbg, 0, 8 * sizeof(unsigned long long), s));
   P.dbg = h->dbg;
+  if (P.validate) CTCB_CUDA(cudaMemsetAsync(P.vkey, 0xff, (size_t)B * 8, s));
   int n = 1;
   while (n < B) n <<= 1;
   size_t order_smem = n <= 8192 ? (size_t)n * 8 : 0;
@@ -633,6 +649,15 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   if (timed) {
     CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed + 1], s));
     h->n_timed++;
+  }
+  if (P.validate) {
+    // rows the decode kernel did not screen (skipped frames, frames after a
+    // dead beam, kernels without the fused check), then the per-utterance
+    // verdict into out_status / out_len / out_count
+    P.vfused = (blk || (fast && !pair && !fused)) ? 1 : 0;
+    ctcb::ctcb_validate_post_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
+    h->launches++;
+    CTCB_CUDA(cudaGetLastError());
   }
   return CTCB_OK;
 }

@@ -236,37 +236,17 @@ __device__ __forceinline__ int block_excl_scan(int v, int tid, int* tmp, int* to
 }
 
 // ------------------------------------------------------------------ token sequences (single-thread slow path)
-// Token sequences of entries ea, eb (plus an extra token each when x >= 0)
-// in Python tuple order.  Both trellis paths are walked back in lockstep
-// until they reach the same entry: everything before it is a common prefix,
-// so only the two tails (collected last token first) are compared.
+// Token-sequence order of two entries (trellis_seq_cmp: lockstep walk back to
+// the merge point of their trellis paths).
 __device__ __forceinline__ int bseq_cmp_full(const Blk& w, int ea, int xa, int eb, int xb, bool* strict) {
   const Params& P = *w.P;
   int* A = P.seqbuf + (size_t)w.u * 3 * (P.T_max + 1);
-  int* Bq = A + P.T_max + 1;
-  int la = 0, lb = 0;
-  if (xa >= 0) A[la++] = xa;
-  if (xb >= 0) Bq[lb++] = xb;
   const uint32_t* tr = P.trellis + (size_t)w.u * P.T_max * P.beam;
-  int sa = ea, sb = eb, i = w.steps_done - 1;
-  for (; i >= 0 && sa != sb; --i) {
-    const uint32_t ra = tr[(size_t)i * P.beam + sa], rb = tr[(size_t)i * P.beam + sb];
-    const int ta = trel_tok(ra), tb = trel_tok(rb);
-    if (ta >= 0) A[la++] = ta;
-    if (tb >= 0) Bq[lb++] = tb;
-    sa = trel_src(ra);
-    sb = trel_src(rb);
-  }
-  atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
-  atomicAdd(&P.dbg[kDbgMatSteps], 2ull * (unsigned long long)(w.steps_done - 1 - i));
-  const int n = la < lb ? la : lb;
-  *strict = true;
-  for (int q = 1; q <= n; q++) {
-    const int x = A[la - q], y = Bq[lb - q];
-    if (x != y) return x < y ? -1 : 1;
-  }
-  *strict = false;
-  return la < lb ? -1 : (la > lb ? 1 : 0);
+  auto rec = [&](int i, int slot) {
+    const uint32_t r = tr[(size_t)i * P.beam + slot];
+    return make_int2(trel_tok(r), trel_src(r));
+  };
+  return trellis_seq_cmp(rec, w.steps_done, ea, xa, eb, xb, A, A + P.T_max + 1, strict, P.dbg);
 }
 // Sequence-order cache: direct-mapped on the unordered pair of sequence
 // hashes, holding the order of the lower hash's sequence against the other.
@@ -1145,6 +1125,20 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
       }
       n_cons++;
       const float* row = (const float*)(w.rows() + (size_t)slot * Blk::row_bytes);
+      // input validation fused into the staging (emissions.py:128-150): warp 0
+      // takes lane partials now and the verdict after the step (no extra
+      // barrier); suspicious rows get the exact check from global memory
+      // (precomputed mode: ctcb_topk_wide_kernel already screened every kept row)
+      const bool vscreen = P.validate && !P.precomp;
+      RowPart vpart{0u, 0xffffffffu, 0u};
+      if (vscreen && tid < 32) vpart = row_partials(row, P.V, tid);
+      auto vfinish = [&]() {
+        if (vscreen && tid < 32 && !row_verdict(vpart, P.validate == 1)) {
+          const int fr = fmap[i];
+          const unsigned long long vk = row_check_exact(ubase + (size_t)fr * P.stride_t, P.V, fr, tid, P.validate == 1);
+          if (tid == 0 && vk != ~0ull) atomicMin(&P.vkey[u], vk);
+        }
+      };
       if (P.precomp) {
         // S of this frame; bstep's first barrier publishes it
         if (tid < k) {
@@ -1160,6 +1154,7 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
         btopk(w, row);
       }
       const int Hn = bstep(w, row, H);
+      vfinish();
       if (Hn == 0) { died = true; break; }
       // ntrel / the row slot are rewritten only after later barriers
       uint32_t* trow = P.trellis + ((size_t)u * P.T_max + i) * P.beam;
@@ -1168,6 +1163,7 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
       H = Hn;
       w.steps_done = i + 1;
     }
+    if (tid == 0) P.vdone[u] = (P.precomp || !died) ? kept : w.steps_done + 1;  // rows screened
     if (died) {
       while (n_cons < n_issue) {
         if (P.bulk_ok) mbar_wait(&w.mbar()[n_cons & 1u], (n_cons >> 1) & 1u);
@@ -1228,11 +1224,24 @@ __global__ void __launch_bounds__(256, 3) ctcb_topk_wide_kernel(const __grid_con
     }
     const int u = lo, i = (int)(g - P.rowoff[u]);
     const float* src = P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
-    uint32_t key[16];  // ord32 + 1 (0: absent), token r * 32 + lane
+    uint32_t key[16];  // ord32 (0: absent), token r * 32 + lane
+    float vs = 0.0f, vmn = INFINITY, vmx = -INFINITY;  // validation screen partials
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const int c = r * 32 + lane;
-      key[r] = (c < V && c != blank) ? ord32(__ldg(src + c)) : 0u;
+      const float x = c < V ? __ldg(src + c) : -1e30f;
+      key[r] = (c < V && c != blank) ? ord32(x) : 0u;
+      vmn = fminf(vmn, x);
+      vmx = fmaxf(vmx, x);
+      vs += ex2_ftz(x * 1.4426950408889634f);
+    }
+    if (P.validate) {  // input validation of every kept row (emissions.py:128-150)
+      const RowPart vp{vs <= 2.0f ? ord32(vmx) : 0xffffffffu, ord32(vmn), (uint32_t)(fminf(vs, 2.0f) * 33554432.0f)};
+      if (!row_verdict(vp, P.validate == 1)) {
+        const int fr = P.frame_map[(size_t)u * P.T_max + i];
+        const unsigned long long vk = row_check_exact(src, V, fr, lane, P.validate == 1);
+        if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[u], vk);
+      }
     }
     // largest T with #{key >= T} >= k
     uint32_t T = 0u;

@@ -227,6 +227,151 @@ __device__ __forceinline__ uint32_t pack_trel(int src, int tok) {
 __device__ __forceinline__ int trel_src(uint32_t r) { return (int)(r >> kSrcShift); }
 __device__ __forceinline__ int trel_tok(uint32_t r) { return (int)(r & kTokMask) - 1; }
 
+// ---------------------------------------------------------------- input validation
+// EmissionMatrix.__post_init__ (emissions.py:128-150) per utterance: any
+// non-finite value (code 1), else any value > MAX_LOG_PROB = 1e-4 (code 2),
+// else (strict) a row whose fp64 log-sum-exp is off 0 by more than
+// ROW_NORM_TOL = 1e-3 (code 3); the first offender in (frame, token) order.
+// Key = code << 62 | frame << 30 | (token + 1): the smallest key of an
+// utterance is the reference's error.  No float lies in (1e-4f, 1e-4], so the
+// fp32 comparison x > 1e-4f equals the reference's fp64 one.
+__device__ __forceinline__ unsigned long long vkey_make(int code, int t, int v) {
+  return ((unsigned long long)code << 62) | ((unsigned long long)(unsigned)t << 30) | (unsigned long long)(v + 1);
+}
+// Exact check of one row by a warp: the smallest key of row `t`, or ~0
+// (cold path, kept out of line).
+static __device__ __noinline__ unsigned long long row_check_exact(const float* row, int V, int t, int lane, bool strict) {
+  int v1 = 0x7fffffff, v2 = 0x7fffffff;
+  float mx = -INFINITY;
+  for (int v = lane; v < V; v += 32) {
+    const float x = row[v];
+    if (!isfinite(x)) v1 = min(v1, v);
+    else if (x > 1e-4f) v2 = min(v2, v);
+    mx = fmaxf(mx, x);
+  }
+  v1 = __reduce_min_sync(0xffffffffu, v1);
+  if (v1 != 0x7fffffff) return vkey_make(1, t, v1);
+  v2 = __reduce_min_sync(0xffffffffu, v2);
+  if (v2 != 0x7fffffff) return vkey_make(2, t, v2);
+  if (!strict) return ~0ull;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double m = (double)mx;
+  double sum = 0.0;
+  for (int v = lane; v < V; v += 32) sum += exp((double)row[v] - m);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  return fabs(m + log(sum)) > 1e-3 ? vkey_make(3, t, -1) : ~0ull;
+}
+// Fast screen of a staged row, split so that the decode kernels keep it off
+// their per-frame critical path: row_partials is lane-local (float4 chunks
+// c4 = lane, lane + 32, ...), row_verdict (three independent REDUX ops) runs
+// later in the frame.  A row passes when it is finite, <= 1e-4 and, if
+// strict, the fp32 sum of exp(x) -- in 2^-25 fixed point per lane, clamped at
+// 2 -- has |log| < 9e-4; the screen's error is < 1e-4 for V <= 2048, so rows
+// near the 1e-3 limit take row_check_exact.
+struct RowPart {
+  uint32_t kmx, kmn, sfx;
+};
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// MAXCH: float4 chunks per lane the caller guarantees (4 for V <= 512), 0 = any.
+// WITH_MAX = false: the caller folds the row maximum into kmx itself.
+template <int MAXCH = 0, bool WITH_MAX = true>
+__device__ __forceinline__ RowPart row_partials(const float* row, int V, int lane) {
+  const float4* r4 = (const float4*)row;
+  constexpr float kL2E = 1.4426950408889634f;
+  float s = 0.0f, mn = INFINITY, mx = -INFINITY;
+  const int nch4 = (V + 3) >> 2;
+  const bool ragged = (V & 3) != 0;
+  auto chunk = [&](int c4) {
+    float4 q = r4[c4];
+    if (ragged && 4 * c4 + 4 > V) {  // tail chunk: neutral values past V
+      const int c = 4 * c4;
+      if (c + 1 >= V) q.y = -1e30f;
+      if (c + 2 >= V) q.z = -1e30f;
+      if (c + 3 >= V) q.w = -1e30f;
+    }
+    mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
+    if (WITH_MAX) mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
+    s += (ex2_ftz(q.x * kL2E) + ex2_ftz(q.y * kL2E)) + (ex2_ftz(q.z * kL2E) + ex2_ftz(q.w * kL2E));  // NaN propagates
+  };
+  if (MAXCH > 0) {
+#pragma unroll
+    for (int j = 0; j < MAXCH; j++)
+      if (lane + 32 * j < nch4) chunk(lane + 32 * j);
+  } else {
+    for (int c4 = lane; c4 < nch4; c4 += 32) chunk(c4);
+  }
+  RowPart r;
+  r.kmx = s <= 2.0f ? (WITH_MAX ? ord32(mx) : 0u) : 0xffffffffu;  // NaN / huge sums fail the max test
+  r.kmn = ord32(mn);
+  r.sfx = (uint32_t)(fminf(s, 2.0f) * 33554432.0f);
+  return r;
+}
+__device__ __forceinline__ bool row_verdict(const RowPart& r, bool strict) {
+  const uint32_t kmx = __reduce_max_sync(0xffffffffu, r.kmx), kmn = __reduce_min_sync(0xffffffffu, r.kmn);
+  const uint32_t sfx = __reduce_add_sync(0xffffffffu, r.sfx);
+  const bool ok = kmx <= ord32(1e-4f) && kmn > ord32(-INFINITY);
+  return ok && (!strict || fabsf(__logf((float)sfx * (1.0f / 33554432.0f))) < 9e-4f);
+}
+__device__ __forceinline__ bool row_screen(const float* row, int V, int lane, bool strict) {
+  return row_verdict(row_partials(row, V, lane), strict);
+}
+// The same screen over a row in global memory (any alignment).
+__device__ __forceinline__ bool row_screen_scalar(const float* row, int V, int lane, bool strict) {
+  float s = 0.0f, mn = INFINITY, mx = -INFINITY;
+  for (int v = lane; v < V; v += 32) {
+    const float x = __ldg(row + v);
+    mn = fminf(mn, x);
+    mx = fmaxf(mx, x);
+    s += __expf(x);
+  }
+  const uint32_t kmx = __reduce_max_sync(0xffffffffu, ord32(mx)), kmn = __reduce_min_sync(0xffffffffu, ord32(mn));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const bool ok = kmx <= ord32(1e-4f) && kmn > ord32(-INFINITY) && isfinite(s);
+  return ok && (!strict || fabsf(__logf(s)) < 9e-4f);
+}
+
+// Python tuple order of seq(ea) + [xa] vs seq(eb) + [xb] (x < 0: no extra
+// token) for two entries of a beam after `steps` frames (exact-tie slow path,
+// one lane).  Both trellis paths are walked back in lockstep until they reach
+// the same entry: everything before it is a common prefix, so only the two
+// tails (collected last token first into A / Bq, T_max + 1 ints each) are
+// compared.  rec(i, slot) -> {token or -1, source slot} of frame i's record.
+// *strict: the sequences differ before the shorter one ends.
+template <class Rec>
+__device__ __forceinline__ int trellis_seq_cmp(Rec rec, int steps, int ea, int xa, int eb, int xb, int* A, int* Bq,
+                                               bool* strict, unsigned long long* dbg) {
+  int la = 0, lb = 0;
+  if (xa >= 0) A[la++] = xa;
+  if (xb >= 0) Bq[lb++] = xb;
+  int sa = ea, sb = eb, i = steps - 1;
+  for (; i >= 0 && sa != sb; --i) {
+    const int2 ra = rec(i, sa), rb = rec(i, sb);
+    if (ra.x >= 0) A[la++] = ra.x;
+    if (rb.x >= 0) Bq[lb++] = rb.x;
+    sa = ra.y;
+    sb = rb.y;
+  }
+  if (dbg) {
+    atomicAdd(&dbg[2], 2ull);                                      // kDbgMaterialize
+    atomicAdd(&dbg[3], 2ull * (unsigned long long)(steps - 1 - i));  // kDbgMatSteps
+  }
+  const int n = la < lb ? la : lb;
+  *strict = true;
+  for (int q = 1; q <= n; q++) {
+    const int x = A[la - q], y = Bq[lb - q];
+    if (x != y) return x < y ? -1 : 1;
+  }
+  *strict = false;
+  return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+
 // ---------------------------------------------------------------- warp
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

@@ -117,19 +117,6 @@ struct FastSmem {
   long long* dG;
 };
 
-// Token sequence of current entry `e` (length len) through the global trellis.
-__device__ int fast_materialize(const Params& P, int u, int steps_done, int e, int len, int* buf) {
-  int pos = len, slot = e;
-  atomicAdd(&P.dbg[kDbgMaterialize], 1ull);
-  atomicAdd(&P.dbg[kDbgMatSteps], (unsigned long long)steps_done);
-  for (int i = steps_done - 1; i >= 0 && pos > 0; --i) {
-    uint32_t r = P.trellis[((size_t)u * P.T_max + i) * P.beam + slot];
-    int tok = trel_tok(r);
-    if (tok >= 0) buf[--pos] = tok;
-    slot = trel_src(r);
-  }
-  return len;
-}
 // Tie-order cache: prefix hashes identify token sequences globally, so a
 // cached "seq(h1) vs seq(h2)" stays valid for the whole decode (and across
 // utterances).  Sibling prefixes with identical scores (a duplicated fp32
@@ -190,17 +177,12 @@ __device__ int fast_seq_cmp(const Params& P, const FastSmem& S, int u, int steps
 __device__ int fast_seq_cmp_full(const Params& P, const FastSmem& S, int u, int steps_done, int ea, int xa, int eb,
                                  int xb, bool* strict) {
   int* A = P.seqbuf + (size_t)u * 3 * (P.T_max + 1);
-  int* Bq = A + P.T_max + 1;
-  int la = fast_materialize(P, u, steps_done, ea, S.hl[ea], A);
-  if (xa >= 0) A[la++] = xa;
-  int lb = fast_materialize(P, u, steps_done, eb, S.hl[eb], Bq);
-  if (xb >= 0) Bq[lb++] = xb;
-  int n = la < lb ? la : lb;
-  *strict = true;
-  for (int i = 0; i < n; i++)
-    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
-  *strict = false;
-  return la < lb ? -1 : (la > lb ? 1 : 0);
+  const uint32_t* tr = P.trellis + (size_t)u * P.T_max * P.beam;
+  auto rec = [&](int i, int slot) {
+    const uint32_t r = tr[(size_t)i * P.beam + slot];
+    return make_int2(trel_tok(r), trel_src(r));
+  };
+  return trellis_seq_cmp(rec, steps_done, ea, xa, eb, xb, A, A + P.T_max + 1, strict, P.dbg);
 }
 // a precedes b in the reference's rank order: score desc, sequence asc, flag asc.
 __device__ bool fast_precedes(const Params& P, const FastSmem& S, int u, int sd, double sa, int ba, int xa, int fa,
@@ -700,7 +682,27 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         for (int c = lane; c < V; c += 32) row[c] = __ldg(src + c);
         __syncwarp();
       }
-      const double eb = (double)row[P.blank];
+      // input validation fused into the staging (emissions.py:128-150): lane
+      // partials now, the warp verdict at the end of the frame (off the
+      // critical path); suspicious rows get the exact check from global memory
+      // (precomputed mode: ctcb_topk_kernel already screened every kept row)
+      // The shortcut pass below provides the non-blank maximum (vmax), so the
+      // screen skips its own (max = max(vmax, blank value)).
+      const bool v_scmax = !tokK && tiny_v;  // == sc_on && !PRE
+      RowPart vpart{0u, 0xffffffffu, 0u};
+      if (!PRE && P.validate)
+        vpart = v_scmax ? row_partials<SMALL ? 4 : 0, false>(row, V, lane) : row_partials<SMALL ? 4 : 0>(row, V, lane);
+      double vmax = -INFINITY;
+      const float eb_f = row[P.blank];
+      auto vfinish = [&]() {
+        if (!PRE && P.validate && v_scmax) vpart.kmx = max(vpart.kmx, ord32(fmaxf((float)vmax, eb_f)));
+        if (!PRE && P.validate && !row_verdict(vpart, P.validate == 1)) {
+          const int fr = fmap[i];
+          const unsigned long long vk = row_check_exact(ubase + (size_t)fr * P.stride_t, V, fr, lane, P.validate == 1);
+          if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[u], vk);
+        }
+      };
+      const double eb = (double)eb_f;
       __syncwarp();
       if (!PRE) {
         if (lane == 0) ((uint32_t*)row)[P.blank] = kSentinel;
@@ -715,7 +717,6 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // (~60 % of cfg4 frames).  vmax comes from a lane-max pass over the
       // staged row (blank holds the sentinel).
       const bool sc_on = !tokK && (PRE || tiny_v);
-      double vmax = -INFINITY;
       if (sc_on && !PRE) {
         const float4* r4 = (const float4*)row;
         float lm = __uint_as_float(kSentinel);
@@ -946,7 +947,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       const uint32_t mhi = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32));
       const uint32_t mlo = __reduce_max_sync(FULL, (uint32_t)(ok64 >> 32) == mhi ? (uint32_t)ok64 : 0u);
       const uint64_t bk = ((uint64_t)mhi << 32) | mlo;
-      if (bk == 0ull) { died = true; died_at = i; break; }  // every extension is -inf (decoder.py:616-620)
+      if (bk == 0ull) { vfinish(); died = true; died_at = i; break; }  // every extension is -inf (decoder.py:616-620)
       const double best = unord64(bk);
       // keep iff score >= best - beam_threshold and score > -inf (decoder.py:621-623)
       const double lo_thr = P.threshold_inf ? -DBL_MAX : best - P.beam_threshold;
@@ -1152,7 +1153,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       }  // !oneshot
       }  // !shortcut
       __syncwarp();
-      if (Hn == 0) { died = true; died_at = i; break; }
+      if (Hn == 0) { vfinish(); died = true; died_at = i; break; }
 
       // ================= commit (decoder.py:683-744) =================
       // lane r builds new entry r from the winning lane's registers
@@ -1200,6 +1201,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         S.tring[(i % kChunk) * 16 + lane] = trel;
       }
       H = Hn;
+      vfinish();
       __syncwarp();
       // trellis checkpoint: ancestor slot at the chunk start for every entry
       if ((i % kChunk) == kChunk - 1 || i == kept - 1) {
@@ -1212,6 +1214,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       }
     }
 
+    if (lane == 0) P.vdone[u] = (PRE || !died) ? kept : died_at + 1;  // rows screened (here or by the top-k kernel)
     if (died) {
       while (n_out > 0) {
         mbar_wait(&S.mbar[slot_c], par_c);
@@ -1434,7 +1437,12 @@ __global__ void __launch_bounds__(256, CTCB_TOPK_MIN_BLOCKS) ctcb_topk_kernel(co
     int cu = lo, ci = (int)(g0 - P.rowoff[lo]);
     while (cu < P.B && ci >= P.kept[cu]) { cu++; ci = 0; }
     for (long long g = g0; g < g1; g++) {
-      const float* src = P.lp + (size_t)cu * P.stride_b + (size_t)P.frame_map[(size_t)cu * P.T_max + ci] * P.stride_t;
+      const int fr = P.frame_map[(size_t)cu * P.T_max + ci];
+      const float* src = P.lp + (size_t)cu * P.stride_b + (size_t)fr * P.stride_t;
+      if (P.validate && !row_screen_scalar(src, V, lane, P.validate == 1)) {  // emissions.py:128-150
+        const unsigned long long vk = row_check_exact(src, V, fr, lane, P.validate == 1);
+        if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[cu], vk);
+      }
       const int st = skey_tok(topk_key_g(S, src, V, P.blank, k, lane, nullptr));
       if (lane < k) {
         const size_t o = ((size_t)cu * P.T_max + ci) * k + lane;
@@ -1492,6 +1500,13 @@ __global__ void __launch_bounds__(256, CTCB_TOPK_MIN_BLOCKS) ctcb_topk_kernel(co
       for (int c = lane; c < V; c += 32) row[c] = __ldg(src + c);
     }
     __syncwarp();
+    // input validation of every kept row (emissions.py:128-150): the beam walk
+    // of precomputed mode leaves it to this frame-parallel pass
+    if (P.validate && !row_screen(row, V, lane, P.validate == 1)) {
+      const int fr = P.frame_map[(size_t)cu * P.T_max + ci];
+      const unsigned long long vk = row_check_exact(src, V, fr, lane, P.validate == 1);
+      if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[cu], vk);
+    }
     if (lane == 0) ((uint32_t*)row)[P.blank] = kSentinel;
     __syncwarp();
     const int st = tiny_v ? topk_small(S, row, V, k, lane, nch4, nullptr)

@@ -147,37 +147,18 @@ __device__ void bitonic_pairs(uint64_t* key, int* idx, int n, int lane) {
 }
 
 // ------------------------------------------------------------------ token sequences
-// Token sequence of current beam entry `e` (len `len`), read back through the
-// trellis.  Single-lane slow path used only to break exact score ties.
-__device__ int materialize(const Warp& w, int e, int len, int* buf) {
-  const Params& P = *w.P;
-  int pos = len, slot = e;
-  for (int i = w.steps_done - 1; i >= 0 && pos > 0; --i) {
-    uint32_t r = P.trellis[((size_t)w.u * P.T_max + i) * P.beam + slot];
-    int tok = trel_tok(r);
-    if (tok >= 0) buf[--pos] = tok;
-    slot = trel_src(r);
-  }
-  return len;
-}
-// Full comparison through the trellis; *strict: the sequences differ before
-// the shorter one ends (then every extension keeps the order).
+// Full comparison through the trellis (trellis_seq_cmp); *strict: the
+// sequences differ before the shorter one ends (then every extension keeps
+// the order).
 __device__ int seq_cmp_full(const Warp& w, int ea, int xa, int eb, int xb, bool* strict) {
   const Params& P = *w.P;
-  atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
-  atomicAdd(&P.dbg[kDbgMatSteps], 2ull * (unsigned long long)w.steps_done);
   int* A = P.seqbuf + (size_t)w.u * 3 * (P.T_max + 1);
-  int* Bq = A + P.T_max + 1;
-  int la = materialize(w, ea, w.cn[ea], A);
-  if (xa >= 0) A[la++] = xa;
-  int lb = materialize(w, eb, w.cn[eb], Bq);
-  if (xb >= 0) Bq[lb++] = xb;
-  int n = la < lb ? la : lb;
-  *strict = true;
-  for (int i = 0; i < n; i++)
-    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
-  *strict = false;
-  return la < lb ? -1 : (la > lb ? 1 : 0);
+  const uint32_t* tr = P.trellis + (size_t)w.u * P.T_max * P.beam;
+  auto rec = [&](int i, int slot) {
+    const uint32_t r = tr[(size_t)i * P.beam + slot];
+    return make_int2(trel_tok(r), trel_src(r));
+  };
+  return trellis_seq_cmp(rec, w.steps_done, ea, xa, eb, xb, A, A + P.T_max + 1, strict, P.dbg);
 }
 // Strict-order cache keyed by prefix hashes (see the fast kernel): orders of
 // sibling lineages with identical scores are computed once.

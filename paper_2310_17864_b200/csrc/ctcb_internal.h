@@ -13,6 +13,10 @@ enum UttStatus : int32_t {
   kUttEmpty = 1,      // len_b == 0: "empty emissions" (decoder.py:117-118)
   kUttBadLen = 2,     // len_b < 0 or len_b > T_max
   kUttBeamDied = 3,   // "beam died" (decoder.py:616-620)
+  // input validation (emissions.py:128-150): out_len[u][0] = frame, out_count[u] = token (-1 for 7)
+  kUttNonFinite = 5,
+  kUttAboveZero = 6,
+  kUttNotNormalized = 7,
 };
 
 struct Params {
@@ -70,6 +74,11 @@ struct Params {
   int sil;                  // silence token (-1: none)
   double sil_score;
   double* out_lm;           // [B, nbest] LM total of each hypothesis, or null
+  // input validation fused into the row staging (ctcb_set_validate)
+  int validate;             // 0 off, 1 strict (normalisation too), 2 finite / <= 1e-4 only
+  unsigned long long* vkey; // [B] smallest offender key (vkey_make) seen, ~0 = none
+  int32_t* vdone;           // [B] leading kept frames the decode kernel checked
+  int vfused;               // the decode kernel wrote vdone (else every frame is checked after it)
 };
 
 // Fused search limits.

@@ -514,17 +514,6 @@ __device__ __forceinline__ uint64_t warp_max64(uint64_t x) {
 }
 
 // ---- token sequences through the trellis (exact-tie resolution; lane-serial)
-__device__ int fmaterialize(const FW& w, int e, int len, int* buf) {
-  const Params& P = *w.P;
-  int pos = len, slot = e;
-  for (int i = w.steps_done - 1; i >= 0 && pos > 0; --i) {
-    const uint32_t r = P.trellis[((size_t)w.u * P.T_max + i) * P.beam + slot];
-    const int tok = trel_tok(r);
-    if (tok >= 0) buf[--pos] = tok;
-    slot = trel_src(r);
-  }
-  return len;
-}
 // Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token)
 __device__ int fseq_cmp(const FW& w, int ea, int xa, int eb, int xb) {
   const Params& P = *w.P;
@@ -533,17 +522,14 @@ __device__ int fseq_cmp(const FW& w, int ea, int xa, int eb, int xb) {
     if (xa < 0 || xb < 0) return xa < 0 ? -1 : 1;
     return xa < xb ? -1 : 1;
   }
-  atomicAdd(&P.dbg[kDbgMaterialize], 2ull);
   int* A = P.seqbuf + (size_t)w.u * 3 * (P.T_max + 1);
-  int* Bq = A + P.T_max + 1;
-  int la = fmaterialize(w, ea, w.cn[ea], A);
-  if (xa >= 0) A[la++] = xa;
-  int lb = fmaterialize(w, eb, w.cn[eb], Bq);
-  if (xb >= 0) Bq[lb++] = xb;
-  const int n = la < lb ? la : lb;
-  for (int i = 0; i < n; i++)
-    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
-  return la < lb ? -1 : (la > lb ? 1 : 0);
+  const uint32_t* tr = P.trellis + (size_t)w.u * P.T_max * P.beam;
+  auto rec = [&](int i, int slot) {
+    const uint32_t r = tr[(size_t)i * P.beam + slot];
+    return make_int2(trel_tok(r), trel_src(r));
+  };
+  bool strict = false;
+  return trellis_seq_cmp(rec, w.steps_done, ea, xa, eb, xb, A, A + P.T_max + 1, &strict, P.dbg);
 }
 struct FDesc { double sc; int base, x, flag; };
 __device__ bool fprecedes(const FW& w, const FDesc& a, const FDesc& b) {

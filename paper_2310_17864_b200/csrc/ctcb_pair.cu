@@ -226,20 +226,6 @@ __device__ PairSmem pair_smem(uint8_t* base) {
 }
 
 // ---------------------------------------------------------------- exact ties
-// Token sequence of current entry `e` (length len) through the 16-bit trellis.
-__device__ int pair_materialize(const Params& P, int u, int steps_done, int e, int len, int* buf) {
-  const uint16_t* tr = (const uint16_t*)P.trellis;
-  int pos = len, slot = e;
-  atomicAdd(&P.dbg[kDbgMaterialize], 1ull);
-  atomicAdd(&P.dbg[kDbgMatSteps], (unsigned long long)steps_done);
-  for (int i = steps_done - 1; i >= 0 && pos > 0; --i) {
-    const uint32_t r = tr[((size_t)u * P.T_max + i) * P.beam + slot];
-    const int tok = ptrel_tok(r);
-    if (tok >= 0) buf[--pos] = tok;
-    slot = ptrel_src(r);
-  }
-  return len;
-}
 __device__ int ptc_lookup(const PairSmem& S, uint64_t ha, uint64_t hb) {
 #pragma unroll 1
   for (int i = 0; i < kTieCache; i++) {
@@ -259,17 +245,12 @@ __device__ void ptc_insert(const PairSmem& S, uint64_t ha, uint64_t hb, int r) {
 __device__ int pair_seq_cmp_full(const Params& P, const PairSmem& S, int u, int sd, int ea, int xa, int eb, int xb,
                                  bool* strict) {
   int* A = P.seqbuf + (size_t)u * 3 * (P.T_max + 1);
-  int* Bq = A + P.T_max + 1;
-  int la = pair_materialize(P, u, sd, ea, S.hl[ea], A);
-  if (xa >= 0) A[la++] = xa;
-  int lb = pair_materialize(P, u, sd, eb, S.hl[eb], Bq);
-  if (xb >= 0) Bq[lb++] = xb;
-  const int n = la < lb ? la : lb;
-  *strict = true;
-  for (int i = 0; i < n; i++)
-    if (A[i] != Bq[i]) return A[i] < Bq[i] ? -1 : 1;
-  *strict = false;
-  return la < lb ? -1 : (la > lb ? 1 : 0);
+  const uint16_t* tr = (const uint16_t*)P.trellis + (size_t)u * P.T_max * P.beam;  // 16-bit records
+  auto rec = [&](int i, int slot) {
+    const uint32_t r = tr[(size_t)i * P.beam + slot];
+    return make_int2(ptrel_tok(r), ptrel_src(r));
+  };
+  return trellis_seq_cmp(rec, sd, ea, xa, eb, xb, A, A + P.T_max + 1, strict, P.dbg);
 }
 // Python tuple order of seq(ea)+[xa] vs seq(eb)+[xb] (x < 0: no extra token).
 __device__ int pair_seq_cmp(const Params& P, const PairSmem& S, int u, int sd, int ea, int xa, int eb, int xb) {

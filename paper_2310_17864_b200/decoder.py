@@ -62,6 +62,21 @@ class DecodeOutput(NamedTuple):
     counts: torch.Tensor      # int32 [B]
     status: torch.Tensor      # int32 [B]
     lm: Optional[torch.Tensor] = None  # float64 [B, nbest] LM totals (decoder with an LM attached)
+    inputs: Optional[torch.Tensor] = None  # the decoded log_prob (validation error messages)
+
+
+def validation_message(code: int, row, t: int, v: int) -> str:
+    """EmissionMatrix.__post_init__'s message (emissions.py:133-150) for check
+    ``code`` (1 non-finite, 2 above 0, 3 not normalized) at frame t, token v;
+    ``row`` is frame t's log-probs (values for the message)."""
+    if code == 1:
+        return f"non-finite log-probability at frame {t}, token {v}"
+    x = torch.as_tensor(row).double().cpu() if row is not None else None
+    if code == 2:
+        return f"log-probability above 0 at frame {t}, token {v}: {float(x[v]) if x is not None else float('nan'):.6g}"
+    norm = float(torch.logsumexp(x, 0)) if x is not None else float("nan")
+    return (f"frame {t} is not normalized: log-sum-exp = {norm:.6g} (tolerance 0.001); "
+            "pass strict=False to skip this check")
 
 
 def _read_vocab(path: str) -> list[str]:
@@ -126,7 +141,7 @@ class CUCTCDecoder:
         blank_skip_threshold: float = _DEFAULT_BLANK_SKIP_THRESHOLD,
         cuda_stream: Optional[torch.cuda.Stream] = None,
         beam_threshold: float = 50.0,
-        validate: bool = False,
+        validate: bool = True,
         device: Optional[Union[int, torch.device]] = None,
     ):
         vocab_list = list(vocab_list)
@@ -165,6 +180,7 @@ class CUCTCDecoder:
         _lib.check(lib.ctcb_create(len(vocab_list), blank_id, beam_size, nbest, ctypes.c_float(self.cutoff),
                                    self.beam_threshold, self.device.index, ctypes.byref(h)), "ctcb_create")
         self._h = h
+        self.set_validate(validate)
         k = ctypes.c_int()
         _lib.check(lib.ctcb_topk_size(h, ctypes.byref(k)), "ctcb_topk_size")
         self.topk = k.value
@@ -229,27 +245,21 @@ class CUCTCDecoder:
             self._ws = torch.empty(max(n.value, 1), dtype=torch.uint8, device=self.device)
         return self._ws
 
-    def _validate(self, log_prob: torch.Tensor, lens: torch.Tensor, offset: int = 0) -> None:
+    def validate_inputs(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor, strict: bool = True) -> None:
+        """Standalone validation pass (ctcb_validate) without decoding: raise
+        the reference's ValueError for the first invalid utterance.  Decodes
+        validate on their own (set_validate); this is the explicit check."""
+        log_prob, lens = self._check_inputs(log_prob, encoder_out_lens)
         lib = _lib.load()
         B, T, _ = log_prob.shape
         err = torch.empty(4, dtype=torch.int64, device=self.device)
-        _lib.check(lib.ctcb_validate(self._h, ctypes.c_void_p(log_prob.data_ptr()), self._strides[0],
-                                     self._strides[1], ctypes.c_void_p(lens.data_ptr()), B, T, 1,
-                                     self._stream(), ctypes.c_void_p(err.data_ptr())), "ctcb_validate")
-        code, b, t, v = err.cpu().tolist()
-        if code == 0:
-            return
-        x = float(log_prob[b, t, v]) if v >= 0 else None
-        u = b + offset
-        # EmissionMatrix.__post_init__ messages (emissions.py:133-150), tagged as decode_batch does
-        if code == 1:
-            raise ValueError(f"utterance {u}: non-finite log-probability at frame {t}, token {v}")
-        if code == 2:
-            raise ValueError(f"utterance {u}: log-probability above 0 at frame {t}, token {v}: {x:.6g}")
-        row = log_prob[b, t].double()
-        norm = float(torch.logsumexp(row, 0))
-        raise ValueError(f"utterance {u}: frame {t} is not normalized: log-sum-exp = {norm:.6g} "
-                         f"(tolerance 0.001); pass strict=False to skip this check")
+        with self._on_stream():
+            _lib.check(lib.ctcb_validate(self._h, ctypes.c_void_p(log_prob.data_ptr()), self._strides[0],
+                                         self._strides[1], ctypes.c_void_p(lens.data_ptr()), B, T, int(strict),
+                                         self._stream(), ctypes.c_void_p(err.data_ptr())), "ctcb_validate")
+            code, b, t, v = err.cpu().tolist()
+        if code:
+            raise ValueError(f"utterance {b}: " + validation_message(code, log_prob[b, t], t, v))
 
     # ------------------------------------------------------------------ API
     def decode(self, log_prob: torch.Tensor, encoder_out_lens: torch.Tensor, timesteps: bool = False,
@@ -262,8 +272,6 @@ class CUCTCDecoder:
 
     def _decode(self, log_prob, encoder_out_lens, timesteps: bool, offset: int) -> DecodeOutput:
         log_prob, lens = self._check_inputs(log_prob, encoder_out_lens)
-        if self.validate:
-            self._validate(log_prob, lens, offset)
         lib = _lib.load()
         B, T, _ = log_prob.shape
         dev = self.device
@@ -284,13 +292,13 @@ class CUCTCDecoder:
                 vp(out_ts.data_ptr()) if out_ts is not None else None, vp(out_len.data_ptr()),
                 vp(out_score.data_ptr()), vp(out_lm.data_ptr()), vp(out_count.data_ptr()),
                 vp(out_status.data_ptr())), "ctcb_decode_lm")
-            return DecodeOutput(out_tok, out_ts, out_len, out_score, out_count, out_status, out_lm)
+            return DecodeOutput(out_tok, out_ts, out_len, out_score, out_count, out_status, out_lm, log_prob)
         _lib.check(lib.ctcb_decode(
             self._h, vp(log_prob.data_ptr()), self._strides[0], self._strides[1], vp(lens.data_ptr()), B, T,
             vp(ws.data_ptr()), ws.numel(), self._stream(), vp(out_tok.data_ptr()),
             vp(out_ts.data_ptr()) if out_ts is not None else None, vp(out_len.data_ptr()),
             vp(out_score.data_ptr()), vp(out_count.data_ptr()), vp(out_status.data_ptr())), "ctcb_decode")
-        return DecodeOutput(out_tok, out_ts, out_len, out_score, out_count, out_status)
+        return DecodeOutput(out_tok, out_ts, out_len, out_score, out_count, out_status, None, log_prob)
 
     def to_host(self, out: DecodeOutput, offset: int = 0):
         """Synchronise and copy results to the host; raise the reference's
@@ -304,7 +312,7 @@ class CUCTCDecoder:
         status = out.status.cpu().numpy()
         counts = out.counts.cpu().numpy()
         lengths = out.lengths.cpu().numpy()
-        self._raise_status(status, out.tokens.shape[2], lengths, offset)
+        self._raise_status(status, out.tokens.shape[2], lengths, offset, counts, out.inputs)
         scores = out.scores.cpu().numpy()
         lmax = int(lengths.max()) if lengths.size else 0
         tokens = out.tokens[:, :, :lmax].cpu().numpy()
@@ -345,7 +353,7 @@ class CUCTCDecoder:
                                         self._stream(), vp(tok.ctypes.data), vp(ts.ctypes.data) if ts is not None else None,
                                         vp(ln.ctypes.data), vp(sc.ctypes.data), vp(cnt.ctypes.data),
                                         vp(status.ctypes.data)), "ctcb_decode_host")
-        self._raise_status(status, T, ln)
+        self._raise_status(status, T, ln, 0, cnt, log_prob)
         lmax = int(ln.max()) if ln.size else 0
         return tok[:, :, :lmax], (ts[:, :, :lmax] if ts is not None else None), ln, sc, cnt
 
@@ -402,10 +410,11 @@ class CUCTCDecoder:
                            "ctcb_decode_host_wait")  # drain before raising
                 err = status.copy()
                 err[:lo] = _lib.UTT_OK
-                self._raise_status(err, T, ln, offset)
+                self._raise_status(err, T, ln, offset, cnt, log_prob)
             yield lo, hi, tok[lo:hi], ln[lo:hi], sc[lo:hi], cnt[lo:hi]
 
-    def _raise_status(self, status: np.ndarray, T: int, lengths=None, offset: int = 0) -> None:
+    def _raise_status(self, status: np.ndarray, T: int, lengths=None, offset: int = 0, counts=None,
+                      inputs=None) -> None:
         # ``offset``: batch index of status[0] in the caller's batch (multi-device ranges)
         if (status < 0).any():
             raise _lib.CtcbError(f"ctcb_decode left {(status < 0).sum()} utterance(s) unprocessed (kernel did not run)")
@@ -415,6 +424,10 @@ class CUCTCDecoder:
             u = b + offset
             if status[b] == _lib.UTT_EMPTY:
                 raise ValueError(f"utterance {u}: empty emissions")
+            if status[b] in (_lib.UTT_NONFINITE, _lib.UTT_ABOVE_ZERO, _lib.UTT_NOT_NORMALIZED):
+                t, v = int(np.asarray(lengths)[b, 0]), int(np.asarray(counts)[b])
+                row = inputs[b, t] if inputs is not None else None
+                raise ValueError(f"utterance {u}: " + validation_message(int(status[b]) - 4, row, t, v))
             if status[b] == _lib.UTT_OVERFLOW:
                 t = int(np.asarray(lengths)[b, 0]) if lengths is not None else "?"
                 raise _lib.CtcbError(f"utterance {u}: frame {t}: more near-tied candidates at the beam cut than "
@@ -536,6 +549,18 @@ class CUCTCDecoder:
         _lib.check(_lib.load().ctcb_set_beam_size_token(self._h, 0 if k is None else int(k)),
                    "ctcb_set_beam_size_token")
         self.beam_size_token = None if k is None or k >= len(self.vocab_list) else int(k)
+
+    def set_validate(self, mode) -> None:
+        """Input validation fused into every decode (ctcb_set_validate), the
+        checks EmissionMatrix(strict=True) runs before ctcforge decodes an
+        utterance (emissions.py:128-150): True / "strict" (default), False /
+        "off", or "nonstrict" (no row-normalisation check).  Failures raise the
+        reference's ValueError when results are read (to_host / __call__)."""
+        m = {True: 1, "strict": 1, False: 0, "off": 0, "nonstrict": 2}.get(mode)
+        if m is None:
+            raise ValueError("validate must be True/'strict', False/'off' or 'nonstrict'")
+        _lib.check(_lib.load().ctcb_set_validate(self._h, m), "ctcb_set_validate")
+        self.validate = mode
 
     def kernel_timing(self, enable: bool = True) -> None:
         """Record CUDA events around the beam-search kernel of every following

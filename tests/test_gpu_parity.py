@@ -671,3 +671,68 @@ def test_block_kernel_ties_small_vocab(V, beam, quant, monkeypatch):
             assert sc[b, j] == sc2[b, j] and ln[b, j] == ln2[b, j], (b, j)
             assert np.array_equal(tok[b, j, : ln[b, j]], tok2[b, j, : ln[b, j]]), (b, j)
             assert np.array_equal(ts[b, j, : ln[b, j]], ts2[b, j, : ln[b, j]]), (b, j)
+
+
+# ---------------------------------------------------------------- fused input validation
+def _val_batch(V=12, B=4, T=20, seed=5):
+    rng = np.random.default_rng(seed)
+    x = rng.normal(size=(B, T, V))
+    return (x - np.log(np.exp(x).sum(-1, keepdims=True))).astype(np.float32)
+
+
+@pytest.mark.parametrize("beam,env", [(10, None), (32, None), (10, "CTCB_FORCE_GENERIC"), (4, "CTCB_TOPK_MODE")])
+def test_fused_validation_default(beam, env, monkeypatch):
+    """Validation is on by default and fused into the decode kernels (fast,
+    block) or done after them (generic); each case raises the reference's
+    message for the first invalid utterance (emissions.py:128-150 run by
+    decode_batch in utterance order)."""
+    if env == "CTCB_TOPK_MODE":
+        monkeypatch.setenv(env, "fused")
+    elif env:
+        monkeypatch.setenv(env, "1")
+    V = 12
+    dec = cuda_ctc_decoder(vocab(V), beam_size=beam, nbest=1, blank_skip_threshold=0.9)
+    lens = torch.tensor([20, 20, 15, 20], dtype=torch.int32).cuda()
+    lp = _val_batch(V)
+    got = dec(torch.from_numpy(lp).cuda(), lens)  # clean batch decodes
+    assert len(got) == 4
+    bad = lp.copy()
+    bad[2, 14, 5] = np.nan
+    bad[1, 3, 7] = 0.5
+    bad[3, 17, 2] = np.nan
+    with pytest.raises(ValueError, match=r"utterance 1: log-probability above 0 at frame 3, token 7: 0\.5"):
+        dec(torch.from_numpy(bad).cuda(), lens)
+    bad[1, 3, 7] = np.log(0.01)  # utterance 1 now unnormalized (strict)
+    with pytest.raises(ValueError, match=r"utterance 1: frame 3 is not normalized"):
+        dec(torch.from_numpy(bad).cuda(), lens)
+    bad[1, 3] = lp[1, 3]
+    with pytest.raises(ValueError, match=r"utterance 2: non-finite log-probability at frame 14, token 5"):
+        dec(torch.from_numpy(bad).cuda(), lens)
+    bad[2, 14] = lp[2, 14]
+    bad[2, 16, 4] = np.nan  # beyond lens[2] = 15: not checked (frames t >= len are padding)
+    with pytest.raises(ValueError, match=r"utterance 3: non-finite log-probability at frame 17, token 2"):
+        dec(torch.from_numpy(bad).cuda(), lens)
+    bad[3, 17] = lp[3, 17]
+    # a blank-skipped frame (blank prob 0.95 >= 0.9) is never staged by the
+    # decode kernel: the follow-up pass checks it
+    row = np.full(V, np.log(0.05 / (V - 1)), dtype=np.float32)
+    row[0] = np.log(0.95)
+    bad[0, 9] = row
+    bad[0, 9, 6] = -np.inf
+    with pytest.raises(ValueError, match=r"utterance 0: non-finite log-probability at frame 9, token 6"):
+        dec(torch.from_numpy(bad).cuda(), lens)
+    dec.set_validate(False)
+    dec(torch.from_numpy(bad).cuda(), lens)  # decodes (garbage in, no error)
+    dec.set_validate("nonstrict")
+    bad[0, 9] = row
+    bad[0, 9, 6] = np.log(0.5)  # unnormalized only: passes without the norm check
+    dec(torch.from_numpy(bad).cuda(), lens)
+
+
+def test_fused_validation_host_path():
+    V = 12
+    dec = cuda_ctc_decoder(vocab(V), beam_size=10, nbest=1)
+    lp = _val_batch(V)
+    lp[2, 4, 1] = np.inf
+    with pytest.raises(ValueError, match=r"utterance 2: non-finite log-probability at frame 4, token 1"):
+        dec(torch.from_numpy(lp), torch.tensor([20, 20, 20, 20], dtype=torch.int32))
