@@ -618,14 +618,25 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
 
     // -- A. blank-skip compaction (emissions.py:298-306); in precomputed-top-k
     //    mode ctcb_framemap_kernel already did it
-    int kept = 0;
-    if (PRE) {
-      kept = P.kept[u];
-    } else {
-      kept = frame_map_warp(P, ubase, len_u, fmap, lane);
-      if (lane == 0) P.kept[u] = kept;
-      __syncwarp();
-    }
+    //    Otherwise frames are classified 32 at a time just ahead of the row
+    //    prefetch, so the blank values read here are still in L2 when the TMA
+    //    fetches the rows (a pass over the whole utterance first costs an extra
+    //    DRAM burst per frame: 6 % of cfg4's traffic)
+    int kept = 0;  // !PRE: kept frames classified so far
+    int ct = 0;    // !PRE: next frame to classify
+    if (PRE) kept = P.kept[u];
+    auto classify_to = [&](int idx) {  // classify until kept frame `idx` is known or frames run out
+      while (!PRE && idx >= kept && ct < len_u) {
+        const int t = ct + lane;
+        bool keep = t < len_u;
+        if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
+        const unsigned bal = __ballot_sync(FULL, keep);
+        if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
+        kept += __popc(bal);
+        ct += 32;
+        __syncwarp();
+      }
+    };
     // precomputed top-k lists, prefetched one frame ahead
     const size_t tk_base = (size_t)u * P.T_max * k;
     int pre_st = 0;
@@ -637,12 +648,13 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
 
     // row staging: lane 0 issues the bulk copy of kept frame `idx`; frame-map
     // entries are read 32 at a time into registers
-    int fm_blk = -1, fm_reg = 0;
+    int fm_blk = -1, fm_reg = 0, fm_hi = 0;
     auto issue = [&](int idx) {
-      if ((idx >> 5) != fm_blk) {
+      if ((idx >> 5) != fm_blk || idx >= fm_hi) {  // (re)load: the block may have grown since
         fm_blk = idx >> 5;
         const int t = (fm_blk << 5) + lane;
         fm_reg = t < kept ? fmap[t] : 0;
+        fm_hi = kept < (fm_blk << 5) + 32 ? kept : (fm_blk << 5) + 32;
       }
       const int fr = __shfl_sync(FULL, fm_reg, idx & 31);
       if (lane == 0) {
@@ -654,6 +666,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       slot_i = slot_i + 1 == ring ? 0 : slot_i + 1;
     };
     int n_out = 0;  // issued, not yet consumed
+    classify_to(ring - 1);
     if (P.bulk_ok) {
       const int pre = kept < ring - 1 ? kept : ring - 1;
       for (int i = 0; i < pre; i++) { issue(i); n_out++; }
@@ -667,7 +680,10 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
     bool died = false;
     int died_at = 0;
 
-    for (int i = 0; i < kept; i++) {
+    int i = 0;
+    for (;; i++) {
+      classify_to(i + ring - 1);
+      if (i >= kept) break;
       float* row;
       if (P.bulk_ok) {
         if (i + ring - 1 < kept) { issue(i + ring - 1); n_out++; }
@@ -1204,7 +1220,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       vfinish();
       __syncwarp();
       // trellis checkpoint: ancestor slot at the chunk start for every entry
-      if ((i % kChunk) == kChunk - 1 || i == kept - 1) {
+      if ((i % kChunk) == kChunk - 1) {
         if (lane < H) {
           int slot = lane;
           for (int t = i % kChunk; t >= 0; --t) slot = trel_src(S.tring[t * 16 + slot]);
@@ -1212,6 +1228,16 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         }
         __syncwarp();
       }
+    }
+    if (!PRE && lane == 0) P.kept[u] = kept;  // (partial if the beam died: later frames unclassified)
+    if (!died && kept % kChunk != 0) {  // checkpoint of the last, partial chunk
+      const int il = kept - 1;
+      if (lane < H) {
+        int slot = lane;
+        for (int t = il % kChunk; t >= 0; --t) slot = trel_src(S.tring[t * 16 + slot]);
+        P.anc[((size_t)u * P.n_chunks + il / kChunk) * 16 + lane] = (uint8_t)slot;
+      }
+      __syncwarp();
     }
 
     if (lane == 0) P.vdone[u] = (PRE || !died) ? kept : died_at + 1;  // rows screened (here or by the top-k kernel)
