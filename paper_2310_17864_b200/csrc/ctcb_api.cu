@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "../../include/ctcb.h"
@@ -616,6 +617,15 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     h->launches++;
     CTCB_CUDA(cudaGetLastError());
   }
+  // diagnostics: CTCB_UTT_TRACE=path dumps a per-utterance timeline of the
+  // fast kernels ([B, 2] uint64: smid << 48 | global warp, start ns; end ns)
+  const char* trace_path = getenv("CTCB_UTT_TRACE");
+  unsigned long long* trace = nullptr;
+  if (trace_path && fast && !pair && !fused) {
+    CTCB_CUDA(cudaMalloc(&trace, (size_t)B * 16));
+    CTCB_CUDA(cudaMemsetAsync(trace, 0, (size_t)B * 16, s));
+    P.utt_trace = trace;
+  }
   const bool timed = h->timing && h->n_timed < 64;
   if (timed) CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed], s));
   if (blk) {
@@ -649,6 +659,16 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   if (timed) {
     CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed + 1], s));
     h->n_timed++;
+  }
+  if (trace) {
+    std::vector<unsigned long long> buf((size_t)B * 2);
+    CTCB_CUDA(cudaMemcpyAsync(buf.data(), trace, (size_t)B * 16, cudaMemcpyDeviceToHost, s));
+    CTCB_CUDA(cudaStreamSynchronize(s));
+    CTCB_CUDA(cudaFree(trace));
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(buf.data(), 8, buf.size(), f);
+      fclose(f);
+    }
   }
   if (P.validate) {
     // rows the decode kernel did not screen (skipped frames, frames after a

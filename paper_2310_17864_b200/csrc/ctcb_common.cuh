@@ -263,6 +263,17 @@ static __device__ __noinline__ unsigned long long row_check_exact(const float* r
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   return fabs(m + log(sum)) > 1e-3 ? vkey_make(3, t, -1) : ~0ull;
 }
+// Diagnostics: SM id and the global nanosecond timer.
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long r;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(r));
+  return r;
+}
 // Fast screen of a staged row, split so that the decode kernels keep it off
 // their per-frame critical path: row_partials is lane-local (float4 chunks
 // c4 = lane, lane + 32, ...), row_verdict (three independent REDUX ops) runs

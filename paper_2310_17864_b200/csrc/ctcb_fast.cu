@@ -23,6 +23,20 @@
 
 #include "ctcb_common.cuh"
 #include "ctcb_internal.h"
+#include <cstdio>
+// Debug builds (-DCTCB_FAST_CHECK): bounds / invariant checks that print the
+// first few failures (compute-sanitizer is not available on the GPU pool).
+#ifdef CTCB_FAST_CHECK
+__device__ int g_fchk_count;
+#define FCHK(c, a, b)                                                                                       \
+  do {                                                                                                     \
+    if (!(c) && atomicAdd(&g_fchk_count, 1) < 16)                                                          \
+      printf("ctcb_fast check failed: %s (line %d, block %d, lane %d) %d %d\n", #c, __LINE__, blockIdx.x,     \
+             (int)(threadIdx.x & 31), (int)(a), (int)(b));                                                 \
+  } while (0)
+#else
+#define FCHK(c, a, b) do { } while (0)
+#endif
 
 namespace ctcb {
 
@@ -122,21 +136,24 @@ struct FastSmem {
 // utterances).  Sibling prefixes with identical scores (a duplicated fp32
 // value in some row) tie again every frame; the cache answers those without
 // re-reading their sequences.
+// Direct-mapped: the slot of a pair is a symmetric hash of the two prefix
+// hashes, so a lookup is one probe (a persistent exact tie asks every frame).
+__device__ __forceinline__ int tc_slot(uint64_t ha, uint64_t hb) {
+  const uint64_t x = (ha ^ hb) * 0x9e3779b97f4a7c15ull;
+  return (int)(x >> 59) & (kTieCache - 1);
+}
 __device__ int tc_lookup(const FastSmem& S, uint64_t ha, uint64_t hb) {
-#pragma unroll 1
-  for (int i = 0; i < kTieCache; i++) {
-    if (S.tc_h[2 * i] == ha && S.tc_h[2 * i + 1] == hb) return S.tc_r[i];
-    if (S.tc_h[2 * i] == hb && S.tc_h[2 * i + 1] == ha) return -S.tc_r[i];
-  }
+  const int i = tc_slot(ha, hb);
+  const uint64_t a = S.tc_h[2 * i], b = S.tc_h[2 * i + 1];
+  if (a == ha && b == hb) return S.tc_r[i];
+  if (a == hb && b == ha) return -S.tc_r[i];
   return 0;
 }
 __device__ void tc_insert(const FastSmem& S, uint64_t ha, uint64_t hb, int r) {
-  if (tc_lookup(S, ha, hb)) return;
-  int i = S.tc_r[kTieCache];
+  const int i = tc_slot(ha, hb);
   S.tc_h[2 * i] = ha;
   S.tc_h[2 * i + 1] = hb;
   S.tc_r[i] = r;
-  S.tc_r[kTieCache] = (i + 1) % kTieCache;
 }
 __device__ int fast_seq_cmp_full(const Params& P, const FastSmem& S, int u, int steps_done, int ea, int xa, int eb,
                                  int xb, bool* strict);
@@ -516,6 +533,7 @@ __device__ __forceinline__ int topk_small(const FastSmem& S, const float* row, i
 // threshold test, decoder.py:621-623).
 constexpr uint32_t kTol = 3u;
 
+
 __device__ __forceinline__ uint32_t f2u_sat(double z) {
   uint32_t r;
   asm("cvt.rzi.u32.f64 %0, %1;" : "=r"(r) : "d"(z));  // saturating: < 0 -> 0, >= 2^32 -> 2^32 - 1
@@ -525,6 +543,80 @@ __device__ __forceinline__ long long f2ll_floor(double z) {
   long long r;
   asm("cvt.rmi.s64.f64 %0, %1;" : "=l"(r) : "d"(z));  // saturating; -inf -> INT64_MIN
   return r;
+}
+
+// Exact order of close-key runs with exactly equal scores: token sequence,
+// then flag (decoder.py:651-681), by lane 0 (insertion sort with
+// fast_precedes); lanes < beam then write the new beam's merge records.
+__device__ __forceinline__ void serial_runs(const Params& P, const FastSmem& S, int u, int i, int beam, int lane,
+                                         uint64_t h, int len, double es, int ba, int xa, int fa, int rec,
+                                         unsigned cm, int bmax) {
+  int* pi = (int*)S.cand;
+  if (lane <= bmax) {
+    S.tie_sc[lane] = es;
+    S.tie_i[lane * 4 + 0] = ba;
+    S.tie_i[lane * 4 + 1] = xa;
+    S.tie_i[lane * 4 + 2] = fa;
+    S.tie_i[lane * 4 + 3] = rec;
+    pi[lane] = lane;
+  }
+  if (lane < 16) { S.hs[lane] = h; S.hl[lane] = len; }
+  __syncwarp();
+  if (lane == 0) {
+    for (int a = 0; a <= bmax;) {
+      int b = a;
+      while (b < bmax && ((cm >> b) & 1u)) b++;
+      for (int q = a + 1; q <= b; q++) {  // insertion sort of positions a..b
+        const int x = pi[q];
+        int r = q;
+        while (r > a) {
+          const int y = pi[r - 1];
+          if (!fast_precedes(P, S, u, i, S.tie_sc[x], S.tie_i[x * 4], S.tie_i[x * 4 + 1], S.tie_i[x * 4 + 2],
+                             S.tie_sc[y], S.tie_i[y * 4], S.tie_i[y * 4 + 1], S.tie_i[y * 4 + 2]))
+            break;
+          pi[r] = y;
+          r--;
+        }
+        pi[r] = x;
+      }
+      a = b + 1;
+    }
+  }
+  __syncwarp();
+  if (lane < beam) S.rec_i[lane] = lane <= bmax ? S.tie_i[pi[lane] * 4 + 3] : rec;
+  __syncwarp();
+}
+
+// Exact order inside runs of close keys (rare; a persistent near-tie between
+// two beam entries recurs every frame).  Lane p holds the p-th largest sorted
+// key; `cl` marks (p, p+1) as possibly misordered and `es` is the exact fp64
+// score of lane p's candidate.  Keys of different runs are ordered exactly, so
+// only the runs up to the beam cut are re-ranked by exact score
+// (decoder.py:651-681).  Returns 1 with `pos` = the candidate's exact rank,
+// 0 when the run at the cut reaches lane 31 (candidates beyond the warp are
+// not visible), 2 when a run holds exactly equal scores (token-sequence
+// order needed).  cm / bmax: run links and the last position that matters.
+__device__ __forceinline__ int close_runs_rank(bool cl, double es, int beam, int lane, int& pos, unsigned& cm,
+                                               int& bmax) {
+  cm = __ballot_sync(FULL, cl);
+  bmax = beam - 1 + (__ffs(~(cm >> (beam - 1))) - 1);  // end of the run holding beam - 1
+  const unsigned starts = ~(cm << 1);
+  const int rs = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+  const unsigned after = lane < 31 ? starts & (0xfffffffeu << lane) : 0u;
+  const int re = after ? __ffs(after) - 2 : 31;
+  int rank = 0;
+  bool tie = false;
+#pragma unroll 1
+  for (int q = 0; q < 32; q++) {
+    const double eq = __shfl_sync(FULL, es, q);
+    if (q <= bmax && q != lane && q >= rs && q <= re) {
+      rank += eq > es ? 1 : 0;
+      tie |= eq == es;
+    }
+  }
+  const bool any_tie = __any_sync(FULL, tie && lane <= bmax);
+  pos = lane <= bmax ? rs + rank : lane;
+  return bmax >= 31 ? 0 : (any_tie ? 2 : 1);
 }
 
 // SMALL: V <= 512, ring 2, rows of 2048 B -- the shared-memory layout is a
@@ -598,13 +690,24 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
   uint32_t par_c = 0u;            // mbarrier phase parity of the consume slot
   const uint32_t row_copy = (uint32_t)V * 4u;
 
+  int tr_u = -1;  // diagnostics timeline (P.utt_trace): utterance in progress
+  auto tr_end = [&]() {
+    if (P.utt_trace && tr_u >= 0 && lane == 0) P.utt_trace[2 * (size_t)tr_u + 1] = globaltimer_ns();
+  };
   for (;;) {
+    tr_end();
     int item = 0;
     if (lane == 0) item = atomicAdd(P.counter, 1);
     item = __shfl_sync(FULL, item, 0);
     if (item >= P.B) break;
     const int u = P.order[item];
     const int len_u = P.lens[u];
+    if (P.utt_trace && lane == 0) {
+      tr_u = u;
+      P.utt_trace[2 * (size_t)u] = ((unsigned long long)smid() << 48) |
+                                   ((unsigned long long)(blockIdx.x * (blockDim.x >> 5) + wid) << 32) |
+                                   (globaltimer_ns() & 0xffffffffull);
+    }
     if (len_u <= 0 || len_u > P.T_max) {
       if (lane == 0) {
         P.status[u] = len_u == 0 ? kUttEmpty : kUttBadLen;
@@ -853,6 +956,16 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       };
       if (!tokK) blank_repeat(true);
 
+      // Exact order inside runs of close keys (rare; a persistent near-tie
+      // between two beam entries recurs every frame).  Lane p holds the p-th
+      // largest sorted key (slot tag in the low 6 bits); `cl` marks (p, p+1) as
+      // possibly misordered.  Keys of different runs are ordered exactly, so
+      // only the runs up to the beam cut are re-ranked, by exact fp64 score
+      // (decoder.py:651-681); exact_of(slot, es, ba, xa, fa) is
+      // warp-collective.  Exactly equal scores inside a run are ordered by
+      // token sequence and flag by lane 0 when `serial` (the shortcut path);
+      // otherwise, or when the run at the cut reaches lane 31, returns false
+      // and the caller takes the exact k-way merge.
       bool shortcut = false;
       int Hn = 0;
       if (sc_on) {
@@ -889,15 +1002,36 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
           const uint32_t nxt = __shfl_down_sync(FULL, key, 1);
           // not separated by a truncated unit, or near the threshold floor:
           // the full path decides this frame
-          const bool bad = lane < beam && key != 0u &&
-                           ((nxt != 0u && (key >> 6) - (nxt >> 6) <= 1u) || key < 256u);
+          const bool cl = lane < 31 && key != 0u && nxt != 0u && (key >> 6) - (nxt >> 6) <= 1u;
+          const bool bad = lane < beam && key != 0u && (cl || key < 256u);
           __syncwarp();
-          if (__any_sync(FULL, bad)) {
-            shortcut = false;
-            if (lane == 0) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
-          } else {
-            Hn = __popc(__ballot_sync(FULL, lane < beam && key != 0u));
+          Hn = __popc(__ballot_sync(FULL, lane < beam && key != 0u));
+          if (!__any_sync(FULL, bad)) {
             if (lane < Hn) S.rec_i[lane] = S.slot_rec[63 - (int)(key & 63u)];
+          } else {
+            // rare: keys near the threshold floor -> the full path; close keys
+            // -> exact order inside their runs (candidate of slot g = 63 - tag:
+            // repeat group of entry g < 16 or blank group of entry g - 16)
+            int rr = 0;
+            if (!__any_sync(FULL, lane < beam && key != 0u && key < 256u)) {
+              const int g = key ? 63 - (int)(key & 63u) : 0;
+              const double r_es = __shfl_sync(FULL, mine, g);
+              const int r_rec = S.slot_rec[g];
+              int r_pos, r_bmax;
+              unsigned r_cm;
+              rr = close_runs_rank(cl, r_es, beam, lane, r_pos, r_cm, r_bmax);
+              if (rr == 1) {
+                if (r_pos < beam) S.rec_i[r_pos] = r_rec;
+              } else if (rr == 2) {
+                serial_runs(P, S, u, i, beam, lane, h, len, r_es, g & 15, -1, g >= 16 ? 1 : 0, r_rec, r_cm, r_bmax);
+                rr = 1;
+              }
+            }
+            if (rr == 0) {
+              shortcut = false;
+              Hn = 0;
+              if (lane == 0) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
+            }
           }
           __syncwarp();
         }
@@ -985,13 +1119,43 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // low 6 bits; adjacent keys within 2 truncated units, or keys near the
       // floor, fall back to the exact k-way merge below.
       bool oneshot = beam <= 10;
+      int ldj_f = ldj;
       if (oneshot) {
         // the dominance count needs every list to hold >= beam valid positions
         // (true with k = 2 beam <= V-1 and the full vocabulary; small V or
         // beam_size_token can leave shorter lists)
         const double gA_prev = __shfl_up_sync(FULL, gA, 1);
-        const bool unsorted = gen && ((me > 0 && !(gA_prev > gA + 1e-9 * (1.0 + fabs(gA)))) || __popc(gv) < beam);
-        oneshot = !__any_sync(FULL, unsorted);
+        const bool shortl = gen && __popc(gv) < beam;
+        const bool unsorted = gen && me > 0 && !(gA_prev > gA + 1e-9 * (1.0 + fabs(gA)));
+        if (__any_sync(FULL, shortl)) {
+          oneshot = false;
+        } else if (__any_sync(FULL, unsorted)) {
+          // prefixes not ordered by A (or tied): the same dominance count with
+          // tiers -- list d keeps beam / (1 + lists whose A exceeds A_d by the
+          // margin) positions; the slots are laid out by a prefix sum
+          int tier = 0;
+          for (int d2 = 0; d2 < nD; d2++) {
+            const double a2 = __shfl_sync(FULL, gA, 16 + d2);
+            tier += (gen && a2 > gA + 1e-9 * (1.0 + fabs(gA))) ? 1 : 0;
+          }
+          const int q = gen ? beam / (tier + 1) : 0;
+          const int qi = warp_incl_scan(q, lane);
+          const int tot = __shfl_sync(FULL, qi, 31);
+          if (tot > 32) {
+            oneshot = false;
+          } else {
+            const int off = qi - q;
+            const unsigned starts = __reduce_or_sync(FULL, q > 0 ? 1u << off : 0u);
+            if (q > 0) S.hist[off] = (uint32_t)me;
+            __syncwarp();
+            ldj_f = 0xff;
+            if (lane < tot) {
+              const int st0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+              ldj_f = (int)S.hist[st0] | ((lane - st0) << 4);
+            }
+            __syncwarp();
+          }
+        }
         if (!oneshot && lane == 0) atomicAdd(&P.dbg[kDbgFrames], 1ull);  // diagnostics: fallback by order/length
       }
       if (oneshot) {
@@ -1010,8 +1174,8 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         __syncwarp();
         // append slot 32 + lane: (d, j) from the quota table
         uint32_t bkey = 0u;
-        const int qd = ldj & 15, qj = ldj >> 4;
-        if (ldj != 0xff && qd < nD) {
+        const int qd = ldj_f & 15, qj = ldj_f >> 4;
+        if (ldj_f != 0xff && qd < nD) {
           // j-th valid position: j plus the excluded positions at or below it
           // (exclusions are the few flag-0 children and last(R))
           uint32_t ex = ~S.dgv[qd] & fullk;
@@ -1037,13 +1201,54 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         akey = max(akey, __shfl_sync(FULL, bkey, 31 - lane));
         akey = merge_desc32(akey, lane);
         const uint32_t nxt = __shfl_down_sync(FULL, akey, 1);
-        const bool close = lane < beam && akey != 0u && nxt != 0u && (akey >> 6) - (nxt >> 6) <= 1u;
-        if (__any_sync(FULL, close || nearfloor)) {
-          oneshot = false;
-          if (lane == 0) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
-        } else {
-          Hn = __popc(__ballot_sync(FULL, lane < beam && akey != 0u));
+        const bool cl = lane < 31 && akey != 0u && nxt != 0u && (akey >> 6) - (nxt >> 6) <= 1u;
+        Hn = __popc(__ballot_sync(FULL, lane < beam && akey != 0u));
+        if (!__any_sync(FULL, (cl && lane < beam) || nearfloor)) {
           if (lane < Hn) S.rec_i[lane] = S.slot_rec[63 - (int)(akey & 63u)];
+        } else if (__any_sync(FULL, nearfloor)) {
+          oneshot = false;
+        } else {
+          // rare: close keys -> exact order inside their runs; the exact score
+          // of slot sl's candidate as the commit below computes it
+          const int sl = akey ? 63 - (int)(akey & 63u) : 0;
+          const int rec = akey != 0u ? S.slot_rec[sl] : (lane & 15);
+          const int wl = rec & 0xff, it = rec >> 8;
+          const int wk = __shfl_sync(FULL, kpack, wl);
+          const double w0 = __shfl_sync(FULL, q0, wl), w1 = __shfl_sync(FULL, q1, wl), w2 = __shfl_sync(FULL, q2, wl);
+          const int bse = __shfl_sync(FULL, gsrc, wl);
+          const double bs1 = __shfl_sync(FULL, s, bse), bs2 = __shfl_sync(FULL, s_p2, bse);
+          const int bp2 = __shfl_sync(FULL, p2, bse), blst = __shfl_sync(FULL, last, bse);
+          double r_es;
+          int r_ba, r_xa, r_fa;
+          if (wl >= 16) {  // append group (R+c, 0)
+            const int itc = it < 32 ? it : 0;
+            const double v = (double)S.sval[itc];
+            r_es = bs1 + v;
+            if (bp2 >= 0) r_es = merge2(r_es, bs2 + v, MX);
+            r_ba = bse;
+            r_xa = S.stok[itc];
+            r_fa = 0;
+          } else {  // special group: blank (R,1), repeat (R,0), last-token append (R+last,0)
+            const int kind = (wk >> (2 * (it & 3))) & 3;
+            r_es = it == 0 ? w0 : (it == 1 ? w1 : w2);
+            r_ba = wl;
+            r_xa = kind == 2 ? blst : -1;
+            r_fa = kind == 0 ? 1 : 0;
+          }
+          int r_pos, r_bmax;
+          unsigned r_cm;
+          const int rr = close_runs_rank(cl, r_es, beam, lane, r_pos, r_cm, r_bmax);
+          if (rr == 1) {
+            if (r_pos < beam) S.rec_i[r_pos] = rec;
+          } else if (rr == 2) {
+            serial_runs(P, S, u, i, beam, lane, h, len, r_es, r_ba, r_xa, r_fa, rec, r_cm, r_bmax);
+          } else {
+            oneshot = false;
+          }
+        }
+        if (!oneshot) {
+          Hn = 0;
+          if (lane == 0) atomicAdd(&P.dbg[kDbgOneshotFallback], 1ull);
         }
         __syncwarp();
       }
@@ -1076,6 +1281,11 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         refill();
       }
       int recw = lane | ((__ffs(gq) - 1) << 8);  // record of the queue head
+#ifdef CTCB_FAST_CHECK
+      {
+        FCHK((kq0 == 0u) == (gq == 0u) || lane < 16, i, (int)gq);
+      }
+#endif
 
       // ================= k-way merge (decoder.py:651-681) =================
       for (int r = 0; r < beam; r++) {
@@ -1150,6 +1360,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         }
         // pop: the record of the head (lane | item << 8) goes to the new rank;
         // losers write their own scratch slot instead of branching
+        FCHK(!win || gq != 0u, i, r * 1000 + (int)kq0);
         S.rec_i[win ? r : 16 + lane] = recw;
         gq = win ? (gq & (gq - 1u)) : gq;
         recw = lane | ((__ffs(gq) - 1) << 8);
@@ -1175,6 +1386,15 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // lane r builds new entry r from the winning lane's registers
       const bool nent = lane < Hn;
       const int rec = S.rec_i[nent ? lane : 0];
+#ifdef CTCB_FAST_CHECK
+      {
+        FCHK(Hn <= beam, Hn, beam);
+        const int wl_ = rec & 0xff, it_ = rec >> 8;
+        FCHK(!nent || (wl_ < 32 && (wl_ >= 16 ? it_ < k : it_ < 3)), rec, i);
+        const unsigned mm = __match_any_sync(FULL, nent ? rec : -1 - lane);
+        FCHK(!nent || __popc(mm) == 1, rec, (int)mm);
+      }
+#endif
       const int wl = nent ? (rec & 0xff) : lane, item2 = rec >> 8;
       const int wk = __shfl_sync(FULL, kpack, wl);
       const double w_q0 = __shfl_sync(FULL, q0, wl), w_q1 = __shfl_sync(FULL, q1, wl), w_q2 = __shfl_sync(FULL, q2, wl);

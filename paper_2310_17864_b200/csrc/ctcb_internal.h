@@ -79,6 +79,7 @@ struct Params {
   unsigned long long* vkey; // [B] smallest offender key (vkey_make) seen, ~0 = none
   int32_t* vdone;           // [B] leading kept frames the decode kernel checked
   int vfused;               // the decode kernel wrote vdone (else every frame is checked after it)
+  unsigned long long* utt_trace;  // diagnostics (CTCB_UTT_TRACE): [B, 2] {smid << 48 | global warp, start ns}, end ns
 };
 
 // Fused search limits.
