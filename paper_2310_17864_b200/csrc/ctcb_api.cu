@@ -622,8 +622,8 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   const char* trace_path = getenv("CTCB_UTT_TRACE");
   unsigned long long* trace = nullptr;
   if (trace_path && fast && !pair && !fused) {
-    CTCB_CUDA(cudaMalloc(&trace, (size_t)B * 16));
-    CTCB_CUDA(cudaMemsetAsync(trace, 0, (size_t)B * 16, s));
+    CTCB_CUDA(cudaMalloc(&trace, (size_t)B * 16 + 16 * 8));  // + phase cycle sums (-DCTCB_PHASES)
+    CTCB_CUDA(cudaMemsetAsync(trace, 0, (size_t)B * 16 + 16 * 8, s));
     P.utt_trace = trace;
   }
   const bool timed = h->timing && h->n_timed < 64;
@@ -661,8 +661,8 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     h->n_timed++;
   }
   if (trace) {
-    std::vector<unsigned long long> buf((size_t)B * 2);
-    CTCB_CUDA(cudaMemcpyAsync(buf.data(), trace, (size_t)B * 16, cudaMemcpyDeviceToHost, s));
+    std::vector<unsigned long long> buf((size_t)B * 2 + 16);
+    CTCB_CUDA(cudaMemcpyAsync(buf.data(), trace, (size_t)B * 16 + 16 * 8, cudaMemcpyDeviceToHost, s));
     CTCB_CUDA(cudaStreamSynchronize(s));
     CTCB_CUDA(cudaFree(trace));
     if (FILE* f = fopen(trace_path, "wb")) {

@@ -37,6 +37,22 @@ __device__ int g_fchk_count;
 #else
 #define FCHK(c, a, b) do { } while (0)
 #endif
+// Diagnostics (-DCTCB_PHASES, with CTCB_UTT_TRACE set): lane 0 accumulates
+// clock() cycles per frame phase; summed per launch after the utterance trace
+// (tools/phase_cycles.py).
+#ifdef CTCB_PHASES
+#define PH(n)                                          \
+  do {                                                 \
+    if (P.utt_trace && lane == 0) {                    \
+      const uint32_t t_ = (uint32_t)clock();           \
+      ph_cyc[ph_cur] += t_ - ph_t;                     \
+      ph_t = t_;                                       \
+      ph_cur = (n);                                    \
+    }                                                  \
+  } while (0)
+#else
+#define PH(n) do { } while (0)
+#endif
 
 namespace ctcb {
 
@@ -691,8 +707,19 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
   const uint32_t row_copy = (uint32_t)V * 4u;
 
   int tr_u = -1;  // diagnostics timeline (P.utt_trace): utterance in progress
+#ifdef CTCB_PHASES
+  unsigned long long ph_cyc[16] = {};
+  uint32_t ph_t = 0;
+  int ph_cur = 15;
+#endif
   auto tr_end = [&]() {
     if (P.utt_trace && tr_u >= 0 && lane == 0) P.utt_trace[2 * (size_t)tr_u + 1] = globaltimer_ns();
+#ifdef CTCB_PHASES
+    if (P.utt_trace && tr_u >= 0 && lane == 0)
+      for (int q = 0; q < 16; q++) atomicAdd(&P.utt_trace[2 * (size_t)P.B + q], ph_cyc[q]);
+    if (lane == 0)
+      for (int q = 0; q < 16; q++) ph_cyc[q] = 0;
+#endif
   };
   for (;;) {
     tr_end();
@@ -785,12 +812,14 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
 
     int i = 0;
     for (;; i++) {
+      PH(0);
       classify_to(i + ring - 1);
       if (i >= kept) break;
       float* row;
       if (P.bulk_ok) {
         if (i + ring - 1 < kept) { issue(i + ring - 1); n_out++; }
         mbar_wait(&S.mbar[slot_c], par_c);
+        PH(1);
         row = (float*)(S.rows + (size_t)slot_c * row_bytes);
         n_out--;
         slot_c++;
@@ -900,6 +929,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         vmax = k > 0 ? (double)v0 : -INFINITY;
       }
 
+      PH(2);
       // ================= merge structure =================
       const bool ent = lane < H;
       const uint64_t ph_m = shfl64(ph, me);
@@ -966,6 +996,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // token sequence and flag by lane 0 when `serial` (the shortcut path);
       // otherwise, or when the run at the cut reaches lane 31, returns false
       // and the caller takes the exact k-way merge.
+      PH(3);
       bool shortcut = false;
       int Hn = 0;
       if (sc_on) {
@@ -1052,8 +1083,13 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       };
       int gsrc = lane;
       if (shortcut) local_order();
+#ifdef CTCB_PHASES
+      if (P.utt_trace && lane == 0) ph_cyc[14] += shortcut ? 1 : 0;
+#endif
       if (!shortcut) {
+        PH(4);
         if (sc_on && !PRE) full_topk();
+        PH(5);
         // S positions of last tokens; flag-0 children exclude their token from
         // the parent's append list (they become repeat groups)
         const int mypos = (ent && last >= 0) ? (int)S.posmap[last] : 0xff;
@@ -1111,6 +1147,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       // [1, 2^32 - 1] for a live list (A > -inf), 0 otherwise
       const long long gG = gv ? f2ll_floor((gA - kbase) * kScale) : 0ll;
       const uint32_t gLow = (gv && gA > -INFINITY) ? 1u : 0u;
+      PH(6);
       // ---- one-shot selection (beam <= 10): when the distinct prefixes are
       // ordered by A with a margin, append (d, j) (j-th valid S position of
       // the d-th prefix) is beaten by the (d+1)(j+1)-1 appends (d' <= d,
@@ -1253,6 +1290,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         __syncwarp();
       }
       if (!oneshot) {
+      PH(7);
       // rank-key queues: each lane pops its candidates in order.  Lanes < 16
       // queue their <= 3 special groups (items 0..2 = local sorted order);
       // lanes 16.. queue the next four valid positions of their append list
@@ -1382,6 +1420,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       __syncwarp();
       if (Hn == 0) { vfinish(); died = true; died_at = i; break; }
 
+      PH(8);
       // ================= commit (decoder.py:683-744) =================
       // lane r builds new entry r from the winning lane's registers
       const bool nent = lane < Hn;
@@ -1437,6 +1476,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         S.tring[(i % kChunk) * 16 + lane] = trel;
       }
       H = Hn;
+      PH(9);
       vfinish();
       __syncwarp();
       // trellis checkpoint: ancestor slot at the chunk start for every entry

@@ -37,7 +37,7 @@ os.environ["CTCB_UTT_TRACE"] = path
 dec.decode(dlp, dlens)
 torch.cuda.synchronize()
 del os.environ["CTCB_UTT_TRACE"]
-tr = np.fromfile(path, dtype=np.uint64).reshape(-1, 2)
+tr = np.fromfile(path, dtype=np.uint64)[: 2 * len(lens)].reshape(-1, 2)
 sm = (tr[:, 0] >> np.uint64(48)).astype(np.int64)
 warp = ((tr[:, 0] >> np.uint64(32)) & np.uint64(0xffff)).astype(np.int64)
 end = tr[:, 1].astype(np.int64)
