@@ -152,24 +152,34 @@ struct FastSmem {
 // utterances).  Sibling prefixes with identical scores (a duplicated fp32
 // value in some row) tie again every frame; the cache answers those without
 // re-reading their sequences.
-// Direct-mapped: the slot of a pair is a symmetric hash of the two prefix
-// hashes, so a lookup is one probe (a persistent exact tie asks every frame).
-__device__ __forceinline__ int tc_slot(uint64_t ha, uint64_t hb) {
+// 4-way set associative (kTieCache / 4 sets): the set of a pair is a
+// symmetric hash of the two prefix hashes, so a lookup is four probes (a
+// persistent exact tie asks every frame); each set replaces round-robin
+// (2-bit cursors packed in tc_r[kTieCache]).
+__device__ __forceinline__ int tc_set(uint64_t ha, uint64_t hb) {
   const uint64_t x = (ha ^ hb) * 0x9e3779b97f4a7c15ull;
-  return (int)(x >> 59) & (kTieCache - 1);
+  return (int)(x >> 59) & (kTieCache / 4 - 1);
 }
 __device__ int tc_lookup(const FastSmem& S, uint64_t ha, uint64_t hb) {
-  const int i = tc_slot(ha, hb);
-  const uint64_t a = S.tc_h[2 * i], b = S.tc_h[2 * i + 1];
-  if (a == ha && b == hb) return S.tc_r[i];
-  if (a == hb && b == ha) return -S.tc_r[i];
+  const int s0 = 4 * tc_set(ha, hb);
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    const uint64_t a = S.tc_h[2 * (s0 + w)], b = S.tc_h[2 * (s0 + w) + 1];
+    if (a == ha && b == hb) return S.tc_r[s0 + w];
+    if (a == hb && b == ha) return -S.tc_r[s0 + w];
+  }
   return 0;
 }
 __device__ void tc_insert(const FastSmem& S, uint64_t ha, uint64_t hb, int r) {
-  const int i = tc_slot(ha, hb);
+  if (tc_lookup(S, ha, hb)) return;
+  const int set = tc_set(ha, hb);
+  const uint32_t cur = (uint32_t)S.tc_r[kTieCache];
+  const int w = (int)((cur >> (2 * set)) & 3u);
+  const int i = 4 * set + w;
   S.tc_h[2 * i] = ha;
   S.tc_h[2 * i + 1] = hb;
   S.tc_r[i] = r;
+  S.tc_r[kTieCache] = (int)((cur & ~(3u << (2 * set))) | ((uint32_t)((w + 1) & 3) << (2 * set)));
 }
 __device__ int fast_seq_cmp_full(const Params& P, const FastSmem& S, int u, int steps_done, int ea, int xa, int eb,
                                  int xb, bool* strict);
