@@ -152,15 +152,18 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 bool use_fast(const ctcb_handle* h);
-// Precomputed-top-k mode for small batches (fewer utterances than ~2 per SM),
-// where one warp per utterance leaves the GPU latency-bound.
+// Precomputed-top-k mode for batches up to 10 utterances per SM: with few
+// warps per SM the walk is latency-bound and the frame-parallel top-k keeps
+// its per-frame latency off the chain (cfg4 shards of 512 / 1024 / 2048
+// utterances: 2.95 / 3.32 / 4.06 ms vs 3.46 / 3.69 / 4.07 fused,
+// tools/shard_modes.py); the full cfg4 batch (27 per SM) is faster fused.
 // CTCB_TOPK_MODE=fused|precomp overrides.
 bool use_precomp(const ctcb_handle* h, int B) {
   if (!use_fast(h)) return false;
   const char* m = getenv("CTCB_TOPK_MODE");
   if (m && strcmp(m, "fused") == 0) return false;
   if (m && strcmp(m, "precomp") == 0) return true;
-  return B <= 2 * h->num_sms;
+  return B <= 10 * h->num_sms;
 }
 
 // Two utterances per warp (ctcb_pair.cu): the headline kernel for beam <= 16,
