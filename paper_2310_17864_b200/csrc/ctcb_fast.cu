@@ -104,6 +104,33 @@ __device__ __forceinline__ uint64_t sort_desc64(uint64_t x, int lane) {
     }
   return x;
 }
+// Descending sort of 32 keys by rank counting through shared memory
+// (`sc`: 64 words): every lane reads all keys with 8 broadcast LDS.128,
+// counts the larger ones and scatters its key to that rank.  About as many
+// instructions as the 15-stage shuffle network but ~1/3 of its latency; the
+// latency-bound small-batch walks (precomputed top-k mode) use it.  Nonzero
+// keys must be distinct (they carry slot tags); zero keys sort last.
+__device__ __forceinline__ uint32_t sort_desc32_rank(uint32_t x, int lane, uint32_t* sc) {
+  sc[lane] = x;
+  __syncwarp();
+  const uint4* s4 = (const uint4*)sc;
+  int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    const uint4 v = s4[q];
+    r0 += v.x > x ? 1 : 0;
+    r1 += v.y > x ? 1 : 0;
+    r2 += v.z > x ? 1 : 0;
+    r3 += v.w > x ? 1 : 0;
+  }
+  sc[32 + lane] = 0u;
+  __syncwarp();
+  if (x) sc[32 + ((r0 + r1) + (r2 + r3))] = x;
+  __syncwarp();
+  const uint32_t y = sc[32 + lane];
+  __syncwarp();
+  return y;
+}
 // Sort a bitonic sequence descending.
 __device__ __forceinline__ uint64_t merge_desc64(uint64_t x, int lane) {
 #pragma unroll
@@ -1039,7 +1066,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
             const uint32_t t = f2u_sat((mine - sbase) * kScale);
             key = ((t > 1u ? t : 1u) & ~63u) | (uint32_t)(63 - lane);
           }
-          key = sort_desc32(key, lane);
+          key = PRE ? sort_desc32_rank(key, lane, (uint32_t*)S.cand) : sort_desc32(key, lane);
           const uint32_t nxt = __shfl_down_sync(FULL, key, 1);
           // not separated by a truncated unit, or near the threshold floor:
           // the full path decides this frame
@@ -1243,8 +1270,13 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
           }
         }
         uint32_t akey = lane < nS ? S.ckey[lane] : 0u;
-        akey = sort_desc32(akey, lane);
-        bkey = sort_desc32(bkey, lane);
+        if (PRE) {  // latency-bound small batches: rank-count sorts
+          akey = sort_desc32_rank(akey, lane, (uint32_t*)S.cand);
+          bkey = sort_desc32_rank(bkey, lane, (uint32_t*)S.cand);
+        } else {
+          akey = sort_desc32(akey, lane);
+          bkey = sort_desc32(bkey, lane);
+        }
         akey = max(akey, __shfl_sync(FULL, bkey, 31 - lane));
         akey = merge_desc32(akey, lane);
         const uint32_t nxt = __shfl_down_sync(FULL, akey, 1);

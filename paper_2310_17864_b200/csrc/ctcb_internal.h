@@ -154,7 +154,7 @@ __host__ __device__ constexpr inline FastLayout make_fast_layout(int V, int ring
   };
   L.rows = take((size_t)ring * row_bytes, 128);
   L.mbar = take((size_t)ring * 8, 8);
-  L.cand = take(64 * 8, 8);
+  L.cand = take(64 * 8, 16);  // 16-B aligned: also the rank-sort scratch (uint4 reads)
   L.tie_sc = take(32 * 8, 8);
   L.hs = take(16 * 8, 8);
   L.sval = take(32 * 4, 4);
