@@ -1270,7 +1270,8 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
           }
         }
         uint32_t akey = lane < nS ? S.ckey[lane] : 0u;
-        if (PRE) {  // latency-bound small batches: rank-count sorts
+        if (PRE) {  // latency-bound small batches: rank-count sorts (the fused
+                    // kernel at 16 warps/SM is faster with the shuffle network: 5.25 vs 5.43 ms)
           akey = sort_desc32_rank(akey, lane, (uint32_t*)S.cand);
           bkey = sort_desc32_rank(bkey, lane, (uint32_t*)S.cand);
         } else {
