@@ -1038,10 +1038,11 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       int Hn = 0;
       if (sc_on) {
         // U: bound of every append score this frame
+        // (an upper bound is enough: the high half of the largest order key
+        // with all-ones low bits, one redux instead of two)
         const uint64_t ak = (isfirst && A > -INFINITY) ? ord64(A) : 0ull;
         const uint32_t ahi = __reduce_max_sync(FULL, (uint32_t)(ak >> 32));
-        const uint32_t alo = __reduce_max_sync(FULL, (uint32_t)(ak >> 32) == ahi ? (uint32_t)ak : 0u);
-        const uint64_t ab = ((uint64_t)ahi << 32) | alo;
+        const uint64_t ab = ahi ? (((uint64_t)ahi << 32) | 0xffffffffull) : 0ull;
         const double U = (ab == 0ull || !(vmax > -INFINITY)) ? -INFINITY : unord64(ab) + vmax;
         const double Um = U + 1e-9 * (1.0 + fabs(U));  // appends are scored ~A + v: fp64 rounding margin
         const bool above_b = lane < 16 && c_blank > Um, above_r = lane < 16 && c_rep > Um;
@@ -1238,9 +1239,11 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         const uint32_t s0 = lane < 16 ? keyof(q0) : 0u, s1 = lane < 16 ? keyof(q1) : 0u,
                        s2 = lane < 16 ? keyof(q2) : 0u;
         const int cS = (s0 != 0u) + (s1 != 0u) + (s2 != 0u);  // q0 >= q1 >= q2: a prefix
-        const int incl = warp_incl_scan(cS, lane);
-        const int sb = incl - cS;
-        const int nS = __shfl_sync(FULL, incl, 31);
+        // slot offsets: exclusive prefix sum of cS in {0..3} from its two bits
+        const unsigned cb0 = __ballot_sync(FULL, cS & 1), cb1 = __ballot_sync(FULL, cS & 2);
+        const unsigned lt_ = lanemask_lt();
+        const int sb = __popc(cb0 & lt_) + 2 * __popc(cb1 & lt_);
+        const int nS = __popc(cb0) + 2 * __popc(cb1);
         bool nearfloor = (s0 != 0u && s0 < 128u) || (s1 != 0u && s1 < 128u) || (s2 != 0u && s2 < 128u);
         if (cS > 0) { S.ckey[sb] = (s0 & ~63u) | (uint32_t)(63 - sb); S.slot_rec[sb] = lane; }
         if (cS > 1) { S.ckey[sb + 1] = (s1 & ~63u) | (uint32_t)(62 - sb); S.slot_rec[sb + 1] = lane | (1 << 8); }
