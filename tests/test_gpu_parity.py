@@ -589,6 +589,31 @@ def test_regression_ties_beam39_bitwise():
     assert got["tokens"] == ref.tokens and got["scores"] == ref.scores
 
 
+def _token_k_ties_case():
+    """fuzz_parity seed 202 iteration 461 (utterance 6): V = 3 quantized rows
+    with exact ties, beam_size_token = 2, skip threshold 0.8, no beam
+    threshold.  At frame 9 two hypotheses tie to ~1e-15; the device
+    logaddexp orders them one ulp differently from glibc, and the beams
+    diverge afterwards (best path tokens equal, score -11.25 vs -10.42)."""
+    x = np.load(os.path.join(os.path.dirname(__file__), "golden", "regress_token_k_ties.npy"))
+    got = run(x[None], [x.shape[0]], 10, 10, 0.8, math.inf, K=2)[0]
+    ref = oracle.decode(x, beam_size=10, n_best=10, blank_skip_threshold=0.8, beam_threshold=math.inf,
+                        beam_size_token=2)
+    return got, ref
+
+
+def test_regression_token_k_ties_best_path():
+    got, ref = _token_k_ties_case()
+    assert got["tokens"][0] == ref.tokens[0]
+
+
+@pytest.mark.xfail(reason="exact score tie at frame 9 ordered one ulp apart; the beams diverge later",
+                   strict=False)
+def test_regression_token_k_ties_bitwise():
+    got, ref = _token_k_ties_case()
+    assert got["tokens"] == ref.tokens and got["scores"] == ref.scores
+
+
 def _lm602_case():
     import json
     from paper_2310_17864_b200 import lm as glm
