@@ -291,7 +291,9 @@ __device__ __forceinline__ float ex2_ftz(float x) {
 }
 // MAXCH: float4 chunks per lane the caller guarantees (4 for V <= 512), 0 = any.
 // WITH_MAX = false: the caller folds the row maximum into kmx itself.
-template <int MAXCH = 0, bool WITH_MAX = true>
+// PADDED: the staged row is padded to 4 * MAXCH * 32 floats with -FLT_MAX
+// (neutral for every partial), so no chunk needs a bounds check.
+template <int MAXCH = 0, bool WITH_MAX = true, bool PADDED = false>
 __device__ __forceinline__ RowPart row_partials(const float* row, int V, int lane) {
   const float4* r4 = (const float4*)row;
   constexpr float kL2E = 1.4426950408889634f;
@@ -300,7 +302,7 @@ __device__ __forceinline__ RowPart row_partials(const float* row, int V, int lan
   const bool ragged = (V & 3) != 0;
   auto chunk = [&](int c4) {
     float4 q = r4[c4];
-    if (ragged && 4 * c4 + 4 > V) {  // tail chunk: neutral values past V
+    if (!PADDED && ragged && 4 * c4 + 4 > V) {  // tail chunk: neutral values past V
       const int c = 4 * c4;
       if (c + 1 >= V) q.y = -1e30f;
       if (c + 2 >= V) q.z = -1e30f;
@@ -313,7 +315,7 @@ __device__ __forceinline__ RowPart row_partials(const float* row, int V, int lan
   if (MAXCH > 0) {
 #pragma unroll
     for (int j = 0; j < MAXCH; j++)
-      if (lane + 32 * j < nch4) chunk(lane + 32 * j);
+      if (PADDED || lane + 32 * j < nch4) chunk(lane + 32 * j);
   } else {
     for (int c4 = lane; c4 < nch4; c4 += 32) chunk(c4);
   }

@@ -735,8 +735,15 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
     for (int s = 0; s < ring; s++) mbar_init(&S.mbar[s], 1);
   for (int c = lane; c < V; c += 32) S.posmap[c] = 0xff;
   // padding beyond V is never written by the row copies: sentinel it once
+  // (SMALL with V > 384: -FLT_MAX, below every log-prob and neutral for the
+  // input screen, so the screen needs no bounds checks; every lane holds real
+  // values for the top-k threshold and the radix fallback reads only c < V)
+  // (V <= 384 keeps the NaN sentinel: whole lanes of padding must not feed
+  // the top-k threshold)
+  const bool padded = SMALL && P.V > 384;
+  const uint32_t pad = padded ? __float_as_uint(-FLT_MAX) : kSentinel;
   for (int s = 0; s < ring; s++)
-    for (int c = V + lane; c < row_bytes / 4; c += 32) ((uint32_t*)(S.rows + (size_t)s * row_bytes))[c] = kSentinel;
+    for (int c = V + lane; c < row_bytes / 4; c += 32) ((uint32_t*)(S.rows + (size_t)s * row_bytes))[c] = pad;
   fence_mbar_init();
   __syncwarp();
   int slot_i = 0, slot_c = 0;     // ring slots of the next issue / consume
@@ -876,7 +883,9 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       const bool v_scmax = !tokK && tiny_v;  // == sc_on && !PRE
       RowPart vpart{0u, 0xffffffffu, 0u};
       if (!PRE && P.validate)
-        vpart = v_scmax ? row_partials<SMALL ? 4 : 0, false>(row, V, lane) : row_partials<SMALL ? 4 : 0>(row, V, lane);
+        vpart = v_scmax ? (padded ? row_partials<4, false, true>(row, V, lane)
+                                  : row_partials<SMALL ? 4 : 0, false>(row, V, lane))
+                        : row_partials<SMALL ? 4 : 0>(row, V, lane);
       double vmax = -INFINITY;
       const float eb_f = row[P.blank];
       auto vfinish = [&]() {
