@@ -123,7 +123,9 @@ bool use_fused(const ctcb_handle* h) { return h->has_lm || (h->sil >= 0 && h->si
 bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->force_generic && !use_fused(h); }
 // Fast kernel variant: compile-time layout when V <= kSmallV (ring 2, 2048-B rows).
 bool fast_small(const ctcb::Params& P) {
-  return P.V <= ctcb::kSmallV && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes && P.tokK == 0;
+  // (32-bit row offsets inside an utterance and utterance strides < 2^32 elements)
+  return P.V <= ctcb::kSmallV && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes && P.tokK == 0 &&
+         P.stride_b < (1ll << 32) && (long long)P.T_max * P.stride_t < (1ll << 32);
 }
 const void* fast_kernel_fn(const ctcb::Params& P, bool pre) {
   const bool sm = fast_small(P);

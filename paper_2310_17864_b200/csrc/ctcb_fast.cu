@@ -787,8 +787,15 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       }
       continue;
     }
-    const float* ubase = P.lp + (size_t)u * P.stride_b;
-    int32_t* fmap = P.frame_map + (size_t)u * P.T_max;
+    // SMALL: the host guarantees stride_b < 2^32 elements, so the offsets are
+    // 32 x 32 -> 64-bit products (one IMAD.WIDE instead of 64-bit multiplies
+    // the compiler rematerialises every frame)
+    const float* ubase = P.lp + (SMALL ? (size_t)(uint32_t)u * (uint32_t)P.stride_b : (size_t)u * P.stride_b);
+    int32_t* fmap = P.frame_map + (size_t)(uint32_t)u * (uint32_t)P.T_max;
+    const uint32_t st32 = (uint32_t)P.stride_t;
+    auto row_of = [&](int fr) -> const float* {  // row fr of this utterance
+      return ubase + (SMALL ? (size_t)((uint32_t)fr * st32) : (size_t)fr * P.stride_t);
+    };
 
     // -- A. blank-skip compaction (emissions.py:298-306); in precomputed-top-k
     //    mode ctcb_framemap_kernel already did it
@@ -803,7 +810,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       while (!PRE && idx >= kept && ct < len_u) {
         const int t = ct + lane;
         bool keep = t < len_u;
-        if (keep && P.skip) keep = !(__ldg(ubase + (size_t)t * P.stride_t + P.blank) >= P.cutoff);
+        if (keep && P.skip) keep = !(__ldg(row_of(t) + P.blank) >= P.cutoff);
         const unsigned bal = __ballot_sync(FULL, keep);
         if (keep) fmap[kept + __popc(bal & lanemask_lt())] = t;
         kept += __popc(bal);
@@ -832,7 +839,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       }
       const int fr = __shfl_sync(FULL, fm_reg, idx & 31);
       if (lane == 0) {
-        const float* src = ubase + (size_t)fr * P.stride_t;
+        const float* src = row_of(fr);
         fence_proxy_async();
         mbar_arrive_expect_tx(&S.mbar[slot_i], row_copy);
         tma_bulk_g2s(S.rows + (size_t)slot_i * row_bytes, src, row_copy, &S.mbar[slot_i]);
@@ -870,7 +877,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         if (slot_c == ring) { slot_c = 0; par_c ^= 1u; }
       } else {
         row = (float*)S.rows;
-        const float* src = ubase + (size_t)fmap[i] * P.stride_t;
+        const float* src = row_of(fmap[i]);
         for (int c = lane; c < V; c += 32) row[c] = __ldg(src + c);
         __syncwarp();
       }
@@ -892,7 +899,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         if (!PRE && P.validate && v_scmax) vpart.kmx = max(vpart.kmx, ord32(fmaxf((float)vmax, eb_f)));
         if (!PRE && P.validate && !row_verdict(vpart, P.validate == 1)) {
           const int fr = fmap[i];
-          const unsigned long long vk = row_check_exact(ubase + (size_t)fr * P.stride_t, V, fr, lane, P.validate == 1);
+          const unsigned long long vk = row_check_exact(row_of(fr), V, fr, lane, P.validate == 1);
           if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[u], vk);
         }
       };
@@ -1527,7 +1534,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         last = x >= 0 ? x : blast;
         len = x >= 0 ? blen + 1 : blen;
         fl = nfl;
-        P.trellis[((size_t)u * P.T_max + i) * beam + lane] = trel;
+        P.trellis[(size_t)(uint32_t)u * (uint32_t)(P.T_max * beam) + (uint32_t)(i * beam + lane)] = trel;
         S.tring[(i % kChunk) * 16 + lane] = trel;
       }
       H = Hn;
