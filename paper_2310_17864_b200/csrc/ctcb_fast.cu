@@ -718,8 +718,11 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
   const int tokK = SMALL ? 0 : P.tokK;
   const int row_bytes = SMALL ? kSmallRowBytes : P.row_bytes;
   const int nch4 = (V + 3) >> 2;
-  const bool small_v = nch4 <= 256;               // general path: predicate bits fit one register
-  const bool tiny_v = SMALL && k <= 31;            // topk_small: <= 4 chunks per lane
+  const bool small_v = SMALL || nch4 <= 256;      // general path: predicate bits fit one register
+  // topk_small (<= 4 chunks per lane, k <= 31): the host picks SMALL only for
+  // k <= 31, so this is a compile-time constant (no per-frame test, and the
+  // general top-k is compiled out of the SMALL kernels)
+  const bool tiny_v = SMALL;
   const uint32_t fullk = k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
   const double kR = P.threshold_inf ? 1048576.0 : fmin(P.beam_threshold, 1048576.0);
   const double kScale = 4294967296.0 / kR;
