@@ -327,6 +327,17 @@ __device__ uint64_t topk_radix_f(const FastSmem& S, KeyOf key_of, int V, int k, 
 __device__ uint64_t topk_radix(const FastSmem& S, const float* row, int V, int k, int lane) {
   return topk_radix_f(S, [&](int c) { return okey(row[c]); }, V, k, lane);
 }
+// The same for the SMALL kernels, out of line (rows with > 64 values above the
+// lane-maximum threshold, e.g. many exact ties): scalar / pointer arguments
+// only, so the hot frame loop keeps its registers and loses ~0.5k instructions
+// of code it almost never runs.
+__device__ __noinline__ uint64_t topk_radix_ool(const float* row, uint32_t* hist, uint64_t* cand, int V, int k,
+                                                int lane) {
+  FastSmem T{};
+  T.hist = hist;
+  T.cand = cand;
+  return topk_radix_f(T, [&](int c) { return okey(row[c]); }, V, k, lane);
+}
 
 }  // namespace
 
@@ -516,7 +527,7 @@ __device__ __forceinline__ int topk_small(const FastSmem& S, const float* row, i
   const int cnt = __reduce_add_sync(FULL, __popc(pm));
   if (cnt > 64) {
     if (lane == 0 && dbg) atomicAdd(&dbg[kDbgRadix], 1ull);
-    const uint64_t sk = topk_radix(S, row, V, k, lane);
+    const uint64_t sk = topk_radix_ool(row, S.hist, S.cand, V, k, lane);
     return skey_tok(sk);
   }
   // per-chunk exclusive offsets: chunk j of lane l starts after all survivors
