@@ -19,3 +19,7 @@ timeout 300 python tools/utt_timeline.py 4 > $O/timeline_cfg4.json 2>&1
 python tools/sanitize_cases.py > $O/checks_plain.log 2>&1; echo "rc=$?" >> $O/checks_plain.log
 if [ -f variants/libctcb_chk.so ]; then CTCB_LIB=variants/libctcb_chk.so python tools/sanitize_cases.py > $O/checks_fchk.log 2>&1; echo "rc=$?" >> $O/checks_fchk.log; fi
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 600 python tools/parity_full.py 4 1 3 > $O/parity_full.log 2>&1
+timeout 900 python tools/fuzz_parity.py 600 401 > $O/fuzz_parity_s401.log 2>&1
+CTCB_TOPK_MODE=fused timeout 900 python tools/fuzz_parity.py 600 402 > $O/fuzz_parity_fused_s402.log 2>&1
+python tools/shard_modes.py 8 4 2 > $O/shard_modes.log 2>&1
