@@ -124,7 +124,8 @@ bool use_fast(const ctcb_handle* h) { return h->beam <= ctcb::kFastBeam && !h->f
 // Fast kernel variant: compile-time layout when V <= kSmallV (ring 2, 2048-B rows).
 bool fast_small(const ctcb::Params& P) {
   // (32-bit row offsets inside an utterance and utterance strides < 2^32 elements)
-  return P.V <= ctcb::kSmallV && P.k <= 31 && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes && P.tokK == 0 &&
+  return P.V <= ctcb::kSmallV && P.k <= 31 && P.bulk_ok && P.ring == 2 && P.row_bytes == ctcb::kSmallRowBytes &&
+         P.tokK == 0 &&
          P.stride_b < (1ll << 32) && (long long)P.T_max * P.stride_t < (1ll << 32);
 }
 const void* fast_kernel_fn(const ctcb::Params& P, bool pre) {

@@ -723,6 +723,8 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
   for (int i = lane; i <= kTieCache; i += 32) S.tc_r[i] = 0;
 
   const int V = P.V, k = P.k, beam = P.beam, ring = SMALL ? 2 : P.ring;
+  // rows staged by TMA (16-B aligned rows): the host picks SMALL only then
+  const bool bulk = SMALL || P.bulk_ok;
   const bool MX = P.merge_max != 0;  // merge_mode="max" (decoder.py:610-613)
   // beam_size_token < V runs on the general-layout kernels only (the host never
   // picks a SMALL variant for it), so its code is compiled out of SMALL
@@ -862,7 +864,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
     };
     int n_out = 0;  // issued, not yet consumed
     classify_to(ring - 1);
-    if (P.bulk_ok) {
+    if (bulk) {
       const int pre = kept < ring - 1 ? kept : ring - 1;
       for (int i = 0; i < pre; i++) { issue(i); n_out++; }
     }
@@ -881,7 +883,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       classify_to(i + ring - 1);
       if (i >= kept) break;
       float* row;
-      if (P.bulk_ok) {
+      if (bulk) {
         if (i + ring - 1 < kept) { issue(i + ring - 1); n_out++; }
         mbar_wait(&S.mbar[slot_c], par_c);
         PH(1);
