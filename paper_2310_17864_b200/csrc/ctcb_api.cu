@@ -2,6 +2,7 @@
 // layout, launch configuration.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -198,7 +199,7 @@ bool use_block_pre(const ctcb_handle* h) {
 }
 
 struct WsLayout {
-  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, rowoff, vkey, vdone, total;
+  size_t frame_map, kept, trellis, order, counter, seqbuf, anc, topk_tok, topk_val, rowoff, ready, vkey, vdone, total;
 };
 WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   WsLayout w{};
@@ -219,6 +220,7 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   w.topk_tok = take(ntk * 4);
   w.topk_val = take(ntk * 4);
   w.rowoff = take(ntk ? ((size_t)B + 1) * 4 : 0);
+  w.ready = take(use_precomp(h, B) ? (size_t)B * T * 4 : 0);
   w.vkey = take((size_t)B * 8);
   w.vdone = take((size_t)B * 4);
   w.total = ctcb::align_up(o, 256);
@@ -278,6 +280,7 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   P.topk_tok = (int32_t*)(base + L.topk_tok);
   P.topk_val = (float*)(base + L.topk_val);
   P.rowoff = (int32_t*)(base + L.rowoff);
+  P.ready = nullptr;  // set by decode_impl when the top-k overlaps the walk
   P.validate = h->validate;
   P.vkey = (unsigned long long*)(base + L.vkey);
   P.vdone = (int32_t*)(base + L.vdone);
@@ -289,6 +292,37 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
   return CTCB_OK;
 }
 
+
+// Overlapped precomputed mode: blocks per SM of ctcb_topk_kernel that fit
+// beside the walk's own blocks (registers, shared memory, threads, block
+// slots), so that both grids are resident at once and the walk consumes the
+// lists while the top-k produces them.  0 = no room: the top-k runs first.
+int topk_beside_walk(const ctcb_handle* h, const void* wfn, int wgrid, int wthreads, size_t wsmem, size_t tsmem,
+                     int tthreads, int tbps) {
+  cudaFuncAttributes fw{}, ft{};
+  if (cudaFuncGetAttributes(&fw, wfn) != cudaSuccess ||
+      cudaFuncGetAttributes(&ft, (const void*)ctcb::ctcb_topk_kernel) != cudaSuccess)
+    return 0;
+  int dev = 0, smem_sm = 0, regs_sm = 0, thr_sm = 0, blk_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+  cudaDeviceGetAttribute(&blk_sm, cudaDevAttrMaxBlocksPerMultiprocessor, dev);
+  auto regs_of = [](int regs, int threads) -> long long {
+    return (long long)((regs * 32 + 255) / 256 * 256) * ((threads + 31) / 32);
+  };
+  const long long wb = (wgrid + h->num_sms - 1) / h->num_sms, reserve = 1024;
+  const long long smem_left = smem_sm - wb * ((long long)wsmem + (long long)fw.sharedSizeBytes + reserve);
+  const long long regs_left = regs_sm - wb * regs_of(fw.numRegs, wthreads);
+  const long long thr_left = thr_sm - wb * wthreads, blk_left = blk_sm - wb;
+  long long fit = tbps;
+  fit = std::min(fit, smem_left / ((long long)tsmem + (long long)ft.sharedSizeBytes + reserve));
+  fit = std::min(fit, regs_left / regs_of(ft.numRegs, tthreads));
+  fit = std::min(fit, thr_left / tthreads);
+  fit = std::min(fit, blk_left);
+  return fit > 0 ? (int)fit : 0;
+}
 
 // Choose the row-ring depth and warps per block: shared memory per warp must
 // fit, then maximise resident warps per SM (occupancy API), and spread small
@@ -599,29 +633,67 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   }
   int grid = h->num_sms * blocks_per_sm;
   if (grid > need) grid = need;
+  // precomputed mode: frame maps -> top-k of every kept frame (frame-parallel)
+  // -> beam walk.  When both grids fit on the SMs together, the top-k runs
+  // frame-major beside the walk (the walk is its programmatic dependent and
+  // waits per list on the ready flags); otherwise it runs first.
+  bool overlap = false;
+  ctcb::Params Q{};
+  size_t tsmem = 0;
+  int tk_grid = 0, tk_threads = 0;
   if (pre) {
-    // frame maps -> top-k of every kept frame (frame-parallel) -> beam walk
     P.precomp = 1;
     ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
     h->launches++;
     CTCB_CUDA(cudaGetLastError());
-    ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
-    h->launches++;
-    CTCB_CUDA(cudaGetLastError());
-    ctcb::Params Q = P;
+    Q = P;
     // V > 512 with 16-B rows: the top-k kernel reads rows from global memory
     // (no staging ring, row_bytes = 0), so far more warps fit per SM
     if (P.V > ctcb::kSmallV && P.bulk_ok && P.V % 4 == 0 && getenv("CTCB_TOPK_STAGED") == nullptr) Q.row_bytes = 0;
     Q.smem_per_warp = (int)ctcb::align_up((size_t)ctcb::kTopkRing * Q.row_bytes + 64 + 64 * 8 + 256 * 4 + 64 * 4 + 64 * 2, 128);
     int twpb = h->max_smem_optin / Q.smem_per_warp;
     twpb = twpb < 1 ? 1 : (twpb > 8 ? 8 : twpb);
-    const size_t tsmem = (size_t)Q.smem_per_warp * twpb;
+    tsmem = (size_t)Q.smem_per_warp * twpb;
+    tk_threads = 32 * twpb;
     CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
     int tbps = 0;
-    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_kernel, 32 * twpb, tsmem));
-    ctcb::ctcb_topk_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 32 * twpb, tsmem, s>>>(Q);
-    h->launches++;
-    CTCB_CUDA(cudaGetLastError());
+    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_kernel, tk_threads, tsmem));
+    tk_grid = h->num_sms * (tbps > 0 ? tbps : 1);
+    // default: overlap for V > 512 (rows from global memory: the top-k is
+    // ~17 % of the sequential step at cfg3, and running it beside the walk
+    // cuts the step by ~7 %); for V <= 512 the top-k is a few % of the step
+    // and sharing the SMs slows the latency-bound walk by more than that
+    // (cfg1 +0.5 %, 512- / 1,024-utterance shards +2 % / +11 %).
+    // CTCB_OVERLAP=1 forces it, 0 disables it; CTCB_OVERLAP_BPS caps the
+    // top-k blocks per SM.
+    const char* ov = getenv("CTCB_OVERLAP");
+    const char* ovb = getenv("CTCB_OVERLAP_BPS");
+    const bool want = ov ? strcmp(ov, "0") != 0 : Q.row_bytes == 0;
+    if (want) {
+      int fit = topk_beside_walk(h, kfn, grid, 32 * P.warps_per_block, smem, tsmem, tk_threads, tbps);
+      if (ovb && atoi(ovb) > 0 && atoi(ovb) < fit) fit = atoi(ovb);
+      if (fit > 0) {
+        overlap = true;
+        tk_grid = h->num_sms * fit;
+      }
+    }
+    if (overlap) {
+      // both kernels prefer the largest shared-memory carve-out, so an SM
+      // configured for one has room for the other
+      CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_topk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      P.ready = (uint32_t*)((char*)P.topk_tok - L.topk_tok + L.ready);
+      Q.ready = P.ready;
+      CTCB_CUDA(cudaMemsetAsync(P.ready, 0, (size_t)B * T * 4, s));
+    } else {
+      ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
+      h->launches++;
+      CTCB_CUDA(cudaGetLastError());
+      Q.rowoff = P.rowoff;
+      ctcb::ctcb_topk_kernel<<<tk_grid, tk_threads, tsmem, s>>>(Q);
+      h->launches++;
+      CTCB_CUDA(cudaGetLastError());
+    }
   }
   // diagnostics: CTCB_UTT_TRACE=path dumps a per-utterance timeline of the
   // fast kernels ([B, 2] uint64: smid << 48 | global warp, start ns; end ns)
@@ -634,6 +706,11 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
   }
   const bool timed = h->timing && h->n_timed < 64;
   if (timed) CTCB_CUDA(cudaEventRecord(h->tev[2 * h->n_timed], s));
+  if (overlap) {  // the walk follows at once as its programmatic dependent
+    ctcb::ctcb_topk_kernel<<<tk_grid, tk_threads, tsmem, s>>>(Q);
+    h->launches++;
+    CTCB_CUDA(cudaGetLastError());
+  }
   if (blk) {
     void* args[] = {(void*)&P};
     CTCB_CUDA(cudaLaunchKernel((const void*)ctcb::ctcb_decode_block_kernel, dim3(grid), dim3(256), args, smem, s));
@@ -652,7 +729,21 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     h->launches++;
   } else if (fast) {
     void* args[] = {(void*)&P};
-    CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
+    if (overlap) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(32 * P.warps_per_block);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      CTCB_CUDA(cudaLaunchKernelExC(&lc, kfn, args));
+    } else {
+      CTCB_CUDA(cudaLaunchKernel(kfn, dim3(grid), dim3(32 * P.warps_per_block), args, smem, s));
+    }
     h->last_kernel = !fast_small(P) ? (pre ? "ctcb_decode_fast_pre_kernel" : "ctcb_decode_fast_kernel")
                                     : (pre ? "ctcb_decode_fast_pre_small_kernel" : "ctcb_decode_fast_small_kernel");
     h->launches++;

@@ -263,6 +263,19 @@ static __device__ __noinline__ unsigned long long row_check_exact(const float* r
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   return fabs(m + log(sum)) > 1e-3 ? vkey_make(3, t, -1) : ~0ull;
 }
+// Producer/consumer flags between the overlapped top-k kernel and the walk
+// (gpu scope), and the programmatic-dependent-launch controls.
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t r;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_primary() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // Diagnostics: SM id and the global nanosecond timer.
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;

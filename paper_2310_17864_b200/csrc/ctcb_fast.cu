@@ -786,7 +786,12 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
     int item = 0;
     if (lane == 0) item = atomicAdd(P.counter, 1);
     item = __shfl_sync(FULL, item, 0);
-    if (item >= P.B) break;
+    if (item >= P.B) {
+      // overlapped top-k: this grid completes only after the top-k grid has
+      // (its validation keys and lists are then visible to later stream work)
+      if (PRE && P.ready != nullptr) pdl_wait_primary();
+      break;
+    }
     const int u = P.order[item];
     const int len_u = P.lens[u];
     if (P.utt_trace && lane == 0) {
@@ -838,10 +843,35 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
     const size_t tk_base = (size_t)u * P.T_max * k;
     int pre_st = 0;
     float pre_sv = 0.0f;
-    if (PRE && kept > 0 && lane < k) {
-      pre_st = P.topk_tok[tk_base + lane];
-      pre_sv = P.topk_val[tk_base + lane];
-    }
+    // overlapped top-k (P.ready): list j is read only once its flag is
+    // published; flags are polled 32 frames at a time (one poll per 32 frames
+    // while the top-k kernel runs ahead), lists are read through L2 (__ldcg)
+    int rdy = 0;
+    auto await_list = [&](int j) {
+      if (!PRE || P.ready == nullptr || j < rdy) return;
+      const uint32_t* fl = P.ready + (size_t)(uint32_t)u * (uint32_t)P.T_max;
+      for (;;) {
+        const int f = rdy + lane;
+        const bool ok = f >= kept || ld_acquire_gpu(fl + f) != 0u;
+        const unsigned bal = __ballot_sync(FULL, ok);
+        rdy += bal == FULL ? 32 : __ffs(~bal) - 1;
+        if (j < rdy) break;
+        __nanosleep(128);
+      }
+      fence_acq_rel_gpu();
+      __syncwarp();
+    };
+    auto load_list = [&](int j) {
+      if (P.ready != nullptr) {
+        pre_st = __ldcg(P.topk_tok + tk_base + (size_t)j * k + lane);
+        pre_sv = __ldcg(P.topk_val + tk_base + (size_t)j * k + lane);
+      } else {
+        pre_st = P.topk_tok[tk_base + (size_t)j * k + lane];
+        pre_sv = P.topk_val[tk_base + (size_t)j * k + lane];
+      }
+    };
+    if (PRE && kept > 0) await_list(0);
+    if (PRE && kept > 0 && lane < k) load_list(0);
 
     // row staging: lane 0 issues the bulk copy of kept frame `idx`; frame-map
     // entries are read 32 at a time into registers
@@ -957,10 +987,8 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
         if (PRE) {
           st = pre_st;
           sv = pre_sv;
-          if (i + 1 < kept && lane < k) {
-            pre_st = P.topk_tok[tk_base + (size_t)(i + 1) * k + lane];
-            pre_sv = P.topk_val[tk_base + (size_t)(i + 1) * k + lane];
-          }
+          if (i + 1 < kept) await_list(i + 1);
+          if (i + 1 < kept && lane < k) load_list(i + 1);
         } else {
           if (tiny_v) st = topk_small(S, row, V, k, lane, nch4, P.dbg);
           else st = skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, P.dbg));
@@ -1753,9 +1781,12 @@ __global__ void __launch_bounds__(1024) ctcb_rowoff_kernel(const __grid_constant
   if (threadIdx.x == 0) P.rowoff[P.B] = carry;
 }
 
-// Frame-parallel top-k (precomputed mode): the kept rows of all utterances,
-// flattened and split evenly over the warps; rows are staged by TMA bulk
-// copies into a per-warp 3-deep ring two rows ahead of use.
+// Frame-parallel top-k (precomputed mode; the per-frame token selection of
+// decoder.py:431-466): the kept rows of all utterances, split over the warps
+// (contiguous flattened ranges when it runs before the walk, frame-major with
+// per-list ready flags when it runs beside it); rows are staged by TMA bulk
+// copies into a per-warp 2-deep ring one row ahead of use (V <= 512) or read
+// straight from global memory (V > 512).
 #ifndef CTCB_TOPK_MIN_BLOCKS
 #define CTCB_TOPK_MIN_BLOCKS 4
 #endif
@@ -1786,59 +1817,96 @@ __global__ void __launch_bounds__(256, CTCB_TOPK_MIN_BLOCKS) ctcb_topk_kernel(co
   fence_mbar_init();
   fence_proxy_async();
   __syncwarp();
-  const long long total = P.rowoff[P.B];
+  // overlapped mode (P.ready): the walk is a programmatic dependent of this
+  // grid; it may launch once every CTA here is running (no CTA of this grid
+  // ever waits on it, so the pair cannot deadlock)
+  pdl_launch_dependents();
+  const bool fm = P.ready != nullptr;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
-  const long long g0 = total * w / nw, g1 = total * (w + 1) / nw;
-  if (g0 >= g1) return;
-  if (P.row_bytes == 0) {
-    // large vocabulary: rows read straight from global memory (topk_key_g)
-    int lo = 0, hi = P.B - 1;
+  // Row cursors.  Flattened split (fm = false): warp w takes the contiguous
+  // range [g0, g1) of the utterance-major (u, kept frame) space.  Frame-major
+  // (fm = true, overlapped with the walk): position p = frame * B + slot,
+  // utterance order[slot] (the walk's longest-first order), warp w takes
+  // p = w, w + nw, ...: the lists of frame i of every utterance are written
+  // before those of frame i + 1, in the order the walks consume them.
+  struct Cur {
+    int u, i;
+    long long p;
+  };
+  const long long G = fm ? (long long)P.B * P.T_max : 0;
+  auto fm_settle = [&](Cur& c) {  // first valid position >= c.p on this warp's stride
+    for (; c.p < G; c.p += nw) {
+      const int uu = P.order[(int)(c.p % P.B)], ii = (int)(c.p / P.B);
+      if (ii < P.kept[uu]) { c.u = uu; c.i = ii; return; }
+    }
+    c.u = P.B;
+  };
+  Cur c0{0, 0, w};
+  long long n = 0;
+  if (fm) {
+    fm_settle(c0);
+    if (c0.u >= P.B) return;
+  } else {
+    const long long total = P.rowoff[P.B];
+    const long long g0 = total * w / nw, g1 = total * (w + 1) / nw;
+    if (g0 >= g1) return;
+    n = g1 - g0;
+    int lo = 0, hi = P.B - 1;  // utterance of the first row: last u with rowoff[u] <= g0
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (P.rowoff[mid] <= g0) lo = mid; else hi = mid - 1;
     }
-    int cu = lo, ci = (int)(g0 - P.rowoff[lo]);
-    while (cu < P.B && ci >= P.kept[cu]) { cu++; ci = 0; }
-    for (long long g = g0; g < g1; g++) {
-      const int fr = P.frame_map[(size_t)cu * P.T_max + ci];
-      const float* src = P.lp + (size_t)cu * P.stride_b + (size_t)fr * P.stride_t;
+    c0.u = lo;
+    c0.i = (int)(g0 - P.rowoff[lo]);
+    while (c0.u < P.B && c0.i >= P.kept[c0.u]) { c0.u++; c0.i = 0; }
+  }
+  auto advance = [&](Cur& c) {
+    if (fm) {
+      c.p += nw;
+      fm_settle(c);
+    } else {
+      c.i++;
+      while (c.u < P.B && c.i >= P.kept[c.u]) { c.u++; c.i = 0; }
+    }
+  };
+  auto more = [&](const Cur& c, long long cnt) { return fm ? c.u < P.B : cnt < n; };
+  auto src_of = [&](int u, int i) -> const float* {
+    return P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
+  };
+  // list (u, i) written by lanes < k: every lane fences its stores, then lane 0
+  // publishes the flag (release, gpu scope)
+  auto publish = [&](const Cur& c) {
+    if (!fm) return;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_gpu(P.ready + (size_t)c.u * P.T_max + c.i, 1u);
+  };
+  if (P.row_bytes == 0) {
+    // large vocabulary: rows read straight from global memory (topk_key_g)
+    Cur c = c0;
+    for (long long g = 0; more(c, g); g++) {
+      const int fr = P.frame_map[(size_t)c.u * P.T_max + c.i];
+      const float* src = P.lp + (size_t)c.u * P.stride_b + (size_t)fr * P.stride_t;
       if (P.validate && !row_screen_scalar(src, V, lane, P.validate == 1)) {  // emissions.py:128-150
         const unsigned long long vk = row_check_exact(src, V, fr, lane, P.validate == 1);
-        if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[cu], vk);
+        if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[c.u], vk);
       }
       const int st = skey_tok(topk_key_g(S, src, V, P.blank, k, lane, nullptr));
       if (lane < k) {
-        const size_t o = ((size_t)cu * P.T_max + ci) * k + lane;
+        const size_t o = ((size_t)c.u * P.T_max + c.i) * k + lane;
         P.topk_tok[o] = st;
         P.topk_val[o] = __ldg(src + st);
       }
       __syncwarp();
-      ci++;
-      while (cu < P.B && ci >= P.kept[cu]) { cu++; ci = 0; }
+      publish(c);
+      advance(c);
     }
     return;
   }
-  // utterance of the first row: last u with rowoff[u] <= g0
-  int lo = 0, hi = P.B - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (P.rowoff[mid] <= g0) lo = mid; else hi = mid - 1;
-  }
-  // (utterance, frame) cursors for issue and consume
-  int iu = lo, ii = (int)(g0 - P.rowoff[lo]);
-  int cu = iu, ci = ii;
+  // staged rows: issue cursor ic runs kRing - 1 rows ahead of consume cursor cc
   const uint32_t row_copy = (uint32_t)V * 4u;
-  auto advance = [&](int& u, int& i) {
-    i++;
-    while (u < P.B && i >= P.kept[u]) { u++; i = 0; }
-  };
-  auto src_of = [&](int u, int i) -> const float* {
-    return P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
-  };
-  while (iu < P.B && ii >= P.kept[iu]) { iu++; ii = 0; }
-  cu = iu; ci = ii;
-  const long long n = g1 - g0;
+  Cur ic = c0, cc = c0;
   int slot_i = 0, slot_c = 0;
   uint32_t par = 0u;
   long long issued = 0;
@@ -1846,18 +1914,18 @@ __global__ void __launch_bounds__(256, CTCB_TOPK_MIN_BLOCKS) ctcb_topk_kernel(co
     if (P.bulk_ok) {
       if (lane == 0) {
         mbar_arrive_expect_tx(&mbar[slot_i], row_copy);
-        tma_bulk_g2s(S.rows + (size_t)slot_i * P.row_bytes, src_of(iu, ii), row_copy, &mbar[slot_i]);
+        tma_bulk_g2s(S.rows + (size_t)slot_i * P.row_bytes, src_of(ic.u, ic.i), row_copy, &mbar[slot_i]);
       }
     }
     slot_i = slot_i + 1 == kRing ? 0 : slot_i + 1;
     issued++;
-    advance(iu, ii);
+    advance(ic);
   };
-  for (int r = 0; r < kRing - 1 && issued < n; r++) issue();
-  for (long long g = 0; g < n; g++) {
-    if (issued < n) issue();
+  for (int r = 0; r < kRing - 1 && more(ic, issued); r++) issue();
+  for (long long g = 0; more(cc, g); g++) {
+    if (more(ic, issued)) issue();
     float* row = (float*)(S.rows + (size_t)slot_c * P.row_bytes);
-    const float* src = src_of(cu, ci);
+    const float* src = src_of(cc.u, cc.i);
     if (P.bulk_ok) {
       mbar_wait(&mbar[slot_c], par);
     } else {
@@ -1867,24 +1935,25 @@ __global__ void __launch_bounds__(256, CTCB_TOPK_MIN_BLOCKS) ctcb_topk_kernel(co
     // input validation of every kept row (emissions.py:128-150): the beam walk
     // of precomputed mode leaves it to this frame-parallel pass
     if (P.validate && !row_screen(row, V, lane, P.validate == 1)) {
-      const int fr = P.frame_map[(size_t)cu * P.T_max + ci];
+      const int fr = P.frame_map[(size_t)cc.u * P.T_max + cc.i];
       const unsigned long long vk = row_check_exact(src, V, fr, lane, P.validate == 1);
-      if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[cu], vk);
+      if (lane == 0 && vk != ~0ull) atomicMin(&P.vkey[cc.u], vk);
     }
     if (lane == 0) ((uint32_t*)row)[P.blank] = kSentinel;
     __syncwarp();
     const int st = tiny_v ? topk_small(S, row, V, k, lane, nch4, nullptr)
                           : skey_tok(topk_key(S, row, V, k, lane, small_v, nch4, nullptr));
     if (lane < k) {
-      const size_t o = ((size_t)cu * P.T_max + ci) * k + lane;
+      const size_t o = ((size_t)cc.u * P.T_max + cc.i) * k + lane;
       P.topk_tok[o] = st;
       P.topk_val[o] = row[st];
     }
     __syncwarp();
+    publish(cc);
     fence_proxy_async();  // generic writes to the slot (blank sentinel) before it is refilled by TMA
     slot_c++;
     if (slot_c == kRing) { slot_c = 0; par ^= 1u; }
-    advance(cu, ci);
+    advance(cc);
   }
 }
 

@@ -60,6 +60,11 @@ struct Params {
   int32_t* topk_tok;        // [B, T_max, k] (precomp mode)
   float* topk_val;          // [B, T_max, k]
   int32_t* rowoff;          // [B + 1] exclusive prefix sums of kept (precomp mode)
+  // overlapped precomp mode: per-list ready flags [B, T_max] (zeroed before the
+  // top-k kernel, set with release semantics after each list is written); the walk
+  // is launched as a programmatic dependent and waits on them.  null = the lists
+  // are complete before the walk starts (flattened split, plain stream order).
+  uint32_t* ready;
   // fused search (ctcb_set_lm / ctcb_set_silence): token-level LM and silence bonus
   const double* lm_score;   // [S, V] natural-log LM score of token c after context s, or null (no LM)
   const int32_t* lm_next;   // [S, V] successor context

@@ -763,3 +763,55 @@ def test_fused_validation_host_path():
     lp[2, 4, 1] = np.inf
     with pytest.raises(ValueError, match=r"utterance 2: non-finite log-probability at frame 4, token 1"):
         dec(torch.from_numpy(lp), torch.tensor([20, 20, 20, 20], dtype=torch.int32))
+
+
+# ---------------------------------------------------------------- overlapped precomputed top-k
+# Precomputed mode runs ctcb_topk_kernel either before the walk or beside it
+# (frame-major lists published through per-list ready flags, the walk launched
+# as its programmatic dependent; CTCB_OVERLAP=1 forces it, 0 disables it).
+# Both schedules must give bit-identical decodes, equal to the oracle.
+
+def _overlap_cases():
+    cases = []
+    cfg = synth.CONFIGS[1]
+    lp, lens = synth.batch(cfg)  # V = 500: staged rows
+    cases.append(("cfg1", lp, lens, cfg.beam, cfg.nbest, cfg.threshold, 64))
+    cfg = synth.CONFIGS[3]
+    lp, lens = synth.batch(cfg, indices=range(24))  # V = 5000: rows from global memory
+    cases.append(("cfg3", lp, lens, cfg.beam, cfg.nbest, cfg.threshold, 6))
+    rng = np.random.default_rng(77)  # odd V > 512: staged, unaligned rows
+    x = rng.normal(size=(5, 90, 1001)) * 2.0
+    x = x - x.max(2, keepdims=True)
+    lp = (x - np.log(np.exp(x).sum(2, keepdims=True))).astype(np.float32)
+    cases.append(("v1001", lp, np.array([90, 3, 47, 1, 88], dtype=np.int32), 10, 3, 0.95, 5))
+    return cases
+
+
+@pytest.mark.parametrize("case", [0, 1, 2])
+def test_overlapped_topk_matches_sequential_and_oracle(monkeypatch, case):
+    name, lp, lens, beam, nb, thr, n_oracle = _overlap_cases()[case]
+    monkeypatch.setenv("CTCB_TOPK_MODE", "precomp")
+    monkeypatch.setenv("CTCB_OVERLAP", "1")
+    ov = run(lp, lens, beam, nb, thr, timesteps=True)
+    ov2 = run(lp, lens, beam, nb, thr, timesteps=True)
+    monkeypatch.setenv("CTCB_OVERLAP", "0")
+    seq = run(lp, lens, beam, nb, thr, timesteps=True)
+    assert ov == seq, name
+    assert ov2 == seq, f"{name}: overlapped decode not deterministic"
+    ref = oracle.decode_batch(lp[:n_oracle], lens[:n_oracle], beam_size=beam, n_best=max(nb, 2),
+                              blank_skip_threshold=thr)
+    for b, r in enumerate(ref):
+        gap = r.scores[0] - r.scores[1] if len(r.scores) > 1 else None
+        assert_same(ov[b], r.tokens[:nb], r.scores[:nb], gap=gap, ctx=f"{name} utt {b}")
+
+
+def test_overlapped_topk_validation_messages(monkeypatch):
+    """validation keys written by the overlapped top-k reach the host check"""
+    monkeypatch.setenv("CTCB_TOPK_MODE", "precomp")
+    monkeypatch.setenv("CTCB_OVERLAP", "1")
+    cfg = synth.CONFIGS[3]
+    lp, lens = synth.batch(cfg, indices=range(8))
+    lp[5, 11, 123] = np.nan
+    dec = cuda_ctc_decoder(vocab(cfg.vocab), beam_size=cfg.beam, blank_skip_threshold=1.0, validate=True)
+    with pytest.raises(ValueError, match="utterance 5: non-finite log-probability at frame 11, token 123"):
+        dec(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
