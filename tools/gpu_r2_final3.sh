@@ -1,0 +1,26 @@
+# Final round-2 measurement set (third session): as gpu_r2_final.sh, shorter fuzz sweeps.
+# Round 2 measurement set: GPU tests, bench lines (cfg4 with CPU baselines / e2e / parity,
+# reference arm, cfg1, cfg2 beam 50/100, cfg3), launch list, ncu --set full of the
+# headline kernel, utterance timeline, checked-build sanitizer substitute, smoke.
+set -x
+mkdir -p gpurun_out/final3
+O=gpurun_out/final3
+nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/gpu.txt
+lscpu | grep -E "Model name|^CPU\(s\)" > $O/host_cpu.txt
+timeout 1200 python -m pytest tests -q -m gpu -rx > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
+timeout 300 python bench.py --workload cfg1 --no-cpu-baseline > $O/bench_cfg1.json 2> $O/bench_cfg1.err
+timeout 300 python bench.py --workload cfg2 --beam 50 --no-cpu-baseline --no-e2e > $O/bench_cfg2_b50.json 2> $O/bench_cfg2_b50.err
+timeout 300 python bench.py --workload cfg2 --beam 100 --no-cpu-baseline --no-e2e > $O/bench_cfg2_b100.json 2> $O/bench_cfg2_b100.err
+timeout 300 python bench.py --workload cfg3 --no-cpu-baseline > $O/bench_cfg3.json 2> $O/bench_cfg3.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:ctcb_decode_fast_small -s 3 -c 1 -o $O/ncu_full_cfg4 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_full.log 2>&1
+timeout 300 python tools/utt_timeline.py 4 > $O/timeline_cfg4.json 2>&1
+python tools/sanitize_cases.py > $O/checks_plain.log 2>&1; echo "rc=$?" >> $O/checks_plain.log
+if [ -f variants/libctcb_chk.so ]; then CTCB_LIB=variants/libctcb_chk.so python tools/sanitize_cases.py > $O/checks_fchk.log 2>&1; echo "rc=$?" >> $O/checks_fchk.log; fi
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 600 python tools/parity_full.py 4 1 3 > $O/parity_full.log 2>&1
+timeout 900 python tools/fuzz_parity.py 250 401 > $O/fuzz_parity_s401.log 2>&1
+CTCB_TOPK_MODE=fused timeout 900 python tools/fuzz_parity.py 250 402 > $O/fuzz_parity_fused_s402.log 2>&1
+python tools/shard_modes.py 8 4 2 > $O/shard_modes.log 2>&1

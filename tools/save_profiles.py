@@ -1,14 +1,16 @@
 """Copy a round's measurement outputs from gpurun_out/ into profiles/<dir>/ and
-summarise the ncu capture of the decode kernel (usage: python tools/save_profiles.py profiles/r01/s2)."""
+summarise the ncu capture of the decode kernel
+(usage: python tools/save_profiles.py profiles/r01/s2 [gpurun_out/subdir])."""
 import csv, io, json, os, shutil, subprocess, sys
 
 dst = sys.argv[1]
+src = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
 os.makedirs(dst, exist_ok=True)
 for f in ("bench.json", "bench_ref.json", "bench_cfg1.json", "launches.csv", "host_cpu.txt", "gpu.txt", "pytest_gpu.log",
           "smoke.log"):
-    if os.path.exists(os.path.join("gpurun_out", f)):
-        shutil.copy(os.path.join("gpurun_out", f), os.path.join(dst, f))
-rep = "gpurun_out/ncu_full_cfg4.ncu-rep"
+    if os.path.exists(os.path.join(src, f)):
+        shutil.copy(os.path.join(src, f), os.path.join(dst, f))
+rep = os.path.join(src, "ncu_full_cfg4.ncu-rep")
 if os.path.exists(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
