@@ -220,7 +220,7 @@ WsLayout ws_layout(const ctcb_handle* h, int B, int T) {
   w.topk_tok = take(ntk * 4);
   w.topk_val = take(ntk * 4);
   w.rowoff = take(ntk ? ((size_t)B + 1) * 4 : 0);
-  w.ready = take(use_precomp(h, B) ? (size_t)B * T * 4 : 0);
+  w.ready = take(use_precomp(h, B) || use_block_pre(h) ? (size_t)B * T * 4 : 0);
   w.vkey = take((size_t)B * 8);
   w.vdone = take((size_t)B * 4);
   w.total = ctcb::align_up(o, 256);
@@ -298,10 +298,9 @@ int make_params(ctcb_handle* h, const float* lp, int64_t sb, int64_t st, const i
 // slots), so that both grids are resident at once and the walk consumes the
 // lists while the top-k produces them.  0 = no room: the top-k runs first.
 int topk_beside_walk(const ctcb_handle* h, const void* wfn, int wgrid, int wthreads, size_t wsmem, size_t tsmem,
-                     int tthreads, int tbps) {
+                     int tthreads, int tbps, const void* tfn) {
   cudaFuncAttributes fw{}, ft{};
-  if (cudaFuncGetAttributes(&fw, wfn) != cudaSuccess ||
-      cudaFuncGetAttributes(&ft, (const void*)ctcb::ctcb_topk_kernel) != cudaSuccess)
+  if (cudaFuncGetAttributes(&fw, wfn) != cudaSuccess || cudaFuncGetAttributes(&ft, tfn) != cudaSuccess)
     return 0;
   int dev = 0, smem_sm = 0, regs_sm = 0, thr_sm = 0, blk_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -598,14 +597,6 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     ctcb::ctcb_framemap_kernel<<<(B + 7) / 8, 256, 0, s>>>(P);
     h->launches++;
     CTCB_CUDA(cudaGetLastError());
-    ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
-    h->launches++;
-    CTCB_CUDA(cudaGetLastError());
-    int tbps = 0;
-    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_wide_kernel, 256, 0));
-    ctcb::ctcb_topk_wide_kernel<<<h->num_sms * (tbps > 0 ? tbps : 1), 256, 0, s>>>(P);
-    h->launches++;
-    CTCB_CUDA(cudaGetLastError());
   }
   if (blk) {  // one 256-thread CTA per utterance
     P.smem_per_warp = (int)ctcb::make_block_layout(ctcb::kBlockMaxBeam, 256, ctcb::kBlockMaxV, ctcb::kBlockMaxV * 4).total;
@@ -670,7 +661,8 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     const char* ovb = getenv("CTCB_OVERLAP_BPS");
     const bool want = ov ? strcmp(ov, "0") != 0 : Q.row_bytes == 0;
     if (want) {
-      int fit = topk_beside_walk(h, kfn, grid, 32 * P.warps_per_block, smem, tsmem, tk_threads, tbps);
+      int fit = topk_beside_walk(h, kfn, grid, 32 * P.warps_per_block, smem, tsmem, tk_threads, tbps,
+                                 (const void*)ctcb::ctcb_topk_kernel);
       if (ovb && atoi(ovb) > 0 && atoi(ovb) < fit) fit = atoi(ovb);
       if (fit > 0) {
         overlap = true;
@@ -695,6 +687,38 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
       CTCB_CUDA(cudaGetLastError());
     }
   }
+  // block kernel, precomputed lists (ctcb_topk_wide_kernel): beside the walk
+  // as in the fast path (default; cfg2 beam 50 / 100: 9.80 -> 9.57 /
+  // 15.14 -> 14.94 ms per step), or before it (CTCB_OVERLAP=0)
+  bool overlap_blk = false;
+  int tkw_grid = 0;
+  if (blk && P.precomp) {
+    int tbps = 0;
+    CTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tbps, ctcb::ctcb_topk_wide_kernel, 256, 0));
+    tkw_grid = h->num_sms * (tbps > 0 ? tbps : 1);
+    const char* ov = getenv("CTCB_OVERLAP");
+    const char* ovb = getenv("CTCB_OVERLAP_BPS");
+    if (!(ov && strcmp(ov, "0") == 0)) {
+      int fit = topk_beside_walk(h, kfn, grid, 256, smem, 0, 256, tbps, (const void*)ctcb::ctcb_topk_wide_kernel);
+      if (ovb && atoi(ovb) > 0 && atoi(ovb) < fit) fit = atoi(ovb);
+      if (fit > 0) {
+        overlap_blk = true;
+        tkw_grid = h->num_sms * fit;
+        CTCB_CUDA(cudaFuncSetAttribute(ctcb::ctcb_topk_wide_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CTCB_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        P.ready = (uint32_t*)((char*)P.topk_tok - L.topk_tok + L.ready);
+        CTCB_CUDA(cudaMemsetAsync(P.ready, 0, (size_t)B * T * 4, s));
+      }
+    }
+    if (!overlap_blk) {
+      ctcb::ctcb_rowoff_kernel<<<1, 1024, 0, s>>>(P);
+      h->launches++;
+      CTCB_CUDA(cudaGetLastError());
+      ctcb::ctcb_topk_wide_kernel<<<tkw_grid, 256, 0, s>>>(P);
+      h->launches++;
+      CTCB_CUDA(cudaGetLastError());
+    }
+  }
   // diagnostics: CTCB_UTT_TRACE=path dumps a per-utterance timeline of the
   // fast kernels ([B, 2] uint64: smid << 48 | global warp, start ns; end ns)
   const char* trace_path = getenv("CTCB_UTT_TRACE");
@@ -711,9 +735,28 @@ static int decode_impl(ctcb_t* h, const float* lp, int64_t sb, int64_t st, const
     h->launches++;
     CTCB_CUDA(cudaGetLastError());
   }
+  if (overlap_blk) {
+    ctcb::ctcb_topk_wide_kernel<<<tkw_grid, 256, 0, s>>>(P);
+    h->launches++;
+    CTCB_CUDA(cudaGetLastError());
+  }
   if (blk) {
     void* args[] = {(void*)&P};
-    CTCB_CUDA(cudaLaunchKernel((const void*)ctcb::ctcb_decode_block_kernel, dim3(grid), dim3(256), args, smem, s));
+    if (overlap_blk) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(256);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      CTCB_CUDA(cudaLaunchKernelExC(&lc, (const void*)ctcb::ctcb_decode_block_kernel, args));
+    } else {
+      CTCB_CUDA(cudaLaunchKernel((const void*)ctcb::ctcb_decode_block_kernel, dim3(grid), dim3(256), args, smem, s));
+    }
     h->last_kernel = "ctcb_decode_block_kernel";
     h->launches++;
   } else if (pair) {

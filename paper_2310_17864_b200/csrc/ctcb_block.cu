@@ -1054,7 +1054,10 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
     __syncthreads();
     const int item = w.misc()[2];
     __syncthreads();
-    if (item >= P.B) break;
+    if (item >= P.B) {
+      if (P.ready != nullptr) pdl_wait_primary();  // complete only after the top-k grid
+      break;
+    }
     const int u = P.order[item];
     w.u = u;
     const int len = P.lens[u];
@@ -1106,10 +1109,41 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
     const size_t tk_base = (size_t)u * P.T_max * k;
     int pre_t = 0;
     float pre_v = 0.0f;
-    if (P.precomp && kept > 0 && tid < k) {
-      pre_t = P.topk_tok[tk_base + tid];
-      pre_v = P.topk_val[tk_base + tid];
-    }
+    // overlapped top-k (P.ready): list j is read only after its flag is
+    // published (warp 0 polls 32 flags per ballot, the block learns the new
+    // bound through misc[15]); lists are read through L2 (__ldcg)
+    int rdy = 0;
+    auto await_list = [&](int j) {  // block-uniform
+      if (P.ready == nullptr || j < rdy) return;
+      if (tid < 32) {
+        const uint32_t* fl = P.ready + (size_t)u * P.T_max;
+        int r = rdy;
+        for (;;) {
+          const int f = r + tid;
+          const bool ok = f >= kept || ld_acquire_gpu(fl + f) != 0u;
+          const unsigned bal = __ballot_sync(FULL, ok);
+          r += bal == FULL ? 32 : __ffs(~bal) - 1;
+          if (j < r) break;
+          __nanosleep(128);
+        }
+        fence_acq_rel_gpu();
+        if (tid == 0) w.misc()[15] = r;
+      }
+      __syncthreads();
+      rdy = w.misc()[15];
+      __syncthreads();
+    };
+    auto load_list = [&](int j) {
+      if (P.ready != nullptr) {
+        pre_t = __ldcg(P.topk_tok + tk_base + (size_t)j * k + tid);
+        pre_v = __ldcg(P.topk_val + tk_base + (size_t)j * k + tid);
+      } else {
+        pre_t = P.topk_tok[tk_base + (size_t)j * k + tid];
+        pre_v = P.topk_val[tk_base + (size_t)j * k + tid];
+      }
+    };
+    if (P.precomp && kept > 0) await_list(0);
+    if (P.precomp && kept > 0 && tid < k) load_list(0);
     __syncthreads();
     bool died = false;
     for (int i = 0; i < kept; i++) {
@@ -1140,15 +1174,13 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
         }
       };
       if (P.precomp) {
+        if (i + 1 < kept) await_list(i + 1);
         // S of this frame; bstep's first barrier publishes it
         if (tid < k) {
           w.stok()[tid] = pre_t;
           w.sval()[tid] = pre_v;
           w.pos()[pre_t] = (uint16_t)tid;
-          if (i + 1 < kept) {
-            pre_t = P.topk_tok[tk_base + (size_t)(i + 1) * k + tid];
-            pre_v = P.topk_val[tk_base + (size_t)(i + 1) * k + tid];
-          }
+          if (i + 1 < kept) load_list(i + 1);
         }
       } else {
         btopk(w, row);
@@ -1213,16 +1245,29 @@ __global__ void __launch_bounds__(256, 3) ctcb_topk_wide_kernel(const __grid_con
   __shared__ uint64_t sbuf[8][256];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t* buf = sbuf[wid];
+  // overlapped mode (P.ready): the block walk is a programmatic dependent of
+  // this grid (see ctcb_topk_kernel); rows go frame-major, g = frame * B + slot
+  // with utterance order[slot], and each list is published by its ready flag
+  pdl_launch_dependents();
+  const bool fm = P.ready != nullptr;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long total = P.rowoff[P.B];
+  const long long total = fm ? (long long)P.B * P.T_max : P.rowoff[P.B];
   const int V = P.V, k = P.k, blank = P.blank;
   for (long long g = (long long)blockIdx.x * (blockDim.x >> 5) + wid; g < total; g += nw) {
-    int lo = 0, hi = P.B - 1;  // utterance: last u with rowoff[u] <= g
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (P.rowoff[mid] <= g) lo = mid; else hi = mid - 1;
+    int u, i;
+    if (fm) {
+      u = P.order[(int)(g % P.B)];
+      i = (int)(g / P.B);
+      if (i >= P.kept[u]) continue;
+    } else {
+      int lo = 0, hi = P.B - 1;  // utterance: last u with rowoff[u] <= g
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (P.rowoff[mid] <= g) lo = mid; else hi = mid - 1;
+      }
+      u = lo;
+      i = (int)(g - P.rowoff[u]);
     }
-    const int u = lo, i = (int)(g - P.rowoff[u]);
     const float* src = P.lp + (size_t)u * P.stride_b + (size_t)P.frame_map[(size_t)u * P.T_max + i] * P.stride_t;
     uint32_t key[16];  // ord32 (0: absent), token r * 32 + lane
     float vs = 0.0f, vmn = INFINITY, vmx = -INFINITY;  // validation screen partials
@@ -1276,6 +1321,11 @@ __global__ void __launch_bounds__(256, 3) ctcb_topk_wide_kernel(const __grid_con
     else if (k <= 128) topk_sort_write<4>(buf, k, src, P.topk_tok + ob, P.topk_val + ob, lane);
     else topk_sort_write<8>(buf, k, src, P.topk_tok + ob, P.topk_val + ob, lane);
     __syncwarp();
+    if (fm) {  // every lane fences its list stores, lane 0 publishes
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu(P.ready + (size_t)u * P.T_max + i, 1u);
+    }
   }
 }
 

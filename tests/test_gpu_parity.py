@@ -815,3 +815,19 @@ def test_overlapped_topk_validation_messages(monkeypatch):
     dec = cuda_ctc_decoder(vocab(cfg.vocab), beam_size=cfg.beam, blank_skip_threshold=1.0, validate=True)
     with pytest.raises(ValueError, match="utterance 5: non-finite log-probability at frame 11, token 123"):
         dec(torch.from_numpy(lp).cuda(), torch.from_numpy(lens).cuda())
+
+
+@pytest.mark.parametrize("beam", [50, 100])
+def test_overlapped_block_topk_matches_sequential_and_oracle(monkeypatch, beam):
+    """block kernel (16 < beam <= 128): ctcb_topk_wide_kernel beside the walk"""
+    cfg = synth.CONFIGS[2]
+    lp, lens = synth.batch(cfg, indices=range(12))
+    monkeypatch.setenv("CTCB_OVERLAP", "1")
+    ov = run(lp, lens, beam, 10, cfg.threshold, timesteps=True)
+    monkeypatch.setenv("CTCB_OVERLAP", "0")
+    seq = run(lp, lens, beam, 10, cfg.threshold, timesteps=True)
+    assert ov == seq
+    ref = oracle.decode_batch(lp[:3], lens[:3], beam_size=beam, n_best=10, blank_skip_threshold=cfg.threshold)
+    for b, r in enumerate(ref):
+        gap = r.scores[0] - r.scores[1] if len(r.scores) > 1 else None
+        assert_same(ov[b], r.tokens[:10], r.scores[:10], gap=gap, ctx=f"beam {beam} utt {b}")
