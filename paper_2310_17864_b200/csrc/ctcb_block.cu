@@ -1113,6 +1113,15 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
     // published (warp 0 polls 32 flags per ballot, the block learns the new
     // bound through misc[15]); lists are read through L2 (__ldcg)
     int rdy = 0;
+    // invalid input rows are never walked (see fast_decode): an utterance with
+    // an offender key from the top-k kernel's screen ends as a dead beam before
+    // its first frame / before the frames of the poll that saw it; misc[14]
+    // makes the verdict block-uniform
+    bool vbad = false;
+    if (tid == 0) w.misc()[14] = (P.precomp && P.validate && P.ready == nullptr && kept > 0 && __ldcg(P.vkey + u) != ~0ull) ? 1 : 0;
+    __syncthreads();
+    vbad = w.misc()[14] != 0;
+    __syncthreads();
     auto await_list = [&](int j) {  // block-uniform
       if (P.ready == nullptr || j < rdy) return;
       if (tid < 32) {
@@ -1127,10 +1136,14 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
           __nanosleep(128);
         }
         fence_acq_rel_gpu();
-        if (tid == 0) w.misc()[15] = r;
+        if (tid == 0) {
+          w.misc()[15] = r;
+          if (P.validate && __ldcg(P.vkey + u) != ~0ull) w.misc()[14] = 1;
+        }
       }
       __syncthreads();
       rdy = w.misc()[15];
+      vbad = w.misc()[14] != 0;
       __syncthreads();
     };
     auto load_list = [&](int j) {
@@ -1147,6 +1160,7 @@ __global__ void __launch_bounds__(NT) ctcb_decode_block_kernel(const __grid_cons
     __syncthreads();
     bool died = false;
     for (int i = 0; i < kept; i++) {
+      if (vbad) { died = true; break; }
       if (i + 1 < kept) issue(i + 1);
       const uint32_t slot = n_cons & 1u;
       if (P.bulk_ok) {

@@ -389,7 +389,9 @@ __device__ __forceinline__ uint64_t topk_key(const FastSmem& S, const float* row
   }
   const int cnt = __reduce_add_sync(FULL, cl);
   uint64_t skey;
-  if (cnt <= 64) {
+  // cnt < k only when NaN values (invalid input, never >= tf) leave too few
+  // survivors: the radix select then keeps every index in range
+  if (cnt <= 64 && cnt >= k) {
     int off = warp_incl_scan(cl, lane) - cl;
     if (small_v) {
       while (pm) {
@@ -457,7 +459,7 @@ __device__ __forceinline__ uint64_t topk_key_g(const FastSmem& S, const float* _
     cl += (q.x >= tf) + (q.y >= tf) + (q.z >= tf) + (q.w >= tf);
   }
   const int cnt = __reduce_add_sync(FULL, cl);
-  if (cnt > 64) {
+  if (cnt > 64 || cnt < k) {  // cnt < k: NaN input (see topk_key)
     if (lane == 0 && dbg) atomicAdd(&dbg[kDbgRadix], 1ull);
     return topk_radix_f(S, [&](int c) { return c == blank ? 0u : okey(__ldg(grow + c)); }, V, k, lane);
   }
@@ -525,7 +527,7 @@ __device__ __forceinline__ int topk_small(const FastSmem& S, const float* row, i
     packed |= (uint32_t)__popc(nib) << (8 * j);
   }
   const int cnt = __reduce_add_sync(FULL, __popc(pm));
-  if (cnt > 64) {
+  if (cnt > 64 || cnt < k) {  // cnt < k: NaN input (see topk_key)
     if (lane == 0 && dbg) atomicAdd(&dbg[kDbgRadix], 1ull);
     const uint64_t sk = topk_radix_ool(row, S.hist, S.cand, V, k, lane);
     return skey_tok(sk);
@@ -847,6 +849,14 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
     // published; flags are polled 32 frames at a time (one poll per 32 frames
     // while the top-k kernel runs ahead), lists are read through L2 (__ldcg)
     int rdy = 0;
+    // Invalid input rows (emissions.py:128-150) are never walked in
+    // precomputed mode: the top-k kernel screens every row before its list
+    // exists, so an utterance with an offender key ends as a dead beam before
+    // its first frame (lists complete) or before the frames of the poll that
+    // saw it (overlapped); ctcb_validate_post_kernel then reports the
+    // offender.  (NaN / +inf scores could otherwise reach the selection.)
+    bool vbad = PRE && P.validate && P.ready == nullptr && kept > 0 &&
+                __shfl_sync(FULL, (int)(__ldcg(P.vkey + u) != ~0ull), 0);
     auto await_list = [&](int j) {
       if (!PRE || P.ready == nullptr || j < rdy) return;
       const uint32_t* fl = P.ready + (size_t)(uint32_t)u * (uint32_t)P.T_max;
@@ -860,6 +870,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       }
       fence_acq_rel_gpu();
       __syncwarp();
+      if (P.validate && __shfl_sync(FULL, (int)(__ldcg(P.vkey + u) != ~0ull), 0)) vbad = true;  // lane 0's view: warp-uniform
     };
     auto load_list = [&](int j) {
       if (P.ready != nullptr) {
@@ -912,6 +923,7 @@ __device__ __forceinline__ void fast_decode(const Params& P) {
       PH(0);
       classify_to(i + ring - 1);
       if (i >= kept) break;
+      if (PRE && vbad) { died = true; died_at = i; break; }
       float* row;
       if (bulk) {
         if (i + ring - 1 < kept) { issue(i + ring - 1); n_out++; }

@@ -325,7 +325,7 @@ __device__ __forceinline__ void pair_topk(const PairSmem& S, const float* row, b
   const int hf = (threadIdx.x >> 4) & 1;
   const int cnt = (int)seg_sum((unsigned)__popc(pm), hf);
   const bool big = __any_sync(FULL, cnt > 32);  // warp-uniform sort width
-  if (__any_sync(FULL, cnt > 64)) {
+  if (__any_sync(FULL, cnt > 64 || cnt < k)) {  // cnt < k: NaN input leaves too few survivors
     // many exact ties above the threshold: exact selection by k rounds of a
     // segmented max over (value desc, index asc) keys (rare)
     // (both halves take this path; it is exact for any row)

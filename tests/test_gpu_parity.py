@@ -831,3 +831,32 @@ def test_overlapped_block_topk_matches_sequential_and_oracle(monkeypatch, beam):
     for b, r in enumerate(ref):
         gap = r.scores[0] - r.scores[1] if len(r.scores) > 1 else None
         assert_same(ov[b], r.tokens[:10], r.scores[:10], gap=gap, ctx=f"beam {beam} utt {b}")
+
+
+@pytest.mark.parametrize("beam,V,overlap", [(10, 12, "0"), (10, 12, "1"), (10, 1000, "1"), (32, 12, "0"),
+                                            (32, 12, "1"), (50, 500, "1")])
+def test_precomputed_modes_never_walk_invalid_rows(monkeypatch, beam, V, overlap):
+    """Rows with NaN / +inf / positive log-probs in every utterance: the
+    precomputed-mode walks (fast and block kernels, lists before or beside the
+    walk) stop at the top-k kernel's offender key instead of walking non-finite
+    scores; the decode raises the reference's message for the first invalid
+    utterance, and the same decoder then decodes a clean batch."""
+    monkeypatch.setenv("CTCB_TOPK_MODE", "precomp")
+    monkeypatch.setenv("CTCB_OVERLAP", overlap)
+    rng = np.random.default_rng(beam * 7 + V)
+    B, T = 8, 40
+    x = rng.normal(size=(B, T, V)) * 2.0
+    lp = (x - np.log(np.exp(x).sum(-1, keepdims=True))).astype(np.float32)
+    lens = torch.tensor([40, 33, 40, 5, 40, 21, 40, 40], dtype=torch.int32).cuda()
+    dec = cuda_ctc_decoder(vocab(V), beam_size=beam, nbest=1, blank_skip_threshold=1.0)
+    clean = dec(torch.from_numpy(lp).cuda(), lens)
+    bad = lp.copy()
+    for b in range(B):
+        for t in rng.choice(min(int(lens[b]), 40), size=2, replace=False):
+            bad[b, t, rng.integers(0, V, size=3)] = [np.nan, np.inf, 3.0]
+    bad[0, :, :] = lp[0]  # utterance 0 clean: utterance 1 is the first offender
+    t1 = min(t for t in range(40) if not np.isfinite(bad[1, t]).all() or (bad[1, t] > 1e-4).any())
+    with pytest.raises(ValueError, match=f"utterance 1: non-finite log-probability at frame {t1}, token "):
+        dec(torch.from_numpy(bad).cuda(), lens)
+    again = dec(torch.from_numpy(lp).cuda(), lens)
+    assert [[h.tokens for h in g] for g in again] == [[h.tokens for h in g] for g in clean]
