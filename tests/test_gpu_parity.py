@@ -834,15 +834,25 @@ def test_overlapped_block_topk_matches_sequential_and_oracle(monkeypatch, beam):
 
 
 @pytest.mark.parametrize("beam,V,overlap", [(10, 12, "0"), (10, 12, "1"), (10, 1000, "1"), (32, 12, "0"),
-                                            (32, 12, "1"), (50, 500, "1")])
+                                            (32, 12, "1"), (50, 500, "1"), (10, 12, "fused"), (10, 500, "fused"),
+                                            (10, 1000, "fused"), (10, 12, "generic"), (24, 12, "inline")])
 def test_precomputed_modes_never_walk_invalid_rows(monkeypatch, beam, V, overlap):
     """Rows with NaN / +inf / positive log-probs in every utterance: the
     precomputed-mode walks (fast and block kernels, lists before or beside the
     walk) stop at the top-k kernel's offender key instead of walking non-finite
     scores; the decode raises the reference's message for the first invalid
     utterance, and the same decoder then decodes a clean batch."""
-    monkeypatch.setenv("CTCB_TOPK_MODE", "precomp")
-    monkeypatch.setenv("CTCB_OVERLAP", overlap)
+    # (also the in-kernel top-k schedules: fused fast kernel, generic kernel,
+    # block kernel with its inline top-k)
+    if overlap == "fused":
+        monkeypatch.setenv("CTCB_TOPK_MODE", "fused")
+    elif overlap == "generic":
+        monkeypatch.setenv("CTCB_FORCE_GENERIC", "1")
+    elif overlap == "inline":
+        monkeypatch.setenv("CTCB_BLOCK_TOPK", "inline")
+    else:
+        monkeypatch.setenv("CTCB_TOPK_MODE", "precomp")
+        monkeypatch.setenv("CTCB_OVERLAP", overlap)
     rng = np.random.default_rng(beam * 7 + V)
     B, T = 8, 40
     x = rng.normal(size=(B, T, V)) * 2.0
