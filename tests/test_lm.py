@@ -339,3 +339,32 @@ def test_reader_and_scorer_match_reference_implementation():
                 sb, y = glm.lm_score(b, sb, str(w))
                 assert x == y and sa.context == sb.context
             assert rlm.lm_finish(a, sa) == glm.lm_finish(b, sb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V,beam", [(12, 10), (40, 16), (500, 10)])
+def test_fused_kernel_invalid_rows_raise(tmp_path, V, beam):
+    """NaN / +inf / positive rows through the LM-fused kernel: the decode
+    raises the reference's validation message for the first offender and the
+    same decoder then decodes a clean batch (no out-of-range indices)."""
+    import torch
+    from paper_2310_17864_b200 import cuda_ctc_decoder
+    rng = np.random.default_rng(V + beam)
+    toks = ["-"] + [f"w{i}" for i in range(1, V)]
+    lm = random_arpa(tmp_path / "m.arpa", rng, toks[1:], 2, keep=min(0.5, 30.0 / V))
+    B, T = 6, 40
+    x = rng.normal(size=(B, T, V)) * 2.0
+    lp = (x - np.log(np.exp(x).sum(2, keepdims=True))).astype(np.float32)
+    lens = torch.tensor([40, 31, 40, 7, 40, 22], dtype=torch.int32).cuda()
+    dec = cuda_ctc_decoder(toks, beam_size=beam, nbest=2, blank_skip_threshold=1.0)
+    dec.set_lm(lm, 1.2)
+    clean = dec(torch.from_numpy(lp).cuda(), lens)
+    bad = lp.copy()
+    for b in range(1, B):
+        for t in rng.choice(int(lens[b]), size=2, replace=False):
+            bad[b, t, rng.integers(0, V, size=3)] = [np.nan, np.inf, 3.0]
+    t1 = min(t for t in range(40) if not np.isfinite(bad[1, t]).all())
+    with pytest.raises(ValueError, match=f"utterance 1: non-finite log-probability at frame {t1}, token "):
+        dec(torch.from_numpy(bad).cuda(), lens)
+    again = dec(torch.from_numpy(lp).cuda(), lens)
+    assert [[h.tokens for h in g] for g in again] == [[h.tokens for h in g] for g in clean]
