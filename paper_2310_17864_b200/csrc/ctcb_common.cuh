@@ -310,7 +310,9 @@ template <int MAXCH = 0, bool WITH_MAX = true, bool PADDED = false>
 __device__ __forceinline__ RowPart row_partials(const float* row, int V, int lane) {
   const float4* r4 = (const float4*)row;
   constexpr float kL2E = 1.4426950408889634f;
-  float s = 0.0f, mn = INFINITY, mx = -INFINITY;
+  const float2 l2e2 = make_float2(kL2E, kL2E);
+  float2 s2 = make_float2(0.0f, 0.0f);  // packed fp32x2 (FMUL2 / FADD2): half the scale and sum instructions
+  float mn = INFINITY, mx = -INFINITY;
   const int nch4 = (V + 3) >> 2;
   const bool ragged = (V & 3) != 0;
   auto chunk = [&](int c4) {
@@ -323,7 +325,8 @@ __device__ __forceinline__ RowPart row_partials(const float* row, int V, int lan
     }
     mn = fminf(mn, fminf(fminf(q.x, q.y), fminf(q.z, q.w)));
     if (WITH_MAX) mx = fmaxf(mx, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
-    s += (ex2_ftz(q.x * kL2E) + ex2_ftz(q.y * kL2E)) + (ex2_ftz(q.z * kL2E) + ex2_ftz(q.w * kL2E));  // NaN propagates
+    const float2 a = __fmul2_rn(make_float2(q.x, q.y), l2e2), b = __fmul2_rn(make_float2(q.z, q.w), l2e2);
+    s2 = __fadd2_rn(s2, __fadd2_rn(make_float2(ex2_ftz(a.x), ex2_ftz(a.y)), make_float2(ex2_ftz(b.x), ex2_ftz(b.y))));  // NaN propagates
   };
   if (MAXCH > 0) {
 #pragma unroll
@@ -332,6 +335,7 @@ __device__ __forceinline__ RowPart row_partials(const float* row, int V, int lan
   } else {
     for (int c4 = lane; c4 < nch4; c4 += 32) chunk(c4);
   }
+  const float s = s2.x + s2.y;
   RowPart r;
   r.kmx = s <= 2.0f ? (WITH_MAX ? ord32(mx) : 0u) : 0xffffffffu;  // NaN / huge sums fail the max test
   r.kmn = ord32(mn);
@@ -342,7 +346,10 @@ __device__ __forceinline__ bool row_verdict(const RowPart& r, bool strict) {
   const uint32_t kmx = __reduce_max_sync(0xffffffffu, r.kmx), kmn = __reduce_min_sync(0xffffffffu, r.kmn);
   const uint32_t sfx = __reduce_add_sync(0xffffffffu, r.sfx);
   const bool ok = kmx <= ord32(1e-4f) && kmn > ord32(-INFINITY);
-  return ok && (!strict || fabsf(__logf((float)sfx * (1.0f / 33554432.0f))) < 9e-4f);
+  // |log(sum)| < 9e-4 as integer bounds on the 2^-25 fixed-point sum:
+  // exp(-9e-4) * 2^25 < sfx < exp(9e-4) * 2^25 (no log, no conversion)
+  constexpr uint32_t kLo = 33524247u, kHi = 33584644u;
+  return ok && (!strict || (sfx > kLo && sfx < kHi));
 }
 __device__ __forceinline__ bool row_screen(const float* row, int V, int lane, bool strict) {
   return row_verdict(row_partials(row, V, lane), strict);
