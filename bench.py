@@ -346,11 +346,13 @@ def main():
     dec.kernel_timing(True)  # event pair around the beam kernel of each step (same stream)
     launches0 = dec.launch_count()
     t_mark = time.monotonic()
-    # a ~30 ms spin kernel ahead of the start event: the K steps are enqueued
-    # while it runs, so host-side stalls (Python, driver locks taken by the
-    # clock sampler's nvidia-smi) cannot leave the GPU idle inside the timed
-    # region; the region itself still holds exactly the K decode steps
-    torch.cuda._sleep(int(0.03 * 1.9e9))
+    # a spin kernel ahead of the start event: the K steps are enqueued while
+    # it runs, so host-side stalls (Python, driver locks taken by the clock
+    # sampler's nvidia-smi) cannot leave the GPU idle inside the timed region;
+    # the region itself still holds exactly the K decode steps.  30 ms was not
+    # always enough (one run in ~10 measured 6.2 ms/step around 4.46 ms
+    # kernels), so the spin covers 5 ms of host time per step, at least 250 ms
+    torch.cuda._sleep(int(max(0.25, 0.005 * args.steps) * 1.9e9))
     ev0.record(stream)
     for _ in range(args.steps):
         out = dec.decode(lp_dev, lens_dev)
